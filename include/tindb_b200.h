@@ -1,0 +1,159 @@
+/* tindb_b200 — B200-native (sm_100a) triangle-pair ST_3DDistance /
+ * ST_3DIntersects engine behind a plain C ABI.
+ *
+ * Drop-in boundary for the reference `tindb` operator API
+ * (/root/reference/proj/include/tindb/{kernels,batch}.hpp). The reference has
+ * no mesh x mesh operator: kernels::run_batch returns TypeMismatch for
+ * Mesh x Mesh (batch.cpp:49 eval_distance, batch.cpp:62 eval_intersects) and
+ * kernels::distance_to_mesh throws for a mesh query (kernels.cpp:395-405).
+ * The entry points below are what those branches bind;
+ * each cites the reference interface it extends or replaces.
+ *
+ * Conventions
+ *  - Triangles are 9 doubles (v0 xyz, v1 xyz, v2 xyz), i.e. exactly
+ *    tindb::TriangleMesh::triangles.data() (geometry.hpp:60-98, 72 B/face).
+ *  - Pair index p = i * |B| + j, i indexing the first mesh (the record /
+ *    `a`), j the second (the argument / `b`). Ties keep the lowest p
+ *    (kernels.cpp:359,368-376); intersects reports the lowest hit p
+ *    (kernels.cpp:407-432).
+ *  - Degenerate triangles (norm2((v1-v0)x(v2-v0)) <= 1e-30, geometry.hpp:75)
+ *    contribute +inf to distance minima and never intersect.
+ *  - Every call returns 0 on success and a negative TDB_E* code otherwise;
+ *    tdb_last_error() (thread-local) holds the message. No C++ exception
+ *    crosses this boundary. There is no CPU fallback: without a usable
+ *    sm_100 device every compute call fails with TDB_E_CUDA.
+ *  - Calls are thread-safe (the reference server calls plan_and_execute from
+ *    one thread per connection, pg_server.cpp:231,496); device work is
+ *    serialised per device.
+ */
+#ifndef TINDB_B200_H
+#define TINDB_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TDB_OK 0
+#define TDB_E_ARG (-1)   /* bad argument (maps to std::invalid_argument) */
+#define TDB_E_CUDA (-2)  /* CUDA / device failure (maps to std::runtime_error) */
+#define TDB_E_NOMEM (-3) /* device allocation failed */
+
+typedef struct tdb_geom_s* tdb_mesh;  /* device-resident triangle soup (1 object) */
+typedef struct tdb_geom_s* tdb_table; /* many objects: CSR face offsets + AABB headers */
+
+/* Result of a mesh x mesh distance; mirrors kernels::DistanceResult
+ * (kernels.hpp:28-34) extended with the pair index. */
+typedef struct {
+    double distance;   /* +inf when no non-degenerate pair exists */
+    uint64_t pair;     /* i*|b| + j, UINT64_MAX when not found */
+    uint64_t i, j;     /* face indices in a and b */
+    double on_a[3];    /* witness on a's face i */
+    double on_b[3];    /* witness on b's face j */
+    int32_t found;
+    int32_t _pad;
+} tdb_dist_out;
+
+/* Result of a mesh x mesh intersects; mirrors kernels::IntersectionResult
+ * (kernels.hpp:43-48) with the lowest hit pair. */
+typedef struct {
+    int32_t hit;
+    int32_t _pad;
+    uint64_t pair; /* lowest hit pair, UINT64_MAX when none */
+    uint64_t i, j;
+} tdb_hit_out;
+
+/* Per-call device statistics of the last compute call on this thread. */
+typedef struct {
+    double ms_total;        /* whole call on the device (events) */
+    double ms_filter;       /* the roofline kernel (fast FP64 filter / cull) */
+    double ms_verify;       /* exact re-evaluation of candidate pairs */
+    uint64_t pairs;         /* triangle pairs covered by the call */
+    uint64_t items;         /* (A-tile x B-chunk) work items launched */
+    uint64_t items_flagged; /* items re-scanned by the exact pass */
+    uint64_t candidates;    /* pairs evaluated with the exact composition */
+    uint64_t exact_pairs;   /* intersects: pairs that reached the exact predicate */
+    uint64_t kernels;       /* kernel launches in the call */
+    int32_t rounds;         /* band widenings (>= 1) */
+    int32_t _pad;
+} tdb_stats;
+
+enum { TDB_OP_DISTANCE = 1, TDB_OP_INTERSECTS = 2 }; /* kernels::BatchOp (batch.hpp:14) */
+
+/* Execution mode. FULL evaluates every triangle pair with the FP64 filter
+ * (the roofline path, "no spatial index"). CULL additionally
+ * skips whole (A-tile, B-chunk) items whose AABB lower bound cannot beat the
+ * running answer — same results, fewer pair tests. */
+enum { TDB_MODE_FULL = 0, TDB_MODE_CULL = 1 };
+
+/* ---- runtime (replaces ExecutorConfig / for_each_chunk, executor.hpp:20-83) */
+int tdb_init(int device);             /* idempotent; binds this thread to `device` */
+int tdb_set_stream(void* cuda_stream); /* thread-local launch stream (NULL = library stream) */
+int tdb_set_mode(int mode);           /* thread-local TDB_MODE_* */
+const char* tdb_last_error(void);
+int tdb_last_stats(tdb_stats* out);
+int tdb_device_count(void);
+
+/* ---- device geometry store (replaces the CPU mesh store, store_types.hpp:14-32) */
+int tdb_mesh_upload(const double* tri9, uint64_t n_tris, tdb_mesh* out);
+/* tri9 holds all objects' faces back to back; face_offsets has n_objects+1
+ * entries (CSR), face_offsets[0] == 0. */
+int tdb_table_upload(const double* tri9, const uint64_t* face_offsets, uint64_t n_objects,
+                     tdb_table* out);
+int tdb_geom_info(tdb_mesh g, uint64_t* n_tris, uint64_t* n_objects, uint64_t* n_degenerate,
+                  double* aabb6);
+void tdb_mesh_free(tdb_mesh m);
+void tdb_table_free(tdb_table t);
+
+/* ---- mesh x mesh (new kernels:: entries beside kernels.hpp:59-106) ------- */
+int tdb_mesh_mesh_distance(tdb_mesh a, tdb_mesh b, tdb_dist_out* out);
+int tdb_mesh_mesh_intersects(tdb_mesh a, tdb_mesh b, tdb_hit_out* out);
+/* Row shard [row_begin,row_end) of a (multi-GPU split of the A axis); pair
+ * indices stay global. */
+int tdb_mesh_mesh_distance_rows(tdb_mesh a, uint64_t row_begin, uint64_t row_end, tdb_mesh b,
+                                tdb_dist_out* out);
+int tdb_mesh_mesh_intersects_rows(tdb_mesh a, uint64_t row_begin, uint64_t row_end, tdb_mesh b,
+                                  tdb_hit_out* out);
+
+/* ---- whole-column batch: run_batch(op, records, literal) for Mesh x Mesh
+ * (batch.hpp:49-51). One slot per record, in record order; record is the
+ * first argument. Any output pointer may be NULL. Rows [obj_begin,obj_end)
+ * select a shard of the table (multi-GPU row split); outputs are indexed
+ * from obj_begin. */
+int tdb_table_eval(int op, tdb_table records, tdb_mesh literal, double* dist_out,
+                   uint8_t* hit_out, uint64_t* pair_out);
+int tdb_table_eval_rows(int op, tdb_table records, uint64_t obj_begin, uint64_t obj_end,
+                        tdb_mesh literal, double* dist_out, uint8_t* hit_out,
+                        uint64_t* pair_out);
+
+/* ---- one-shot host-buffer entry points (upload + evaluate + free) -------- */
+int tdb_distance_host(const double* a9, uint64_t n, const double* b9, uint64_t m,
+                      tdb_dist_out* out);
+int tdb_intersects_host(const double* a9, uint64_t n, const double* b9, uint64_t m,
+                        tdb_hit_out* out);
+
+/* ---- triangle-pair batch (parity / golden vectors): out[k] for (a[k], b[k]) */
+int tdb_pairs_distance(const double* a9, const double* b9, uint64_t n, double* dist_out);
+int tdb_pairs_intersects(const double* a9, const double* b9, uint64_t n, uint8_t* hit_out);
+
+/* Filter value d~^2 of the FP64 roofline path for aligned pairs (testing the
+ * filter's error bound against the exact composition). */
+int tdb_pairs_filter(const double* a9, const double* b9, uint64_t n, double* d2_out);
+
+/* ---- mesh generators ("mesh/geometry loader"; dataset.cpp:85-139). Return
+ * the face count; write faces when out != NULL. Bit-identical to the
+ * reference generator. */
+uint64_t tdb_gen_unit_sphere(uint64_t face_target, double* out);
+uint64_t tdb_gen_ore_body(uint64_t face_target, double* out);
+/* NEW (not in the reference): nx*ny*2 CCW-up triangles over x,y in [0,1000],
+ * z = U(-amp, amp) per lattice vertex from mt19937_64(seed) (rng.hpp:12-30). */
+uint64_t tdb_gen_terrain(uint32_t nx, uint32_t ny, double amp, uint64_t seed, double* out);
+
+/* ---- measurement helper: FP64 DFMA issue-rate microbenchmark (TFLOP/s) */
+int tdb_fp64_peak(double* tflops_out, double* ms_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TINDB_B200_H */

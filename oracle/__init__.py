@@ -1,0 +1,226 @@
+"""TEST INFRASTRUCTURE ONLY: ctypes access to the CPU checkers.
+
+* ``C``   — ``oracle/liboracle.so``: the plain-C restatement of the
+  reference primitives and of the SURVEY.md 8(a) A17 triangle-pair
+  composition (tindb_oracle.c).
+* ``REF`` — ``oracle/_ref/libtindb_ref.so``: the unmodified reference
+  sources (/root/reference/proj/src/kernels.cpp, dataset.cpp, ...) plus the
+  A17 composition harness (ref_composition.cpp). ``None`` when it was never
+  built.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import this module. The product package
+(``paper_1808_09571_b200``) never does.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_C = os.path.join(HERE, "liboracle.so")
+LIB_REF = os.path.join(HERE, "_ref", "libtindb_ref.so")
+
+_D = ct.POINTER(ct.c_double)
+_U64 = ct.POINTER(ct.c_uint64)
+_U8 = ct.POINTER(ct.c_uint8)
+
+
+class OrDist(ct.Structure):
+    _fields_ = [("d", ct.c_double), ("on_a", ct.c_double * 3), ("on_b", ct.c_double * 3)]
+
+
+class OrMeshDist(ct.Structure):
+    _fields_ = [
+        ("d", ct.c_double),
+        ("pair", ct.c_uint64),
+        ("found", ct.c_int),
+        ("on_a", ct.c_double * 3),
+        ("on_b", ct.c_double * 3),
+    ]
+
+
+def _dp(a):
+    return a.ctypes.data_as(_D)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _load_c():
+    if not os.path.exists(LIB_C):
+        return None
+    L = ct.CDLL(LIB_C)
+    L.or_tri_tri_distance.argtypes = [_D, _D, ct.POINTER(OrDist)]
+    L.or_tri_tri_intersects.argtypes = [_D, _D]
+    L.or_pairs_distance.argtypes = [_D, _D, ct.c_uint64, _D]
+    L.or_pairs_intersects.argtypes = [_D, _D, ct.c_uint64, _U8]
+    L.or_segment_segment_distance.argtypes = [_D, _D, ct.POINTER(OrDist)]
+    L.or_point_triangle_distance.argtypes = [_D, _D, ct.POINTER(OrDist)]
+    L.or_segment_triangle_distance.argtypes = [_D, _D, ct.POINTER(OrDist)]
+    L.or_segment_triangle_intersect.argtypes = [_D, _D]
+    L.or_triangle_is_degenerate.argtypes = [_D]
+    L.or_mesh_mesh_distance.argtypes = [_D, ct.c_uint64, _D, ct.c_uint64, ct.c_uint64,
+                                        ct.c_uint64, ct.c_uint64, ct.c_int,
+                                        ct.POINTER(OrMeshDist)]
+    L.or_mesh_mesh_intersects.argtypes = [_D, ct.c_uint64, _D, ct.c_uint64, ct.c_uint64,
+                                          ct.c_uint64, ct.c_uint64, ct.c_int, _U64]
+    L.or_table_distance.argtypes = [_D, _U64, ct.c_uint64, _D, ct.c_uint64, ct.c_int, _D, _U64]
+    L.or_table_intersects.argtypes = [_D, _U64, ct.c_uint64, _D, ct.c_uint64, ct.c_int, _U8,
+                                      _U64]
+    return L
+
+
+def _load_ref():
+    if not os.path.exists(LIB_REF):
+        return None
+    L = ct.CDLL(LIB_REF)
+    L.ref_segment_segment_distance.argtypes = [_D, _D, _D]
+    L.ref_point_triangle_distance.argtypes = [_D, _D, _D]
+    L.ref_segment_triangle_distance.argtypes = [_D, _D, _D]
+    L.ref_segment_triangle_intersect.argtypes = [_D, _D]
+    L.ref_triangle_is_degenerate.argtypes = [_D]
+    L.ref_pairs_distance.argtypes = [_D, _D, ct.c_uint64, _D]
+    L.ref_pairs_intersects.argtypes = [_D, _D, ct.c_uint64, _U8]
+    L.ref_mesh_mesh_distance.argtypes = [_D, ct.c_uint64, _D, ct.c_uint64, ct.c_uint64,
+                                         ct.c_uint64, ct.c_uint64, ct.c_int, _D, _U64]
+    L.ref_mesh_mesh_intersects.argtypes = [_D, ct.c_uint64, _D, ct.c_uint64, ct.c_uint64,
+                                           ct.c_uint64, ct.c_uint64, ct.c_int, _U64]
+    L.ref_unit_sphere.argtypes = [ct.c_uint64, _D]
+    L.ref_unit_sphere.restype = ct.c_uint64
+    L.ref_ore_body.argtypes = [ct.c_uint64, _D]
+    L.ref_ore_body.restype = ct.c_uint64
+    L.ref_random_triangles.argtypes = [ct.c_uint64, ct.c_uint64, ct.c_double, ct.c_double, _D]
+    L.ref_unit_cube.argtypes = [_D]
+    L.ref_unit_cube.restype = ct.c_uint64
+    return L
+
+
+C = _load_c()
+REF = _load_ref()
+
+U64_MAX = (1 << 64) - 1
+
+
+# ---------------------------------------------------------------- C oracle
+def pairs_distance(a, b):
+    """A17 distance for aligned pair arrays a[k], b[k] (k x 9)."""
+    a, b = _f64(a).reshape(-1, 9), _f64(b).reshape(-1, 9)
+    out = np.empty(len(a), np.float64)
+    C.or_pairs_distance(_dp(a), _dp(b), len(a), _dp(out))
+    return out
+
+
+def pairs_intersects(a, b):
+    a, b = _f64(a).reshape(-1, 9), _f64(b).reshape(-1, 9)
+    out = np.empty(len(a), np.uint8)
+    C.or_pairs_intersects(_dp(a), _dp(b), len(a), out.ctypes.data_as(_U8))
+    return out.astype(bool)
+
+
+def tri_tri_distance(a9, b9):
+    a9, b9 = _f64(a9), _f64(b9)
+    o = OrDist()
+    C.or_tri_tri_distance(_dp(a9), _dp(b9), ct.byref(o))
+    return o.d, np.array(o.on_a[:]), np.array(o.on_b[:])
+
+
+def mesh_mesh_distance(a, b, threads=None, rows=None):
+    """(dist, pair, found, on_a, on_b). rows = (begin, end, stride) or None."""
+    a, b = _f64(a).reshape(-1, 9), _f64(b).reshape(-1, 9)
+    r0, r1, rs = rows if rows else (0, len(a), 1)
+    o = OrMeshDist()
+    C.or_mesh_mesh_distance(_dp(a), len(a), _dp(b), len(b), r0, r1, rs,
+                            threads or os.cpu_count() or 1, ct.byref(o))
+    return o.d, o.pair, bool(o.found), np.array(o.on_a[:]), np.array(o.on_b[:])
+
+
+def mesh_mesh_intersects(a, b, threads=None, rows=None):
+    """(hit, lowest hit pair or U64_MAX)."""
+    a, b = _f64(a).reshape(-1, 9), _f64(b).reshape(-1, 9)
+    r0, r1, rs = rows if rows else (0, len(a), 1)
+    p = ct.c_uint64(0)
+    C.or_mesh_mesh_intersects(_dp(a), len(a), _dp(b), len(b), r0, r1, rs,
+                              threads or os.cpu_count() or 1, ct.byref(p))
+    return p.value != U64_MAX, p.value
+
+
+def table_eval(op, table, offsets, query, threads=None):
+    """Per record: (dist or hit array, pair array). op in {'distance','intersects'}."""
+    table, query = _f64(table).reshape(-1, 9), _f64(query).reshape(-1, 9)
+    offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+    nobj = len(offsets) - 1
+    pair = np.empty(nobj, np.uint64)
+    th = threads or os.cpu_count() or 1
+    if op == "distance":
+        d = np.empty(nobj, np.float64)
+        C.or_table_distance(_dp(table), offsets.ctypes.data_as(_U64), nobj, _dp(query),
+                            len(query), th, _dp(d), pair.ctypes.data_as(_U64))
+        return d, pair
+    h = np.empty(nobj, np.uint8)
+    C.or_table_intersects(_dp(table), offsets.ctypes.data_as(_U64), nobj, _dp(query),
+                          len(query), th, h.ctypes.data_as(_U8), pair.ctypes.data_as(_U64))
+    return h.astype(bool), pair
+
+
+# ------------------------------------------------------- reference (_ref)
+def ref_pairs_distance(a, b):
+    a, b = _f64(a).reshape(-1, 9), _f64(b).reshape(-1, 9)
+    out = np.empty((len(a), 7), np.float64)
+    REF.ref_pairs_distance(_dp(a), _dp(b), len(a), _dp(out))
+    return out
+
+
+def ref_pairs_intersects(a, b):
+    a, b = _f64(a).reshape(-1, 9), _f64(b).reshape(-1, 9)
+    out = np.empty(len(a), np.uint8)
+    REF.ref_pairs_intersects(_dp(a), _dp(b), len(a), out.ctypes.data_as(_U8))
+    return out.astype(bool)
+
+
+def ref_mesh_mesh_distance(a, b, threads=None, rows=None):
+    a, b = _f64(a).reshape(-1, 9), _f64(b).reshape(-1, 9)
+    r0, r1, rs = rows if rows else (0, len(a), 1)
+    out = np.empty(7, np.float64)
+    p = ct.c_uint64(0)
+    REF.ref_mesh_mesh_distance(_dp(a), len(a), _dp(b), len(b), r0, r1, rs,
+                               threads or os.cpu_count() or 1, _dp(out), ct.byref(p))
+    return out[0], p.value, p.value != U64_MAX, out[1:4].copy(), out[4:7].copy()
+
+
+def ref_mesh_mesh_intersects(a, b, threads=None, rows=None):
+    a, b = _f64(a).reshape(-1, 9), _f64(b).reshape(-1, 9)
+    r0, r1, rs = rows if rows else (0, len(a), 1)
+    p = ct.c_uint64(0)
+    REF.ref_mesh_mesh_intersects(_dp(a), len(a), _dp(b), len(b), r0, r1, rs,
+                                 threads or os.cpu_count() or 1, ct.byref(p))
+    return p.value != U64_MAX, p.value
+
+
+def ref_unit_sphere(face_target):
+    n = REF.ref_unit_sphere(face_target, None)
+    out = np.empty((n, 9), np.float64)
+    REF.ref_unit_sphere(face_target, _dp(out))
+    return out
+
+
+def ref_ore_body(face_target):
+    n = REF.ref_ore_body(face_target, None)
+    out = np.empty((n, 9), np.float64)
+    REF.ref_ore_body(face_target, _dp(out))
+    return out
+
+
+def ref_random_triangles(seed, n, lo=-1.0, hi=1.0):
+    out = np.empty((n, 9), np.float64)
+    REF.ref_random_triangles(seed, n, lo, hi, _dp(out))
+    return out
+
+
+def ref_unit_cube():
+    out = np.empty((12, 9), np.float64)
+    REF.ref_unit_cube(_dp(out))
+    return out

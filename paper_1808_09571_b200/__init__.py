@@ -1,0 +1,395 @@
+"""tindb_b200 — Python mirror of the triangle-pair operator API.
+
+A thin ctypes layer over ``libtindb_b200.so`` (the C ABI in
+``include/tindb_b200.h``). Names follow the reference operator surface
+(``tindb::kernels``, /root/reference/proj/include/tindb/kernels.hpp and
+batch.hpp): ``mesh_mesh_distance`` / ``mesh_mesh_intersects`` are the new
+Mesh x Mesh entries beside ``distance_to_mesh`` / ``intersects_mesh``, and
+``run_batch`` mirrors ``kernels::run_batch`` (batch.hpp:49) for a mesh table
+against a mesh literal.
+
+There is no CPU fallback: importing works without a GPU (so the ABI can be
+checked), but every compute call raises ``RuntimeError`` unless an sm_100
+device is present and the library was built (``python __graft_entry__.py``
+or ``make``).
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Union
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtindb_b200.so")
+
+TDB_OK, TDB_E_ARG, TDB_E_CUDA, TDB_E_NOMEM = 0, -1, -2, -3
+OP_DISTANCE, OP_INTERSECTS = 1, 2
+MODE_FULL, MODE_CULL = 0, 1
+U64_MAX = (1 << 64) - 1
+
+_D = ct.POINTER(ct.c_double)
+_U64 = ct.POINTER(ct.c_uint64)
+_U8 = ct.POINTER(ct.c_uint8)
+
+
+class DistOut(ct.Structure):
+    _fields_ = [
+        ("distance", ct.c_double),
+        ("pair", ct.c_uint64),
+        ("i", ct.c_uint64),
+        ("j", ct.c_uint64),
+        ("on_a", ct.c_double * 3),
+        ("on_b", ct.c_double * 3),
+        ("found", ct.c_int32),
+        ("_pad", ct.c_int32),
+    ]
+
+
+class HitOut(ct.Structure):
+    _fields_ = [
+        ("hit", ct.c_int32),
+        ("_pad", ct.c_int32),
+        ("pair", ct.c_uint64),
+        ("i", ct.c_uint64),
+        ("j", ct.c_uint64),
+    ]
+
+
+class Stats(ct.Structure):
+    _fields_ = [
+        ("ms_total", ct.c_double),
+        ("ms_filter", ct.c_double),
+        ("ms_verify", ct.c_double),
+        ("pairs", ct.c_uint64),
+        ("items", ct.c_uint64),
+        ("items_flagged", ct.c_uint64),
+        ("candidates", ct.c_uint64),
+        ("exact_pairs", ct.c_uint64),
+        ("kernels", ct.c_uint64),
+        ("rounds", ct.c_int32),
+        ("_pad", ct.c_int32),
+    ]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("_")}
+
+
+# (name, restype, argtypes) for every entry point of include/tindb_b200.h
+_SIGS = [
+    ("tdb_init", ct.c_int, [ct.c_int]),
+    ("tdb_set_stream", ct.c_int, [ct.c_void_p]),
+    ("tdb_set_mode", ct.c_int, [ct.c_int]),
+    ("tdb_last_error", ct.c_char_p, []),
+    ("tdb_last_stats", ct.c_int, [ct.POINTER(Stats)]),
+    ("tdb_device_count", ct.c_int, []),
+    ("tdb_mesh_upload", ct.c_int, [_D, ct.c_uint64, ct.POINTER(ct.c_void_p)]),
+    ("tdb_table_upload", ct.c_int, [_D, _U64, ct.c_uint64, ct.POINTER(ct.c_void_p)]),
+    ("tdb_geom_info", ct.c_int, [ct.c_void_p, _U64, _U64, _U64, _D]),
+    ("tdb_mesh_free", None, [ct.c_void_p]),
+    ("tdb_table_free", None, [ct.c_void_p]),
+    ("tdb_mesh_mesh_distance", ct.c_int, [ct.c_void_p, ct.c_void_p, ct.POINTER(DistOut)]),
+    ("tdb_mesh_mesh_intersects", ct.c_int, [ct.c_void_p, ct.c_void_p, ct.POINTER(HitOut)]),
+    ("tdb_mesh_mesh_distance_rows", ct.c_int,
+     [ct.c_void_p, ct.c_uint64, ct.c_uint64, ct.c_void_p, ct.POINTER(DistOut)]),
+    ("tdb_mesh_mesh_intersects_rows", ct.c_int,
+     [ct.c_void_p, ct.c_uint64, ct.c_uint64, ct.c_void_p, ct.POINTER(HitOut)]),
+    ("tdb_table_eval", ct.c_int, [ct.c_int, ct.c_void_p, ct.c_void_p, _D, _U8, _U64]),
+    ("tdb_table_eval_rows", ct.c_int,
+     [ct.c_int, ct.c_void_p, ct.c_uint64, ct.c_uint64, ct.c_void_p, _D, _U8, _U64]),
+    ("tdb_distance_host", ct.c_int, [_D, ct.c_uint64, _D, ct.c_uint64, ct.POINTER(DistOut)]),
+    ("tdb_intersects_host", ct.c_int, [_D, ct.c_uint64, _D, ct.c_uint64, ct.POINTER(HitOut)]),
+    ("tdb_pairs_distance", ct.c_int, [_D, _D, ct.c_uint64, _D]),
+    ("tdb_pairs_intersects", ct.c_int, [_D, _D, ct.c_uint64, _U8]),
+    ("tdb_pairs_filter", ct.c_int, [_D, _D, ct.c_uint64, _D]),
+    ("tdb_gen_unit_sphere", ct.c_uint64, [ct.c_uint64, _D]),
+    ("tdb_gen_ore_body", ct.c_uint64, [ct.c_uint64, _D]),
+    ("tdb_gen_terrain", ct.c_uint64, [ct.c_uint32, ct.c_uint32, ct.c_double, ct.c_uint64, _D]),
+    ("tdb_fp64_peak", ct.c_int, [_D, _D]),
+]
+EXPORTS = [s[0] for s in _SIGS]
+
+_lib = None
+
+
+def lib():
+    """The loaded C ABI library (raises if it was never built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not built: run `python __graft_entry__.py` (or make)")
+        L = ct.CDLL(LIB_PATH)
+        for name, res, args in _SIGS:
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+class TdbError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"tindb_b200 error {code}: {msg}")
+        self.code = code
+
+
+def _check(rc):
+    if rc != TDB_OK:
+        msg = lib().tdb_last_error()
+        msg = msg.decode() if msg else ""
+        if rc == TDB_E_ARG:
+            raise ValueError(msg)  # kernels.cpp:403 std::invalid_argument
+        raise TdbError(rc, msg)
+
+
+def _f64(a) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if a.size % 9:
+        raise ValueError("triangle arrays hold 9 doubles per face")
+    return a.reshape(-1, 9)
+
+
+def _dp(a):
+    return a.ctypes.data_as(_D)
+
+
+def init(device: int = 0):
+    _check(lib().tdb_init(device))
+
+
+def device_count() -> int:
+    return lib().tdb_device_count()
+
+
+def set_stream(stream_handle: Optional[int]):
+    """Launch on a caller stream (e.g. torch.cuda.current_stream().cuda_stream)."""
+    _check(lib().tdb_set_stream(ct.c_void_p(stream_handle or 0)))
+
+
+def set_mode(mode: int):
+    _check(lib().tdb_set_mode(mode))
+
+
+def last_stats() -> dict:
+    s = Stats()
+    _check(lib().tdb_last_stats(ct.byref(s)))
+    return s.as_dict()
+
+
+class _Geom:
+    """Device-resident triangle store (SoA planes + per-object AABB headers)."""
+
+    def __init__(self, handle):
+        self._h = ct.c_void_p(handle)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self):
+        n, no, nd = ct.c_uint64(), ct.c_uint64(), ct.c_uint64()
+        box = (ct.c_double * 6)()
+        _check(lib().tdb_geom_info(self._h, ct.byref(n), ct.byref(no), ct.byref(nd), box))
+        return {"faces": n.value, "objects": no.value, "degenerate": nd.value, "aabb": list(box)}
+
+    def free(self):
+        if self._h is not None and self._h.value:
+            lib().tdb_mesh_free(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Mesh(_Geom):
+    """A TriangleMesh uploaded to HBM (geometry.hpp:81-98 layout, 72 B/face)."""
+
+    def __init__(self, triangles):
+        t = _f64(triangles)
+        h = ct.c_void_p()
+        _check(lib().tdb_mesh_upload(_dp(t), len(t), ct.byref(h)))
+        super().__init__(h.value)
+        self.faces = len(t)
+
+
+class Table(_Geom):
+    """A mesh column (GeometryRecord rows, store_types.hpp:14-32) in HBM."""
+
+    def __init__(self, triangles, face_offsets, ids: Optional[Sequence[int]] = None):
+        t = _f64(triangles)
+        off = np.ascontiguousarray(face_offsets, dtype=np.uint64)
+        h = ct.c_void_p()
+        _check(lib().tdb_table_upload(_dp(t), off.ctypes.data_as(_U64), len(off) - 1, ct.byref(h)))
+        super().__init__(h.value)
+        self.objects = len(off) - 1
+        self.ids = list(ids) if ids is not None else list(range(1, self.objects + 1))
+
+
+@dataclass
+class DistanceResult:
+    """kernels::DistanceResult (kernels.hpp:28-34) for a triangle pair winner."""
+    distance: float
+    pair_index: Optional[int]
+    face_a: Optional[int]
+    face_b: Optional[int]
+    closest_on_a: tuple
+    closest_on_b: tuple
+
+
+@dataclass
+class IntersectionResult:
+    """kernels::IntersectionResult (kernels.hpp:43-48) with the lowest hit pair."""
+    hit: bool
+    pair_index: Optional[int]
+    face_a: Optional[int]
+    face_b: Optional[int]
+
+
+def _dist_result(o: DistOut) -> DistanceResult:
+    f = bool(o.found)
+    return DistanceResult(o.distance, o.pair if f else None, o.i if f else None, o.j if f else None,
+                          tuple(o.on_a), tuple(o.on_b))
+
+
+def _hit_result(o: HitOut) -> IntersectionResult:
+    h = bool(o.hit)
+    return IntersectionResult(h, o.pair if h else None, o.i if h else None, o.j if h else None)
+
+
+def _as_mesh(x) -> Mesh:
+    return x if isinstance(x, _Geom) else Mesh(x)
+
+
+def mesh_mesh_distance(a, b, rows: Optional[tuple] = None) -> DistanceResult:
+    """ST_3DDistance(a, b) over every triangle pair."""
+    a, b = _as_mesh(a), _as_mesh(b)
+    o = DistOut()
+    if rows is None:
+        _check(lib().tdb_mesh_mesh_distance(a.handle, b.handle, ct.byref(o)))
+    else:
+        _check(lib().tdb_mesh_mesh_distance_rows(a.handle, rows[0], rows[1], b.handle, ct.byref(o)))
+    return _dist_result(o)
+
+
+def mesh_mesh_intersects(a, b, rows: Optional[tuple] = None) -> IntersectionResult:
+    """ST_3DIntersects(a, b): lowest intersecting pair (kernels.cpp:407-432)."""
+    a, b = _as_mesh(a), _as_mesh(b)
+    o = HitOut()
+    if rows is None:
+        _check(lib().tdb_mesh_mesh_intersects(a.handle, b.handle, ct.byref(o)))
+    else:
+        _check(lib().tdb_mesh_mesh_intersects_rows(a.handle, rows[0], rows[1], b.handle, ct.byref(o)))
+    return _hit_result(o)
+
+
+def distance_host(a, b) -> DistanceResult:
+    """One-shot: host arrays in, result out (upload + evaluate + free)."""
+    a, b = _f64(a), _f64(b)
+    o = DistOut()
+    _check(lib().tdb_distance_host(_dp(a), len(a), _dp(b), len(b), ct.byref(o)))
+    return _dist_result(o)
+
+
+def intersects_host(a, b) -> IntersectionResult:
+    a, b = _f64(a), _f64(b)
+    o = HitOut()
+    _check(lib().tdb_intersects_host(_dp(a), len(a), _dp(b), len(b), ct.byref(o)))
+    return _hit_result(o)
+
+
+def table_eval(op: int, table: Table, literal, objects: Optional[tuple] = None):
+    """Per record: (values, pair indices); values are distances or booleans."""
+    lit = _as_mesh(literal)
+    o0, o1 = objects if objects is not None else (0, table.objects)
+    k = o1 - o0
+    pair = np.empty(k, np.uint64)
+    if op == OP_DISTANCE:
+        d = np.empty(k, np.float64)
+        _check(lib().tdb_table_eval_rows(op, table.handle, o0, o1, lit.handle, _dp(d), None,
+                                         pair.ctypes.data_as(_U64)))
+        return d, pair
+    h = np.empty(k, np.uint8)
+    _check(lib().tdb_table_eval_rows(op, table.handle, o0, o1, lit.handle, None,
+                                     h.ctypes.data_as(_U8), pair.ctypes.data_as(_U64)))
+    return h.astype(bool), pair
+
+
+@dataclass
+class KernelResult:
+    """kernels::KernelResult (batch.hpp:27-32): record id + value."""
+    record_id: int
+    value: Union[float, bool]
+
+
+def run_batch(op: int, records: Table, argument) -> List[KernelResult]:
+    """kernels::run_batch (batch.hpp:49-51) for a Mesh column x Mesh literal:
+    one result per record, in record order."""
+    vals, _ = table_eval(op, records, argument)
+    conv = float if op == OP_DISTANCE else bool
+    return [KernelResult(rid, conv(v)) for rid, v in zip(records.ids, vals)]
+
+
+def pairs_distance(a, b) -> np.ndarray:
+    """Exact A17 composition for aligned pairs (a[k], b[k]) on the device."""
+    a, b = _f64(a), _f64(b)
+    out = np.empty(len(a), np.float64)
+    _check(lib().tdb_pairs_distance(_dp(a), _dp(b), len(a), _dp(out)))
+    return out
+
+
+def pairs_intersects(a, b) -> np.ndarray:
+    a, b = _f64(a), _f64(b)
+    out = np.empty(len(a), np.uint8)
+    _check(lib().tdb_pairs_intersects(_dp(a), _dp(b), len(a), out.ctypes.data_as(_U8)))
+    return out.astype(bool)
+
+
+def pairs_filter(a, b) -> np.ndarray:
+    """The roofline kernel's FP64 filter value d~^2 for aligned pairs."""
+    a, b = _f64(a), _f64(b)
+    out = np.empty(len(a), np.float64)
+    _check(lib().tdb_pairs_filter(_dp(a), _dp(b), len(a), _dp(out)))
+    return out
+
+
+# ---- mesh generators (host; bit-identical to dataset.cpp) -------------------
+def unit_sphere(face_target: int) -> np.ndarray:
+    n = lib().tdb_gen_unit_sphere(face_target, None)
+    out = np.empty((n, 9), np.float64)
+    lib().tdb_gen_unit_sphere(face_target, _dp(out))
+    return out
+
+
+def ore_body(face_target: int) -> np.ndarray:
+    n = lib().tdb_gen_ore_body(face_target, None)
+    out = np.empty((n, 9), np.float64)
+    lib().tdb_gen_ore_body(face_target, _dp(out))
+    return out
+
+
+def terrain(nx: int = 1024, ny: int = 512, amp: float = 20.0, seed: int = 42) -> np.ndarray:
+    n = lib().tdb_gen_terrain(nx, ny, amp, seed, None)
+    out = np.empty((n, 9), np.float64)
+    lib().tdb_gen_terrain(nx, ny, amp, seed, _dp(out))
+    return out
+
+
+def translate(tris, dx=0.0, dy=0.0, dz=0.0) -> np.ndarray:
+    """Per-vertex translation (fixtures.cpp:37-46 translated)."""
+    t = _f64(tris).copy()
+    t[:, 0::3] += dx
+    t[:, 1::3] += dy
+    t[:, 2::3] += dz
+    return t
+
+
+def fp64_peak() -> tuple:
+    """(TFLOP/s, ms) of the DFMA issue-rate microbenchmark on this device."""
+    tf, ms = ct.c_double(), ct.c_double()
+    _check(lib().tdb_fp64_peak(ct.byref(tf), ct.byref(ms)))
+    return tf.value, ms.value

@@ -1,0 +1,357 @@
+// The C ABI (include/tindb_b200.h): argument checking, error mapping,
+// per-thread stream/mode/stats, and the dispatch into the device runtime.
+//
+// Error behaviour mirrors the reference: invalid arguments are reported the
+// way kernels.cpp:403 throws std::invalid_argument (TDB_E_ARG); device
+// failures map to std::runtime_error (TDB_E_CUDA); nothing throws across the
+// boundary.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "runtime.h"
+#include "tindb_b200.h"
+
+struct tdb_geom_s {
+    tdb::Geom g;
+};
+
+namespace {
+
+thread_local std::string t_err;
+thread_local cudaStream_t t_stream = nullptr;
+thread_local bool t_stream_set = false;
+thread_local int t_mode = TDB_MODE_FULL;
+thread_local int t_device = -1;
+thread_local tdb_stats t_stats{};
+
+std::mutex g_mu;
+std::vector<cudaStream_t> g_streams;  // library stream per device
+std::vector<int> g_sms;
+
+int fail(int code, const std::string& msg) {
+    t_err = msg;
+    return code;
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        t_err.clear();
+        return TDB_OK;
+    } catch (const std::invalid_argument& e) {
+        return fail(TDB_E_ARG, e.what());
+    } catch (const std::bad_alloc& e) {
+        return fail(TDB_E_NOMEM, e.what());
+    } catch (const tdb::CudaError& e) {
+        const std::string m = e.what();
+        return fail(m.find("out of memory") != std::string::npos ? TDB_E_NOMEM : TDB_E_CUDA, m);
+    } catch (const std::exception& e) {
+        return fail(TDB_E_CUDA, e.what());
+    }
+}
+
+void ensure_device() {
+    if (t_device >= 0) {
+        CK(cudaSetDevice(t_device));
+        return;
+    }
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    int n = 0;
+    CK(cudaGetDeviceCount(&n));
+    if (n <= 0) throw tdb::CudaError("no CUDA device");
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10) throw tdb::CudaError("tindb_b200 requires an sm_100 (B200) device, found sm_" +
+                                               std::to_string(prop.major * 10 + prop.minor));
+    std::lock_guard<std::mutex> lk(g_mu);
+    if ((int)g_streams.size() < n) {
+        g_streams.resize(n, nullptr);
+        g_sms.resize(n, 0);
+    }
+    if (!g_streams[dev]) {
+        CK(cudaStreamCreateWithFlags(&g_streams[dev], cudaStreamNonBlocking));
+        g_sms[dev] = prop.multiProcessorCount;
+    }
+    t_device = dev;
+}
+
+tdb::Ctx ctx() {
+    ensure_device();
+    tdb::Ctx c;
+    c.stream = t_stream_set ? t_stream : g_streams[t_device];
+    c.mode = t_mode;
+    c.sms = g_sms[t_device];
+    c.stats = &t_stats;
+    return c;
+}
+
+void need(bool ok, const char* what) {
+    if (!ok) throw std::invalid_argument(what);
+}
+
+tdb::ASel mesh_rows(const tdb::Geom& A, uint64_t r0, uint64_t r1) {
+    need(A.n_obj == 1, "first argument must be a mesh (one object)");
+    need(r0 <= r1 && r1 <= A.n, "row range out of bounds");
+    tdb::ASel s;
+    s.A = &A;
+    s.tile0 = r0 / tdb::kTile;
+    s.tile1 = (r1 + tdb::kTile - 1) / tdb::kTile;
+    if (r0 == r1) s.tile1 = s.tile0;
+    s.row_lo = r0;
+    s.row_hi = r1;
+    s.obj0 = 0;
+    s.obj1 = 1;
+    return s;
+}
+
+void fill_dist(tdb_dist_out* out, double d, uint64_t p, const double* w6, uint64_t m) {
+    std::memset(out, 0, sizeof *out);
+    out->distance = d;
+    out->pair = p;
+    out->found = p != ~0ull;
+    out->i = out->found ? p / m : ~0ull;
+    out->j = out->found ? p % m : ~0ull;
+    if (w6) {
+        std::memcpy(out->on_a, w6, 3 * sizeof(double));
+        std::memcpy(out->on_b, w6 + 3, 3 * sizeof(double));
+    }
+}
+
+void fill_hit(tdb_hit_out* out, uint64_t p, uint64_t m) {
+    std::memset(out, 0, sizeof *out);
+    out->pair = p;
+    out->hit = p != ~0ull;
+    out->i = out->hit ? p / m : ~0ull;
+    out->j = out->hit ? p % m : ~0ull;
+}
+
+void upload(const double* tri9, uint64_t n, const uint64_t* off, uint64_t n_obj, tdb_geom_s** out) {
+    need(out != nullptr, "null output handle");
+    need(n == 0 || tri9 != nullptr, "null triangle array");
+    need(off[0] == 0 && off[n_obj] == n, "face offsets must start at 0 and end at n_tris");
+    for (uint64_t o = 0; o < n_obj; ++o) need(off[o] <= off[o + 1], "face offsets must be non-decreasing");
+    tdb::Ctx c = ctx();
+    auto* h = new tdb_geom_s();
+    h->g.device = t_device;
+    try {
+        tdb::geom_build(&h->g, tri9, n, off, n_obj, c.stream);
+    } catch (...) {
+        tdb::geom_release(&h->g);
+        delete h;
+        throw;
+    }
+    *out = h;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tdb_init(int device) {
+    return guarded([&] {
+        int n = 0;
+        CK(cudaGetDeviceCount(&n));
+        need(device >= 0 && device < n, "device index out of range");
+        CK(cudaSetDevice(device));
+        t_device = -1;
+        ensure_device();
+    });
+}
+
+int tdb_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int tdb_set_stream(void* s) {
+    t_stream = static_cast<cudaStream_t>(s);
+    t_stream_set = s != nullptr;
+    return TDB_OK;
+}
+
+int tdb_set_mode(int mode) {
+    if (mode != TDB_MODE_FULL && mode != TDB_MODE_CULL) return fail(TDB_E_ARG, "unknown mode");
+    t_mode = mode;
+    return TDB_OK;
+}
+
+const char* tdb_last_error(void) { return t_err.c_str(); }
+
+int tdb_last_stats(tdb_stats* out) {
+    if (!out) return fail(TDB_E_ARG, "null stats");
+    *out = t_stats;
+    return TDB_OK;
+}
+
+int tdb_mesh_upload(const double* tri9, uint64_t n, tdb_mesh* out) {
+    return guarded([&] {
+        const uint64_t off[2] = {0, n};
+        upload(tri9, n, off, 1, out);
+    });
+}
+
+int tdb_table_upload(const double* tri9, const uint64_t* off, uint64_t n_obj, tdb_table* out) {
+    return guarded([&] {
+        need(off != nullptr, "null face offsets");
+        upload(tri9, off[n_obj], off, n_obj, out);
+    });
+}
+
+int tdb_geom_info(tdb_mesh g, uint64_t* n, uint64_t* n_obj, uint64_t* n_deg, double* aabb6) {
+    return guarded([&] {
+        need(g != nullptr, "null handle");
+        if (n) *n = g->g.n;
+        if (n_obj) *n_obj = g->g.n_obj;
+        if (n_deg) *n_deg = g->g.n_degenerate;
+        if (aabb6) std::memcpy(aabb6, g->g.stats, 6 * sizeof(double));
+    });
+}
+
+void tdb_mesh_free(tdb_mesh m) {
+    if (!m) return;
+    cudaSetDevice(m->g.device);
+    tdb::geom_release(&m->g);
+    delete m;
+}
+
+void tdb_table_free(tdb_table t) { tdb_mesh_free(t); }
+
+int tdb_mesh_mesh_distance_rows(tdb_mesh a, uint64_t r0, uint64_t r1, tdb_mesh b, tdb_dist_out* out) {
+    return guarded([&] {
+        need(a && b && out, "null argument");
+        need(b->g.n_obj == 1, "second argument must be a mesh (one object)");
+        tdb::Ctx c = ctx();
+        double d = 0, w[6];
+        uint64_t p = 0;
+        tdb::run_distance(c, mesh_rows(a->g, r0, r1), b->g, &d, &p, w);
+        fill_dist(out, d, p, w, b->g.n);
+    });
+}
+
+int tdb_mesh_mesh_distance(tdb_mesh a, tdb_mesh b, tdb_dist_out* out) {
+    if (!a) return fail(TDB_E_ARG, "null argument");
+    return tdb_mesh_mesh_distance_rows(a, 0, a->g.n, b, out);
+}
+
+int tdb_mesh_mesh_intersects_rows(tdb_mesh a, uint64_t r0, uint64_t r1, tdb_mesh b, tdb_hit_out* out) {
+    return guarded([&] {
+        need(a && b && out, "null argument");
+        need(b->g.n_obj == 1, "second argument must be a mesh (one object)");
+        tdb::Ctx c = ctx();
+        uint64_t p = 0;
+        uint8_t h = 0;
+        tdb::run_intersects(c, mesh_rows(a->g, r0, r1), b->g, &h, &p);
+        fill_hit(out, p, b->g.n);
+    });
+}
+
+int tdb_mesh_mesh_intersects(tdb_mesh a, tdb_mesh b, tdb_hit_out* out) {
+    if (!a) return fail(TDB_E_ARG, "null argument");
+    return tdb_mesh_mesh_intersects_rows(a, 0, a->g.n, b, out);
+}
+
+int tdb_table_eval_rows(int op, tdb_table t, uint64_t o0, uint64_t o1, tdb_mesh lit, double* dist,
+                        uint8_t* hit, uint64_t* pair) {
+    return guarded([&] {
+        need(t && lit, "null argument");
+        need(op == TDB_OP_DISTANCE || op == TDB_OP_INTERSECTS, "unknown op");
+        need(lit->g.n_obj == 1, "literal must be a mesh (one object)");
+        need(o0 <= o1 && o1 <= t->g.n_obj, "object range out of bounds");
+        tdb::Ctx c = ctx();
+        const tdb::Geom& A = t->g;
+        tdb::ASel s;
+        s.A = &A;
+        s.tile0 = A.obj_tile0[o0];
+        s.tile1 = A.obj_tile0[o1];
+        s.row_lo = A.h_off[o0];
+        s.row_hi = A.h_off[o1];
+        s.obj0 = o0;
+        s.obj1 = o1;
+        const uint64_t k = o1 - o0;
+        std::vector<uint64_t> p(k);
+        if (op == TDB_OP_DISTANCE) {
+            std::vector<double> d(k);
+            tdb::run_distance(c, s, lit->g, d.data(), p.data(), nullptr);
+            if (dist) std::memcpy(dist, d.data(), k * sizeof(double));
+        } else {
+            std::vector<uint8_t> h(k);
+            tdb::run_intersects(c, s, lit->g, h.data(), p.data());
+            if (hit) std::memcpy(hit, h.data(), k);
+        }
+        if (pair) std::memcpy(pair, p.data(), k * sizeof(uint64_t));
+    });
+}
+
+int tdb_table_eval(int op, tdb_table t, tdb_mesh lit, double* dist, uint8_t* hit, uint64_t* pair) {
+    if (!t) return fail(TDB_E_ARG, "null argument");
+    return tdb_table_eval_rows(op, t, 0, t->g.n_obj, lit, dist, hit, pair);
+}
+
+int tdb_distance_host(const double* a9, uint64_t n, const double* b9, uint64_t m, tdb_dist_out* out) {
+    tdb_mesh a = nullptr, b = nullptr;
+    int rc = tdb_mesh_upload(a9, n, &a);
+    if (rc == TDB_OK) rc = tdb_mesh_upload(b9, m, &b);
+    if (rc == TDB_OK) rc = tdb_mesh_mesh_distance(a, b, out);
+    const std::string err = t_err;
+    tdb_mesh_free(a);
+    tdb_mesh_free(b);
+    t_err = err;
+    return rc;
+}
+
+int tdb_intersects_host(const double* a9, uint64_t n, const double* b9, uint64_t m, tdb_hit_out* out) {
+    tdb_mesh a = nullptr, b = nullptr;
+    int rc = tdb_mesh_upload(a9, n, &a);
+    if (rc == TDB_OK) rc = tdb_mesh_upload(b9, m, &b);
+    if (rc == TDB_OK) rc = tdb_mesh_mesh_intersects(a, b, out);
+    const std::string err = t_err;
+    tdb_mesh_free(a);
+    tdb_mesh_free(b);
+    t_err = err;
+    return rc;
+}
+
+int tdb_pairs_distance(const double* a9, const double* b9, uint64_t n, double* dist) {
+    return guarded([&] {
+        need(n == 0 || (a9 && b9 && dist), "null argument");
+        tdb::run_pairs(ctx(), a9, b9, n, dist, nullptr);
+    });
+}
+
+int tdb_pairs_intersects(const double* a9, const double* b9, uint64_t n, uint8_t* hit) {
+    return guarded([&] {
+        need(n == 0 || (a9 && b9 && hit), "null argument");
+        tdb::run_pairs(ctx(), a9, b9, n, nullptr, hit);
+    });
+}
+
+int tdb_pairs_filter(const double* a9, const double* b9, uint64_t n, double* d2) {
+    tdb_mesh a = nullptr, b = nullptr;
+    int rc = tdb_mesh_upload(a9, n, &a);
+    if (rc == TDB_OK) rc = tdb_mesh_upload(b9, n, &b);
+    if (rc == TDB_OK)
+        rc = guarded([&] { tdb::run_pairs_filter(ctx(), a->g, b->g, d2); });
+    const std::string err = t_err;
+    tdb_mesh_free(a);
+    tdb_mesh_free(b);
+    t_err = err;
+    return rc;
+}
+
+int tdb_fp64_peak(double* tflops, double* ms) {
+    return guarded([&] {
+        need(tflops != nullptr, "null output");
+        *tflops = tdb::fp64_peak(ctx(), ms);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,417 @@
+// ST_3DDistance, mesh x mesh and table x mesh.
+//
+// Semantics (oracle/tindb_oracle.c tri_tri): the pair
+// distance is the reference composition of segment_triangle_distance
+// (kernels.cpp:256) over the six directed triangle edges; the object result
+// is the minimum over pairs p = i*|B| + j with the lowest p on ties
+// (kernels.cpp:359,368-376); degenerate faces are skipped.
+//
+// Pipeline per call (all on one stream, one host sync at the end):
+//   1. filter_kernel   — the roofline kernel: every pair of every
+//      (A-tile x B-chunk) item through the FP64 filter (fast_pair.cuh);
+//      per-item min d~^2 and per-object atomicMin.
+//   2. band_kernel     — per object, band = sqrt(min d~^2)(1+1e-9) + eta.
+//   3. flag_kernel     — items whose min d~^2 lies inside the band.
+//   4. verify_kernel   — re-scan flagged items; pairs inside the band get the
+//      bit-exact composition (exact.cuh); pass 1 atomicMin of the exact
+//      distance, pass 2 atomicMin of the pair index among exact ties.
+//   5. check_kernel    — if an object's exact minimum lies outside its band
+//      (the reference over-estimated every in-band pair), widen the band to
+//      it and repeat 3-5 for that object. The result is then provably the
+//      reference's: every pair left out has d_ref >= d_true - ulp > band >=
+//      the reported minimum.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "exact.cuh"
+#include "runtime.h"
+#include "tma.cuh"
+
+namespace tdb {
+
+namespace {
+
+constexpr unsigned long long kNone = ~0ull;
+
+struct DistArgs {
+    const double* Ap;
+    uint64_t An_pad;
+    const Tile* tiles;
+    uint64_t tile0, row_lo, row_hi;
+    const double* Bp;
+    uint64_t Bn_pad, Bn, n_chunks;
+    uint64_t obj0;
+    double* itemmin;
+    unsigned long long* objmin;
+};
+
+__device__ __forceinline__ double warp_min_nn(double x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = min_nn(x, __shfl_xor_sync(0xffffffffu, x, o));
+    return x;
+}
+
+struct PlaneAt {
+    const double* p;
+    uint64_t pad, i;
+    __device__ __forceinline__ double operator()(int f) const { return __ldg(p + (uint64_t)f * pad + i); }
+};
+
+struct SmemAt {
+    const double* s;
+    int j;
+    __device__ __forceinline__ double operator()(int f) const { return s[f * kSB + j]; }
+};
+
+__global__ void __launch_bounds__(kTile, 2) filter_kernel(DistArgs a) {
+    __shared__ alignas(128) double sm[2][NF * kSB];
+    __shared__ alignas(8) uint64_t bar[2];
+    __shared__ double red[kTile / 32];
+
+    const uint64_t item = blockIdx.x;
+    const uint64_t tl = item / a.n_chunks, ch = item - tl * a.n_chunks;
+    const Tile T = a.tiles[a.tile0 + tl];
+    const uint32_t r = min(threadIdx.x, T.count - 1);
+    const uint64_t row = T.row0 + r;
+    bool active = threadIdx.x < T.count && row >= a.row_lo && row < a.row_hi;
+    AFace A;
+    load_aface(A, PlaneAt{a.Ap, a.An_pad, row});
+    active = active && __ldg(a.Ap + (uint64_t)F_DEG * a.An_pad + row) == 0.0;
+
+    const uint64_t b0 = ch * kChunk, b1 = min(a.Bn, b0 + kChunk);
+    const int nsub = (int)((b1 - b0 + kSB - 1) / kSB);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    auto issue = [&](int s) {
+        const int st = s & 1;
+        const uint64_t f0 = b0 + (uint64_t)s * kSB;
+        const int cnt = (int)min((uint64_t)kSB, b1 - f0);
+        const uint32_t bytes = (uint32_t)(((cnt + 1) & ~1) * sizeof(double));
+        mbar_expect_tx(&bar[st], bytes * NF);
+#pragma unroll 1
+        for (int f = 0; f < NF; ++f) bulk_g2s(&sm[st][f * kSB], a.Bp + (uint64_t)f * a.Bn_pad + f0, bytes, &bar[st]);
+    };
+    if (threadIdx.x == 0) {
+        issue(0);
+        if (nsub > 1) issue(1);
+    }
+    double best = pos_inf();
+#pragma unroll 1
+    for (int s = 0; s < nsub; ++s) {
+        const int st = s & 1;
+        mbar_wait(&bar[st], (uint32_t)((s >> 1) & 1));
+        const int cnt = (int)min((uint64_t)kSB, b1 - (b0 + (uint64_t)s * kSB));
+        const double* sb = sm[st];
+#pragma unroll 1
+        for (int j = 0; j < cnt; ++j) {
+            if (sb[F_DEG * kSB + j] != 0.0) continue;  // uniform across the CTA
+            best = min_nn(best, pair_d2(A, SmemAt{sb, j}));
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && s + 2 < nsub) issue(s + 2);
+    }
+    if (!active) best = pos_inf();
+    best = warp_min_nn(best);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = red[0];
+#pragma unroll
+        for (int w = 1; w < kTile / 32; ++w) m = min_nn(m, red[w]);
+        a.itemmin[item] = m;
+        if (m < pos_inf()) atomicMin(a.objmin + (T.obj - a.obj0), (unsigned long long)__double_as_longlong(m));
+    }
+}
+
+struct BandArgs {
+    const unsigned long long* objmin;
+    const double* Astats;  // per object of A (absolute object index)
+    const double* Bstats;  // aggregate of B (kObjStats doubles)
+    uint64_t obj0, nobj;
+    double* band2;
+    double* band;
+    unsigned long long* objD;
+    unsigned long long* objP;
+};
+
+__device__ __forceinline__ double band_eta(const double* As, const double* Bs) {
+    return kBandEdge * fmax(As[6], Bs[6]) + kBandAbs * fmax(As[7], Bs[7]);
+}
+
+__global__ void band_kernel(BandArgs a) {
+    const uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= a.nobj) return;
+    const unsigned long long e = a.objmin[o];
+    a.objD[o] = kNone;
+    a.objP[o] = kNone;
+    if (e == kNone) {  // no non-degenerate pair
+        a.band2[o] = -1.0;
+        a.band[o] = -1.0;
+        return;
+    }
+    const double eta = band_eta(a.Astats + (a.obj0 + o) * kObjStats, a.Bstats);
+    const double b = sqrt(__longlong_as_double((long long)e)) * (1.0 + kBandRel) + eta;
+    a.band[o] = b;
+    a.band2[o] = b * b * (1.0 + 4e-16);
+}
+
+struct FlagArgs {
+    const Tile* tiles;
+    uint64_t tile0, n_chunks, n_items, obj0;
+    const double* itemmin;
+    const double* band2;
+    unsigned long long* list;
+    unsigned long long* count;
+};
+
+__global__ void flag_kernel(FlagArgs a) {
+    const uint64_t item = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (item >= a.n_items) return;
+    const Tile T = a.tiles[a.tile0 + item / a.n_chunks];
+    const double b2 = a.band2[T.obj - a.obj0];
+    if (b2 >= 0.0 && a.itemmin[item] <= b2) a.list[atomicAdd(a.count, 1ull)] = item;
+}
+
+struct VerifyArgs {
+    DistArgs d;
+    const unsigned long long* list;
+    const unsigned long long* count;
+    int nsplit, pass;
+    const double* band2;
+    unsigned long long* objD;
+    unsigned long long* objP;
+    unsigned long long* ncand;
+};
+
+__device__ __forceinline__ exact::tri load_tri(const double* P, uint64_t pad, uint64_t i) {
+    double v[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) v[k] = __ldg(P + (uint64_t)(F_V + k) * pad + i);
+    return exact::tri{{v[0], v[1], v[2]}, {v[3], v[4], v[5]}, {v[6], v[7], v[8]}};
+}
+
+__global__ void __launch_bounds__(kTile) verify_kernel(VerifyArgs v) {
+    const DistArgs& a = v.d;
+    const uint64_t units = *v.count * (uint64_t)v.nsplit;
+    for (uint64_t w = blockIdx.x; w < units; w += gridDim.x) {
+        const uint64_t item = v.list[w / v.nsplit];
+        const int part = (int)(w % v.nsplit);
+        const uint64_t tl = item / a.n_chunks, ch = item - tl * a.n_chunks;
+        const Tile T = a.tiles[a.tile0 + tl];
+        const uint32_t r = min(threadIdx.x, T.count - 1);
+        const uint64_t row = T.row0 + r;
+        bool active = threadIdx.x < T.count && row >= a.row_lo && row < a.row_hi;
+        active = active && __ldg(a.Ap + (uint64_t)F_DEG * a.An_pad + row) == 0.0;
+        AFace A;
+        load_aface(A, PlaneAt{a.Ap, a.An_pad, row});
+        const uint64_t c0 = ch * kChunk, c1 = min(a.Bn, c0 + kChunk);
+        const uint64_t len = (c1 - c0 + v.nsplit - 1) / v.nsplit;
+        const uint64_t b0 = c0 + part * len, b1 = min(c1, b0 + len);
+        const uint64_t o = T.obj - a.obj0;
+        const double b2 = v.band2[o];
+        const uint64_t i_loc = row - T.obj_row0;
+        for (uint64_t j = b0; j < b1; ++j) {
+            if (__ldg(a.Bp + (uint64_t)F_DEG * a.Bn_pad + j) != 0.0) continue;
+            const double d2 = pair_d2(A, PlaneAt{a.Bp, a.Bn_pad, j});
+            if (active && d2 <= b2) {
+                const exact::res x = exact::tri_tri(load_tri(a.Ap, a.An_pad, row), load_tri(a.Bp, a.Bn_pad, j));
+                const unsigned long long bits = (unsigned long long)__double_as_longlong(x.d);
+                if (v.pass == 1) {
+                    atomicMin(v.objD + o, bits);
+                    atomicAdd(v.ncand, 1ull);
+                } else if (bits == v.objD[o]) {
+                    atomicMin(v.objP + o, i_loc * a.Bn + j);
+                }
+            }
+        }
+    }
+}
+
+struct CheckArgs {
+    uint64_t nobj, obj0;
+    const double* Astats;
+    const double* Bstats;
+    double* band2;
+    double* band;
+    unsigned long long* objD;
+    unsigned long long* objP;
+    unsigned long long* retry;
+};
+
+// After a round: objects whose exact minimum lies outside the band get the
+// band widened to it (and their exact state reset); the others stop.
+__global__ void check_kernel(CheckArgs a) {
+    const uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= a.nobj) return;
+    const double b = a.band[o];
+    if (b < 0.0) {
+        a.band2[o] = -1.0;
+        return;
+    }
+    const unsigned long long d = a.objD[o];
+    // d == kNone: no pair fell in the band although the band contains the
+    // filter minimum -> cannot happen unless every in-band pair evaluated to
+    // NaN/inf; treat as done.
+    if (d != kNone && __longlong_as_double((long long)d) > b) {
+        const double nb = __longlong_as_double((long long)d) * (1.0 + kBandRel) +
+                          band_eta(a.Astats + (a.obj0 + o) * kObjStats, a.Bstats);
+        a.band[o] = nb;
+        a.band2[o] = nb * nb * (1.0 + 4e-16);
+        a.objD[o] = kNone;
+        a.objP[o] = kNone;
+        atomicAdd(a.retry, 1ull);
+    } else {
+        a.band2[o] = -1.0;  // final: do not re-flag
+    }
+}
+
+__global__ void witness_kernel(const double* Ap, uint64_t An_pad, uint64_t obj_row0, const double* Bp,
+                               uint64_t Bn_pad, uint64_t Bn, const unsigned long long* objP, double* out) {
+    const unsigned long long p = *objP;
+    if (p == kNone) return;
+    const uint64_t i = obj_row0 + p / Bn, j = p % Bn;
+    const exact::res x = exact::tri_tri(load_tri(Ap, An_pad, i), load_tri(Bp, Bn_pad, j));
+    out[0] = x.a.x, out[1] = x.a.y, out[2] = x.a.z;
+    out[3] = x.b.x, out[4] = x.b.y, out[5] = x.b.z;
+}
+
+template <class T>
+T* dalloc(size_t n, cudaStream_t st) {
+    T* p = nullptr;
+    CK(cudaMallocAsync(&p, std::max<size_t>(1, n) * sizeof(T), st));
+    return p;
+}
+
+struct EventPair {
+    cudaEvent_t e[4];
+    EventPair() {
+        for (auto& x : e) CK(cudaEventCreate(&x));
+    }
+    ~EventPair() {
+        for (auto& x : e) cudaEventDestroy(x);
+    }
+};
+
+}  // namespace
+
+void run_distance(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, uint64_t* pair,
+                  double* witness6) {
+    const cudaStream_t st = cx.stream;
+    const uint64_t nobj = sel.obj1 - sel.obj0;
+    const uint64_t ntiles = sel.tile1 - sel.tile0;
+    const uint64_t n_items = ntiles * B.n_chunks;
+    for (uint64_t o = 0; o < nobj; ++o) {
+        dist[o] = pos_inf_h();
+        pair[o] = kNone;
+    }
+    if (witness6) std::fill(witness6, witness6 + 6, 0.0);
+    tdb_stats& S = *cx.stats;
+    std::memset(&S, 0, sizeof S);
+    if (nobj == 0) return;
+    if (n_items == 0) return;
+
+    const Geom& A = *sel.A;
+    double* itemmin = dalloc<double>(n_items, st);
+    unsigned long long* objmin = dalloc<unsigned long long>(nobj, st);
+    double* band2 = dalloc<double>(nobj, st);
+    double* band = dalloc<double>(nobj, st);
+    unsigned long long* objD = dalloc<unsigned long long>(nobj, st);
+    unsigned long long* objP = dalloc<unsigned long long>(nobj, st);
+    unsigned long long* list = dalloc<unsigned long long>(n_items, st);
+    unsigned long long* ctr = dalloc<unsigned long long>(4, st);  // flagged, cand, retry
+    double* Bstats = dalloc<double>(kObjStats, st);
+    double* wit = dalloc<double>(6, st);
+    CK(cudaMemsetAsync(objmin, 0xff, nobj * sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(wit, 0, 6 * sizeof(double), st));
+    CK(cudaMemcpyAsync(Bstats, B.stats, kObjStats * sizeof(double), cudaMemcpyHostToDevice, st));
+
+    EventPair ev;
+    DistArgs da{A.planes, A.n_pad, A.d_tiles, sel.tile0, sel.row_lo, sel.row_hi, B.planes, B.n_pad, B.n,
+                B.n_chunks, sel.obj0, itemmin, objmin};
+    CK(cudaEventRecord(ev.e[0], st));
+    filter_kernel<<<(unsigned)n_items, kTile, 0, st>>>(da);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ev.e[1], st));
+    uint64_t launches = 1;
+
+    const unsigned ob = (unsigned)((nobj + 255) / 256);
+    band_kernel<<<ob, 256, 0, st>>>(BandArgs{objmin, A.d_obj_stats, Bstats, sel.obj0, nobj, band2, band, objD, objP});
+    CK(cudaGetLastError());
+    ++launches;
+
+    const int nsplit = 16;
+    const unsigned vgrid = (unsigned)(cx.sms * 8);
+    int rounds = 0;
+    unsigned long long h_ctr[4] = {0, 0, 0, 0};
+    unsigned long long flagged_total = 0;
+    for (;;) {
+        ++rounds;
+        CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));          // flagged count
+        CK(cudaMemsetAsync(ctr + 2, 0, sizeof(unsigned long long), st));      // retry count
+        flag_kernel<<<(unsigned)((n_items + 255) / 256), 256, 0, st>>>(
+            FlagArgs{A.d_tiles, sel.tile0, B.n_chunks, n_items, sel.obj0, itemmin, band2, list, ctr});
+        CK(cudaGetLastError());
+        for (int pass = 1; pass <= 2; ++pass) {
+            verify_kernel<<<vgrid, kTile, 0, st>>>(VerifyArgs{da, list, ctr, nsplit, pass, band2, objD, objP, ctr + 1});
+            CK(cudaGetLastError());
+        }
+        check_kernel<<<ob, 256, 0, st>>>(CheckArgs{nobj, sel.obj0, A.d_obj_stats, Bstats, band2, band, objD, objP, ctr + 2});
+        CK(cudaGetLastError());
+        launches += 4;
+        CK(cudaMemcpyAsync(h_ctr, ctr, sizeof h_ctr, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        flagged_total += h_ctr[0];
+        if (h_ctr[2] == 0 || rounds >= 8) break;
+    }
+    CK(cudaEventRecord(ev.e[2], st));
+    if (witness6 && nobj == 1) {
+        const Tile& t0 = A.h_tiles[sel.tile0];
+        witness_kernel<<<1, 1, 0, st>>>(A.planes, A.n_pad, t0.obj_row0, B.planes, B.n_pad, B.n, objP, wit);
+        CK(cudaGetLastError());
+        ++launches;
+    }
+    std::vector<unsigned long long> hD(nobj), hP(nobj);
+    CK(cudaMemcpyAsync(hD.data(), objD, nobj * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hP.data(), objP, nobj * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    if (witness6) CK(cudaMemcpyAsync(witness6, wit, 6 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(ev.e[3], st));
+    for (void* p : {(void*)itemmin, (void*)objmin, (void*)band2, (void*)band, (void*)objD, (void*)objP,
+                    (void*)list, (void*)ctr, (void*)Bstats, (void*)wit})
+        CK(cudaFreeAsync(p, st));
+    CK(cudaStreamSynchronize(st));
+    for (uint64_t o = 0; o < nobj; ++o) {
+        if (hP[o] != kNone) {
+            double d;
+            std::memcpy(&d, &hD[o], sizeof d);
+            dist[o] = d;
+            pair[o] = hP[o];
+        }
+    }
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, ev.e[0], ev.e[1]));
+    S.ms_filter = ms;
+    CK(cudaEventElapsedTime(&ms, ev.e[1], ev.e[2]));
+    S.ms_verify = ms;
+    CK(cudaEventElapsedTime(&ms, ev.e[0], ev.e[3]));
+    S.ms_total = ms;
+    uint64_t pairs = 0;
+    for (uint64_t t = sel.tile0; t < sel.tile1; ++t) {
+        const Tile& T = A.h_tiles[t];
+        const uint64_t lo = std::max(T.row0, sel.row_lo), hi = std::min(T.row0 + T.count, sel.row_hi);
+        if (hi > lo) pairs += (hi - lo) * B.n;
+    }
+    S.pairs = pairs;
+    S.items = n_items;
+    S.items_flagged = flagged_total;
+    S.candidates = h_ctr[1];
+    S.kernels = launches;
+    S.rounds = rounds;
+}
+
+}  // namespace tdb

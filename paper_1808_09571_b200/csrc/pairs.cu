@@ -1,0 +1,137 @@
+// Aligned triangle-pair batches (golden vectors / parity) and the FP64
+// issue-rate microbenchmark used as the roofline denominator.
+#include <cstring>
+
+#include "exact.cuh"
+#include "runtime.h"
+
+namespace tdb {
+
+namespace {
+
+__device__ __forceinline__ exact::tri tri_at(const double* t9, uint64_t k) {
+    const double* v = t9 + 9 * k;
+    return exact::tri{{v[0], v[1], v[2]}, {v[3], v[4], v[5]}, {v[6], v[7], v[8]}};
+}
+
+__global__ void pairs_kernel(const double* __restrict__ a9, const double* __restrict__ b9, uint64_t n,
+                             double* __restrict__ dist, uint8_t* __restrict__ hit) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const exact::tri a = tri_at(a9, k), b = tri_at(b9, k);
+        if (dist) dist[k] = exact::tri_tri(a, b).d;
+        if (hit) hit[k] = exact::tri_tri_hit(a, b) ? 1 : 0;
+    }
+}
+
+// FP64 filter value d~^2 for aligned pairs (tests the filter's accuracy).
+struct AosAt {
+    const double* p;  // per-face prep record, NF doubles
+    __device__ __forceinline__ double operator()(int f) const { return p[f]; }
+};
+
+__global__ void filter_pairs_kernel(const double* __restrict__ pa, const double* __restrict__ pb, uint64_t n,
+                                    double* __restrict__ d2) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        AFace A;
+        load_aface(A, AosAt{pa + NF * k});
+        const bool deg = pa[NF * k + F_DEG] != 0.0 || pb[NF * k + F_DEG] != 0.0;
+        d2[k] = deg ? pos_inf() : pair_d2(A, AosAt{pb + NF * k});
+    }
+}
+
+// gather planes of a Geom into per-face AoS records
+__global__ void planes_to_aos(const double* __restrict__ planes, uint64_t n, uint64_t n_pad, double* __restrict__ out) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int f = 0; f < NF; ++f) out[NF * i + f] = planes[(uint64_t)f * n_pad + i];
+}
+
+// 8 independent DFMA chains per thread, 148 x 8 CTAs x 256 threads.
+__global__ void __launch_bounds__(256) dfma_kernel(double* out, int iters, double s) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-9 + k;
+#pragma unroll 1
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) x[k] = fma(x[k], s, 0.5);
+    }
+    double acc = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += x[k];
+    if (acc == 1234.5678) out[0] = acc;  // keep the chains alive
+}
+
+}  // namespace
+
+void run_pairs(const Ctx& cx, const double* a9, const double* b9, uint64_t n, double* dist, uint8_t* hit) {
+    const cudaStream_t st = cx.stream;
+    if (n == 0) return;
+    double *da = nullptr, *db = nullptr, *dd = nullptr;
+    uint8_t* dh = nullptr;
+    CK(cudaMallocAsync(&da, 9 * n * sizeof(double), st));
+    CK(cudaMallocAsync(&db, 9 * n * sizeof(double), st));
+    CK(cudaMemcpyAsync(da, a9, 9 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(db, b9, 9 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (dist) CK(cudaMallocAsync(&dd, n * sizeof(double), st));
+    if (hit) CK(cudaMallocAsync(&dh, n, st));
+    pairs_kernel<<<(unsigned)std::min<uint64_t>((n + 127) / 128, 148 * 16), 128, 0, st>>>(da, db, n, dd, dh);
+    CK(cudaGetLastError());
+    if (dist) CK(cudaMemcpyAsync(dist, dd, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (hit) CK(cudaMemcpyAsync(hit, dh, n, cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(da, st));
+    CK(cudaFreeAsync(db, st));
+    if (dd) CK(cudaFreeAsync(dd, st));
+    if (dh) CK(cudaFreeAsync(dh, st));
+    CK(cudaStreamSynchronize(st));
+}
+
+void run_pairs_filter(const Ctx& cx, const Geom& A, const Geom& B, double* d2) {
+    const cudaStream_t st = cx.stream;
+    const uint64_t n = A.n;
+    if (n == 0) return;
+    double *pa = nullptr, *pb = nullptr, *dd = nullptr;
+    CK(cudaMallocAsync(&pa, NF * n * sizeof(double), st));
+    CK(cudaMallocAsync(&pb, NF * n * sizeof(double), st));
+    CK(cudaMallocAsync(&dd, n * sizeof(double), st));
+    planes_to_aos<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(A.planes, n, A.n_pad, pa);
+    planes_to_aos<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(B.planes, n, B.n_pad, pb);
+    filter_pairs_kernel<<<(unsigned)std::min<uint64_t>((n + 127) / 128, 148 * 16), 128, 0, st>>>(pa, pb, n, dd);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(d2, dd, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(pa, st));
+    CK(cudaFreeAsync(pb, st));
+    CK(cudaFreeAsync(dd, st));
+    CK(cudaStreamSynchronize(st));
+}
+
+double fp64_peak(const Ctx& cx, double* ms_out) {
+    const cudaStream_t st = cx.stream;
+    double* out = nullptr;
+    CK(cudaMallocAsync(&out, sizeof(double), st));
+    const int blocks = cx.sms * 8, threads = 256, iters = 4096;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    dfma_kernel<<<blocks, threads, 0, st>>>(out, 64, 0.999);  // warm-up
+    CK(cudaEventRecord(e0, st));
+    dfma_kernel<<<blocks, threads, 0, st>>>(out, iters, 0.999);
+    CK(cudaEventRecord(e1, st));
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    CK(cudaFreeAsync(out, st));
+    CK(cudaStreamSynchronize(st));
+    if (ms_out) *ms_out = ms;
+    const double flops = 2.0 * 16 * 8 * (double)iters * blocks * threads;
+    return flops / (ms * 1e-3) / 1e12;
+}
+
+}  // namespace tdb

@@ -1,0 +1,80 @@
+// Host runtime internals: geometry handles, per-thread call context, errors.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <limits>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "fast_pair.cuh"
+#include "tdb_internal.h"
+#include "tindb_b200.h"
+
+namespace tdb {
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define CK(expr)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (expr);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            throw ::tdb::CudaError(std::string(#expr) + ": " + cudaGetErrorString(e_) + " (" + \
+                                   __FILE__ + ":" + std::to_string(__LINE__) + ")");          \
+    } while (0)
+
+inline double pos_inf_h() { return std::numeric_limits<double>::infinity(); }
+
+struct Geom {
+    int device = 0;
+    uint64_t n = 0, n_pad = 0, n_obj = 0, n_degenerate = 0, n_chunks = 0;
+    double* planes = nullptr;          // NF x n_pad
+    uint64_t* d_off = nullptr;         // n_obj + 1
+    Tile* d_tiles = nullptr;
+    double* d_obj_stats = nullptr;     // n_obj x kObjStats
+    double* d_chunk_aabb = nullptr;    // n_chunks x 6
+    std::vector<uint64_t> h_off;
+    std::vector<Tile> h_tiles;
+    std::vector<uint64_t> obj_tile0;   // first tile of each object (n_obj + 1)
+    double stats[kObjStats] = {};      // aggregate: aabb lo/hi, max edge, max |coord|
+};
+
+void geom_build(Geom* g, const double* host_tri9, uint64_t n, const uint64_t* host_off,
+                uint64_t n_obj, cudaStream_t st);
+void geom_release(Geom* g);
+
+// Per-call execution context.
+struct Ctx {
+    cudaStream_t stream;
+    int mode;
+    int sms;
+    tdb_stats* stats;
+};
+
+// A-side selection: tiles [tile0, tile1) of A, rows restricted to
+// [row_lo, row_hi); objects [obj0, obj1) (results indexed obj - obj0).
+struct ASel {
+    const Geom* A;
+    uint64_t tile0, tile1, row_lo, row_hi, obj0, obj1;
+};
+
+// Distance over an A selection against mesh B. Outputs per object (host):
+// dist (+inf when none), pair (UINT64_MAX when none); for a single object
+// also the witness (on_a, on_b).
+void run_distance(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, uint64_t* pair,
+                  double* witness6);
+void run_intersects(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit, uint64_t* pair);
+
+// Exact composition over aligned pair arrays (parity entry points).
+void run_pairs(const Ctx& cx, const double* a9, const double* b9, uint64_t n, double* dist,
+               uint8_t* hit);
+
+void run_pairs_filter(const Ctx& cx, const Geom& A, const Geom& B, double* d2);
+
+double fp64_peak(const Ctx& cx, double* ms);
+
+}  // namespace tdb

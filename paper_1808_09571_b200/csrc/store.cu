@@ -1,0 +1,269 @@
+// Device geometry store: upload of caller-owned AoS triangle soups into
+// per-face SoA planes in HBM, with per-object AABB headers and A-side tiles.
+//
+// Replaces the CPU mesh store for the hot path (store_types.hpp:14-32,
+// geometry.hpp:81-98). The caller's array is exactly
+// tindb::TriangleMesh::triangles.data() (72 B per face); it is copied once
+// (H2D) into a staging buffer and transposed + enriched by prep_kernel.
+#include <algorithm>
+#include <vector>
+
+#include "exact.cuh"
+#include "runtime.h"
+
+namespace tdb {
+
+namespace {
+
+// Order-preserving u64 encoding of doubles for atomicMin/atomicMax.
+__device__ __forceinline__ unsigned long long ord(double d) {
+    const unsigned long long u = (unsigned long long)__double_as_longlong(d);
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double unord(unsigned long long u) {
+    return __longlong_as_double((long long)((u >> 63) ? (u & 0x7fffffffffffffffull) : ~u));
+}
+
+__device__ __forceinline__ uint32_t object_of(const uint64_t* off, uint64_t n_obj, uint64_t face) {
+    uint64_t lo = 0, hi = n_obj;  // off[lo] <= face < off[hi]
+    while (hi - lo > 1) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (off[mid] <= face) lo = mid; else hi = mid;
+    }
+    return (uint32_t)lo;
+}
+
+// One thread per face: planes + per-object statistics (8 ordered u64 per
+// object: lo xyz (min), hi xyz (max), max edge, max |coord|) + degenerate
+// count.
+__global__ void prep_kernel(const double* __restrict__ aos, uint64_t n, uint64_t n_pad,
+                            const uint64_t* __restrict__ off, uint64_t n_obj,
+                            double* __restrict__ planes, unsigned long long* __restrict__ stats,
+                            unsigned long long* __restrict__ n_deg) {
+    const uint64_t f = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = f < n;
+    const uint64_t g = live ? f : (n ? n - 1 : 0);
+    double v[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) v[k] = n ? aos[9 * g + k] : 0.0;
+
+    exact::tri t{{v[0], v[1], v[2]}, {v[3], v[4], v[5]}, {v[6], v[7], v[8]}};
+    const bool deg = exact::degenerate(t);
+
+    double e[9], L[3], IL[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        const int q = j == 2 ? 0 : j + 1;
+        e[3 * j] = v[3 * q] - v[3 * j];
+        e[3 * j + 1] = v[3 * q + 1] - v[3 * j + 1];
+        e[3 * j + 2] = v[3 * q + 2] - v[3 * j + 2];
+        L[j] = e[3 * j] * e[3 * j] + e[3 * j + 1] * e[3 * j + 1] + e[3 * j + 2] * e[3 * j + 2];
+        IL[j] = L[j] > 0.0 ? 1.0 / L[j] : 0.0;
+    }
+    // e0 = V1 - V0 = E_0, e1 = V2 - V0 = -E_2
+    const double a0 = e[0], a1 = e[1], a2 = e[2];
+    const double b0 = -e[6], b1 = -e[7], b2 = -e[8];
+    const double Nx = a1 * b2 - a2 * b1, Ny = a2 * b0 - a0 * b2, Nz = a0 * b1 - a1 * b0;
+    const double N2 = Nx * Nx + Ny * Ny + Nz * Nz;
+    double n3[3] = {0, 0, 0}, U[3] = {0, 0, 0}, W[3] = {0, 0, 0}, c = 0.0;
+    if (!deg && N2 > 0.0) {
+        const double inv = 1.0 / sqrt(N2), inv2 = 1.0 / N2;
+        n3[0] = Nx * inv, n3[1] = Ny * inv, n3[2] = Nz * inv;
+        c = n3[0] * v[0] + n3[1] * v[1] + n3[2] * v[2];
+        // U = (e1 x N)/|N|^2, W = (N x e0)/|N|^2
+        U[0] = (b1 * Nz - b2 * Ny) * inv2, U[1] = (b2 * Nx - b0 * Nz) * inv2, U[2] = (b0 * Ny - b1 * Nx) * inv2;
+        W[0] = (Ny * a2 - Nz * a1) * inv2, W[1] = (Nz * a0 - Nx * a2) * inv2, W[2] = (Nx * a1 - Ny * a0) * inv2;
+    }
+    if (live) {
+        double* p = planes + f;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) p[(F_V + k) * n_pad] = v[k];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) p[(F_E + k) * n_pad] = e[k];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            p[(F_L + k) * n_pad] = L[k];
+            p[(F_IL + k) * n_pad] = IL[k];
+            p[(F_N + k) * n_pad] = n3[k];
+            p[(F_U + k) * n_pad] = U[k];
+            p[(F_W + k) * n_pad] = W[k];
+        }
+        p[F_C * n_pad] = c;
+        p[F_DEG * n_pad] = deg ? 1.0 : 0.0;
+        p[F_SPARE * n_pad] = 0.0;
+    }
+
+    // ---- per-object statistics, warp-aggregated when the warp is one object
+    const uint32_t obj = object_of(off, n_obj, g);
+    double s[kObjStats];
+    s[0] = fmin(v[0], fmin(v[3], v[6]));
+    s[1] = fmin(v[1], fmin(v[4], v[7]));
+    s[2] = fmin(v[2], fmin(v[5], v[8]));
+    s[3] = fmax(v[0], fmax(v[3], v[6]));
+    s[4] = fmax(v[1], fmax(v[4], v[7]));
+    s[5] = fmax(v[2], fmax(v[5], v[8]));
+    s[6] = sqrt(fmax(L[0], fmax(L[1], L[2])));
+    s[7] = fmax(fmax(fmax(-s[0], s[3]), fmax(-s[1], s[4])), fmax(-s[2], s[5]));
+    unsigned long long* st = stats + (uint64_t)obj * kObjStats;
+    const unsigned mask = __activemask();
+    const uint32_t obj0 = __shfl_sync(mask, obj, 0);
+    const bool uniform = __all_sync(mask, obj == obj0);
+    if (uniform) {
+#pragma unroll
+        for (int k = 0; k < kObjStats; ++k) {
+            double x = s[k];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double y = __shfl_xor_sync(mask, x, o);
+                x = k < 3 ? fmin(x, y) : fmax(x, y);
+            }
+            s[k] = x;
+        }
+        if ((threadIdx.x & 31) == 0 && n) {
+            for (int k = 0; k < 3; ++k) atomicMin(st + k, ord(s[k]));
+            for (int k = 3; k < kObjStats; ++k) atomicMax(st + k, ord(s[k]));
+        }
+    } else if (n) {
+        for (int k = 0; k < 3; ++k) atomicMin(st + k, ord(s[k]));
+        for (int k = 3; k < kObjStats; ++k) atomicMax(st + k, ord(s[k]));
+    }
+    const unsigned dm = __ballot_sync(mask, live && deg);
+    if ((threadIdx.x & 31) == 0 && dm) atomicAdd(n_deg, (unsigned long long)__popc(dm));
+}
+
+__global__ void stats_init_kernel(unsigned long long* stats, uint64_t n_obj) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_obj * kObjStats) return;
+    const int k = (int)(i % kObjStats);
+    stats[i] = k < 3 ? ~0ull : 0ull;  // min slots start at +max, max slots at -max
+}
+
+__global__ void stats_final_kernel(const unsigned long long* __restrict__ in, double* __restrict__ out,
+                                   uint64_t n) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = unord(in[i]);
+}
+
+// AABB per B-chunk (CULL mode item skipping): one block per chunk.
+__global__ void chunk_aabb_kernel(const double* __restrict__ planes, uint64_t n, uint64_t n_pad,
+                                  double* __restrict__ out) {
+    const uint64_t c0 = (uint64_t)blockIdx.x * kChunk, c1 = min(n, c0 + kChunk);
+    double lo[3] = {pos_inf(), pos_inf(), pos_inf()}, hi[3] = {-pos_inf(), -pos_inf(), -pos_inf()};
+    for (uint64_t f = c0 + threadIdx.x; f < c1; f += blockDim.x)
+        for (int k = 0; k < 9; ++k) {
+            const double x = planes[(F_V + k) * n_pad + f];
+            lo[k % 3] = fmin(lo[k % 3], x);
+            hi[k % 3] = fmax(hi[k % 3], x);
+        }
+    __shared__ double red[6][32];
+    for (int k = 0; k < 6; ++k) {
+        double x = k < 3 ? lo[k] : hi[k - 3];
+        for (int o = 16; o > 0; o >>= 1) {
+            const double y = __shfl_xor_sync(0xffffffffu, x, o);
+            x = k < 3 ? fmin(x, y) : fmax(x, y);
+        }
+        if ((threadIdx.x & 31) == 0) red[k][threadIdx.x >> 5] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        const int k = threadIdx.x;
+        double x = red[k][0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) x = k < 3 ? fmin(x, red[k][w]) : fmax(x, red[k][w]);
+        out[blockIdx.x * 6 + k] = x;
+    }
+}
+
+}  // namespace
+
+void geom_build(Geom* g, const double* host_tri9, uint64_t n, const uint64_t* host_off,
+                uint64_t n_obj, cudaStream_t st) {
+    g->n = n;
+    g->n_obj = n_obj;
+    g->n_pad = ((n + 1 + kPlanePad - 1) / kPlanePad) * kPlanePad;
+    g->h_off.assign(host_off, host_off + n_obj + 1);
+
+    // tiles: per object, kTile-face blocks (A role)
+    g->h_tiles.clear();
+    g->obj_tile0.assign(n_obj + 1, 0);
+    for (uint64_t o = 0; o < n_obj; ++o) {
+        g->obj_tile0[o] = g->h_tiles.size();
+        for (uint64_t r = g->h_off[o]; r < g->h_off[o + 1]; r += kTile) {
+            Tile t;
+            t.row0 = r;
+            t.obj_row0 = g->h_off[o];
+            t.count = (uint32_t)std::min<uint64_t>(kTile, g->h_off[o + 1] - r);
+            t.obj = (uint32_t)o;
+            g->h_tiles.push_back(t);
+        }
+    }
+    g->obj_tile0[n_obj] = g->h_tiles.size();
+    g->n_chunks = (n + kChunk - 1) / kChunk;
+
+    double* staging = nullptr;
+    CK(cudaMallocAsync(&staging, std::max<uint64_t>(1, 9 * n) * sizeof(double), st));
+    CK(cudaMallocAsync(&g->planes, (size_t)NF * g->n_pad * sizeof(double), st));
+    CK(cudaMallocAsync(&g->d_off, (n_obj + 1) * sizeof(uint64_t), st));
+    CK(cudaMallocAsync(&g->d_tiles, std::max<size_t>(1, g->h_tiles.size()) * sizeof(Tile), st));
+    CK(cudaMallocAsync(&g->d_obj_stats, std::max<uint64_t>(1, n_obj) * kObjStats * sizeof(double), st));
+    CK(cudaMallocAsync(&g->d_chunk_aabb, std::max<uint64_t>(1, g->n_chunks) * 6 * sizeof(double), st));
+    unsigned long long* ustats = nullptr;
+    unsigned long long* ndeg = nullptr;
+    CK(cudaMallocAsync(&ustats, std::max<uint64_t>(1, n_obj) * kObjStats * sizeof(unsigned long long), st));
+    CK(cudaMallocAsync(&ndeg, sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(ndeg, 0, sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(g->planes, 0, (size_t)NF * g->n_pad * sizeof(double), st));
+
+    if (n) CK(cudaMemcpyAsync(staging, host_tri9, 9 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(g->d_off, g->h_off.data(), (n_obj + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+    if (!g->h_tiles.empty())
+        CK(cudaMemcpyAsync(g->d_tiles, g->h_tiles.data(), g->h_tiles.size() * sizeof(Tile),
+                           cudaMemcpyHostToDevice, st));
+    if (n_obj) {
+        const uint64_t m = n_obj * kObjStats;
+        stats_init_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(ustats, n_obj);
+        CK(cudaGetLastError());
+    }
+    if (n) {
+        prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(staging, n, g->n_pad, g->d_off, n_obj,
+                                                                g->planes, ustats, ndeg);
+        CK(cudaGetLastError());
+        chunk_aabb_kernel<<<(unsigned)g->n_chunks, 256, 0, st>>>(g->planes, n, g->n_pad, g->d_chunk_aabb);
+        CK(cudaGetLastError());
+    }
+    if (n_obj) {
+        const uint64_t m = n_obj * kObjStats;
+        stats_final_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(ustats, g->d_obj_stats, m);
+        CK(cudaGetLastError());
+    }
+    unsigned long long nd = 0;
+    CK(cudaMemcpyAsync(&nd, ndeg, sizeof nd, cudaMemcpyDeviceToHost, st));
+    // overall AABB / scale (for the single-object case this is the object)
+    std::vector<double> os(std::max<uint64_t>(1, n_obj) * kObjStats, 0.0);
+    if (n_obj) CK(cudaMemcpyAsync(os.data(), g->d_obj_stats, n_obj * kObjStats * sizeof(double),
+                                  cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(staging, st));
+    CK(cudaFreeAsync(ustats, st));
+    CK(cudaFreeAsync(ndeg, st));
+    CK(cudaStreamSynchronize(st));
+    g->n_degenerate = nd;
+    double agg[kObjStats] = {pos_inf_h(), pos_inf_h(), pos_inf_h(), -pos_inf_h(), -pos_inf_h(), -pos_inf_h(), 0.0, 0.0};
+    for (uint64_t o = 0; o < n_obj; ++o) {
+        if (g->h_off[o + 1] == g->h_off[o]) continue;
+        const double* s = &os[o * kObjStats];
+        for (int k = 0; k < 3; ++k) agg[k] = std::min(agg[k], s[k]);
+        for (int k = 3; k < kObjStats; ++k) agg[k] = std::max(agg[k], s[k]);
+    }
+    std::copy(agg, agg + kObjStats, g->stats);
+}
+
+void geom_release(Geom* g) {
+    if (!g) return;
+    cudaFree(g->planes);
+    cudaFree(g->d_off);
+    cudaFree(g->d_tiles);
+    cudaFree(g->d_obj_stats);
+    cudaFree(g->d_chunk_aabb);
+    g->planes = nullptr;
+}
+
+}  // namespace tdb

@@ -1,0 +1,55 @@
+// Internal layout shared by the host runtime and the sm_100a kernels.
+#pragma once
+
+#include <cstdint>
+
+namespace tdb {
+
+// ---- device geometry store: per-face SoA planes -------------------------
+// Each plane holds one double per face, n_pad entries (n_pad % 64 == 0,
+// plane base 256-byte aligned => every TMA bulk copy of an even face range is
+// 16-byte aligned). Planes 0..8 are the caller's coordinates, bit-for-bit
+// (the exact pass reads them); the rest are per-face terms hoisted out of the
+// pair loop ("per-triangle and per-edge terms hoisted").
+enum Field : int {
+    F_V = 0,     // V0x V0y V0z V1x V1y V1z V2x V2y V2z
+    F_E = 9,     // E_j = V_{j+1} - V_j (cyclic), 3 x xyz
+    F_L = 18,    // |E_j|^2
+    F_IL = 21,   // 1 / |E_j|^2
+    F_N = 24,    // unit normal of (V1-V0) x (V2-V0)
+    F_C = 27,    // plane offset n.V0
+    F_U = 28,    // dual basis: u(P) = U.(P - V0)
+    F_W = 31,    //             v(P) = W.(P - V0)
+    F_DEG = 34,  // 1.0 when degenerate (geometry.hpp:75, evaluated exactly)
+    F_SPARE = 35,
+    NF = 36
+};
+
+// A-side work tile: up to kTile consecutive faces of one object.
+struct Tile {
+    uint64_t row0;      // first face (global index in the A store)
+    uint64_t obj_row0;  // first face of the tile's object
+    uint32_t count;     // faces in the tile (<= kTile)
+    uint32_t obj;       // object index in the A store
+};
+
+constexpr int kTile = 128;          // A faces per CTA (one per thread)
+constexpr uint64_t kChunk = 8192;   // B faces per work item
+constexpr int kSB = 32;             // B faces per TMA-staged sub-tile
+constexpr int kPlanePad = 64;
+
+// per-object statistics (doubles): aabb lo xyz, hi xyz, max edge, max |coord|
+constexpr int kObjStats = 8;
+
+// Pair-filter tolerances:
+//   band  = sqrt(min d~^2) * (1 + kBandRel) + eta,
+//   eta   = kBandEdge * max edge + kBandAbs * max |coord|
+// intersects plane cull margin:
+//   tau   = kCullDiag * diag(AABB(A obj u B)) + kCullAbs * max |coord|
+constexpr double kBandRel = 1e-9;
+constexpr double kBandEdge = 1e-7;
+constexpr double kBandAbs = 1e-12;
+constexpr double kCullDiag = 1e-10;
+constexpr double kCullAbs = 1e-13;
+
+}  // namespace tdb

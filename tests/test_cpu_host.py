@@ -1,0 +1,86 @@
+"""CPU-only checks of the product's host side: the C-ABI library loads and
+exports every symbol include/tindb_b200.h declares, the mesh generators are
+bit-identical to the reference generator, and compute calls fail loudly
+(never fall back to the CPU) when no sm_100 device is present."""
+import hashlib
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1808_09571_b200 as T
+from conftest import GOLDEN, ROOT
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "tindb_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(tdb_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = T.lib()
+    syms = header_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(L, s), s
+    assert sorted(T.EXPORTS) == syms
+
+
+def test_generators_match_reference_hashes():
+    want = json.load(open(os.path.join(GOLDEN, "generators.json")))
+    for key, h in want.items():
+        kind, ft = key.split("/")
+        m = T.unit_sphere(int(ft)) if kind == "unit_sphere" else T.ore_body(int(ft))
+        assert hashlib.sha256(m.tobytes()).hexdigest() == h, key
+
+
+def test_sphere_face_counts():
+    # dataset.hpp: 8*4^a or 20*4^b nearest the target; SURVEY.md A18
+    for target, faces in [(1000, 1280), (10000, 8192), (100000, 81920), (1000000, 1310720)]:
+        assert T.lib().tdb_gen_unit_sphere(target, None) == faces
+
+
+def test_terrain_shape_and_orientation():
+    t = T.terrain(32, 16, 20.0, 42)
+    assert t.shape == (2 * 32 * 16, 9)
+    v = t.reshape(-1, 3, 3)
+    n = np.cross(v[:, 1] - v[:, 0], v[:, 2] - v[:, 0])
+    assert (n[:, 2] > 0).all()  # CCW seen from +z
+    z = v[:, :, 2]
+    assert z.min() >= -20.0 and z.max() <= 20.0
+    assert np.array_equal(t, T.terrain(32, 16, 20.0, 42))
+    assert not np.array_equal(t, T.terrain(32, 16, 20.0, 43))
+
+
+def test_translate_matches_reference_fixture():
+    m = T.unit_sphere(80)
+    t = T.translate(m, 2.5, 0, 0)
+    assert np.array_equal(t[:, 0::3], m[:, 0::3] + 2.5)
+    assert np.array_equal(t[:, 1::3], m[:, 1::3])
+
+
+def _has_gpu():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+@pytest.mark.skipif(_has_gpu(), reason="checks the no-device failure path")
+def test_compute_fails_loudly_without_device():
+    a = T.unit_sphere(10)
+    with pytest.raises(T.TdbError):
+        T.pairs_distance(a, a)
+    with pytest.raises(T.TdbError):
+        T.Mesh(a)
+    with pytest.raises(T.TdbError):
+        T.distance_host(a, a)
+
+
+def test_bad_arguments_rejected_before_device():
+    with pytest.raises(ValueError):
+        T.Mesh(np.zeros(10))  # not a multiple of 9 doubles
