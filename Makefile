@@ -15,7 +15,7 @@ CU_OBJS  := $(patsubst $(SRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
 CPP_OBJS := $(BUILD)/generators.o
 HDRS     := $(wildcard $(SRC)/*.h $(SRC)/*.cuh) include/tindb_b200.h
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v -Iinclude -I$(SRC) \
-            --expt-relaxed-constexpr
+            --expt-relaxed-constexpr $(EXTRA)
 CXXFLAGS := -O2 -fPIC -std=c++17 -ffp-contract=off -Iinclude
 
 all: lib oracle

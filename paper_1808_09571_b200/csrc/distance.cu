@@ -52,19 +52,10 @@ __device__ __forceinline__ double warp_min_nn(double x) {
     return x;
 }
 
-struct PlaneAt {
-    const double* p;
-    uint64_t pad, i;
-    __device__ __forceinline__ double operator()(int f) const { return __ldg(p + (uint64_t)f * pad + i); }
-};
-
-struct SmemAt {
-    const double* s;
-    int j;
-    __device__ __forceinline__ double operator()(int f) const { return s[f * kSB + j]; }
-};
-
-__global__ void __launch_bounds__(kTile, 2) filter_kernel(DistArgs a) {
+#ifndef TDB_FILTER_MINB
+#define TDB_FILTER_MINB 3
+#endif
+__global__ void __launch_bounds__(kTile, TDB_FILTER_MINB) filter_kernel(DistArgs a) {
     __shared__ alignas(128) double sm[2][NF * kSB];
     __shared__ alignas(8) uint64_t bar[2];
     __shared__ double red[kTile / 32];
@@ -76,7 +67,7 @@ __global__ void __launch_bounds__(kTile, 2) filter_kernel(DistArgs a) {
     const uint64_t row = T.row0 + r;
     bool active = threadIdx.x < T.count && row >= a.row_lo && row < a.row_hi;
     AFace A;
-    load_aface(A, PlaneAt{a.Ap, a.An_pad, row});
+    load_aface(A, FaceRefLdg{a.Ap + row, a.An_pad});
     active = active && __ldg(a.Ap + (uint64_t)F_DEG * a.An_pad + row) == 0.0;
 
     const uint64_t b0 = ch * kChunk, b1 = min(a.Bn, b0 + kChunk);
@@ -109,8 +100,8 @@ __global__ void __launch_bounds__(kTile, 2) filter_kernel(DistArgs a) {
         const double* sb = sm[st];
 #pragma unroll 1
         for (int j = 0; j < cnt; ++j) {
-            if (sb[F_DEG * kSB + j] != 0.0) continue;  // uniform across the CTA
-            best = min_nn(best, pair_d2(A, SmemAt{sb, j}));
+            if (reinterpret_cast<const int*>(sb + F_DEG * kSB + j)[1] != 0) continue;  // uniform across the CTA
+            best = min_nn(best, pair_d2(A, FaceRef{sb + j, (uint64_t)kSB}, a.Ap + row, a.An_pad));
         }
         __syncthreads();
         if (threadIdx.x == 0 && s + 2 < nsub) issue(s + 2);
@@ -155,7 +146,7 @@ __global__ void band_kernel(BandArgs a) {
         return;
     }
     const double eta = band_eta(a.Astats + (a.obj0 + o) * kObjStats, a.Bstats);
-    const double b = sqrt(__longlong_as_double((long long)e)) * (1.0 + kBandRel) + eta;
+    const double b = sqrt(__longlong_as_double((long long)e)) * (1.0 + kBandRel) + 2.0 * eta;
     a.band[o] = b;
     a.band2[o] = b * b * (1.0 + 4e-16);
 }
@@ -208,7 +199,7 @@ __global__ void __launch_bounds__(kTile) verify_kernel(VerifyArgs v) {
         bool active = threadIdx.x < T.count && row >= a.row_lo && row < a.row_hi;
         active = active && __ldg(a.Ap + (uint64_t)F_DEG * a.An_pad + row) == 0.0;
         AFace A;
-        load_aface(A, PlaneAt{a.Ap, a.An_pad, row});
+        load_aface(A, FaceRefLdg{a.Ap + row, a.An_pad});
         const uint64_t c0 = ch * kChunk, c1 = min(a.Bn, c0 + kChunk);
         const uint64_t len = (c1 - c0 + v.nsplit - 1) / v.nsplit;
         const uint64_t b0 = c0 + part * len, b1 = min(c1, b0 + len);
@@ -217,7 +208,7 @@ __global__ void __launch_bounds__(kTile) verify_kernel(VerifyArgs v) {
         const uint64_t i_loc = row - T.obj_row0;
         for (uint64_t j = b0; j < b1; ++j) {
             if (__ldg(a.Bp + (uint64_t)F_DEG * a.Bn_pad + j) != 0.0) continue;
-            const double d2 = pair_d2(A, PlaneAt{a.Bp, a.Bn_pad, j});
+            const double d2 = pair_d2(A, FaceRefLdg{a.Bp + j, a.Bn_pad}, a.Ap + row, a.An_pad);
             if (active && d2 <= b2) {
                 const exact::res x = exact::tri_tri(load_tri(a.Ap, a.An_pad, row), load_tri(a.Bp, a.Bn_pad, j));
                 const unsigned long long bits = (unsigned long long)__double_as_longlong(x.d);
@@ -257,9 +248,9 @@ __global__ void check_kernel(CheckArgs a) {
     // d == kNone: no pair fell in the band although the band contains the
     // filter minimum -> cannot happen unless every in-band pair evaluated to
     // NaN/inf; treat as done.
-    if (d != kNone && __longlong_as_double((long long)d) > b) {
-        const double nb = __longlong_as_double((long long)d) * (1.0 + kBandRel) +
-                          band_eta(a.Astats + (a.obj0 + o) * kObjStats, a.Bstats);
+    const double eta = band_eta(a.Astats + (a.obj0 + o) * kObjStats, a.Bstats);
+    if (d != kNone && __longlong_as_double((long long)d) > b - eta) {
+        const double nb = __longlong_as_double((long long)d) * (1.0 + kBandRel) + 2.0 * eta;
         a.band[o] = nb;
         a.band2[o] = nb * nb * (1.0 + 4e-16);
         a.objD[o] = kNone;

@@ -6,12 +6,13 @@
 //     clamped t — covers vertex/edge and vertex/vertex contacts too), and
 //   * 6 vertex/face pairs (vertex projecting inside the other triangle).
 // Intersecting pairs are caught by a plane-straddle test followed by a
-// division-free piercing test (rare branch). Everything is squared distances
-// with FMA; the only reciprocal is rcp.approx (MUFU.RCP64H) for the first s,
-// which only perturbs the evaluated point pair to second order (the value is
-// always a distance between two real points of the triangles). Per pair:
-// 27 DADD (vertex differences) + 6 x 12 (vertex/face) + 9 x 27 (edge/edge)
-// = 342 FP64 pipe instructions, no DDIV/DSQRT.
+// division-free piercing test (rare branch, out of line). Everything is
+// squared distances with FMA; the only reciprocal is rcp.approx
+// (MUFU.RCP64H) for the first s, which only perturbs the evaluated point pair
+// to second order (the value is always a distance between two real points of
+// the triangles). Per pair: 27 DADD (vertex differences) + 6 x 12
+// (vertex/face) + 9 x 27 (edge/edge) = 342 FP64 pipe instructions, no
+// DDIV/DSQRT.
 //
 // The value d~^2 approximates the A17 composition's distance
 // closely enough to bound it: the exact pass (distance.cu) re-evaluates with
@@ -53,6 +54,20 @@ __device__ __forceinline__ bool all_nonneg(double a, double b, double c) {
     return (__double2hiint(a) | __double2hiint(b) | __double2hiint(c)) >= 0;
 }
 
+// Field access: field f of a face lives at p[f * stride] (SoA planes in HBM:
+// stride = n_pad; staged sub-tile in SMEM: stride = kSB; AoS record: 1).
+struct FaceRef {
+    const double* p;
+    uint64_t stride;
+    __device__ __forceinline__ double operator()(int f) const { return p[(uint64_t)f * stride]; }
+};
+
+struct FaceRefLdg {
+    const double* p;
+    uint64_t stride;
+    __device__ __forceinline__ double operator()(int f) const { return __ldg(p + (uint64_t)f * stride); }
+};
+
 // A-side face held in registers for the whole B chunk.
 struct AFace {
     double v[9];   // vertices
@@ -83,11 +98,10 @@ __device__ __forceinline__ double dot3(const double* a, double x, double y, doub
     return fma(a[0], x, fma(a[1], y, a[2] * z));
 }
 
-// Division-free piercing test (rare branch): does an edge of one triangle
-// cross the other? Heights h (signed, scaled) and barycentrics (u, v) of the
-// three vertices of the piercing triangle w.r.t. the pierced one. Crossing of
-// edge k->k+1 at lambda = h_k/(h_k - h_k+1); u(X)*(h_k - h_k+1) =
-// h_k u_k+1 - h_k+1 u_k, likewise for v and for 1 - u - v.
+// Division-free piercing test: does an edge of the triangle with vertex
+// heights h (w.r.t. the other's plane) and barycentrics (u, v) cross the
+// other triangle? Crossing of edge k->k+1 at lambda = h_k/(h_k - h_k+1);
+// u(X)*(h_k - h_k+1) = h_k u_k+1 - h_k+1 u_k, likewise for v and 1 - u - v.
 __device__ __forceinline__ bool edges_pierce(const double h[3], const double u[3], const double v[3]) {
     bool hit = false;
 #pragma unroll
@@ -98,19 +112,66 @@ __device__ __forceinline__ bool edges_pierce(const double h[3], const double u[3
             const double uD = fma(h[k], u[q], -h[q] * u[k]);
             const double vD = fma(h[k], v[q], -h[q] * v[k]);
             const double tD = D - uD - vD;
-            const bool pos = D > 0.0;
-            hit |= pos ? (uD >= 0.0 && vD >= 0.0 && tD >= 0.0) : (uD <= 0.0 && vD <= 0.0 && tD <= 0.0);
+            hit |= D > 0.0 ? (uD >= 0.0 && vD >= 0.0 && tD >= 0.0) : (uD <= 0.0 && vD <= 0.0 && tD <= 0.0);
         }
     }
     return hit;
 }
 
-// d~^2 for face A (registers) against face j of the B accessor.
-// `bt(f)` returns field f of the B face.
+// Out-of-line (rare) piercing test for a pair whose triangles both straddle
+// the other's plane; reloads both faces so the hot path keeps no state.
+static __device__ __noinline__ bool pierce_slow(const double* ap, uint64_t as, const double* bp, uint64_t bs) {
+    const FaceRef A{ap, as}, B{bp, bs};
+    double hb[3], ub[3], vb[3], ha[3], ua[3], va[3];
+    const double a0x = A(F_V), a0y = A(F_V + 1), a0z = A(F_V + 2);
+    const double b0x = B(F_V), b0y = B(F_V + 1), b0z = B(F_V + 2);
+    const double na[3] = {A(F_N), A(F_N + 1), A(F_N + 2)}, nb[3] = {B(F_N), B(F_N + 1), B(F_N + 2)};
+    const double Ua[3] = {A(F_U), A(F_U + 1), A(F_U + 2)}, Ub[3] = {B(F_U), B(F_U + 1), B(F_U + 2)};
+    const double Wa[3] = {A(F_W), A(F_W + 1), A(F_W + 2)}, Wb[3] = {B(F_W), B(F_W + 1), B(F_W + 2)};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double wx = B(F_V + 3 * k) - a0x, wy = B(F_V + 3 * k + 1) - a0y, wz = B(F_V + 3 * k + 2) - a0z;
+        hb[k] = dot3(na, wx, wy, wz);
+        ub[k] = dot3(Ua, wx, wy, wz);
+        vb[k] = dot3(Wa, wx, wy, wz);
+        const double qx = A(F_V + 3 * k) - b0x, qy = A(F_V + 3 * k + 1) - b0y, qz = A(F_V + 3 * k + 2) - b0z;
+        ha[k] = dot3(nb, qx, qy, qz);
+        ua[k] = dot3(Ub, qx, qy, qz);
+        va[k] = dot3(Wb, qx, qy, qz);
+    }
+    return edges_pierce(hb, ub, vb) || edges_pierce(ha, ua, va);
+}
+
+// clamp to [0,1] on the high word only (the low word is dropped: relative
+// truncation <= 2^-20). Used for the first parameter estimate, whose
+// precision is already bounded by rcp.approx.
+__device__ __forceinline__ double clamp01_hi(double x) {
+    return __hiloint2double(min(max(__double2hiint(x), 0), 0x3ff00000), 0);
+}
+
+constexpr int kInfHi = 0x7ff00000;  // high word of +inf
+
+// Barycentric inside test u >= 0, v >= 0, u + v < 1 with one FP64 add: the
+// sum is non-negative when u, v are, so "< 1" is a high-word compare
+// (u + v in [1, 1 + 2^-20) reads as outside: a boundary case the edge/edge
+// candidates cover exactly).
+__device__ __forceinline__ bool inside(double u, double v) {
+    return ((__double2hiint(u) | __double2hiint(v)) >= 0) & (__double2hiint(u + v) < 0x3ff00000);
+}
+
+// d~^2 for face A (registers) against face B, truncated to its high word
+// (a lower bound within a relative 2^-20 of the value; the minima are kept
+// as 32-bit integers — one VIMNMX per candidate). `ap`/`as` locate A's
+// fields again for the out-of-line piercing test.
+//
+// Edge/edge dot products run incrementally across the 3x3 grid:
+//   cw_{j,k+1} = cw_{j,k} + bb_{j,k}   (w_{j,k+1} = w_{j,k} + Eb_k)
+//   fw_{j+1,k} = fw_{j,k} - bb_{j,k}   (w_{j+1,k} = w_{j,k} - Ea_j)
 template <class P>
-__device__ __forceinline__ double pair_d2(const AFace& A, const P& bt) {
-    double best = pos_inf();
-    double hb[3], ha[3];
+__device__ __forceinline__ double pair_d2(const AFace& A, const P& bt, const double* ap, uint64_t as) {
+    int best = kInfHi;
+    int hb_or = 0, hb_and = -1, ha_or = 0, ha_and = -1;  // sign words of the plane heights
+    double cw_prev[3], bb_prev[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         const double bx = bt(F_V + 3 * k), by = bt(F_V + 3 * k + 1), bz = bt(F_V + 3 * k + 2);
@@ -125,9 +186,9 @@ __device__ __forceinline__ double pair_d2(const AFace& A, const P& bt) {
             const double h = dot3(A.n, w[0][0], w[0][1], w[0][2]);
             const double u = dot3(A.U, w[0][0], w[0][1], w[0][2]);
             const double v = dot3(A.W, w[0][0], w[0][1], w[0][2]);
-            const double t = (1.0 - u) - v;
-            hb[k] = h;
-            best = min_nn(best, all_nonneg(u, v, t) ? h * h : pos_inf());
+            hb_or |= __double2hiint(h);
+            hb_and &= __double2hiint(h);
+            best = min(best, inside(u, v) ? __double2hiint(h * h) : kInfHi);
         }
         if (k == 0) {  // vertices A_j against face B: A_j - B_0 = -w_j
             const double nb[3] = {bt(F_N), bt(F_N + 1), bt(F_N + 2)};
@@ -138,53 +199,38 @@ __device__ __forceinline__ double pair_d2(const AFace& A, const P& bt) {
                 const double h = dot3(nb, w[j][0], w[j][1], w[j][2]);
                 const double u = -dot3(ub, w[j][0], w[j][1], w[j][2]);
                 const double v = -dot3(vb, w[j][0], w[j][1], w[j][2]);
-                const double t = (1.0 - u) - v;
-                ha[j] = h;
-                best = min_nn(best, all_nonneg(u, v, t) ? h * h : pos_inf());
+                ha_or |= __double2hiint(h);
+                ha_and &= __double2hiint(h);
+                best = min(best, inside(u, v) ? __double2hiint(h * h) : kInfHi);
             }
         }
         const double ebx = bt(F_E + 3 * k), eby = bt(F_E + 3 * k + 1), ebz = bt(F_E + 3 * k + 2);
         const double Lb = bt(F_L + k), ILb = bt(F_IL + k);
+        double fw = fma(ebx, w[0][0], fma(eby, w[0][1], ebz * w[0][2]));
 #pragma unroll
         for (int j = 0; j < 3; ++j) {  // edge A_j->A_j+1 against edge B_k->B_k+1
             const double* ea = A.e + 3 * j;
-            const double cw = dot3(ea, w[j][0], w[j][1], w[j][2]);
-            const double fw = fma(ebx, w[j][0], fma(eby, w[j][1], ebz * w[j][2]));
             const double bb = dot3(ea, ebx, eby, ebz);
+            const double cw = k == 0 ? dot3(ea, w[j][0], w[j][1], w[j][2]) : cw_prev[j] + bb_prev[j];
             const double den = fma(-bb, bb, A.L[j] * Lb);
             const double num = fma(cw, Lb, -(bb * fw));
-            double s = clamp01(num * rcp_approx(den));
+            double s = clamp01_hi(num * rcp_approx(den));
             const double t = clamp01(fma(bb, s, -fw) * ILb);
             s = clamp01(fma(bb, t, cw) * A.IL[j]);
             const double dx = fma(s, ea[0], fma(-t, ebx, -w[j][0]));
             const double dy = fma(s, ea[1], fma(-t, eby, -w[j][1]));
             const double dz = fma(s, ea[2], fma(-t, ebz, -w[j][2]));
-            best = min_nn(best, fma(dx, dx, fma(dy, dy, dz * dz)));
+            best = min(best, __double2hiint(fma(dx, dx, fma(dy, dy, dz * dz))));
+            cw_prev[j] = cw;
+            bb_prev[j] = bb;
+            fw = fw - bb;
         }
     }
     // Both triangles straddle the other's plane: an edge may pierce a face.
-    const bool sa = !(all_nonneg(hb[0], hb[1], hb[2]) || ((__double2hiint(hb[0]) & __double2hiint(hb[1]) & __double2hiint(hb[2])) < 0));
-    const bool sb = !(all_nonneg(ha[0], ha[1], ha[2]) || ((__double2hiint(ha[0]) & __double2hiint(ha[1]) & __double2hiint(ha[2])) < 0));
-    if (sa && sb) {
-        double u[3], v[3], u2[3], v2[3];
-        const double nb[3] = {bt(F_N), bt(F_N + 1), bt(F_N + 2)};
-        const double ub[3] = {bt(F_U), bt(F_U + 1), bt(F_U + 2)};
-        const double vb[3] = {bt(F_W), bt(F_W + 1), bt(F_W + 2)};
-        const double b0x = bt(F_V), b0y = bt(F_V + 1), b0z = bt(F_V + 2);
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            const double wx = bt(F_V + 3 * k) - A.v[0], wy = bt(F_V + 3 * k + 1) - A.v[1],
-                         wz = bt(F_V + 3 * k + 2) - A.v[2];
-            u[k] = dot3(A.U, wx, wy, wz);
-            v[k] = dot3(A.W, wx, wy, wz);
-            const double qx = A.v[3 * k] - b0x, qy = A.v[3 * k + 1] - b0y, qz = A.v[3 * k + 2] - b0z;
-            u2[k] = dot3(ub, qx, qy, qz);
-            v2[k] = dot3(vb, qx, qy, qz);
-        }
-        (void)nb;
-        if (edges_pierce(hb, u, v) || edges_pierce(ha, u2, v2)) best = 0.0;
-    }
-    return best;
+    const bool sb = !(hb_or >= 0 || hb_and < 0);
+    const bool sa = !(ha_or >= 0 || ha_and < 0);
+    if (sa && sb && pierce_slow(ap, as, bt.p, bt.stride)) best = 0;
+    return __hiloint2double(best, 0);
 }
 
 }  // namespace tdb

@@ -25,19 +25,15 @@ __global__ void pairs_kernel(const double* __restrict__ a9, const double* __rest
 }
 
 // FP64 filter value d~^2 for aligned pairs (tests the filter's accuracy).
-struct AosAt {
-    const double* p;  // per-face prep record, NF doubles
-    __device__ __forceinline__ double operator()(int f) const { return p[f]; }
-};
 
 __global__ void filter_pairs_kernel(const double* __restrict__ pa, const double* __restrict__ pb, uint64_t n,
                                     double* __restrict__ d2) {
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
          k += (uint64_t)gridDim.x * blockDim.x) {
         AFace A;
-        load_aface(A, AosAt{pa + NF * k});
+        load_aface(A, FaceRef{pa + NF * k, 1});
         const bool deg = pa[NF * k + F_DEG] != 0.0 || pb[NF * k + F_DEG] != 0.0;
-        d2[k] = deg ? pos_inf() : pair_d2(A, AosAt{pb + NF * k});
+        d2[k] = deg ? pos_inf() : pair_d2(A, FaceRef{pb + NF * k, 1}, pa + NF * k, 1);
     }
 }
 

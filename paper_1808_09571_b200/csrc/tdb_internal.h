@@ -42,11 +42,14 @@ constexpr int kPlanePad = 64;
 constexpr int kObjStats = 8;
 
 // Pair-filter tolerances:
-//   band  = sqrt(min d~^2) * (1 + kBandRel) + eta,
-//   eta   = kBandEdge * max edge + kBandAbs * max |coord|
+//   eta   = kBandEdge * max edge + kBandAbs * max |coord|   (>= filter error
+//           |d~ - d_true| plus the rounding of the reference's witnesses)
+//   band  = sqrt(min d~^2) * (1 + kBandRel) + 2 eta          (candidates: d~ <= band)
+//   done when the exact minimum D <= band - eta, else band = D (1 + kBandRel) + 2 eta
+// kBandRel covers the 2^-20 high-word truncation of d~^2 (fast_pair.cuh).
 // intersects plane cull margin:
 //   tau   = kCullDiag * diag(AABB(A obj u B)) + kCullAbs * max |coord|
-constexpr double kBandRel = 1e-9;
+constexpr double kBandRel = 4e-6;
 constexpr double kBandEdge = 1e-7;
 constexpr double kBandAbs = 1e-12;
 constexpr double kCullDiag = 1e-10;
