@@ -37,6 +37,17 @@ $(LIB): $(CU_OBJS) $(CPP_OBJS)
 oracle:
 	$(MAKE) -C oracle
 
+# C++ shim (include/tindb_b200/kernels.hpp) against the reference's own types
+# and dispatch; only buildable where /root/reference exists (the binary then
+# travels to the GPU box with the snapshot).
+REF ?= /root/reference/proj
+shimtest: $(LIB) oracle
+	@if [ -d "$(REF)/include" ]; then \
+	  $(CXX) -std=c++20 -O2 -ffp-contract=off -Dtindb=tindb_ref -I$(REF)/include -Iinclude \
+	    tests/cpp/shim_test.cpp -o $(BUILD)/shim_test -Loracle/_ref -ltindb_ref -L$(PKG) -ltindb_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../oracle/_ref' -Wl,-rpath,'$$ORIGIN/../$(PKG)'; \
+	else echo "shimtest: $(REF) absent; keeping prebuilt $(BUILD)/shim_test"; fi
+
 sass: $(LIB)
 	cuobjdump -sass $(LIB) > $(BUILD)/libtindb_b200.sass
 
@@ -44,4 +55,4 @@ clean:
 	rm -rf $(BUILD) $(LIB)
 	$(MAKE) -C oracle clean
 
-.PHONY: all lib oracle sass clean
+.PHONY: all lib oracle sass clean shimtest

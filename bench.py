@@ -208,20 +208,11 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    from paper_1808_09571_b200 import shard
+
     def combine(d, p):
         """Lexicographic (distance, pair) min over ranks: NCCL all_gather."""
-        if world == 1:
-            return d, p
-        t = torch.tensor([d, float(np.uint64(p).view(np.float64))], dtype=torch.float64, device="cuda")
-        g = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(g, t)
-        best = None
-        for x in g:
-            dd = float(x[0].item())
-            pp = int(np.float64(x[1].item()).view(np.uint64))
-            if best is None or (dd, pp) < best:
-                best = (dd, pp)
-        return best
+        return shard.combine_min(d, p, device="cuda")
 
     fp64_tf, _ = T.fp64_peak()
     ter, ore = make_meshes()

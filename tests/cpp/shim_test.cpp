@@ -1,0 +1,118 @@
+// Drives include/tindb_b200/kernels.hpp against the REFERENCE's own types
+// and dispatch (compiled with -Dtindb=tindb_ref and linked with
+// oracle/_ref/libtindb_ref.so, i.e. the unmodified reference sources).
+// Run by tests/test_gpu_shim.py on a B200; prints "SHIM OK".
+#include <tindb/batch.hpp>
+#include <tindb/dataset.hpp>
+
+#include <cstdio>
+#include <cstring>
+#include <cstdint>
+
+#include "tindb_b200/kernels.hpp"
+
+extern "C" int ref_mesh_mesh_distance(const double*, std::uint64_t, const double*, std::uint64_t,
+                                      std::uint64_t, std::uint64_t, std::uint64_t, int, double*,
+                                      std::uint64_t*);
+extern "C" int ref_mesh_mesh_intersects(const double*, std::uint64_t, const double*, std::uint64_t,
+                                        std::uint64_t, std::uint64_t, std::uint64_t, int,
+                                        std::uint64_t*);
+
+using namespace tindb;
+namespace K = tindb::kernels;
+
+static int fails = 0;
+#define EXPECT(c)                                                        \
+    do {                                                                 \
+        if (!(c)) {                                                      \
+            std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #c);     \
+            ++fails;                                                     \
+        }                                                                \
+    } while (0)
+
+static TriangleMesh shifted(const TriangleMesh& m, double dx, double dy, double dz, double s = 1.0) {
+    TriangleMesh o = m;
+    for (Triangle& t : o.triangles)
+        for (Point3* p : {&t.v0, &t.v1, &t.v2}) *p = Point3{p->x * s + dx, p->y * s + dy, p->z * s + dz};
+    return o;
+}
+
+static const double* F(const TriangleMesh& m) { return reinterpret_cast<const double*>(m.triangles.data()); }
+
+static bool same_bits(double a, double b) { return std::memcmp(&a, &b, sizeof a) == 0; }
+
+int main() {
+    const TriangleMesh s = bench::unit_sphere(1000);
+    const TriangleMesh far = shifted(s, 2.5, 0, 0);
+    const TriangleMesh cross = shifted(s, 0.5, 0.1, 0);
+    auto cfg = K::ExecutorConfig::parallel(4);
+
+    // mesh_mesh_distance vs the reference composition (A17)
+    for (const TriangleMesh* b : {&far, &cross}) {
+        K::b200::MeshPairInfo info;
+        K::DistanceResult r = K::b200::mesh_mesh_distance(s, *b, cfg, &info);
+        double o7[7];
+        std::uint64_t p = 0;
+        ref_mesh_mesh_distance(F(s), s.triangles.size(), F(*b), b->triangles.size(), 0, s.triangles.size(), 1,
+                               4, o7, &p);
+        EXPECT(same_bits(r.distance, o7[0]));
+        EXPECT(info.pair_index && *info.pair_index == p);
+        EXPECT(r.face_index && *r.face_index == p / b->triangles.size());
+        EXPECT(same_bits(r.closest_on_a.x, o7[1]) && same_bits(r.closest_on_b.z, o7[6]));
+        std::uint64_t hp = 0;
+        const int hit = ref_mesh_mesh_intersects(F(s), s.triangles.size(), F(*b), b->triangles.size(), 0,
+                                                 s.triangles.size(), 1, 4, &hp);
+        K::IntersectionResult h = K::b200::mesh_mesh_intersects(s, *b, cfg, &info);
+        EXPECT(h.hit == (hit != 0));
+        if (h.hit) EXPECT(info.pair_index && *info.pair_index == hp);
+    }
+
+    // the missing batch.cpp:49/:62 branch
+    EXPECT(!K::b200::eval_mesh_mesh(K::BatchOp::Distance, Geometry{LineSegment{{0, 0, 0}, {1, 1, 1}}},
+                                    Geometry{s}, cfg));
+    auto v = K::b200::eval_mesh_mesh(K::BatchOp::Distance, Geometry{s}, Geometry{far}, cfg);
+    EXPECT(v && std::holds_alternative<double>(*v) && std::get<double>(*v) == 0.5);
+
+    // whole-column run_batch: meshes on the device, everything else through
+    // the reference dispatch, results in record order with record ids
+    std::vector<store::GeometryRecord> recs;
+    recs.push_back({11, Geometry{shifted(s, 0.3, 0, 0, 0.5)}});
+    recs.push_back({12, Geometry{LineSegment{{3, 0, 0}, {4, 0, 0}}}});
+    recs.push_back({13, Geometry{shifted(s, -3.0, 1.0, 0, 0.2)}});
+    recs.push_back({14, Geometry{Point3{0, 0, 5}}});
+    recs.push_back({15, Geometry{LineString{{{0, 0, 0}, {1, 0, 0}, {1, 1, 0}}}}});
+    const std::optional<Geometry> lit = Geometry{s};
+    for (K::BatchOp op : {K::BatchOp::Distance, K::BatchOp::Intersects}) {
+        auto got = K::b200::run_batch_b200(op, recs, lit, cfg);
+        auto ref = K::run_batch(op, recs, lit, cfg);  // TypeMismatch for Mesh x Mesh
+        EXPECT(got.size() == recs.size());
+        for (std::size_t i = 0; i < recs.size(); ++i) {
+            EXPECT(got[i].record_id == recs[i].id);
+            if (kind_of(recs[i].geometry) == GeometryKind::Mesh) {
+                EXPECT(ref[i].is_error());
+                const auto& m = std::get<TriangleMesh>(recs[i].geometry);
+                if (op == K::BatchOp::Distance) {
+                    double o7[7];
+                    std::uint64_t p = 0;
+                    ref_mesh_mesh_distance(F(m), m.triangles.size(), F(s), s.triangles.size(), 0,
+                                           m.triangles.size(), 1, 4, o7, &p);
+                    EXPECT(std::holds_alternative<double>(got[i].value) &&
+                           same_bits(std::get<double>(got[i].value), o7[0]));
+                } else {
+                    std::uint64_t hp = 0;
+                    const int hit = ref_mesh_mesh_intersects(F(m), m.triangles.size(), F(s), s.triangles.size(),
+                                                             0, m.triangles.size(), 1, 4, &hp);
+                    EXPECT(std::holds_alternative<bool>(got[i].value) && std::get<bool>(got[i].value) == (hit != 0));
+                }
+            } else {
+                EXPECT(got[i].value.index() == ref[i].value.index());
+                if (std::holds_alternative<double>(ref[i].value))
+                    EXPECT(same_bits(std::get<double>(got[i].value), std::get<double>(ref[i].value)));
+                if (std::holds_alternative<bool>(ref[i].value))
+                    EXPECT(std::get<bool>(got[i].value) == std::get<bool>(ref[i].value));
+            }
+        }
+    }
+    if (fails == 0) std::printf("SHIM OK\n");
+    return fails ? 1 : 0;
+}
