@@ -44,7 +44,8 @@ sys.path.insert(0, ROOT)
 
 W_D = 975.0          # algorithmic FP64 flops per triangle pair
 W_REF = 2838.0       # reference-composition flops per pair (op-counted)
-FILTER_DP_INSTR = 342  # FP64-pipe instructions per pair in fast_pair.cuh
+FILTER_DP_INSTR = 318  # FP64-pipe instructions per pair in filter_kernel (cuobjdump -sass count)
+FILTER_FLOPS = 492     # executed FP64 flops per pair (174 DFMA x 2 + 93 DMUL + 51 DADD)
 METRIC = "triangle-pair tests/sec (3DDistance, 3DIntersects) at 1/2/4/8 B200 vs CPU ref"
 UNIT = "pairs/s"
 WORKLOAD = "C2: terrain 1,048,576 tris vs orebody 1,310,720 tris, ST_3DDistance (FP64, all pairs)"
@@ -293,6 +294,7 @@ def main():
         "peak_source": "measured in this run: DFMA issue-rate microbenchmark (tdb_fp64_peak); "
                        "spec 148 SM x 64 FMA x 2 x 1.965 GHz = 37.2",
         "fp64_pipe_frac": FILTER_DP_INSTR * f_pairs / (f_ms * 1e-3) / (fp64_tf * 1e12 / 2),
+        "executed_fp64_tflops": FILTER_FLOPS * f_pairs / (f_ms * 1e-3) / 1e12,
         "filter_share_of_step": sum(filt_ms) / ms if world == 1 else None,
     }
 
