@@ -170,6 +170,7 @@ __device__ __forceinline__ bool inside(double u, double v) {
 template <class P>
 __device__ __forceinline__ double pair_d2(const AFace& A, const P& bt, const double* ap, uint64_t as) {
     int best = kInfHi;
+    int hmin = kInfHi;  // min |h| (high word) over vertices projecting inside the other face
     int hb_or = 0, hb_and = -1, ha_or = 0, ha_and = -1;  // sign words of the plane heights
     double cw_prev[3], bb_prev[3];
 #pragma unroll
@@ -188,7 +189,7 @@ __device__ __forceinline__ double pair_d2(const AFace& A, const P& bt, const dou
             const double v = dot3(A.W, w[0][0], w[0][1], w[0][2]);
             hb_or |= __double2hiint(h);
             hb_and &= __double2hiint(h);
-            best = min(best, inside(u, v) ? __double2hiint(h * h) : kInfHi);
+            hmin = min(hmin, inside(u, v) ? (__double2hiint(h) & 0x7fffffff) : kInfHi);
         }
         if (k == 0) {  // vertices A_j against face B: A_j - B_0 = -w_j
             const double nb[3] = {bt(F_N), bt(F_N + 1), bt(F_N + 2)};
@@ -201,7 +202,7 @@ __device__ __forceinline__ double pair_d2(const AFace& A, const P& bt, const dou
                 const double v = -dot3(vb, w[j][0], w[j][1], w[j][2]);
                 ha_or |= __double2hiint(h);
                 ha_and &= __double2hiint(h);
-                best = min(best, inside(u, v) ? __double2hiint(h * h) : kInfHi);
+                hmin = min(hmin, inside(u, v) ? (__double2hiint(h) & 0x7fffffff) : kInfHi);
             }
         }
         const double ebx = bt(F_E + 3 * k), eby = bt(F_E + 3 * k + 1), ebz = bt(F_E + 3 * k + 2);
@@ -212,8 +213,10 @@ __device__ __forceinline__ double pair_d2(const AFace& A, const P& bt, const dou
             const double* ea = A.e + 3 * j;
             const double bb = dot3(ea, ebx, eby, ebz);
             const double cw = k == 0 ? dot3(ea, w[j][0], w[j][1], w[j][2]) : cw_prev[j] + bb_prev[j];
-            const double den = fma(-bb, bb, A.L[j] * Lb);
-            const double num = fma(cw, Lb, -(bb * fw));
+            // s0 = (cw Lb - bb fw) / (La Lb - bb^2), both terms divided by Lb
+            const double bbI = bb * ILb;
+            const double den = fma(-bbI, bb, A.L[j]);
+            const double num = fma(-bbI, fw, cw);
             double s = clamp01_hi(num * rcp_approx(den));
             const double t = clamp01(fma(bb, s, -fw) * ILb);
             s = clamp01(fma(bb, t, cw) * A.IL[j]);
@@ -229,6 +232,10 @@ __device__ __forceinline__ double pair_d2(const AFace& A, const P& bt, const dou
     // Both triangles straddle the other's plane: an edge may pierce a face.
     const bool sb = !(hb_or >= 0 || hb_and < 0);
     const bool sa = !(ha_or >= 0 || ha_and < 0);
+    {
+        const double hv = __hiloint2double(hmin, 0);  // truncated |h|: one square per pair
+        best = min(best, __double2hiint(hv * hv));
+    }
     if (sa && sb && pierce_slow(ap, as, bt.p, bt.stride)) best = 0;
     return __hiloint2double(best, 0);
 }

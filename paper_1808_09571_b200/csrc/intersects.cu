@@ -10,16 +10,24 @@
 // Per pair the kernel first runs a conservative separating-plane test in
 // FP64: if all three vertices of one triangle lie strictly on one side of
 // the other's plane by more than tau (tdb_internal.h: 1e-10 x diag of the
-// pair's bounding box + 1e-13 x max |coord|, >= 30x the reference
-// predicate's worst rounding of t at that separation), no directed edge can
-// pass the reference predicate. Survivors run
-// the bit-exact predicate (exact.cuh), so booleans and indices are the
-// reference's.
+// pair's bounding box + 1e-13 x max |coord|), no directed edge can pass the
+// reference predicate. Why: with heights h_P, h_Q of an edge's endpoints
+// above the other plane (same sign, |h| > tau), the reference's
+// t = h_P / (h_P - h_Q) lies outside [-1e-12, 1+1e-12] unless
+// min|h| <= (c*u + 2e-12)*|w| with |w| <= diag (kernels.cpp:243-244,
+// kernels.hpp:53-54), which tau exceeds >= 30x; an edge of the other
+// triangle lies in its own plane, at distance >= tau from this triangle.
+// Survivors run the bit-exact predicate (exact.cuh), so booleans and indices
+// are the reference's (tests/test_gpu_parity.py).
 //
-// Early exit: an item is skipped when the object's current lowest hit is
-// below the item's smallest pair index (kernels.cpp:413-415), and an object
-// whose AABB is separated from B's by more than tau is skipped whole (the
-// per-object AABB header).
+// Layout: one warp per A-tile, each lane holds four rows (register blocking:
+// one staged B face feeds four pair tests); B sub-tiles of kSBH faces are
+// TMA bulk copies (14 SoA planes) double-buffered on mbarriers.
+//
+// Early exit: a warp skips its tile when the object's current lowest hit is
+// below the tile's smallest pair index (kernels.cpp:413-415); a row stops at
+// its first hit; an object whose AABB header is separated from B's by more
+// than tau is skipped whole.
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -33,16 +41,18 @@ namespace tdb {
 namespace {
 
 constexpr unsigned long long kNone = ~0ull;
-// staged B planes: V (0..8), N (24..26), C (27) -> copy planes [0,9) and [24,28), plus DEG
-constexpr int kHitPlanes = 14;
+constexpr int kHitPlanes = 14;  // V (9), N (3), C, DEG
 __device__ __constant__ int kHitPlaneOf[kHitPlanes] = {0, 1, 2, 3, 4, 5, 6, 7, 8, F_N, F_N + 1, F_N + 2, F_C, F_DEG};
 enum { HS_V = 0, HS_N = 9, HS_C = 12, HS_DEG = 13 };
+constexpr int kSBH = 128;          // B faces per staged sub-tile
+constexpr int kRows = 4;           // A rows per lane
+constexpr int kWarps = 4;          // tiles per CTA (one per warp)
 
 struct HitArgs {
     const double* Ap;
     uint64_t An_pad;
     const Tile* tiles;
-    uint64_t tile0, row_lo, row_hi;
+    uint64_t tile0, ntiles, row_lo, row_hi;
     const double* Bp;
     uint64_t Bn_pad, Bn, n_chunks;
     uint64_t obj0;
@@ -68,18 +78,39 @@ __device__ __forceinline__ bool separated(double h0, double h1, double h2, doubl
            q0 != 0.0 && q1 != 0.0 && q2 != 0.0;
 }
 
-__global__ void __launch_bounds__(kTile, 4) hit_kernel(HitArgs a) {
-    __shared__ alignas(128) double sm[2][kHitPlanes * kSB];
+// Second plane test + exact reference predicate (rare path, out of line).
+static __device__ __noinline__ bool slow_pair(const double* Ap, uint64_t An_pad, uint64_t row, const double* sb,
+                                              int j, double tau) {
+    double av[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) av[k] = __ldg(Ap + (uint64_t)(F_V + k) * An_pad + row);
+    const double bn0 = sb[(HS_N + 0) * kSBH + j], bn1 = sb[(HS_N + 1) * kSBH + j], bn2 = sb[(HS_N + 2) * kSBH + j],
+                 bc = sb[HS_C * kSBH + j];
+    const double g0 = fma(bn0, av[0], fma(bn1, av[1], fma(bn2, av[2], -bc)));
+    const double g1 = fma(bn0, av[3], fma(bn1, av[4], fma(bn2, av[5], -bc)));
+    const double g2 = fma(bn0, av[6], fma(bn1, av[7], fma(bn2, av[8], -bc)));
+    if (separated(g0, g1, g2, tau)) return false;
+    const double* bv = sb + HS_V * kSBH + j;
+    const exact::tri ta{{av[0], av[1], av[2]}, {av[3], av[4], av[5]}, {av[6], av[7], av[8]}};
+    const exact::tri tb{{bv[0], bv[kSBH], bv[2 * kSBH]}, {bv[3 * kSBH], bv[4 * kSBH], bv[5 * kSBH]},
+                        {bv[6 * kSBH], bv[7 * kSBH], bv[8 * kSBH]}};
+    return exact::tri_tri_hit(ta, tb);
+}
+
+__global__ void __launch_bounds__(32 * kWarps) hit_kernel(HitArgs a) {
+    __shared__ alignas(128) double sm[2][kHitPlanes * kSBH];
     __shared__ alignas(8) uint64_t bar[2];
 
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t groups = (a.ntiles + kWarps - 1) / kWarps;
     const uint64_t item = blockIdx.x;
-    const uint64_t tl = item / a.n_chunks, ch = item - tl * a.n_chunks;
-    const Tile T = a.tiles[a.tile0 + tl];
+    const uint64_t grp = item / a.n_chunks, ch = item - grp * a.n_chunks;
+    const uint64_t tl = grp * kWarps + warp;
+    const bool has_tile = tl < a.ntiles;
+    const Tile T = a.tiles[a.tile0 + (has_tile ? tl : a.ntiles - 1)];
     const uint64_t o = T.obj - a.obj0;
     const uint64_t b0 = ch * kChunk, b1 = min(a.Bn, b0 + kChunk);
-    const uint64_t first_row = max(T.row0, a.row_lo);
-    const uint64_t pmin = (first_row - T.obj_row0) * a.Bn + b0;
-    if (*(volatile unsigned long long*)(a.objhit + o) < pmin) return;  // a lower pair already hit
+    (void)groups;
 
     // per-object AABB header vs B's AABB, expanded by tau
     const double* As = a.Astats + (uint64_t)T.obj * kObjStats;
@@ -94,22 +125,37 @@ __global__ void __launch_bounds__(kTile, 4) hit_kernel(HitArgs a) {
     const double tau = kCullDiag * sqrt(diag2) + kCullAbs * fmax(As[7], Bs[7]);
 #pragma unroll
     for (int k = 0; k < 3; ++k) apart |= (As[k] > Bs[3 + k] + tau) || (Bs[k] > As[3 + k] + tau);
-    if (apart) return;
 
-    const uint32_t r = min(threadIdx.x, T.count - 1);
-    const uint64_t row = T.row0 + r;
-    bool active = threadIdx.x < T.count && row >= a.row_lo && row < a.row_hi;
-    active = active && __ldg(a.Ap + (uint64_t)F_DEG * a.An_pad + row) == 0.0;
-    double av[9], an[3], ac;
+    // this lane's rows: lane, lane+32, lane+64, lane+96 of the warp's tile
+    double an[kRows][3], ac[kRows];
+    uint64_t rowv[kRows];
+    unsigned live = 0;  // bit r: row r still searching
 #pragma unroll
-    for (int k = 0; k < 9; ++k) av[k] = __ldg(a.Ap + (uint64_t)(F_V + k) * a.An_pad + row);
+    for (int r = 0; r < kRows; ++r) {
+        const uint32_t idx = lane + 32 * r;
+        const uint64_t row = T.row0 + min(idx, T.count - 1);
+        rowv[r] = row;
+        const bool ok = has_tile && !apart && idx < T.count && row >= a.row_lo && row < a.row_hi &&
+                        __ldg(a.Ap + (uint64_t)F_DEG * a.An_pad + row) == 0.0;
+        live |= ok ? 1u << r : 0u;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) an[k] = __ldg(a.Ap + (uint64_t)(F_N + k) * a.An_pad + row);
-    ac = __ldg(a.Ap + (uint64_t)F_C * a.An_pad + row);
-    const uint64_t i_loc = row - T.obj_row0;
-    bool done = !active;
+        for (int k = 0; k < 3; ++k) an[r][k] = __ldg(a.Ap + (uint64_t)(F_N + k) * a.An_pad + row);
+        ac[r] = __ldg(a.Ap + (uint64_t)F_C * a.An_pad + row);
+    }
+    const uint64_t Bn = a.Bn;
+    auto row_pmin = [&](int r, uint64_t f0) { return (rowv[r] - T.obj_row0) * Bn + f0; };
+    {  // a lower pair of this object already hit: nothing here can lower it
+        const unsigned long long h = *(volatile unsigned long long*)(a.objhit + o);
+        if (h != kNone) {
+#pragma unroll
+            for (int r = 0; r < kRows; ++r)
+                if (h < row_pmin(r, b0)) live &= ~(1u << r);
+        }
+    }
+    const bool cta_idle = __syncthreads_and(live == 0);
+    if (cta_idle) return;
 
-    const int nsub = (int)((b1 - b0 + kSB - 1) / kSB);
+    const int nsub = (int)((b1 - b0 + kSBH - 1) / kSBH);
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -118,13 +164,13 @@ __global__ void __launch_bounds__(kTile, 4) hit_kernel(HitArgs a) {
     __syncthreads();
     auto issue = [&](int s) {
         const int st = s & 1;
-        const uint64_t f0 = b0 + (uint64_t)s * kSB;
-        const int cnt = (int)min((uint64_t)kSB, b1 - f0);
+        const uint64_t f0 = b0 + (uint64_t)s * kSBH;
+        const int cnt = (int)min((uint64_t)kSBH, b1 - f0);
         const uint32_t bytes = (uint32_t)(((cnt + 1) & ~1) * sizeof(double));
         mbar_expect_tx(&bar[st], bytes * kHitPlanes);
 #pragma unroll 1
         for (int f = 0; f < kHitPlanes; ++f)
-            bulk_g2s(&sm[st][f * kSB], a.Bp + (uint64_t)kHitPlaneOf[f] * a.Bn_pad + f0, bytes, &bar[st]);
+            bulk_g2s(&sm[st][f * kSBH], a.Bp + (uint64_t)kHitPlaneOf[f] * a.Bn_pad + f0, bytes, &bar[st]);
     };
     if (threadIdx.x == 0) {
         issue(0);
@@ -135,34 +181,42 @@ __global__ void __launch_bounds__(kTile, 4) hit_kernel(HitArgs a) {
     for (int s = 0; s < nsub; ++s) {
         const int st = s & 1;
         mbar_wait(&bar[st], (uint32_t)((s >> 1) & 1));
-        const uint64_t f0 = b0 + (uint64_t)s * kSB;
-        const int cnt = (int)min((uint64_t)kSB, b1 - f0);
+        const uint64_t f0 = b0 + (uint64_t)s * kSBH;
+        const int cnt = (int)min((uint64_t)kSBH, b1 - f0);
         const double* sb = sm[st];
-        // stop rows whose smallest remaining pair cannot beat the object's hit
-        if (!done && *(volatile unsigned long long*)(a.objhit + o) < i_loc * a.Bn + f0) done = true;
-        if (!__syncthreads_and(done)) {
+        {
+            const unsigned long long h = *(volatile unsigned long long*)(a.objhit + o);
+            if (h != kNone) {
+#pragma unroll
+                for (int r = 0; r < kRows; ++r)
+                    if (h < row_pmin(r, f0)) live &= ~(1u << r);
+            }
+        }
+        if (__any_sync(0xffffffffu, live != 0)) {
 #pragma unroll 1
             for (int j = 0; j < cnt; ++j) {
-                if (sb[HS_DEG * kSB + j] != 0.0) continue;
-                if (done) continue;
-                const double* bv = sb + HS_V * kSB + j;
-                const double h0 = fma(an[0], bv[0], fma(an[1], bv[kSB], fma(an[2], bv[2 * kSB], -ac)));
-                const double h1 = fma(an[0], bv[3 * kSB], fma(an[1], bv[4 * kSB], fma(an[2], bv[5 * kSB], -ac)));
-                const double h2 = fma(an[0], bv[6 * kSB], fma(an[1], bv[7 * kSB], fma(an[2], bv[8 * kSB], -ac)));
-                if (separated(h0, h1, h2, tau)) continue;
-                const double bn0 = sb[(HS_N + 0) * kSB + j], bn1 = sb[(HS_N + 1) * kSB + j],
-                             bn2 = sb[(HS_N + 2) * kSB + j], bc = sb[HS_C * kSB + j];
-                const double g0 = fma(bn0, av[0], fma(bn1, av[1], fma(bn2, av[2], -bc)));
-                const double g1 = fma(bn0, av[3], fma(bn1, av[4], fma(bn2, av[5], -bc)));
-                const double g2 = fma(bn0, av[6], fma(bn1, av[7], fma(bn2, av[8], -bc)));
-                if (separated(g0, g1, g2, tau)) continue;
-                ++nex;
-                const exact::tri ta{{av[0], av[1], av[2]}, {av[3], av[4], av[5]}, {av[6], av[7], av[8]}};
-                const exact::tri tb{{bv[0], bv[kSB], bv[2 * kSB]}, {bv[3 * kSB], bv[4 * kSB], bv[5 * kSB]},
-                                    {bv[6 * kSB], bv[7 * kSB], bv[8 * kSB]}};
-                if (exact::tri_tri_hit(ta, tb)) {
-                    atomicMin(a.objhit + o, i_loc * a.Bn + f0 + j);
-                    done = true;  // later j of this row only give larger p
+                if (reinterpret_cast<const int*>(sb + HS_DEG * kSBH + j)[1] != 0) continue;  // uniform
+                const double* bv = sb + HS_V * kSBH + j;
+                const double x0 = bv[0], y0 = bv[kSBH], z0 = bv[2 * kSBH];
+                const double x1 = bv[3 * kSBH], y1 = bv[4 * kSBH], z1 = bv[5 * kSBH];
+                const double x2 = bv[6 * kSBH], y2 = bv[7 * kSBH], z2 = bv[8 * kSBH];
+                unsigned need = 0;
+#pragma unroll
+                for (int r = 0; r < kRows; ++r) {
+                    const double h0 = fma(an[r][0], x0, fma(an[r][1], y0, fma(an[r][2], z0, -ac[r])));
+                    const double h1 = fma(an[r][0], x1, fma(an[r][1], y1, fma(an[r][2], z1, -ac[r])));
+                    const double h2 = fma(an[r][0], x2, fma(an[r][1], y2, fma(an[r][2], z2, -ac[r])));
+                    need |= separated(h0, h1, h2, tau) ? 0u : 1u << r;
+                }
+                need &= live;
+                while (need) {  // rare: second plane + exact predicate
+                    const int r = __ffs(need) - 1;
+                    need &= need - 1;
+                    ++nex;
+                    if (slow_pair(a.Ap, a.An_pad, rowv[r], sb, j, tau)) {
+                        atomicMin(a.objhit + o, row_pmin(r, f0 + j));
+                        live &= ~(1u << r);  // later j of this row only give larger p
+                    }
                 }
             }
         }
@@ -178,7 +232,8 @@ void run_intersects(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit,
     const cudaStream_t st = cx.stream;
     const uint64_t nobj = sel.obj1 - sel.obj0;
     const uint64_t ntiles = sel.tile1 - sel.tile0;
-    const uint64_t n_items = ntiles * B.n_chunks;
+    const uint64_t groups = (ntiles + kWarps - 1) / kWarps;
+    const uint64_t n_items = groups * B.n_chunks;
     tdb_stats& S = *cx.stats;
     std::memset(&S, 0, sizeof S);
     for (uint64_t o = 0; o < nobj; ++o) {
@@ -201,9 +256,10 @@ void run_intersects(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit,
     CK(cudaEventCreate(&e1));
     CK(cudaEventCreate(&e2));
     CK(cudaEventRecord(e0, st));
-    hit_kernel<<<(unsigned)n_items, kTile, 0, st>>>(HitArgs{A.planes, A.n_pad, A.d_tiles, sel.tile0, sel.row_lo,
-                                                            sel.row_hi, B.planes, B.n_pad, B.n, B.n_chunks,
-                                                            sel.obj0, A.d_obj_stats, Bstats, objhit, nex});
+    hit_kernel<<<(unsigned)n_items, 32 * kWarps, 0, st>>>(HitArgs{A.planes, A.n_pad, A.d_tiles, sel.tile0, ntiles,
+                                                                  sel.row_lo, sel.row_hi, B.planes, B.n_pad, B.n,
+                                                                  B.n_chunks, sel.obj0, A.d_obj_stats, Bstats,
+                                                                  objhit, nex});
     CK(cudaGetLastError());
     CK(cudaEventRecord(e1, st));
     std::vector<unsigned long long> hp(nobj);
