@@ -1,30 +1,34 @@
 #!/usr/bin/env python
-"""Triangle-pair ST_3DDistance benchmark (BASELINE.json metric).
+"""Triangle-pair benchmark (BASELINE.json metric: triangle-pair tests/sec for
+3DDistance / 3DIntersects at 1/2/4/8 B200 vs the CPU reference).
 
-Workload (BASELINE.json configs[1]): synthetic terrain
-(1024 x 512 cells, 1,048,576 CCW-up triangles, z ~ U(-20,20), seed 42)
-against the reference ore body (make_ore_body, face target 1e6 ->
-1,310,720 triangles), ST_3DDistance over every triangle pair, FP64.
+Default workload (BASELINE.json configs[1]): a synthetic
+terrain (1024 x 512 cells, 1,048,576 CCW-up triangles, z ~ U(-20,20), seed 42)
+against the reference ore body (make_ore_body, face target 1e6 -> 1,310,720
+triangles); ST_3DDistance over every triangle pair, FP64.
 
-A step is one pass of the hot path over one batch of terrain rows
-(--batch-rows, default 65,536 rows x 1,310,720 ore faces = 8.6e10 pairs);
-16 batches are the whole 1M x 1M job, so the default --steps 16 times the
-full configuration. Under torchrun each rank takes its own batches (weak
-scaling); per-step results are combined with an NCCL all_gather of 16 B per
-rank (the lexicographic (distance, pair) min).
+A step is one pass of the hot path over one batch of A rows (default 65,536
+terrain rows x 1,310,720 ore faces = 8.6e10 pairs); 16 batches are the whole
+1M x 1M job, so the default --steps 16 times the full configuration. Under
+torchrun each rank takes its own batches (weak scaling); per-step answers are
+combined with an NCCL all_gather of 16 B per rank (the lexicographic
+(distance, pair) min).
 
-  value : pairs/s with both meshes resident in HBM (device events, max over
-          ranks)
-  e2e   : same metric through the one-shot C-ABI call with pinned host
-          buffers (tdb_distance_host: H2D of the step's meshes, prep, filter,
-          exact pass, D2H of the result inside the timed region)
-  roofline : the filter kernel (the roofline kernel) against the FP64 peak
-          measured in this run by a DFMA microbenchmark; algorithmic work
-          W_d = 975 FP64 flops per pair.
-  cpu_baseline : the reference's own primitives (oracle/_ref, the A17
-          composition) on this host's cores on a row sample.
+  value        pairs/s with the meshes resident in HBM (CUDA events on the
+               launch stream, max over ranks)
+  e2e          same metric through the one-shot C-ABI calls from pinned host
+               buffers (upload, prep, kernels, exact pass, D2H of the result
+               inside the timed region)
+  roofline     the roofline kernel (filter_kernel for distance, hit_kernel for
+               intersects) against the FP64 peak measured in this run by a
+               DFMA microbenchmark; algorithmic work W_d = 975 / W_i = 282
+               FP64 flops per pair
+  cpu_baseline the reference's own primitives (oracle/_ref: the A17
+               composition over kernels.cpp) on this host's cores, on a sample
 
---impl reference times only that CPU reference (rank 0) on the same metric.
+Other configurations (--config c1|c3|c4|c5) print the same
+line for their workload. --impl reference times only the CPU reference
+(rank 0) on the selected configuration.
 """
 from __future__ import annotations
 
@@ -42,13 +46,13 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-W_D = 975.0          # algorithmic FP64 flops per triangle pair
-W_REF = 2838.0       # reference-composition flops per pair (op-counted)
-FILTER_DP_INSTR = 318  # FP64-pipe instructions per pair in filter_kernel (cuobjdump -sass count)
-FILTER_FLOPS = 492     # executed FP64 flops per pair (174 DFMA x 2 + 93 DMUL + 51 DADD)
 METRIC = "triangle-pair tests/sec (3DDistance, 3DIntersects) at 1/2/4/8 B200 vs CPU ref"
 UNIT = "pairs/s"
-WORKLOAD = "C2: terrain 1,048,576 tris vs orebody 1,310,720 tris, ST_3DDistance (FP64, all pairs)"
+W_D = 975.0            # algorithmic FP64 flops per pair, distance
+W_I = 282.0            # algorithmic FP64 flops per pair, intersects no-hit
+FILTER_DP_INSTR = 304  # FP64-pipe instructions per pair in filter_kernel (cuobjdump -sass count)
+FILTER_FLOPS = 478     # executed FP64 flops per pair (174 DFMA x 2 + 79 DMUL + 51 DADD)
+U64_MAX = (1 << 64) - 1
 
 
 def env_int(k, d):
@@ -58,13 +62,186 @@ def env_int(k, d):
         return d
 
 
-def make_meshes():
-    import paper_1808_09571_b200 as T
-    ter = T.terrain(1024, 512, 20.0, 42)
-    ore = T.ore_body(1_000_000)
-    return ter, ore
+# --------------------------------------------------------------------------
+# workloads
+# --------------------------------------------------------------------------
+class MeshWorkload:
+    """A x B mesh workload; a step is a batch of A rows against all of B."""
+
+    table = False
+
+    def __init__(self, name, op, desc, make, batch_rows):
+        self.name, self.op, self.desc, self._make, self.batch_rows = name, op, desc, make, batch_rows
+
+    def build(self, T, ref=False):
+        self.A, self.B = self._make(T, ref)
+        self.NA, self.M = len(self.A), len(self.B)
+        self.BR = min(self.batch_rows, self.NA)
+        self.n_batches = (self.NA + self.BR - 1) // self.BR
+
+    def batch(self, b):
+        b %= self.n_batches
+        return b * self.BR, min(self.NA, (b + 1) * self.BR)
+
+    def pairs(self, b):
+        r0, r1 = self.batch(b)
+        return (r1 - r0) * self.M
+
+    def upload(self, T):
+        self.dA, self.dB = T.Mesh(self.A), T.Mesh(self.B)
+
+    def run(self, T, b):
+        r0, r1 = self.batch(b)
+        if self.op == "distance":
+            r = T.mesh_mesh_distance(self.dA, self.dB, rows=(r0, r1))
+            return (r.distance, r.pair_index if r.pair_index is not None else U64_MAX)
+        h = T.mesh_mesh_intersects(self.dA, self.dB, rows=(r0, r1))
+        return (0.0 if h.hit else float("inf"), h.pair_index if h.hit else U64_MAX)
+
+    def run_host(self, T, pinA, pinB, b):
+        r0, r1 = self.batch(b)
+        if self.op == "distance":
+            r = T.distance_host(pinA[r0:r1], pinB)
+            res = (r.distance, r.pair_index)
+        else:
+            h = T.intersects_host(pinA[r0:r1], pinB)
+            res = (h.hit, h.pair_index)
+        return res, (r1 - r0 + self.M) * 72, 96
+
+    def cpu_rate(self, rows, threads):
+        import oracle as O
+        rows = min(rows, self.NA)
+        stride = max(1, self.NA // rows)
+        kind = "reference" if O.REF is not None else "port"
+        t0 = time.perf_counter()
+        if self.op == "distance":
+            f = O.ref_mesh_mesh_distance if O.REF is not None else O.mesh_mesh_distance
+        else:
+            f = O.ref_mesh_mesh_intersects if O.REF is not None else O.mesh_mesh_intersects
+        f(self.A, self.B, threads=threads, rows=(0, stride * rows, stride))
+        dt = time.perf_counter() - t0
+        return rows * self.M / dt, dt, kind, f"{rows} strided A rows x {self.M} B faces ({rows * self.M:.3g} pairs)"
+
+    def cpu_default_rows(self, threads):
+        per_row = self.M / (1.0e6 if self.op == "distance" else 6.0e6)  # s per row on one core
+        return max(threads, int(10.0 * threads / max(per_row, 1e-6)))
 
 
+class TableWorkload:
+    """C4: a table of small objects (records) x one query mesh; a step is a
+    batch of records, each record getting its own distance (run_batch)."""
+
+    table = True
+
+    def __init__(self, n_objects, batch_objects, op):
+        self.name, self.op = "c4", op
+        self.n_objects, self.batch_objects = n_objects, batch_objects
+        self.desc = (f"C4: query orebody 81,920 tris vs table of {n_objects:,} objects x 1,280 tris "
+                     f"(unit_sphere(1000) x U[2,10] + U(box)), per-record ST_3D{'Distance' if op == 'distance' else 'Intersects'}")
+
+    def build(self, T, ref=False):
+        import oracle as O
+        self.Q = O.ref_ore_body(100_000) if (ref and O.REF is not None) else T.ore_body(100_000)
+        base = T.unit_sphere(1000)
+        rng = np.random.default_rng(42)
+        scale = rng.uniform(2.0, 10.0, self.n_objects)
+        ctr = np.stack([rng.uniform(0, 1000, self.n_objects), rng.uniform(0, 1000, self.n_objects),
+                        rng.uniform(-400, 0, self.n_objects)], 1)
+        self.nf = len(base)
+        tab = np.empty((self.n_objects, self.nf, 9))
+        for c in range(3):
+            tab[:, :, c::3] = base[None, :, c::3] * scale[:, None, None] + ctr[:, None, c, None]
+        self.tab = tab.reshape(-1, 9)
+        self.M = len(self.Q)
+        self.n_batches = (self.n_objects + self.batch_objects - 1) // self.batch_objects
+        self.NA = len(self.tab)
+
+    def objs(self, b):
+        b %= self.n_batches
+        return b * self.batch_objects, min(self.n_objects, (b + 1) * self.batch_objects)
+
+    def pairs(self, b):
+        o0, o1 = self.objs(b)
+        return (o1 - o0) * self.nf * self.M
+
+    def upload(self, T):
+        off = np.arange(self.n_objects + 1, dtype=np.uint64) * self.nf
+        self.dT, self.dQ = T.Table(self.tab, off), T.Mesh(self.Q)
+
+    def run(self, T, b):
+        op = T.OP_DISTANCE if self.op == "distance" else T.OP_INTERSECTS
+        v, p = T.table_eval(op, self.dT, self.dQ, objects=self.objs(b))
+        return (float(np.min(v)) if self.op == "distance" else float(np.any(v)), int(p.min()) if len(p) else U64_MAX)
+
+    def run_host(self, T, pinT, pinQ, b):
+        o0, o1 = self.objs(b)
+        off = np.arange(o1 - o0 + 1, dtype=np.uint64) * self.nf
+        t = T.Table(pinT[o0 * self.nf:o1 * self.nf], off)
+        q = T.Mesh(pinQ)
+        op = T.OP_DISTANCE if self.op == "distance" else T.OP_INTERSECTS
+        v, p = T.table_eval(op, t, q)
+        t.free()
+        q.free()
+        return (v, p), ((o1 - o0) * self.nf + self.M) * 72, (o1 - o0) * 16
+
+    def cpu_rate(self, rows, threads):
+        import oracle as O
+        kind = "reference" if O.REF is not None else "port"
+        f = O.ref_mesh_mesh_distance if O.REF is not None else O.mesh_mesh_distance
+        objs = max(1, rows)
+        t0 = time.perf_counter()
+        for o in range(objs):
+            f(self.tab[o * self.nf:(o + 1) * self.nf], self.Q, threads=threads)
+        dt = time.perf_counter() - t0
+        return objs * self.nf * self.M / dt, dt, kind, f"{objs} records x {self.nf} faces x {self.M} query faces"
+
+    def cpu_default_rows(self, threads):
+        return max(1, int(10.0 * threads * 1e6 / (self.nf * self.M)))
+
+
+def workload(name, op_override, objects):
+    def c1(T, ref):
+        import oracle as O
+        a = O.ref_unit_sphere(10000) if (ref and O.REF is not None) else T.unit_sphere(10000)
+        return a, T.translate(a, 2.5 if op_override != "intersects" else 0.5, 0, 0)
+
+    def c2(T, ref):
+        import oracle as O
+        ore = O.ref_ore_body(1_000_000) if (ref and O.REF is not None) else T.ore_body(1_000_000)
+        return T.terrain(1024, 512, 20.0, 42), ore
+
+    def c3(T, ref):
+        import oracle as O
+        a = O.ref_unit_sphere(1_000_000) if (ref and O.REF is not None) else T.unit_sphere(1_000_000)
+        return a, a * 0.9
+
+    def c5(T, ref):
+        import oracle as O
+        a = O.ref_unit_sphere(10_000_000) if (ref and O.REF is not None) else T.unit_sphere(10_000_000)
+        return a, T.translate(a, 2.5, 0, 0)
+
+    if name == "c1":
+        op = op_override or "distance"
+        return MeshWorkload("c1", op, f"C1: two 8,192-tri spheres ({'offset 2.5' if op == 'distance' else 'shift 0.5'}), "
+                            f"ST_3D{'Distance' if op == 'distance' else 'Intersects'}", c1, 8192)
+    if name == "c2":
+        op = op_override or "distance"
+        return MeshWorkload("c2", op, "C2: terrain 1,048,576 tris vs orebody 1,310,720 tris, "
+                            f"ST_3D{'Distance' if op == 'distance' else 'Intersects'} (FP64, all pairs)", c2, 65536)
+    if name == "c3":
+        op = op_override or "intersects"
+        return MeshWorkload("c3", op, "C3: 1,310,720-tri sphere vs 0.9x copy (overlapping AABBs, no hit: "
+                            f"worst case), ST_3D{'Intersects' if op == 'intersects' else 'Distance'}", c3,
+                            131072 if op == "intersects" else 65536)
+    if name == "c4":
+        return TableWorkload(objects, 1000, op_override or "distance")
+    if name == "c5":
+        op = op_override or "distance"
+        return MeshWorkload("c5", op, "C5: 8,388,608-tri spheres offset 2.5, ST_3DDistance", c5, 65536)
+    raise SystemExit(f"unknown config {name}")
+
+
+# --------------------------------------------------------------------------
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -73,9 +250,7 @@ class ClockSampler:
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
-        self.index = index
-        self.proc = None
-        self.lines = []
+        self.index, self.proc, self.lines = index, None, []
 
     def start(self):
         try:
@@ -121,49 +296,38 @@ class ClockSampler:
                 "power_w_max": max(power), "samples": len(sm)}
 
 
-def cpu_reference_rate(ter, ore, rows, threads):
-    """The reference's primitives (oracle/_ref) on `rows` strided terrain rows
-    x all ore faces; falls back to the C restatement if _ref is absent."""
-    import oracle as O
-    n = len(ter)
-    stride = max(1, n // rows)
-    kind = "reference" if O.REF is not None else "port"
-    t0 = time.perf_counter()
-    if O.REF is not None:
-        r = O.ref_mesh_mesh_distance(ter, ore, threads=threads, rows=(0, stride * rows, stride))
-    else:
-        r = O.mesh_mesh_distance(ter, ore, threads=threads, rows=(0, stride * rows, stride))
-    dt = time.perf_counter() - t0
-    return rows * len(ore) / dt, dt, kind, r
+def base_line(args, wl, world, value, ms):
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+    }
 
 
-def run_reference(args, rank, world):
+def run_reference(args, wl, rank, world):
     """--impl reference: the reference CPU path on the host cores (rank 0)."""
     if rank != 0:
         return
-    import oracle as O
     import paper_1808_09571_b200 as T
-    ter = T.terrain(1024, 512, 20.0, 42)   # new generator (no reference terrain)
-    ore = O.ref_ore_body(1_000_000) if O.REF is not None else T.ore_body(1_000_000)
+    wl.build(T, ref=True)
     threads = os.cpu_count() or 1
-    rows = max(1, args.ref_rows or threads)
+    rows = max(1, args.ref_rows or max(1, wl.cpu_default_rows(threads) // 8))
     for _ in range(args.warmup):
-        cpu_reference_rate(ter, ore, rows, threads)
-    total_pairs, total_t, kind = 0, 0.0, "reference"
+        wl.cpu_rate(rows, threads)
+    total_pairs, total_t, kind, sample = 0.0, 0.0, "reference", ""
     for _ in range(args.steps):
-        rate, dt, kind, _ = cpu_reference_rate(ter, ore, rows, threads)
-        total_pairs += rows * len(ore)
+        rate, dt, kind, sample = wl.cpu_rate(rows, threads)
+        total_pairs += rate * dt
         total_t += dt
     value = total_pairs / total_t
-    sample = f"{rows} strided terrain rows x {len(ore)} ore faces per step"
-    out = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_t / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": WORKLOAD, "parallelism": f"cpu{threads}"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+    out = base_line(args, wl, world, value, 1e3 * total_t)
+    out.update({
+        "impl": "reference",
+        "config": {"workload": wl.desc, "op": wl.op, "parallelism": f"cpu{threads}"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": sample + " per step"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
+    })
     print(json.dumps(out), flush=True)
 
 
@@ -173,27 +337,36 @@ def main():
     ap.add_argument("--steps", type=int, default=16)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch-rows", type=int, default=65536)
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--op", default=None, choices=[None, "distance", "intersects"])
+    ap.add_argument("--batch-rows", type=int, default=0, help="A rows per step (0 = config default)")
+    ap.add_argument("--objects", type=int, default=100_000, help="c4 table records")
     ap.add_argument("--e2e-steps", type=int, default=None)
-    ap.add_argument("--cpu-rows", type=int, default=0, help="rows for cpu_baseline (0 = auto)")
+    ap.add_argument("--cpu-rows", type=int, default=0, help="cpu_baseline sample rows (0 = ~10 s)")
     ap.add_argument("--ref-rows", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--mode", default="full", choices=["full", "cull"])
     args = ap.parse_args()
     assert args.warmup >= 0 and args.steps >= 1
 
+    wl = workload(args.config, args.op, args.objects)
+    if args.batch_rows and not wl.table:
+        wl.batch_rows = args.batch_rows
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
-        return run_reference(args, rank, world)
+        return run_reference(args, wl, rank, world)
 
     import torch
     import torch.distributed as dist
 
     import paper_1808_09571_b200 as T
+    from paper_1808_09571_b200 import shard
 
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     T.init(local)
+    T.set_mode(T.MODE_CULL if args.mode == "cull" else T.MODE_FULL)
     stream = torch.cuda.current_stream()
     T.set_stream(stream.cuda_stream)
 
@@ -209,38 +382,24 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    from paper_1808_09571_b200 import shard
-
-    def combine(d, p):
-        """Lexicographic (distance, pair) min over ranks: NCCL all_gather."""
-        return shard.combine_min(d, p, device="cuda")
-
     fp64_tf, _ = T.fp64_peak()
-    ter, ore = make_meshes()
-    NA, M = len(ter), len(ore)
-    BR = min(args.batch_rows, NA)
-    n_batches = (NA + BR - 1) // BR
-    A, B = T.Mesh(ter), T.Mesh(ore)
+    wl.build(T)
+    wl.upload(T)
 
-    def batch_rows(s):
-        b = (s * world + rank) % n_batches
-        return b * BR, min(NA, (b + 1) * BR)
-
-    results = []
-    filt_ms, filt_pairs, kernels = [], [], 0
+    results, k_ms, k_pairs, kernels = [], [], [], 0
 
     def step(s, record=True):
         nonlocal kernels
-        r0, r1 = batch_rows(s)
-        r = T.mesh_mesh_distance(A, B, rows=(r0, r1))
+        b = s * world + rank
+        d, p = wl.run(T, b)
         st = T.last_stats()
-        d, p = combine(r.distance, r.pair_index if r.pair_index is not None else (1 << 64) - 1)
+        d, p = shard.combine_min(d, p, device="cuda")  # NCCL all_gather, 16 B per rank
         if record:
-            results.append((r0, r1, d, p))
-            filt_ms.append(st["ms_filter"])
-            filt_pairs.append(st["pairs"])
+            results.append((d, p))
+            k_ms.append(st["ms_filter"])
+            k_pairs.append(st["pairs"])
             kernels += st["kernels"]
-        return (r1 - r0) * M
+        return wl.pairs(b)
 
     for s in range(args.warmup):
         step(s, record=False)
@@ -256,72 +415,74 @@ def main():
     barrier()
     clk = clocks.stop()
     ms = max_over_ranks(e0.elapsed_time(e1))
-    pairs_total = pairs_rank * world
+    pairs_total = max_over_ranks(float(pairs_rank)) * world
     value = pairs_total / (ms * 1e-3)
 
-    # ---- e2e: one-shot C-ABI call from pinned host buffers -----------------
+    # ---- e2e: one-shot C-ABI calls from pinned host buffers -----------------
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else args.steps
-    pin_a = torch.from_numpy(ter).pin_memory()
-    pin_b = torch.from_numpy(ore).pin_memory()
-    na_pin, nb_pin = pin_a.numpy(), pin_b.numpy()
-    h2d = 0
+    if wl.table:
+        pinA, pinB = torch.from_numpy(wl.tab).pin_memory().numpy(), torch.from_numpy(wl.Q).pin_memory().numpy()
+    else:
+        pinA, pinB = torch.from_numpy(wl.A).pin_memory().numpy(), torch.from_numpy(wl.B).pin_memory().numpy()
+    h2d = d2h = 0
+    e2e_pairs = 0
     barrier()
     t0 = time.perf_counter()
-    e2 = torch.cuda.Event(enable_timing=True)
-    e3 = torch.cuda.Event(enable_timing=True)
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
-    e2e_pairs = 0
     for s in range(e2e_steps):
-        r0, r1 = batch_rows(args.warmup + s)
-        r = T.distance_host(na_pin[r0:r1], nb_pin)
-        h2d += (r1 - r0 + M) * 72
-        e2e_pairs += (r1 - r0) * M
+        b = (args.warmup + s) * world + rank
+        _, hb, db = wl.run_host(T, pinA, pinB, b)
+        h2d += hb
+        d2h += db
+        e2e_pairs += wl.pairs(b)
     e3.record(stream)
     barrier()
     wall_e2e = time.perf_counter() - t0
     ms_e2e = max_over_ranks(max(e2.elapsed_time(e3), wall_e2e * 1e3))
-    e2e_value = e2e_pairs * world / (ms_e2e * 1e-3)
+    e2e_value = max_over_ranks(float(e2e_pairs)) * world / (ms_e2e * 1e-3)
 
-    # ---- roofline of the filter kernel --------------------------------------
-    f_ms = sum(filt_ms) / len(filt_ms)
-    f_pairs = sum(filt_pairs) / len(filt_pairs)
-    achieved_tf = W_D * f_pairs / (f_ms * 1e-3) / 1e12
+    # ---- roofline of the roofline kernel -------------------------------------
+    f_ms = sum(k_ms) / len(k_ms)
+    f_pairs = sum(k_pairs) / len(k_pairs)
+    w = W_D if wl.op == "distance" else W_I
+    achieved_tf = w * f_pairs / (f_ms * 1e-3) / 1e12
     roofline = {
         "bound": "fp64", "achieved": achieved_tf, "peak": fp64_tf, "unit": "TFLOP/s",
         "frac": achieved_tf / fp64_tf, "traffic": None,
-        "kernel": "filter_kernel (fast_pair.cuh)",
-        "work_per_pair_flops": W_D,
+        "kernel": "filter_kernel (fast_pair.cuh)" if wl.op == "distance" else "hit_kernel (intersects.cu)",
+        "work_per_pair_flops": w,
         "peak_source": "measured in this run: DFMA issue-rate microbenchmark (tdb_fp64_peak); "
                        "spec 148 SM x 64 FMA x 2 x 1.965 GHz = 37.2",
-        "fp64_pipe_frac": FILTER_DP_INSTR * f_pairs / (f_ms * 1e-3) / (fp64_tf * 1e12 / 2),
-        "executed_fp64_tflops": FILTER_FLOPS * f_pairs / (f_ms * 1e-3) / 1e12,
-        "filter_share_of_step": sum(filt_ms) / ms if world == 1 else None,
+        "kernel_share_of_step": sum(k_ms) / ms if world == 1 else None,
     }
+    if wl.op == "distance":
+        roofline["fp64_pipe_frac"] = FILTER_DP_INSTR * f_pairs / (f_ms * 1e-3) / (fp64_tf * 1e12 / 2)
+        roofline["executed_fp64_tflops"] = FILTER_FLOPS * f_pairs / (f_ms * 1e-3) / 1e12
+    else:
+        roofline["note"] = ("culled pairs skip the W_i work (conservative separating-plane test, "
+                            "DESIGN.md 4.3): frac > 1 is algorithmic, not hardware")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        rows = args.cpu_rows or 8 * threads
-        rate, dt, kind, _ = cpu_reference_rate(ter, ore, rows, threads)
-        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind,
-               "sample": f"{rows} strided terrain rows x {M} ore faces ({rows * M:.3g} pairs, {dt:.1f} s)"}
+        rows = args.cpu_rows or wl.cpu_default_rows(threads)
+        rate, dt, kind, sample = wl.cpu_rate(rows, threads)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind, "sample": f"{sample}, {dt:.1f} s"}
 
     if rank == 0:
-        best = min(((d, p) for (_, _, d, p) in results), default=(None, None))
-        out = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "batch_rows": BR, "pairs_per_step": BR * M * world,
-                       "batches_per_job": n_batches, "parallelism": f"rows{world}",
-                       "l2": "inputs larger than L2 (B store 377 MB of SoA planes)",
-                       "op": "ST_3DDistance"},
+        best = min(results) if results else (None, None)
+        out = base_line(args, wl, world, value, ms)
+        out.update({
+            "config": {"workload": wl.desc, "op": wl.op, "mode": args.mode,
+                       "pairs_per_step": wl.pairs(0) * world, "steps_per_job": wl.n_batches,
+                       "parallelism": f"rows{world}",
+                       "l2": "inputs larger than L2 (B / table stores of 288 B per face in HBM)"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d // max(1, e2e_steps),
-                    "d2h_bytes_per_step": 96, "steps": e2e_steps},
-            "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
-            "gpu_launches": kernels,
-            "result": {"min_distance_seen": best[0], "pair": best[1]},
-        }
+                    "d2h_bytes_per_step": d2h // max(1, e2e_steps), "steps": e2e_steps},
+            "roofline": roofline, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": kernels,
+            "result": {"best_value_seen": best[0], "pair": best[1]},
+        })
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
