@@ -40,7 +40,7 @@ struct DistArgs {
     const Tile* tiles;
     uint64_t tile0, row_lo, row_hi;
     const double* Bp;
-    uint64_t Bn_pad, Bn, n_chunks;
+    uint64_t Bn_pad, Bn, n_chunks, chunk;
     uint64_t obj0;
     double* itemmin;
     unsigned long long* objmin;
@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kTile, TDB_FILTER_MINB) filter_kernel(DistArgs
     load_aface(A, FaceRefLdg{a.Ap + row, a.An_pad});
     active = active && __ldg(a.Ap + (uint64_t)F_DEG * a.An_pad + row) == 0.0;
 
-    const uint64_t b0 = ch * kChunk, b1 = min(a.Bn, b0 + kChunk);
+    const uint64_t b0 = ch * a.chunk, b1 = min(a.Bn, b0 + a.chunk);
     const int nsub = (int)((b1 - b0 + kSB - 1) / kSB);
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(kTile) verify_kernel(VerifyArgs v) {
         active = active && __ldg(a.Ap + (uint64_t)F_DEG * a.An_pad + row) == 0.0;
         AFace A;
         load_aface(A, FaceRefLdg{a.Ap + row, a.An_pad});
-        const uint64_t c0 = ch * kChunk, c1 = min(a.Bn, c0 + kChunk);
+        const uint64_t c0 = ch * a.chunk, c1 = min(a.Bn, c0 + a.chunk);
         const uint64_t len = (c1 - c0 + v.nsplit - 1) / v.nsplit;
         const uint64_t b0 = c0 + part * len, b1 = min(c1, b0 + len);
         const uint64_t o = T.obj - a.obj0;
@@ -295,7 +295,9 @@ void run_distance(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, u
     const cudaStream_t st = cx.stream;
     const uint64_t nobj = sel.obj1 - sel.obj0;
     const uint64_t ntiles = sel.tile1 - sel.tile0;
-    const uint64_t n_items = ntiles * B.n_chunks;
+    const uint64_t chunk = pick_chunk(ntiles, B.n, cx.sms, 12);
+    const uint64_t n_chunks = (B.n + chunk - 1) / chunk;
+    const uint64_t n_items = ntiles * n_chunks;
     for (uint64_t o = 0; o < nobj; ++o) {
         dist[o] = pos_inf_h();
         pair[o] = kNone;
@@ -324,7 +326,7 @@ void run_distance(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, u
 
     EventPair ev;
     DistArgs da{A.planes, A.n_pad, A.d_tiles, sel.tile0, sel.row_lo, sel.row_hi, B.planes, B.n_pad, B.n,
-                B.n_chunks, sel.obj0, itemmin, objmin};
+                n_chunks, chunk, sel.obj0, itemmin, objmin};
     CK(cudaEventRecord(ev.e[0], st));
     filter_kernel<<<(unsigned)n_items, kTile, 0, st>>>(da);
     CK(cudaGetLastError());
@@ -346,7 +348,7 @@ void run_distance(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, u
         CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));          // flagged count
         CK(cudaMemsetAsync(ctr + 2, 0, sizeof(unsigned long long), st));      // retry count
         flag_kernel<<<(unsigned)((n_items + 255) / 256), 256, 0, st>>>(
-            FlagArgs{A.d_tiles, sel.tile0, B.n_chunks, n_items, sel.obj0, itemmin, band2, list, ctr});
+            FlagArgs{A.d_tiles, sel.tile0, n_chunks, n_items, sel.obj0, itemmin, band2, list, ctr});
         CK(cudaGetLastError());
         for (int pass = 1; pass <= 2; ++pass) {
             verify_kernel<<<vgrid, kTile, 0, st>>>(VerifyArgs{da, list, ctr, nsplit, pass, band2, objD, objP, ctr + 1});

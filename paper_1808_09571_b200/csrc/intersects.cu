@@ -54,7 +54,7 @@ struct HitArgs {
     const Tile* tiles;
     uint64_t tile0, ntiles, row_lo, row_hi;
     const double* Bp;
-    uint64_t Bn_pad, Bn, n_chunks;
+    uint64_t Bn_pad, Bn, n_chunks, chunk;
     uint64_t obj0;
     const double* Astats;
     const double* Bstats;
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(32 * kWarps) hit_kernel(HitArgs a) {
     const bool has_tile = tl < a.ntiles;
     const Tile T = a.tiles[a.tile0 + (has_tile ? tl : a.ntiles - 1)];
     const uint64_t o = T.obj - a.obj0;
-    const uint64_t b0 = ch * kChunk, b1 = min(a.Bn, b0 + kChunk);
+    const uint64_t b0 = ch * a.chunk, b1 = min(a.Bn, b0 + a.chunk);
     (void)groups;
 
     // per-object AABB header vs B's AABB, expanded by tau
@@ -233,7 +233,9 @@ void run_intersects(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit,
     const uint64_t nobj = sel.obj1 - sel.obj0;
     const uint64_t ntiles = sel.tile1 - sel.tile0;
     const uint64_t groups = (ntiles + kWarps - 1) / kWarps;
-    const uint64_t n_items = groups * B.n_chunks;
+    const uint64_t chunk = pick_chunk(groups, B.n, cx.sms, 12);
+    const uint64_t n_chunks = (B.n + chunk - 1) / chunk;
+    const uint64_t n_items = groups * n_chunks;
     tdb_stats& S = *cx.stats;
     std::memset(&S, 0, sizeof S);
     for (uint64_t o = 0; o < nobj; ++o) {
@@ -258,7 +260,7 @@ void run_intersects(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit,
     CK(cudaEventRecord(e0, st));
     hit_kernel<<<(unsigned)n_items, 32 * kWarps, 0, st>>>(HitArgs{A.planes, A.n_pad, A.d_tiles, sel.tile0, ntiles,
                                                                   sel.row_lo, sel.row_hi, B.planes, B.n_pad, B.n,
-                                                                  B.n_chunks, sel.obj0, A.d_obj_stats, Bstats,
+                                                                  n_chunks, chunk, sel.obj0, A.d_obj_stats, Bstats,
                                                                   objhit, nex});
     CK(cudaGetLastError());
     CK(cudaEventRecord(e1, st));

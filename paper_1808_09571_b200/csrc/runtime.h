@@ -62,6 +62,17 @@ struct ASel {
     uint64_t tile0, tile1, row_lo, row_hi, obj0, obj1;
 };
 
+// B-chunk length (faces per work item) for a launch of `a_units` A-side
+// CTA units against nB faces: kChunk, halved (down to 256, a multiple of the
+// TMA sub-tiles) until there are >= `waves` CTAs per SM, so small problems
+// still fill all SMs.
+inline uint64_t pick_chunk(uint64_t a_units, uint64_t nB, int sms, int waves) {
+    uint64_t chunk = kChunk;
+    const uint64_t target = (uint64_t)sms * (uint64_t)waves;
+    while (chunk > 256 && a_units * ((nB + chunk - 1) / chunk) < target) chunk >>= 1;
+    return chunk;
+}
+
 // Distance over an A selection against mesh B. Outputs per object (host):
 // dist (+inf when none), pair (UINT64_MAX when none); for a single object
 // also the witness (on_a, on_b).
