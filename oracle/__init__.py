@@ -68,6 +68,9 @@ def _load_c():
                                         ct.POINTER(OrMeshDist)]
     L.or_mesh_mesh_intersects.argtypes = [_D, ct.c_uint64, _D, ct.c_uint64, ct.c_uint64,
                                           ct.c_uint64, ct.c_uint64, ct.c_int, _U64]
+    L.or_mesh_mesh_distance_pruned.argtypes = [_D, ct.c_uint64, _D, ct.c_uint64, ct.c_double, ct.c_int,
+                                               ct.POINTER(OrMeshDist)]
+    L.or_mesh_mesh_intersects_pruned.argtypes = [_D, ct.c_uint64, _D, ct.c_uint64, ct.c_int, _U64]
     L.or_table_distance.argtypes = [_D, _U64, ct.c_uint64, _D, ct.c_uint64, ct.c_int, _D, _U64]
     L.or_table_intersects.argtypes = [_D, _U64, ct.c_uint64, _D, ct.c_uint64, ct.c_int, _U8,
                                       _U64]
@@ -145,6 +148,25 @@ def mesh_mesh_intersects(a, b, threads=None, rows=None):
     p = ct.c_uint64(0)
     C.or_mesh_mesh_intersects(_dp(a), len(a), _dp(b), len(b), r0, r1, rs,
                               threads or os.cpu_count() or 1, ct.byref(p))
+    return p.value != U64_MAX, p.value
+
+
+def mesh_mesh_distance_pruned(a, b, ub, threads=None):
+    """Exact (dist, pair, found, on_a, on_b) among pairs with distance <= ub
+    (the full answer whenever ub >= the true minimum), AABB-pruned."""
+    a, b = _f64(a).reshape(-1, 9), _f64(b).reshape(-1, 9)
+    o = OrMeshDist()
+    C.or_mesh_mesh_distance_pruned(_dp(a), len(a), _dp(b), len(b), float(ub),
+                                   threads or os.cpu_count() or 1, ct.byref(o))
+    return o.d, o.pair, bool(o.found), np.array(o.on_a[:]), np.array(o.on_b[:])
+
+
+def mesh_mesh_intersects_pruned(a, b, threads=None):
+    """Exact (hit, lowest hit pair), AABB-pruned."""
+    a, b = _f64(a).reshape(-1, 9), _f64(b).reshape(-1, 9)
+    p = ct.c_uint64(0)
+    C.or_mesh_mesh_intersects_pruned(_dp(a), len(a), _dp(b), len(b), threads or os.cpu_count() or 1,
+                                     ct.byref(p))
     return p.value != U64_MAX, p.value
 
 

@@ -506,3 +506,216 @@ void or_table_intersects(const double* table9, const uint64_t* offsets, uint64_t
                          uint64_t* pair) {
     table_run(1, table9, offsets, n_objects, query9, mq, threads, NULL, hit, pair);
 }
+
+/* ---- pruned exact oracles (full-size parity) -------- */
+typedef struct {
+    double lo[3], hi[3];
+} box_t;
+
+static box_t face_box(const double* t) {
+    box_t b;
+    for (int k = 0; k < 3; ++k) {
+        b.lo[k] = fmin(t[k], fmin(t[3 + k], t[6 + k]));
+        b.hi[k] = fmax(t[k], fmax(t[3 + k], t[6 + k]));
+    }
+    return b;
+}
+
+static double box_dist2(const box_t* a, const box_t* b) {
+    double s = 0.0;
+    for (int k = 0; k < 3; ++k) {
+        double g = fmax(0.0, fmax(a->lo[k] - b->hi[k], b->lo[k] - a->hi[k]));
+        s += g * g;
+    }
+    return s;
+}
+
+/* Faces binned by centroid into a uniform grid of ~n/cap cells; CSR order. */
+typedef struct {
+    uint64_t ncell;
+    uint64_t* start; /* ncell + 1 */
+    uint64_t* face;  /* n, face ids grouped by cell (ascending within a cell) */
+    box_t* cbox;     /* tight box of each cell's faces */
+    box_t* fbox;     /* per face */
+} grid_t;
+
+static void grid_build(const double* t9, uint64_t n, grid_t* g) {
+    g->fbox = (box_t*)malloc(sizeof(box_t) * (n ? n : 1));
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (uint64_t i = 0; i < n; ++i) {
+        g->fbox[i] = face_box(t9 + 9 * i);
+        for (int k = 0; k < 3; ++k) {
+            lo[k] = fmin(lo[k], g->fbox[i].lo[k]);
+            hi[k] = fmax(hi[k], g->fbox[i].hi[k]);
+        }
+    }
+    double ext[3], vol = 1.0;
+    int dims = 0;
+    for (int k = 0; k < 3; ++k) {
+        ext[k] = n ? hi[k] - lo[k] : 0.0;
+        if (ext[k] > 0.0) vol *= ext[k], ++dims;
+    }
+    const double target = (double)(n / 64 + 1);
+    const double side = dims ? pow(vol / target, 1.0 / dims) : 1.0;
+    uint64_t d[3];
+    for (int k = 0; k < 3; ++k) {
+        d[k] = ext[k] > 0.0 && side > 0.0 ? (uint64_t)ceil(ext[k] / side) : 1;
+        if (d[k] < 1) d[k] = 1;
+        if (d[k] > 512) d[k] = 512;
+    }
+    g->ncell = d[0] * d[1] * d[2];
+    g->start = (uint64_t*)calloc(g->ncell + 1, sizeof(uint64_t));
+    uint64_t* cell = (uint64_t*)malloc(sizeof(uint64_t) * (n ? n : 1));
+    for (uint64_t i = 0; i < n; ++i) {
+        uint64_t c = 0;
+        for (int k = 2; k >= 0; --k) {
+            const double x = (t9[9 * i + k] + t9[9 * i + 3 + k] + t9[9 * i + 6 + k]) / 3.0;
+            int64_t q = ext[k] > 0.0 ? (int64_t)((x - lo[k]) / ext[k] * (double)d[k]) : 0;
+            if (q < 0) q = 0;
+            if (q >= (int64_t)d[k]) q = (int64_t)d[k] - 1;
+            c = c * d[k] + (uint64_t)q;
+        }
+        cell[i] = c;
+        g->start[c + 1]++;
+    }
+    for (uint64_t c = 0; c < g->ncell; ++c) g->start[c + 1] += g->start[c];
+    uint64_t* fill = (uint64_t*)malloc(sizeof(uint64_t) * (g->ncell + 1));
+    memcpy(fill, g->start, sizeof(uint64_t) * (g->ncell + 1));
+    g->face = (uint64_t*)malloc(sizeof(uint64_t) * (n ? n : 1));
+    for (uint64_t i = 0; i < n; ++i) g->face[fill[cell[i]]++] = i;
+    g->cbox = (box_t*)malloc(sizeof(box_t) * g->ncell);
+    for (uint64_t c = 0; c < g->ncell; ++c) {
+        box_t b = {{INFINITY, INFINITY, INFINITY}, {-INFINITY, -INFINITY, -INFINITY}};
+        for (uint64_t s = g->start[c]; s < g->start[c + 1]; ++s) {
+            const box_t* f = &g->fbox[g->face[s]];
+            for (int k = 0; k < 3; ++k) {
+                b.lo[k] = fmin(b.lo[k], f->lo[k]);
+                b.hi[k] = fmax(b.hi[k], f->hi[k]);
+            }
+        }
+        g->cbox[c] = b;
+    }
+    free(fill);
+    free(cell);
+}
+
+static void grid_free(grid_t* g) {
+    free(g->start);
+    free(g->face);
+    free(g->cbox);
+    free(g->fbox);
+}
+
+typedef struct {
+    const double *a9, *b9;
+    uint64_t m;
+    const grid_t *ga, *gb;
+    double thr2;
+    int op; /* 0 distance, 1 intersects */
+    atomic_uint_fast64_t next;
+    pthread_mutex_t mu;
+    double best_d;
+    uint64_t best_p;
+    res_t best_r;
+    int found;
+} pr_job;
+
+static void* pr_worker(void* arg) {
+    pr_job* J = (pr_job*)arg;
+    double bd = INFINITY;
+    uint64_t bp = UINT64_MAX;
+    res_t br;
+    int found = 0;
+    for (;;) {
+        const uint64_t ca = atomic_fetch_add(&J->next, 1);
+        if (ca >= J->ga->ncell) break;
+        if (J->ga->start[ca] == J->ga->start[ca + 1]) continue;
+        for (uint64_t cb = 0; cb < J->gb->ncell; ++cb) {
+            if (J->gb->start[cb] == J->gb->start[cb + 1]) continue;
+            if (box_dist2(&J->ga->cbox[ca], &J->gb->cbox[cb]) > J->thr2) continue;
+            for (uint64_t s = J->ga->start[ca]; s < J->ga->start[ca + 1]; ++s) {
+                const uint64_t i = J->ga->face[s];
+                const tri_t a = ld_tri(J->a9 + 9 * i);
+                for (uint64_t u = J->gb->start[cb]; u < J->gb->start[cb + 1]; ++u) {
+                    const uint64_t j = J->gb->face[u];
+                    if (box_dist2(&J->ga->fbox[i], &J->gb->fbox[j]) > J->thr2) continue;
+                    const uint64_t p = i * J->m + j;
+                    if (J->op == 1) {
+                        if (p < bp) {
+                            const tri_t b = ld_tri(J->b9 + 9 * j);
+                            if (tri_tri_hit(&a, &b)) bp = p, found = 1;
+                        }
+                        continue;
+                    }
+                    const tri_t b = ld_tri(J->b9 + 9 * j);
+                    const res_t r = tri_tri(&a, &b);
+                    if (r.d < bd || (r.d == bd && p < bp)) {
+                        bd = r.d, bp = p, br = r, found = 1;
+                    }
+                }
+            }
+        }
+    }
+    pthread_mutex_lock(&J->mu);
+    if (found) {
+        if (J->op == 1) {
+            if (!J->found || bp < J->best_p) J->best_p = bp;
+        } else if (!J->found || bd < J->best_d || (bd == J->best_d && bp < J->best_p)) {
+            J->best_d = bd, J->best_p = bp, J->best_r = br;
+        }
+        J->found = 1;
+    }
+    pthread_mutex_unlock(&J->mu);
+    return NULL;
+}
+
+static double scale_of(const grid_t* g) {
+    double s = 0.0;
+    for (uint64_t c = 0; c < g->ncell; ++c)
+        for (int k = 0; k < 3; ++k)
+            if (g->start[c] != g->start[c + 1]) s = fmax(s, fmax(fabs(g->cbox[c].lo[k]), fabs(g->cbox[c].hi[k])));
+    return s;
+}
+
+static int pruned_run(int op, const double* a9, uint64_t n, const double* b9, uint64_t m, double ub,
+                      int threads, pr_job* J) {
+    grid_t ga, gb;
+    grid_build(a9, n, &ga);
+    grid_build(b9, m, &gb);
+    const double margin = 1e-9 * (1.0 + fmax(scale_of(&ga), scale_of(&gb)));
+    const double thr = ub + margin;
+    memset(J, 0, sizeof *J);
+    J->a9 = a9, J->b9 = b9, J->m = m, J->ga = &ga, J->gb = &gb, J->op = op;
+    J->thr2 = thr * thr;
+    J->best_d = INFINITY;
+    J->best_p = UINT64_MAX;
+    atomic_init(&J->next, 0);
+    pthread_mutex_init(&J->mu, NULL);
+    run_pool(threads, pr_worker, J);
+    pthread_mutex_destroy(&J->mu);
+    grid_free(&ga);
+    grid_free(&gb);
+    return J->found;
+}
+
+int or_mesh_mesh_distance_pruned(const double* a9, uint64_t n, const double* b9, uint64_t m, double ub,
+                                 int threads, or_mesh_dist* out) {
+    pr_job J;
+    pruned_run(0, a9, n, b9, m, ub, threads, &J);
+    const int ok = J.found && J.best_d <= ub;
+    out->d = ok ? J.best_d : INFINITY;
+    out->pair = ok ? J.best_p : UINT64_MAX;
+    out->found = ok;
+    out->on_a[0] = J.best_r.a.x, out->on_a[1] = J.best_r.a.y, out->on_a[2] = J.best_r.a.z;
+    out->on_b[0] = J.best_r.b.x, out->on_b[1] = J.best_r.b.y, out->on_b[2] = J.best_r.b.z;
+    if (!ok) memset(out->on_a, 0, sizeof out->on_a), memset(out->on_b, 0, sizeof out->on_b);
+    return ok;
+}
+
+int or_mesh_mesh_intersects_pruned(const double* a9, uint64_t n, const double* b9, uint64_t m,
+                                   int threads, uint64_t* pair_out) {
+    pr_job J;
+    pruned_run(1, a9, n, b9, m, 0.0, threads, &J);
+    *pair_out = J.found ? J.best_p : UINT64_MAX;
+    return J.found;
+}

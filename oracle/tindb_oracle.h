@@ -57,6 +57,20 @@ int or_mesh_mesh_intersects(const double* a9, uint64_t n, const double* b9, uint
                             uint64_t row_begin, uint64_t row_end, uint64_t row_stride, int threads,
                             uint64_t* pair_out);
 
+/* Pruned exact oracles for full-size configurations.
+ * Distance: the lexicographic minimum (d, p) over every pair whose exact
+ * composition distance is <= ub, found by evaluating A17 only on face pairs
+ * whose AABB distance is <= ub (+ a 1e-9-relative margin; face AABB distance
+ * <= true distance <= reference distance + ulps). Equals the full answer
+ * whenever ub >= the true minimum; found = 0 when no pair is <= ub.
+ * Intersects: the lowest hit p among face pairs whose AABBs overlap within
+ * the same margin (a hit needs the triangles to touch within the reference's
+ * 1e-12 slack). Uniform cell grids on both meshes prune cell pairs first. */
+int or_mesh_mesh_distance_pruned(const double* a9, uint64_t n, const double* b9, uint64_t m, double ub,
+                                 int threads, or_mesh_dist* out);
+int or_mesh_mesh_intersects_pruned(const double* a9, uint64_t n, const double* b9, uint64_t m,
+                                   int threads, uint64_t* pair_out);
+
 /* table: per record r (faces offsets[r]..offsets[r+1]) vs the query mesh,
  * record as the first argument (batch.cpp:31 eval_distance(record, arg)). */
 void or_table_distance(const double* table9, const uint64_t* offsets, uint64_t n_objects,
