@@ -75,7 +75,8 @@ typedef struct {
     uint64_t candidates;    /* pairs evaluated with the exact composition */
     uint64_t exact_pairs;   /* intersects: pairs that reached the exact predicate */
     uint64_t kernels;       /* kernel launches in the call */
-    int32_t rounds;         /* band widenings (>= 1) */
+    uint64_t pairs_evaluated; /* pairs run through the per-pair filter (== pairs in FULL mode) */
+    int32_t rounds;         /* exact-pass rounds (>= 1; > 1 when a band was widened) */
     int32_t _pad;
 } tdb_stats;
 

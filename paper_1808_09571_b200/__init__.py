@@ -69,6 +69,7 @@ class Stats(ct.Structure):
         ("candidates", ct.c_uint64),
         ("exact_pairs", ct.c_uint64),
         ("kernels", ct.c_uint64),
+        ("pairs_evaluated", ct.c_uint64),
         ("rounds", ct.c_int32),
         ("_pad", ct.c_int32),
     ]

@@ -24,6 +24,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "exact.cuh"
 #include "runtime.h"
 #include "tma.cuh"
@@ -44,6 +46,11 @@ struct DistArgs {
     uint64_t obj0;
     double* itemmin;
     unsigned long long* objmin;
+    // CULL mode (null in FULL): items in ascending order of their AABB lower
+    // bound (squared), and the sorted bounds
+    const unsigned long long* perm;
+    const unsigned long long* lb2;
+    unsigned long long* evaluated;  // pairs actually run through the filter
 };
 
 __device__ __forceinline__ double warp_min_nn(double x) {
@@ -60,9 +67,19 @@ __global__ void __launch_bounds__(kTile, TDB_FILTER_MINB) filter_kernel(DistArgs
     __shared__ alignas(8) uint64_t bar[2];
     __shared__ double red[kTile / 32];
 
-    const uint64_t item = blockIdx.x;
+    const uint64_t item = a.perm ? a.perm[blockIdx.x] : blockIdx.x;
     const uint64_t tl = item / a.n_chunks, ch = item - tl * a.n_chunks;
     const Tile T = a.tiles[a.tile0 + tl];
+    if (a.perm) {  // CULL: no pair of this item can beat the object's current minimum
+        __shared__ int skip;
+        if (threadIdx.x == 0) {  // one read, so the whole CTA takes the same branch
+            const unsigned long long lb = a.lb2[blockIdx.x];
+            skip = lb > *(volatile unsigned long long*)(a.objmin + (T.obj - a.obj0));
+            if (skip) a.itemmin[item] = __longlong_as_double((long long)lb);
+        }
+        __syncthreads();
+        if (skip) return;
+    }
     const uint32_t r = min(threadIdx.x, T.count - 1);
     const uint64_t row = T.row0 + r;
     bool active = threadIdx.x < T.count && row >= a.row_lo && row < a.row_hi;
@@ -109,12 +126,13 @@ __global__ void __launch_bounds__(kTile, TDB_FILTER_MINB) filter_kernel(DistArgs
     if (!active) best = pos_inf();
     best = warp_min_nn(best);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
-    __syncthreads();
+    const int rows_live = __syncthreads_count(active);
     if (threadIdx.x == 0) {
         double m = red[0];
 #pragma unroll
         for (int w = 1; w < kTile / 32; ++w) m = min_nn(m, red[w]);
         a.itemmin[item] = m;
+        atomicAdd(a.evaluated, (unsigned long long)rows_live * (b1 - b0));
         if (m < pos_inf()) atomicMin(a.objmin + (T.obj - a.obj0), (unsigned long long)__double_as_longlong(m));
     }
 }
@@ -271,6 +289,27 @@ __global__ void witness_kernel(const double* Ap, uint64_t An_pad, uint64_t obj_r
     out[3] = x.b.x, out[4] = x.b.y, out[5] = x.b.z;
 }
 
+// CULL: squared AABB distance between each item's A tile and B chunk (a lower
+// bound of every pair distance in the item), as sortable u64 keys.
+__global__ void item_bound_kernel(const double* __restrict__ tile_aabb, uint64_t tile0,
+                                  const double* __restrict__ chunk_aabb, uint64_t n_chunks, uint64_t n_items,
+                                  unsigned long long* __restrict__ keys, unsigned long long* __restrict__ vals) {
+    const uint64_t item = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (item >= n_items) return;
+    const uint64_t tl = item / n_chunks, ch = item - tl * n_chunks;
+    const double* a = tile_aabb + (tile0 + tl) * 6;
+    const double* b = chunk_aabb + ch * 6;
+    double d2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double g = fmax(0.0, fmax(a[k] - b[3 + k], b[k] - a[3 + k]));
+        d2 = fma(g, g, d2);
+    }
+    // round down: a bound, never above the true squared gap
+    keys[item] = (unsigned long long)__double_as_longlong(__dmul_rd(d2, 1.0 - 1e-15));
+    vals[item] = item;
+}
+
 template <class T>
 T* dalloc(size_t n, cudaStream_t st) {
     T* p = nullptr;
@@ -325,13 +364,35 @@ void run_distance(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, u
     CK(cudaMemcpyAsync(Bstats, B.stats, kObjStats * sizeof(double), cudaMemcpyHostToDevice, st));
 
     EventPair ev;
-    DistArgs da{A.planes, A.n_pad, A.d_tiles, sel.tile0, sel.row_lo, sel.row_hi, B.planes, B.n_pad, B.n,
-                n_chunks, chunk, sel.obj0, itemmin, objmin};
     CK(cudaEventRecord(ev.e[0], st));
+    uint64_t launches = 0;
+    unsigned long long *perm = nullptr, *lb2 = nullptr;
+    void* cull_mem[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    if (cx.mode == TDB_MODE_CULL) {
+        // branch and bound: items in ascending lower-bound order, skipped once
+        // the bound exceeds the object's running minimum
+        double* caabb = dalloc<double>(n_chunks * 6, st);
+        unsigned long long* keys = dalloc<unsigned long long>(n_items, st);
+        unsigned long long* vals = dalloc<unsigned long long>(n_items, st);
+        lb2 = dalloc<unsigned long long>(n_items, st);
+        perm = dalloc<unsigned long long>(n_items, st);
+        chunk_aabbs(B, chunk, caabb, st);
+        item_bound_kernel<<<(unsigned)((n_items + 255) / 256), 256, 0, st>>>(A.d_tile_aabb, sel.tile0, caabb,
+                                                                            n_chunks, n_items, keys, vals);
+        CK(cudaGetLastError());
+        size_t tmp_bytes = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, lb2, vals, perm, (int)n_items, 0, 64, st));
+        void* tmp = dalloc<unsigned char>(tmp_bytes, st);
+        CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, lb2, vals, perm, (int)n_items, 0, 64, st));
+        cull_mem[0] = caabb, cull_mem[1] = keys, cull_mem[2] = vals, cull_mem[3] = tmp;
+        launches += 3;
+    }
+    DistArgs da{A.planes, A.n_pad, A.d_tiles, sel.tile0, sel.row_lo, sel.row_hi, B.planes, B.n_pad, B.n,
+                n_chunks, chunk, sel.obj0, itemmin, objmin, perm, lb2, ctr + 3};
     filter_kernel<<<(unsigned)n_items, kTile, 0, st>>>(da);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ev.e[1], st));
-    uint64_t launches = 1;
+    ++launches;
 
     const unsigned ob = (unsigned)((nobj + 255) / 256);
     band_kernel<<<ob, 256, 0, st>>>(BandArgs{objmin, A.d_obj_stats, Bstats, sel.obj0, nobj, band2, band, objD, objP});
@@ -375,8 +436,9 @@ void run_distance(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, u
     if (witness6) CK(cudaMemcpyAsync(witness6, wit, 6 * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaEventRecord(ev.e[3], st));
     for (void* p : {(void*)itemmin, (void*)objmin, (void*)band2, (void*)band, (void*)objD, (void*)objP,
-                    (void*)list, (void*)ctr, (void*)Bstats, (void*)wit})
-        CK(cudaFreeAsync(p, st));
+                    (void*)list, (void*)ctr, (void*)Bstats, (void*)wit, (void*)perm, (void*)lb2, cull_mem[0],
+                    cull_mem[1], cull_mem[2], cull_mem[3]})
+        if (p) CK(cudaFreeAsync(p, st));
     CK(cudaStreamSynchronize(st));
     for (uint64_t o = 0; o < nobj; ++o) {
         if (hP[o] != kNone) {
@@ -404,6 +466,7 @@ void run_distance(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, u
     S.items_flagged = flagged_total;
     S.candidates = h_ctr[1];
     S.kernels = launches;
+    S.pairs_evaluated = h_ctr[3];
     S.rounds = rounds;
 }
 

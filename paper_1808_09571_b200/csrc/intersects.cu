@@ -60,6 +60,9 @@ struct HitArgs {
     const double* Bstats;
     unsigned long long* objhit;
     unsigned long long* nexact;
+    // CULL mode (null in FULL): per-tile and per-chunk AABBs
+    const double* tile_aabb;
+    const double* chunk_aabb;
 };
 
 __device__ __forceinline__ exact::tri load_tri(const double* P, uint64_t pad, uint64_t i) {
@@ -125,6 +128,12 @@ __global__ void __launch_bounds__(32 * kWarps) hit_kernel(HitArgs a) {
     const double tau = kCullDiag * sqrt(diag2) + kCullAbs * fmax(As[7], Bs[7]);
 #pragma unroll
     for (int k = 0; k < 3; ++k) apart |= (As[k] > Bs[3 + k] + tau) || (Bs[k] > As[3 + k] + tau);
+    if (a.chunk_aabb) {  // CULL: the warp's tile box vs this item's B-chunk box
+        const double* ta = a.tile_aabb + (a.tile0 + (has_tile ? tl : a.ntiles - 1)) * 6;
+        const double* cb = a.chunk_aabb + ch * 6;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) apart |= (ta[k] > cb[3 + k] + tau) || (cb[k] > ta[3 + k] + tau);
+    }
 
     // this lane's rows: lane, lane+32, lane+64, lane+96 of the warp's tile
     double an[kRows][3], ac[kRows];
@@ -257,11 +266,17 @@ void run_intersects(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit,
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     CK(cudaEventCreate(&e2));
+    double* caabb = nullptr;
+    if (cx.mode == TDB_MODE_CULL) {
+        CK(cudaMallocAsync(&caabb, n_chunks * 6 * sizeof(double), st));
+        chunk_aabbs(B, chunk, caabb, st);
+    }
     CK(cudaEventRecord(e0, st));
     hit_kernel<<<(unsigned)n_items, 32 * kWarps, 0, st>>>(HitArgs{A.planes, A.n_pad, A.d_tiles, sel.tile0, ntiles,
                                                                   sel.row_lo, sel.row_hi, B.planes, B.n_pad, B.n,
                                                                   n_chunks, chunk, sel.obj0, A.d_obj_stats, Bstats,
-                                                                  objhit, nex});
+                                                                  objhit, nex, caabb ? A.d_tile_aabb : nullptr,
+                                                                  caabb});
     CK(cudaGetLastError());
     CK(cudaEventRecord(e1, st));
     std::vector<unsigned long long> hp(nobj);
@@ -272,6 +287,7 @@ void run_intersects(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit,
     CK(cudaFreeAsync(objhit, st));
     CK(cudaFreeAsync(nex, st));
     CK(cudaFreeAsync(Bstats, st));
+    if (caabb) CK(cudaFreeAsync(caabb, st));
     CK(cudaStreamSynchronize(st));
     for (uint64_t o = 0; o < nobj; ++o) {
         pair[o] = hp[o];
@@ -294,6 +310,7 @@ void run_intersects(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit,
     S.pairs = pairs;
     S.items = n_items;
     S.exact_pairs = hn;
+    S.pairs_evaluated = pairs;  // covered (early exit and culls are not subtracted)
     S.kernels = 1;
     S.rounds = 1;
 }

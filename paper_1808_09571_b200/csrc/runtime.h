@@ -36,7 +36,7 @@ struct Geom {
     uint64_t* d_off = nullptr;         // n_obj + 1
     Tile* d_tiles = nullptr;
     double* d_obj_stats = nullptr;     // n_obj x kObjStats
-    double* d_chunk_aabb = nullptr;    // n_chunks x 6
+    double* d_tile_aabb = nullptr;     // per A tile: lo xyz, hi xyz
     std::vector<uint64_t> h_off;
     std::vector<Tile> h_tiles;
     std::vector<uint64_t> obj_tile0;   // first tile of each object (n_obj + 1)
@@ -46,6 +46,8 @@ struct Geom {
 void geom_build(Geom* g, const double* host_tri9, uint64_t n, const uint64_t* host_off,
                 uint64_t n_obj, cudaStream_t st);
 void geom_release(Geom* g);
+// AABBs (lo xyz, hi xyz) of the uniform face chunks [c*len, (c+1)*len) of g.
+void chunk_aabbs(const Geom& g, uint64_t len, double* out, cudaStream_t st);
 
 // Per-call execution context.
 struct Ctx {

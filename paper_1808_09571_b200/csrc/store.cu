@@ -144,10 +144,18 @@ __global__ void stats_final_kernel(const unsigned long long* __restrict__ in, do
     if (i < n) out[i] = unord(in[i]);
 }
 
-// AABB per B-chunk (CULL mode item skipping): one block per chunk.
-__global__ void chunk_aabb_kernel(const double* __restrict__ planes, uint64_t n, uint64_t n_pad,
-                                  double* __restrict__ out) {
-    const uint64_t c0 = (uint64_t)blockIdx.x * kChunk, c1 = min(n, c0 + kChunk);
+// AABB of face ranges, one block per range: the A tiles (tiles != null) or
+// uniform B chunks of `len` faces. Used by CULL mode item bounds.
+__global__ void range_aabb_kernel(const double* __restrict__ planes, uint64_t n, uint64_t n_pad,
+                                  const Tile* __restrict__ tiles, uint64_t len, double* __restrict__ out) {
+    uint64_t c0, c1;
+    if (tiles) {
+        c0 = tiles[blockIdx.x].row0;
+        c1 = c0 + tiles[blockIdx.x].count;
+    } else {
+        c0 = (uint64_t)blockIdx.x * len;
+        c1 = min(n, c0 + len);
+    }
     double lo[3] = {pos_inf(), pos_inf(), pos_inf()}, hi[3] = {-pos_inf(), -pos_inf(), -pos_inf()};
     for (uint64_t f = c0 + threadIdx.x; f < c1; f += blockDim.x)
         for (int k = 0; k < 9; ++k) {
@@ -205,7 +213,7 @@ void geom_build(Geom* g, const double* host_tri9, uint64_t n, const uint64_t* ho
     CK(cudaMallocAsync(&g->d_off, (n_obj + 1) * sizeof(uint64_t), st));
     CK(cudaMallocAsync(&g->d_tiles, std::max<size_t>(1, g->h_tiles.size()) * sizeof(Tile), st));
     CK(cudaMallocAsync(&g->d_obj_stats, std::max<uint64_t>(1, n_obj) * kObjStats * sizeof(double), st));
-    CK(cudaMallocAsync(&g->d_chunk_aabb, std::max<uint64_t>(1, g->n_chunks) * 6 * sizeof(double), st));
+    CK(cudaMallocAsync(&g->d_tile_aabb, std::max<size_t>(1, g->h_tiles.size()) * 6 * sizeof(double), st));
     unsigned long long* ustats = nullptr;
     unsigned long long* ndeg = nullptr;
     CK(cudaMallocAsync(&ustats, std::max<uint64_t>(1, n_obj) * kObjStats * sizeof(unsigned long long), st));
@@ -227,8 +235,11 @@ void geom_build(Geom* g, const double* host_tri9, uint64_t n, const uint64_t* ho
         prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(staging, n, g->n_pad, g->d_off, n_obj,
                                                                 g->planes, ustats, ndeg);
         CK(cudaGetLastError());
-        chunk_aabb_kernel<<<(unsigned)g->n_chunks, 256, 0, st>>>(g->planes, n, g->n_pad, g->d_chunk_aabb);
-        CK(cudaGetLastError());
+        if (!g->h_tiles.empty()) {
+            range_aabb_kernel<<<(unsigned)g->h_tiles.size(), 128, 0, st>>>(g->planes, n, g->n_pad, g->d_tiles, 0,
+                                                                          g->d_tile_aabb);
+            CK(cudaGetLastError());
+        }
     }
     if (n_obj) {
         const uint64_t m = n_obj * kObjStats;
@@ -256,13 +267,20 @@ void geom_build(Geom* g, const double* host_tri9, uint64_t n, const uint64_t* ho
     std::copy(agg, agg + kObjStats, g->stats);
 }
 
+void chunk_aabbs(const Geom& g, uint64_t len, double* out, cudaStream_t st) {
+    const uint64_t n_chunks = (g.n + len - 1) / len;
+    if (!n_chunks) return;
+    range_aabb_kernel<<<(unsigned)n_chunks, 256, 0, st>>>(g.planes, g.n, g.n_pad, nullptr, len, out);
+    CK(cudaGetLastError());
+}
+
 void geom_release(Geom* g) {
     if (!g) return;
     cudaFree(g->planes);
     cudaFree(g->d_off);
     cudaFree(g->d_tiles);
     cudaFree(g->d_obj_stats);
-    cudaFree(g->d_chunk_aabb);
+    cudaFree(g->d_tile_aabb);
     g->planes = nullptr;
 }
 
