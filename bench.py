@@ -447,9 +447,18 @@ def main():
     f_pairs = sum(k_pairs) / len(k_pairs)
     w = W_D if wl.op == "distance" else W_I
     achieved_tf = w * f_pairs / (f_ms * 1e-3) / 1e12
+    kname = "filter_kernel" if wl.op == "distance" else "hit_kernel"
+    traffic = None
+    try:  # DRAM bytes per pair from the committed ncu --set full capture, scaled to this launch
+        tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))[kname]
+        traffic = tj["dram_bytes_per_pair"] * f_pairs
+    except (OSError, KeyError, ValueError):
+        pass
     roofline = {
         "bound": "fp64", "achieved": achieved_tf, "peak": fp64_tf, "unit": "TFLOP/s",
-        "frac": achieved_tf / fp64_tf, "traffic": None,
+        "frac": achieved_tf / fp64_tf, "traffic": traffic,
+        "traffic_note": "dram__bytes_read+write per launch from profiles/traffic.json (ncu --set full), "
+                        "scaled to this launch's pairs; algorithmic bytes = 288 B per B face per 128-row tile",
         "kernel": "filter_kernel (fast_pair.cuh)" if wl.op == "distance" else "hit_kernel (intersects.cu)",
         "work_per_pair_flops": w,
         "peak_source": "measured in this run: DFMA issue-rate microbenchmark (tdb_fp64_peak); "
