@@ -128,6 +128,12 @@ int tdb_table_eval_rows(int op, tdb_table records, uint64_t obj_begin, uint64_t 
                         tdb_mesh literal, double* dist_out, uint8_t* hit_out,
                         uint64_t* pair_out);
 
+/* ---- ST_3DVolume: mesh_volume (kernels.hpp:64-70, kernels.cpp:27-46),
+ * permissive policy, bit-identical to the reference for the same chunk_size
+ * (0 = ExecutorConfig default 4096; the chunk tree fixes the summation order,
+ * executor.hpp:20-49). */
+int tdb_mesh_volume(tdb_mesh m, uint64_t chunk_size, double* volume_out);
+
 /* ---- one-shot host-buffer entry points (upload + evaluate + free) -------- */
 int tdb_distance_host(const double* a9, uint64_t n, const double* b9, uint64_t m,
                       tdb_dist_out* out);

@@ -97,6 +97,8 @@ def _load_ref():
     L.ref_ore_body.argtypes = [ct.c_uint64, _D]
     L.ref_ore_body.restype = ct.c_uint64
     L.ref_random_triangles.argtypes = [ct.c_uint64, ct.c_uint64, ct.c_double, ct.c_double, _D]
+    L.ref_mesh_volume.argtypes = [_D, ct.c_uint64, ct.c_uint64, ct.POINTER(ct.c_int)]
+    L.ref_mesh_volume.restype = ct.c_double
     L.ref_unit_cube.argtypes = [_D]
     L.ref_unit_cube.restype = ct.c_uint64
     return L
@@ -240,6 +242,14 @@ def ref_random_triangles(seed, n, lo=-1.0, hi=1.0):
     out = np.empty((n, 9), np.float64)
     REF.ref_random_triangles(seed, n, lo, hi, _dp(out))
     return out
+
+
+def ref_mesh_volume(tris, chunk=4096):
+    """(volume, closed) from the reference mesh_volume (kernels.cpp:27-46)."""
+    t = _f64(tris).reshape(-1, 9)
+    c = ct.c_int(0)
+    v = REF.ref_mesh_volume(_dp(t), len(t), chunk, ct.byref(c))
+    return v, bool(c.value)
 
 
 def ref_unit_cube():

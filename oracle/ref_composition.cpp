@@ -248,4 +248,18 @@ void ref_random_triangles(std::uint64_t seed, std::uint64_t n, double lo, double
 
 std::uint64_t ref_unit_cube(double* out) { return copy_mesh(tindb::fixtures::unit_cube(), out); }
 
+// kernels.cpp:27-46 mesh_volume (permissive policy) with a given chunk size;
+// closed_out receives validate_closed (closure.cpp:41) when non-null.
+double ref_mesh_volume(const double* t9, std::uint64_t n, std::uint64_t chunk, int* closed_out) {
+    TriangleMesh m;
+    m.triangles = load_mesh(t9, n);
+    m.refresh_degeneracy_flag();
+    K::ExecutorConfig cfg = K::ExecutorConfig::sequential();
+    cfg.chunk_size = chunk;
+    bool closed = false;
+    const double v = K::mesh_volume(m, cfg, closed_out ? &closed : nullptr);
+    if (closed_out) *closed_out = closed ? 1 : 0;
+    return v;
+}
+
 }  // extern "C"

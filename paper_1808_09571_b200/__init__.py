@@ -109,6 +109,7 @@ _SIGS = [
     ("tdb_gen_ore_body", ct.c_uint64, [ct.c_uint64, _D]),
     ("tdb_gen_terrain", ct.c_uint64, [ct.c_uint32, ct.c_uint32, ct.c_double, ct.c_uint64, _D]),
     ("tdb_fp64_peak", ct.c_int, [_D, _D]),
+    ("tdb_mesh_volume", ct.c_int, [ct.c_void_p, ct.c_uint64, _D]),
 ]
 EXPORTS = [s[0] for s in _SIGS]
 
@@ -356,6 +357,15 @@ def pairs_filter(a, b) -> np.ndarray:
     out = np.empty(len(a), np.float64)
     _check(lib().tdb_pairs_filter(_dp(a), _dp(b), len(a), _dp(out)))
     return out
+
+
+def mesh_volume(mesh, chunk_size: int = 4096) -> float:
+    """ST_3DVolume: kernels::mesh_volume (kernels.cpp:27-46) bit for bit, for
+    the same ExecutorConfig::chunk_size (permissive policy)."""
+    m = _as_mesh(mesh)
+    v = ct.c_double()
+    _check(lib().tdb_mesh_volume(m.handle, chunk_size, ct.byref(v)))
+    return v.value
 
 
 # ---- mesh generators (host; bit-identical to dataset.cpp) -------------------

@@ -347,6 +347,14 @@ int tdb_pairs_filter(const double* a9, const double* b9, uint64_t n, double* d2)
     return rc;
 }
 
+int tdb_mesh_volume(tdb_mesh m, uint64_t chunk_size, double* volume_out) {
+    return guarded([&] {
+        need(m && volume_out, "null argument");
+        need(m->g.n_obj == 1, "volume takes a mesh (one object)");
+        *volume_out = tdb::run_volume(ctx(), m->g, chunk_size);
+    });
+}
+
 int tdb_fp64_peak(double* tflops, double* ms) {
     return guarded([&] {
         need(tflops != nullptr, "null output");

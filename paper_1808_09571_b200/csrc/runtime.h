@@ -90,4 +90,7 @@ void run_pairs_filter(const Ctx& cx, const Geom& A, const Geom& B, double* d2);
 
 double fp64_peak(const Ctx& cx, double* ms);
 
+// mesh_volume (kernels.cpp:27-46) with the reference's fixed chunk tree.
+double run_volume(const Ctx& cx, const Geom& g, uint64_t chunk);
+
 }  // namespace tdb

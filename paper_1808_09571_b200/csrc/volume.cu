@@ -1,0 +1,85 @@
+// ST_3DVolume (the paper's third operator): signed divergence-theorem volume
+// of a mesh, bit-identical to the reference mesh_volume (kernels.cpp:23-46).
+//
+// The reference fixes the summation tree so every backend agrees: faces are
+// cut into chunks of cfg.chunk_size (executor.hpp:20-44, default 4096), each
+// chunk is summed sequentially in face order, and the chunk partials are
+// combined by the pairwise tree of pairwise_tree_sum (kernels.cpp:11-21).
+// Here one thread sums one chunk in order with round-to-nearest intrinsics
+// (no contraction), and one thread walks the tree — the same operations in
+// the same order, so the same bits.
+//
+// Volume policy: permissive (the reference default) — the signed sum is
+// returned for any mesh; watertightness (validate_closed, closure.cpp) is not
+// evaluated on the device.
+#include <algorithm>
+#include <cstring>
+
+#include "exact.cuh"
+#include "runtime.h"
+
+namespace tdb {
+
+namespace {
+
+// kernels.cpp:23-25: dot(v0, (v1-v0) x (v2-v0)) / 6
+__device__ __forceinline__ double face_term(const double* P, uint64_t pad, uint64_t i) {
+    const exact::v3 v0{P[(F_V + 0) * pad + i], P[(F_V + 1) * pad + i], P[(F_V + 2) * pad + i]};
+    const exact::v3 v1{P[(F_V + 3) * pad + i], P[(F_V + 4) * pad + i], P[(F_V + 5) * pad + i]};
+    const exact::v3 v2{P[(F_V + 6) * pad + i], P[(F_V + 7) * pad + i], P[(F_V + 8) * pad + i]};
+    const exact::v3 n = exact::cross(exact::sub(v1, v0), exact::sub(v2, v0));
+    return __ddiv_rn(exact::dot(v0, n), 6.0);
+}
+
+__global__ void chunk_sums_kernel(const double* __restrict__ P, uint64_t pad, uint64_t n, uint64_t chunk,
+                                  uint64_t n_chunks, double* __restrict__ leaves) {
+    const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_chunks) return;
+    const uint64_t b = k * chunk, e = min(n, b + chunk);
+    double acc = 0.0;
+    for (uint64_t i = b; i < e; ++i) acc = __dadd_rn(acc, face_term(P, pad, i));
+    leaves[k] = acc;
+}
+
+// kernels.cpp:11-21 pairwise_tree_sum, in place
+__global__ void tree_sum_kernel(double* leaves, uint64_t size, double* out) {
+    if (size == 0) {
+        *out = 0.0;
+        return;
+    }
+    while (size > 1) {
+        uint64_t w = 0, i = 0;
+        for (; i + 1 < size; i += 2) leaves[w++] = __dadd_rn(leaves[i], leaves[i + 1]);
+        if (i < size) leaves[w++] = leaves[i];
+        size = w;
+    }
+    *out = leaves[0];
+}
+
+}  // namespace
+
+double run_volume(const Ctx& cx, const Geom& g, uint64_t chunk) {
+    const cudaStream_t st = cx.stream;
+    if (chunk == 0) chunk = 4096;  // ExecutorConfig::chunk_size default (executor.hpp:23)
+    const uint64_t n_chunks = (g.n + chunk - 1) / chunk;
+    double *leaves = nullptr, *out = nullptr;
+    CK(cudaMallocAsync(&leaves, std::max<uint64_t>(1, n_chunks) * sizeof(double), st));
+    CK(cudaMallocAsync(&out, sizeof(double), st));
+    if (n_chunks) {
+        chunk_sums_kernel<<<(unsigned)((n_chunks + 127) / 128), 128, 0, st>>>(g.planes, g.n_pad, g.n, chunk,
+                                                                             n_chunks, leaves);
+        CK(cudaGetLastError());
+    }
+    tree_sum_kernel<<<1, 1, 0, st>>>(leaves, n_chunks, out);
+    CK(cudaGetLastError());
+    double v = 0.0;
+    CK(cudaMemcpyAsync(&v, out, sizeof v, cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(leaves, st));
+    CK(cudaFreeAsync(out, st));
+    CK(cudaStreamSynchronize(st));
+    std::memset(cx.stats, 0, sizeof *cx.stats);
+    cx.stats->kernels = n_chunks ? 2 : 1;
+    return v;
+}
+
+}  // namespace tdb

@@ -203,6 +203,19 @@ def main():
         gens[f"ore_body/{ft}"] = sha(O.ref_ore_body(ft))
     with open(os.path.join(OUT, "generators.json"), "w") as f:
         json.dump(gens, f, indent=1, sort_keys=True)
+    # mesh_volume (kernels.cpp:27-46) bits for several chunk sizes
+    import paper_1808_09571_b200 as T
+    vol_meshes = {"sphere_1280": O.ref_unit_sphere(1000), "ore_81920": O.ref_ore_body(100_000),
+                  "cube": O.ref_unit_cube(), "terrain_16x8": T.terrain(16, 8, 20.0, 42),
+                  "soup_300": O.ref_random_triangles(101, 300)}
+    vols = {}
+    for name, m in vol_meshes.items():
+        for chunk in (1, 7, 4096):
+            v, closed = O.ref_mesh_volume(m, chunk)
+            vols[f"{name}/{chunk}"] = {"bits": np.float64(v).view(np.uint64).item(), "value": v, "closed": closed}
+    np.savez_compressed(os.path.join(OUT, "volume_meshes.npz"), **vol_meshes)
+    with open(os.path.join(OUT, "volumes.json"), "w") as f:
+        json.dump(vols, f, indent=1, sort_keys=True)
     print("pairs:", len(A), "hits:", int(h.sum()), "meshes:", len(meshes))
 
 
