@@ -128,6 +128,21 @@ int tdb_table_eval_rows(int op, tdb_table records, uint64_t obj_begin, uint64_t 
                         tdb_mesh literal, double* dist_out, uint8_t* hit_out,
                         uint64_t* pair_out);
 
+/* ---- segment / point x mesh: the paper's drill-hole workload.
+ * One result per query, in query order: distance_to_mesh (kernels.hpp:68-78,
+ * kernels.cpp:382-405: min over non-degenerate faces, lowest face index on
+ * ties, a zero-length segment is a point query) and intersects_mesh
+ * (kernels.hpp:80-84, kernels.cpp:407-432: lowest hit face). face_out =
+ * UINT64_MAX when there is none. Queries are host arrays: segments are 6
+ * doubles (p0 xyz, p1 xyz, geometry.hpp:46-54), points 3. */
+int tdb_segments_mesh_distance(const double* seg6, uint64_t n, tdb_mesh mesh, double* dist_out,
+                               uint64_t* face_out);
+int tdb_points_mesh_distance(const double* pt3, uint64_t n, tdb_mesh mesh, double* dist_out,
+                             uint64_t* face_out);
+int tdb_segments_mesh_intersects(const double* seg6, uint64_t n, tdb_mesh mesh, uint8_t* hit_out,
+                                 uint64_t* face_out);
+uint64_t tdb_gen_drills(uint64_t seed, uint64_t count, int style, double* out6); /* dataset.cpp:141 */
+
 /* ---- ST_3DVolume: mesh_volume (kernels.hpp:64-70, kernels.cpp:27-46),
  * permissive policy, bit-identical to the reference for the same chunk_size
  * (0 = ExecutorConfig default 4096; the chunk tree fixes the summation order,

@@ -71,6 +71,9 @@ def _load_c():
     L.or_mesh_mesh_distance_pruned.argtypes = [_D, ct.c_uint64, _D, ct.c_uint64, ct.c_double, ct.c_int,
                                                ct.POINTER(OrMeshDist)]
     L.or_mesh_mesh_intersects_pruned.argtypes = [_D, ct.c_uint64, _D, ct.c_uint64, ct.c_int, _U64]
+    for fn in ("or_segments_mesh_distance", "or_points_mesh_distance"):
+        getattr(L, fn).argtypes = [_D, ct.c_uint64, _D, ct.c_uint64, ct.c_int, _D, _U64]
+    L.or_segments_mesh_intersects.argtypes = [_D, ct.c_uint64, _D, ct.c_uint64, ct.c_int, _U8, _U64]
     L.or_table_distance.argtypes = [_D, _U64, ct.c_uint64, _D, ct.c_uint64, ct.c_int, _D, _U64]
     L.or_table_intersects.argtypes = [_D, _U64, ct.c_uint64, _D, ct.c_uint64, ct.c_int, _U8,
                                       _U64]
@@ -97,6 +100,11 @@ def _load_ref():
     L.ref_ore_body.argtypes = [ct.c_uint64, _D]
     L.ref_ore_body.restype = ct.c_uint64
     L.ref_random_triangles.argtypes = [ct.c_uint64, ct.c_uint64, ct.c_double, ct.c_double, _D]
+    for fn in ("ref_segments_mesh_distance", "ref_points_mesh_distance"):
+        getattr(L, fn).argtypes = [_D, ct.c_uint64, _D, ct.c_uint64, ct.c_int, _D, _U64]
+    L.ref_segments_mesh_intersects.argtypes = [_D, ct.c_uint64, _D, ct.c_uint64, ct.c_int, _U8, _U64]
+    L.ref_make_drills.argtypes = [ct.c_uint64, ct.c_uint64, ct.c_int, _D]
+    L.ref_make_drills.restype = ct.c_uint64
     L.ref_mesh_volume.argtypes = [_D, ct.c_uint64, ct.c_uint64, ct.POINTER(ct.c_int)]
     L.ref_mesh_volume.restype = ct.c_double
     L.ref_unit_cube.argtypes = [_D]
@@ -170,6 +178,55 @@ def mesh_mesh_intersects_pruned(a, b, threads=None):
     C.or_mesh_mesh_intersects_pruned(_dp(a), len(a), _dp(b), len(b), threads or os.cpu_count() or 1,
                                      ct.byref(p))
     return p.value != U64_MAX, p.value
+
+
+def _queries(lib, prefix, kind, q, mesh, threads):
+    width = 3 if kind == "points" else 6
+    q = _f64(q).reshape(-1, width)
+    mesh = _f64(mesh).reshape(-1, 9)
+    face = np.empty(len(q), np.uint64)
+    th = threads or os.cpu_count() or 1
+    if kind == "intersects":
+        hit = np.empty(len(q), np.uint8)
+        getattr(lib, prefix + "segments_mesh_intersects")(_dp(q), len(q), _dp(mesh), len(mesh), th,
+                                                          hit.ctypes.data_as(_U8), face.ctypes.data_as(_U64))
+        return hit.astype(bool), face
+    d = np.empty(len(q), np.float64)
+    getattr(lib, prefix + f"{kind}_mesh_distance")(_dp(q), len(q), _dp(mesh), len(mesh), th, _dp(d),
+                                                   face.ctypes.data_as(_U64))
+    return d, face
+
+
+def segments_mesh_distance(segs, mesh, threads=None):
+    """(distance, face) per segment: distance_to_mesh (kernels.cpp:388)."""
+    return _queries(C, "or_", "segments", segs, mesh, threads)
+
+
+def points_mesh_distance(pts, mesh, threads=None):
+    return _queries(C, "or_", "points", pts, mesh, threads)
+
+
+def segments_mesh_intersects(segs, mesh, threads=None):
+    """(hit, face) per segment: intersects_mesh (kernels.cpp:407)."""
+    return _queries(C, "or_", "intersects", segs, mesh, threads)
+
+
+def ref_segments_mesh_distance(segs, mesh, threads=None):
+    return _queries(REF, "ref_", "segments", segs, mesh, threads)
+
+
+def ref_points_mesh_distance(pts, mesh, threads=None):
+    return _queries(REF, "ref_", "points", pts, mesh, threads)
+
+
+def ref_segments_mesh_intersects(segs, mesh, threads=None):
+    return _queries(REF, "ref_", "intersects", segs, mesh, threads)
+
+
+def ref_make_drills(seed, count, style=0):
+    out = np.empty((count, 6), np.float64)
+    REF.ref_make_drills(seed, count, style, _dp(out))
+    return out
 
 
 def table_eval(op, table, offsets, query, threads=None):

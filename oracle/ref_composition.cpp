@@ -248,6 +248,68 @@ void ref_random_triangles(std::uint64_t seed, std::uint64_t n, double lo, double
 
 std::uint64_t ref_unit_cube(double* out) { return copy_mesh(tindb::fixtures::unit_cube(), out); }
 
+// ---- segment / point x mesh: the reference's own distance_to_mesh and
+// intersects_mesh (kernels.cpp:382-432) per query, record-parallel like
+// run_batch (batch.cpp:94-103). face = UINT64_MAX when none.
+static TriangleMesh mesh_of(const double* t9, std::uint64_t m) {
+    TriangleMesh mesh;
+    mesh.triangles = load_mesh(t9, m);
+    mesh.refresh_degeneracy_flag();
+    return mesh;
+}
+
+void ref_segments_mesh_distance(const double* s6, std::uint64_t n, const double* t9, std::uint64_t m, int threads,
+                                double* dist, std::uint64_t* face) {
+    const TriangleMesh mesh = mesh_of(t9, m);
+    const auto inner = K::ExecutorConfig::sequential();
+    K::for_each_chunk(row_cfg(threads), n, [&](std::size_t, std::size_t lo, std::size_t hi) {
+        for (std::size_t k = lo; k < hi; ++k) {
+            const LineSegment seg{{s6[6 * k], s6[6 * k + 1], s6[6 * k + 2]}, {s6[6 * k + 3], s6[6 * k + 4], s6[6 * k + 5]}};
+            const K::DistanceResult r = K::distance_to_mesh(seg, mesh, inner);
+            dist[k] = r.distance;
+            face[k] = r.face_index ? *r.face_index : ~std::uint64_t(0);
+        }
+    });
+}
+
+void ref_points_mesh_distance(const double* p3, std::uint64_t n, const double* t9, std::uint64_t m, int threads,
+                              double* dist, std::uint64_t* face) {
+    const TriangleMesh mesh = mesh_of(t9, m);
+    const auto inner = K::ExecutorConfig::sequential();
+    K::for_each_chunk(row_cfg(threads), n, [&](std::size_t, std::size_t lo, std::size_t hi) {
+        for (std::size_t k = lo; k < hi; ++k) {
+            const K::DistanceResult r = K::distance_to_mesh(Point3{p3[3 * k], p3[3 * k + 1], p3[3 * k + 2]}, mesh, inner);
+            dist[k] = r.distance;
+            face[k] = r.face_index ? *r.face_index : ~std::uint64_t(0);
+        }
+    });
+}
+
+void ref_segments_mesh_intersects(const double* s6, std::uint64_t n, const double* t9, std::uint64_t m, int threads,
+                                  std::uint8_t* hit, std::uint64_t* face) {
+    const TriangleMesh mesh = mesh_of(t9, m);
+    const auto inner = K::ExecutorConfig::sequential();
+    K::for_each_chunk(row_cfg(threads), n, [&](std::size_t, std::size_t lo, std::size_t hi) {
+        for (std::size_t k = lo; k < hi; ++k) {
+            const LineSegment seg{{s6[6 * k], s6[6 * k + 1], s6[6 * k + 2]}, {s6[6 * k + 3], s6[6 * k + 4], s6[6 * k + 5]}};
+            const K::IntersectionResult r = K::intersects_mesh(seg, mesh, inner);
+            hit[k] = r.hit ? 1 : 0;
+            face[k] = r.face_index ? *r.face_index : ~std::uint64_t(0);
+        }
+    });
+}
+
+// dataset.cpp:141-165 make_drills (default box; style 0 vertical, 1 uniform)
+std::uint64_t ref_make_drills(std::uint64_t seed, std::uint64_t count, int style, double* out6) {
+    tindb::bench::DatasetSpec spec;
+    spec.seed = seed;
+    spec.segment_count = count;
+    spec.drill_style = style ? tindb::bench::DrillStyle::UniformRandom : tindb::bench::DrillStyle::VerticalJittered;
+    const auto d = tindb::bench::make_drills(spec);
+    if (out6) std::memcpy(out6, d.data(), d.size() * sizeof(LineSegment));
+    return d.size();
+}
+
 // kernels.cpp:27-46 mesh_volume (permissive policy) with a given chunk size;
 // closed_out receives validate_closed (closure.cpp:41) when non-null.
 double ref_mesh_volume(const double* t9, std::uint64_t n, std::uint64_t chunk, int* closed_out) {

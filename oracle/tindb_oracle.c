@@ -507,6 +507,81 @@ void or_table_intersects(const double* table9, const uint64_t* offsets, uint64_t
     table_run(1, table9, offsets, n_objects, query9, mq, threads, NULL, hit, pair);
 }
 
+/* ---- segment / point x mesh (kernels.cpp:347-432) ------------------------ */
+typedef struct {
+    const double *q, *t9;
+    uint64_t n, m;
+    int kind; /* 0 segment distance, 1 point distance, 2 segment intersects */
+    atomic_uint_fast64_t next;
+    double* dist;
+    uint8_t* hit;
+    uint64_t* face;
+} q_job;
+
+static void* q_worker(void* arg) {
+    q_job* J = (q_job*)arg;
+    for (;;) {
+        const uint64_t k = atomic_fetch_add(&J->next, 1);
+        if (k >= J->n) break;
+        if (J->kind == 2) { /* intersects_mesh: lowest hit face, no degenerate skip */
+            const double* s = J->q + 6 * k;
+            uint64_t f = UINT64_MAX;
+            for (uint64_t i = 0; i < J->m; ++i) {
+                const tri_t t = ld_tri(J->t9 + 9 * i);
+                if (seg_tri_hit(ld3(s), ld3(s + 3), &t)) {
+                    f = i;
+                    break;
+                }
+            }
+            J->hit[k] = (uint8_t)(f != UINT64_MAX);
+            J->face[k] = f;
+            continue;
+        }
+        /* reduce_min_over_faces: strict '<' keeps the lowest face index */
+        v3 p0, p1;
+        int point = J->kind == 1;
+        if (point) {
+            p0 = p1 = ld3(J->q + 3 * k);
+        } else {
+            p0 = ld3(J->q + 6 * k), p1 = ld3(J->q + 6 * k + 3);
+            point = same(p0, p1); /* kernels.cpp:388: degenerate segment -> point */
+        }
+        double best = INFINITY;
+        uint64_t f = UINT64_MAX;
+        for (uint64_t i = 0; i < J->m; ++i) {
+            const tri_t t = ld_tri(J->t9 + 9 * i);
+            if (tri_degenerate(&t)) continue;
+            const double d = point ? pt_tri(p0, &t).d : seg_tri(p0, p1, &t).d;
+            if (d < best) best = d, f = i;
+        }
+        J->dist[k] = best;
+        J->face[k] = f;
+    }
+    return NULL;
+}
+
+static void q_run(int kind, const double* q, uint64_t n, const double* t9, uint64_t m, int threads, double* dist,
+                  uint8_t* hit, uint64_t* face) {
+    q_job J;
+    memset(&J, 0, sizeof J);
+    J.q = q, J.t9 = t9, J.n = n, J.m = m, J.kind = kind, J.dist = dist, J.hit = hit, J.face = face;
+    atomic_init(&J.next, 0);
+    run_pool(threads, q_worker, &J);
+}
+
+void or_segments_mesh_distance(const double* s6, uint64_t n, const double* t9, uint64_t m, int threads,
+                               double* dist, uint64_t* face) {
+    q_run(0, s6, n, t9, m, threads, dist, NULL, face);
+}
+void or_points_mesh_distance(const double* p3, uint64_t n, const double* t9, uint64_t m, int threads,
+                             double* dist, uint64_t* face) {
+    q_run(1, p3, n, t9, m, threads, dist, NULL, face);
+}
+void or_segments_mesh_intersects(const double* s6, uint64_t n, const double* t9, uint64_t m, int threads,
+                                 uint8_t* hit, uint64_t* face) {
+    q_run(2, s6, n, t9, m, threads, NULL, hit, face);
+}
+
 /* ---- pruned exact oracles (full-size parity) -------- */
 typedef struct {
     double lo[3], hi[3];

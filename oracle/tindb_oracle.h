@@ -71,6 +71,18 @@ int or_mesh_mesh_distance_pruned(const double* a9, uint64_t n, const double* b9,
 int or_mesh_mesh_intersects_pruned(const double* a9, uint64_t n, const double* b9, uint64_t m,
                                    int threads, uint64_t* pair_out);
 
+/* Per-query segment / point x mesh (kernels.cpp:382-432 distance_to_mesh,
+ * intersects_mesh): distance + lowest face index (degenerate faces skipped,
+ * kernels.cpp:350-357; a zero-length segment is a point query, :388), and
+ * the lowest hit face (no degenerate skip, :407-432). face = UINT64_MAX when
+ * none. Query-parallel over `threads`. */
+void or_segments_mesh_distance(const double* s6, uint64_t n, const double* t9, uint64_t m, int threads,
+                               double* dist, uint64_t* face);
+void or_points_mesh_distance(const double* p3, uint64_t n, const double* t9, uint64_t m, int threads,
+                             double* dist, uint64_t* face);
+void or_segments_mesh_intersects(const double* s6, uint64_t n, const double* t9, uint64_t m, int threads,
+                                 uint8_t* hit, uint64_t* face);
+
 /* table: per record r (faces offsets[r]..offsets[r+1]) vs the query mesh,
  * record as the first argument (batch.cpp:31 eval_distance(record, arg)). */
 void or_table_distance(const double* table9, const uint64_t* offsets, uint64_t n_objects,

@@ -110,6 +110,10 @@ _SIGS = [
     ("tdb_gen_terrain", ct.c_uint64, [ct.c_uint32, ct.c_uint32, ct.c_double, ct.c_uint64, _D]),
     ("tdb_fp64_peak", ct.c_int, [_D, _D]),
     ("tdb_mesh_volume", ct.c_int, [ct.c_void_p, ct.c_uint64, _D]),
+    ("tdb_segments_mesh_distance", ct.c_int, [_D, ct.c_uint64, ct.c_void_p, _D, _U64]),
+    ("tdb_points_mesh_distance", ct.c_int, [_D, ct.c_uint64, ct.c_void_p, _D, _U64]),
+    ("tdb_segments_mesh_intersects", ct.c_int, [_D, ct.c_uint64, ct.c_void_p, _U8, _U64]),
+    ("tdb_gen_drills", ct.c_uint64, [ct.c_uint64, ct.c_uint64, ct.c_int, _D]),
 ]
 EXPORTS = [s[0] for s in _SIGS]
 
@@ -356,6 +360,47 @@ def pairs_filter(a, b) -> np.ndarray:
     a, b = _f64(a), _f64(b)
     out = np.empty(len(a), np.float64)
     _check(lib().tdb_pairs_filter(_dp(a), _dp(b), len(a), _dp(out)))
+    return out
+
+
+def _qarr(q, width):
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    if q.size % width:
+        raise ValueError(f"queries hold {width} doubles each")
+    return q.reshape(-1, width)
+
+
+def segments_mesh_distance(segments, mesh):
+    """distance_to_mesh(segment, mesh) per segment (kernels.cpp:388):
+    (distance array, face index array; UINT64_MAX = none)."""
+    s, m = _qarr(segments, 6), _as_mesh(mesh)
+    d, f = np.empty(len(s)), np.empty(len(s), np.uint64)
+    _check(lib().tdb_segments_mesh_distance(_dp(s), len(s), m.handle, _dp(d), f.ctypes.data_as(_U64)))
+    return d, f
+
+
+def points_mesh_distance(points, mesh):
+    """distance_to_mesh(point, mesh) per point (kernels.cpp:382)."""
+    p, m = _qarr(points, 3), _as_mesh(mesh)
+    d, f = np.empty(len(p)), np.empty(len(p), np.uint64)
+    _check(lib().tdb_points_mesh_distance(_dp(p), len(p), m.handle, _dp(d), f.ctypes.data_as(_U64)))
+    return d, f
+
+
+def segments_mesh_intersects(segments, mesh):
+    """intersects_mesh(segment, mesh) per segment (kernels.cpp:407):
+    (hit array, lowest hit face array)."""
+    s, m = _qarr(segments, 6), _as_mesh(mesh)
+    h, f = np.empty(len(s), np.uint8), np.empty(len(s), np.uint64)
+    _check(lib().tdb_segments_mesh_intersects(_dp(s), len(s), m.handle, h.ctypes.data_as(_U8),
+                                              f.ctypes.data_as(_U64)))
+    return h.astype(bool), f
+
+
+def drills(count: int, seed: int = 42, style: int = 0) -> np.ndarray:
+    """make_drills (dataset.cpp:141-165): style 0 vertical jittered, 1 uniform."""
+    out = np.empty((count, 6), np.float64)
+    lib().tdb_gen_drills(seed, count, style, _dp(out))
     return out
 
 

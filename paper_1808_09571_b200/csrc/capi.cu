@@ -347,6 +347,30 @@ int tdb_pairs_filter(const double* a9, const double* b9, uint64_t n, double* d2)
     return rc;
 }
 
+int tdb_segments_mesh_distance(const double* seg6, uint64_t n, tdb_mesh mesh, double* dist_out, uint64_t* face_out) {
+    return guarded([&] {
+        need(mesh && (n == 0 || (seg6 && dist_out && face_out)), "null argument");
+        need(mesh->g.n_obj == 1, "the argument must be a mesh (one object)");
+        tdb::run_queries(ctx(), 0, TDB_OP_DISTANCE, seg6, n, mesh->g, dist_out, nullptr, face_out);
+    });
+}
+
+int tdb_points_mesh_distance(const double* pt3, uint64_t n, tdb_mesh mesh, double* dist_out, uint64_t* face_out) {
+    return guarded([&] {
+        need(mesh && (n == 0 || (pt3 && dist_out && face_out)), "null argument");
+        need(mesh->g.n_obj == 1, "the argument must be a mesh (one object)");
+        tdb::run_queries(ctx(), 1, TDB_OP_DISTANCE, pt3, n, mesh->g, dist_out, nullptr, face_out);
+    });
+}
+
+int tdb_segments_mesh_intersects(const double* seg6, uint64_t n, tdb_mesh mesh, uint8_t* hit_out, uint64_t* face_out) {
+    return guarded([&] {
+        need(mesh && (n == 0 || (seg6 && hit_out && face_out)), "null argument");
+        need(mesh->g.n_obj == 1, "the argument must be a mesh (one object)");
+        tdb::run_queries(ctx(), 0, TDB_OP_INTERSECTS, seg6, n, mesh->g, nullptr, hit_out, face_out);
+    });
+}
+
 int tdb_mesh_volume(tdb_mesh m, uint64_t chunk_size, double* volume_out) {
     return guarded([&] {
         need(m && volume_out, "null argument");

@@ -154,6 +154,36 @@ extern "C" uint64_t tdb_gen_ore_body(uint64_t face_target, double* out) {
     return faces;
 }
 
+// dataset.cpp:141-165 make_drills over the default DatasetSpec box; style 0 =
+// VerticalJittered (collar on the top face, tilted hole), 1 = UniformRandom.
+// Same mt19937_64 stream and the same draw order as the reference.
+extern "C" uint64_t tdb_gen_drills(uint64_t seed, uint64_t count, int style, double* out6) {
+    if (!out6) return count;
+    std::mt19937_64 eng(seed);
+    auto uniform = [&](double lo, double hi) { return lo + (hi - lo) * (double(eng() >> 11) * 0x1.0p-53); };
+    const P3 lo{0.0, 0.0, -400.0}, hi{1000.0, 1000.0, 0.0};
+    for (uint64_t i = 0; i < count; ++i) {
+        double* o = out6 + 6 * i;
+        if (style == 1) {
+            for (int e = 0; e < 2; ++e) {
+                o[3 * e] = uniform(lo.x, hi.x);
+                o[3 * e + 1] = uniform(lo.y, hi.y);
+                o[3 * e + 2] = uniform(lo.z, hi.z);
+            }
+            continue;
+        }
+        const double cx = uniform(lo.x, hi.x);
+        const double cy = uniform(lo.y, hi.y);
+        const double cz = hi.z;
+        const double depth = uniform(0.4, 1.0) * (hi.z - lo.z);
+        const double tx = uniform(-0.15, 0.15);
+        const double ty = uniform(-0.15, 0.15);
+        o[0] = cx, o[1] = cy, o[2] = cz;
+        o[3] = cx + tx * depth, o[4] = cy + ty * depth, o[5] = cz - depth;
+    }
+    return count;
+}
+
 extern "C" uint64_t tdb_gen_terrain(uint32_t nx, uint32_t ny, double amp, uint64_t seed,
                                     double* out) {
     const uint64_t faces = 2ull * nx * ny;

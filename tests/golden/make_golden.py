@@ -203,6 +203,24 @@ def main():
         gens[f"ore_body/{ft}"] = sha(O.ref_ore_body(ft))
     with open(os.path.join(OUT, "generators.json"), "w") as f:
         json.dump(gens, f, indent=1, sort_keys=True)
+    # segment / point x mesh (distance_to_mesh, intersects_mesh): the paper's
+    # drill workload (make_drills, dataset.cpp:141) plus uniform segments,
+    # zero-length segments and points, against a 512- and a 20,480-face ore
+    drills = O.ref_make_drills(42, 3000, 0)
+    unif = O.ref_make_drills(43, 2000, 1)
+    zero = drills[:64].copy()
+    zero[:, 3:] = zero[:, :3]
+    segs = np.concatenate([drills, unif, zero])
+    pts = np.random.default_rng(9).uniform([0, 0, -400], [1000, 1000, 0], (3000, 3))
+    q = {"segments": segs, "points": pts}
+    for name, ft in (("ore512", 500), ("ore20480", 20000)):
+        ore = O.ref_ore_body(ft)
+        d, f = O.ref_segments_mesh_distance(segs, ore)
+        h, hf = O.ref_segments_mesh_intersects(segs, ore)
+        pd, pf = O.ref_points_mesh_distance(pts, ore)
+        q.update({f"{name}/mesh": ore, f"{name}/seg_dist": d, f"{name}/seg_face": f, f"{name}/seg_hit": h,
+                  f"{name}/seg_hit_face": hf, f"{name}/pt_dist": pd, f"{name}/pt_face": pf})
+    np.savez_compressed(os.path.join(OUT, "queries.npz"), **q)
     # mesh_volume (kernels.cpp:27-46) bits for several chunk sizes
     import paper_1808_09571_b200 as T
     vol_meshes = {"sphere_1280": O.ref_unit_sphere(1000), "ore_81920": O.ref_ore_body(100_000),
