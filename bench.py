@@ -199,7 +199,77 @@ class TableWorkload:
         return max(1, int(10.0 * threads * 1e6 / (self.nf * self.M)))
 
 
+class QueryWorkload:
+    """The paper's own workload: drill segments
+    (make_drills, seed 42) x the ore body, per-segment distance_to_mesh /
+    intersects_mesh. A step is one batch of drills against the whole ore."""
+
+    table = False
+
+    def __init__(self, n_drills, face_target, op, batch):
+        self.name, self.op, self.n_drills, self.face_target, self.batch_rows = "paper", op, n_drills, face_target, batch
+        self.desc = (f"paper: {n_drills:,} drill segments (make_drills) x ore body ({face_target}-face target), "
+                     f"per-segment ST_3D{'Distance' if op == 'distance' else 'Intersects'} "
+                     "(PAPER.md:352-361: 5M x 500 faces, 0.685 s on V100)")
+
+    def build(self, T, ref=False):
+        import oracle as O
+        self.A = O.ref_make_drills(42, self.n_drills, 0) if (ref and O.REF is not None) else T.drills(self.n_drills, 42)
+        self.B = O.ref_ore_body(self.face_target) if (ref and O.REF is not None) else T.ore_body(self.face_target)
+        self.NA, self.M = len(self.A), len(self.B)
+        self.BR = min(self.batch_rows, self.NA)
+        self.n_batches = (self.NA + self.BR - 1) // self.BR
+
+    def batch(self, b):
+        b %= self.n_batches
+        return b * self.BR, min(self.NA, (b + 1) * self.BR)
+
+    def pairs(self, b):
+        r0, r1 = self.batch(b)
+        return (r1 - r0) * self.M
+
+    def upload(self, T):
+        self.dB = T.Mesh(self.B)
+
+    def run(self, T, b):
+        r0, r1 = self.batch(b)
+        if self.op == "distance":
+            d, f = T.segments_mesh_distance(self.A[r0:r1], self.dB)
+            k = int(np.argmin(d))
+            return float(d[k]), int(f[k])
+        h, f = T.segments_mesh_intersects(self.A[r0:r1], self.dB)
+        return (0.0, int(f[h].min())) if h.any() else (float("inf"), U64_MAX)
+
+    def run_host(self, T, pinA, pinB, b):
+        r0, r1 = self.batch(b)
+        m = T.Mesh(pinB)
+        if self.op == "distance":
+            res = T.segments_mesh_distance(pinA[r0:r1], m)
+        else:
+            res = T.segments_mesh_intersects(pinA[r0:r1], m)
+        m.free()
+        return res, (r1 - r0) * 48 + self.M * 72, (r1 - r0) * 16
+
+    def cpu_rate(self, rows, threads):
+        import oracle as O
+        rows = min(rows, self.NA)
+        kind = "reference" if O.REF is not None else "port"
+        f = {("distance", True): O.ref_segments_mesh_distance, ("distance", False): O.segments_mesh_distance,
+             ("intersects", True): O.ref_segments_mesh_intersects,
+             ("intersects", False): O.segments_mesh_intersects}[(self.op, O.REF is not None)]
+        t0 = time.perf_counter()
+        f(self.A[:rows], self.B, threads=threads)
+        dt = time.perf_counter() - t0
+        return rows * self.M / dt, dt, kind, f"{rows} drills x {self.M} ore faces ({rows * self.M:.3g} pairs)"
+
+    def cpu_default_rows(self, threads):
+        per_row = self.M / (3.0e6 if self.op == "distance" else 2.0e7)
+        return max(threads, int(10.0 * threads / max(per_row, 1e-9)))
+
+
 def workload(name, op_override, objects):
+    if name == "paper":
+        return QueryWorkload(5_000_000, 500, op_override or "distance", 5_000_000)
     def c1(T, ref):
         import oracle as O
         a = O.ref_unit_sphere(10000) if (ref and O.REF is not None) else T.unit_sphere(10000)
@@ -337,7 +407,7 @@ def main():
     ap.add_argument("--steps", type=int, default=16)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "paper"])
     ap.add_argument("--op", default=None, choices=[None, "distance", "intersects"])
     ap.add_argument("--batch-rows", type=int, default=0, help="A rows per step (0 = config default)")
     ap.add_argument("--objects", type=int, default=100_000, help="c4 table records")
@@ -445,9 +515,13 @@ def main():
     # ---- roofline of the roofline kernel -------------------------------------
     f_ms = sum(k_ms) / len(k_ms)
     f_pairs = sum(k_pairs) / len(k_pairs)
-    w = W_D if wl.op == "distance" else W_I
+    if wl.name == "paper":  # segment x triangle: SURVEY.md 8(a) A10 / A11 op counts
+        w = 473.0 if wl.op == "distance" else 75.0
+        kname = "q_filter_kernel" if wl.op == "distance" else "q_hit_kernel"
+    else:
+        w = W_D if wl.op == "distance" else W_I
+        kname = "filter_kernel" if wl.op == "distance" else "hit_kernel"
     achieved_tf = w * f_pairs / (f_ms * 1e-3) / 1e12
-    kname = "filter_kernel" if wl.op == "distance" else "hit_kernel"
     traffic = None
     try:  # DRAM bytes per pair from the committed ncu --set full capture, scaled to this launch
         tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))[kname]
@@ -459,13 +533,13 @@ def main():
         "frac": achieved_tf / fp64_tf, "traffic": traffic,
         "traffic_note": "dram__bytes_read+write per launch from profiles/traffic.json (ncu --set full), "
                         "scaled to this launch's pairs; algorithmic bytes = 288 B per B face per 128-row tile",
-        "kernel": "filter_kernel (fast_pair.cuh)" if wl.op == "distance" else "hit_kernel (intersects.cu)",
+        "kernel": kname,
         "work_per_pair_flops": w,
         "peak_source": "measured in this run: DFMA issue-rate microbenchmark (tdb_fp64_peak); "
                        "spec 148 SM x 64 FMA x 2 x 1.965 GHz = 37.2",
         "kernel_share_of_step": sum(k_ms) / ms if world == 1 else None,
     }
-    if wl.op == "distance":
+    if wl.op == "distance" and wl.name != "paper":
         roofline["fp64_pipe_frac"] = FILTER_DP_INSTR * f_pairs / (f_ms * 1e-3) / (fp64_tf * 1e12 / 2)
         roofline["executed_fp64_tflops"] = FILTER_FLOPS * f_pairs / (f_ms * 1e-3) / 1e12
     else:
