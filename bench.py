@@ -230,14 +230,15 @@ class QueryWorkload:
 
     def upload(self, T):
         self.dB = T.Mesh(self.B)
+        self.dQ = [T.Queries(self.A[slice(*self.batch(b))]) for b in range(self.n_batches)]
 
     def run(self, T, b):
-        r0, r1 = self.batch(b)
+        q = self.dQ[b % self.n_batches]
         if self.op == "distance":
-            d, f = T.segments_mesh_distance(self.A[r0:r1], self.dB)
+            d, f = T.queries_mesh_distance(q, self.dB)
             k = int(np.argmin(d))
             return float(d[k]), int(f[k])
-        h, f = T.segments_mesh_intersects(self.A[r0:r1], self.dB)
+        h, f = T.queries_mesh_intersects(q, self.dB)
         return (0.0, int(f[h].min())) if h.any() else (float("inf"), U64_MAX)
 
     def run_host(self, T, pinA, pinB, b):

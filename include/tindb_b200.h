@@ -135,6 +135,13 @@ int tdb_table_eval_rows(int op, tdb_table records, uint64_t obj_begin, uint64_t 
  * (kernels.hpp:80-84, kernels.cpp:407-432: lowest hit face). face_out =
  * UINT64_MAX when there is none. Queries are host arrays: segments are 6
  * doubles (p0 xyz, p1 xyz, geometry.hpp:46-54), points 3. */
+typedef struct tdb_queries_s* tdb_queries; /* device-resident segment or point column */
+enum { TDB_QUERY_SEGMENTS = 0, TDB_QUERY_POINTS = 1 };
+int tdb_queries_upload(const double* q, uint64_t n, int kind, tdb_queries* out);
+void tdb_queries_free(tdb_queries q);
+int tdb_queries_mesh_distance(tdb_queries q, tdb_mesh mesh, double* dist_out, uint64_t* face_out);
+int tdb_queries_mesh_intersects(tdb_queries q, tdb_mesh mesh, uint8_t* hit_out, uint64_t* face_out);
+/* one-shot forms: upload the host queries, evaluate, free */
 int tdb_segments_mesh_distance(const double* seg6, uint64_t n, tdb_mesh mesh, double* dist_out,
                                uint64_t* face_out);
 int tdb_points_mesh_distance(const double* pt3, uint64_t n, tdb_mesh mesh, double* dist_out,

@@ -114,6 +114,10 @@ _SIGS = [
     ("tdb_points_mesh_distance", ct.c_int, [_D, ct.c_uint64, ct.c_void_p, _D, _U64]),
     ("tdb_segments_mesh_intersects", ct.c_int, [_D, ct.c_uint64, ct.c_void_p, _U8, _U64]),
     ("tdb_gen_drills", ct.c_uint64, [ct.c_uint64, ct.c_uint64, ct.c_int, _D]),
+    ("tdb_queries_upload", ct.c_int, [_D, ct.c_uint64, ct.c_int, ct.POINTER(ct.c_void_p)]),
+    ("tdb_queries_free", None, [ct.c_void_p]),
+    ("tdb_queries_mesh_distance", ct.c_int, [ct.c_void_p, ct.c_void_p, _D, _U64]),
+    ("tdb_queries_mesh_intersects", ct.c_int, [ct.c_void_p, ct.c_void_p, _U8, _U64]),
 ]
 EXPORTS = [s[0] for s in _SIGS]
 
@@ -370,9 +374,55 @@ def _qarr(q, width):
     return q.reshape(-1, width)
 
 
+QUERY_SEGMENTS, QUERY_POINTS = 0, 1
+
+
+class Queries:
+    """A device-resident column of segments (6 doubles) or points (3)."""
+
+    def __init__(self, q, kind=QUERY_SEGMENTS):
+        a = _qarr(q, 6 if kind == QUERY_SEGMENTS else 3)
+        h = ct.c_void_p()
+        _check(lib().tdb_queries_upload(_dp(a), len(a), kind, ct.byref(h)))
+        self._h, self.n, self.kind = h, len(a), kind
+
+    @property
+    def handle(self):
+        return self._h
+
+    def free(self):
+        if self._h is not None and self._h.value:
+            lib().tdb_queries_free(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def queries_mesh_distance(q: Queries, mesh):
+    """distance_to_mesh per resident query: (distance, face) arrays."""
+    m = _as_mesh(mesh)
+    d, f = np.empty(q.n), np.empty(q.n, np.uint64)
+    _check(lib().tdb_queries_mesh_distance(q.handle, m.handle, _dp(d), f.ctypes.data_as(_U64)))
+    return d, f
+
+
+def queries_mesh_intersects(q: Queries, mesh):
+    """intersects_mesh per resident segment: (hit, lowest hit face) arrays."""
+    m = _as_mesh(mesh)
+    h, f = np.empty(q.n, np.uint8), np.empty(q.n, np.uint64)
+    _check(lib().tdb_queries_mesh_intersects(q.handle, m.handle, h.ctypes.data_as(_U8), f.ctypes.data_as(_U64)))
+    return h.astype(bool), f
+
+
 def segments_mesh_distance(segments, mesh):
     """distance_to_mesh(segment, mesh) per segment (kernels.cpp:388):
     (distance array, face index array; UINT64_MAX = none)."""
+    if isinstance(segments, Queries):
+        return queries_mesh_distance(segments, mesh)
     s, m = _qarr(segments, 6), _as_mesh(mesh)
     d, f = np.empty(len(s)), np.empty(len(s), np.uint64)
     _check(lib().tdb_segments_mesh_distance(_dp(s), len(s), m.handle, _dp(d), f.ctypes.data_as(_U64)))
@@ -381,6 +431,8 @@ def segments_mesh_distance(segments, mesh):
 
 def points_mesh_distance(points, mesh):
     """distance_to_mesh(point, mesh) per point (kernels.cpp:382)."""
+    if isinstance(points, Queries):
+        return queries_mesh_distance(points, mesh)
     p, m = _qarr(points, 3), _as_mesh(mesh)
     d, f = np.empty(len(p)), np.empty(len(p), np.uint64)
     _check(lib().tdb_points_mesh_distance(_dp(p), len(p), m.handle, _dp(d), f.ctypes.data_as(_U64)))
@@ -390,6 +442,8 @@ def points_mesh_distance(points, mesh):
 def segments_mesh_intersects(segments, mesh):
     """intersects_mesh(segment, mesh) per segment (kernels.cpp:407):
     (hit array, lowest hit face array)."""
+    if isinstance(segments, Queries):
+        return queries_mesh_intersects(segments, mesh)
     s, m = _qarr(segments, 6), _as_mesh(mesh)
     h, f = np.empty(len(s), np.uint8), np.empty(len(s), np.uint64)
     _check(lib().tdb_segments_mesh_intersects(_dp(s), len(s), m.handle, h.ctypes.data_as(_U8),

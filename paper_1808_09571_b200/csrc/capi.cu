@@ -21,6 +21,10 @@ struct tdb_geom_s {
     tdb::Geom g;
 };
 
+struct tdb_queries_s {
+    tdb::QuerySet q;
+};
+
 namespace {
 
 thread_local std::string t_err;
@@ -347,28 +351,73 @@ int tdb_pairs_filter(const double* a9, const double* b9, uint64_t n, double* d2)
     return rc;
 }
 
-int tdb_segments_mesh_distance(const double* seg6, uint64_t n, tdb_mesh mesh, double* dist_out, uint64_t* face_out) {
+int tdb_queries_upload(const double* q, uint64_t n, int kind, tdb_queries* out) {
     return guarded([&] {
-        need(mesh && (n == 0 || (seg6 && dist_out && face_out)), "null argument");
-        need(mesh->g.n_obj == 1, "the argument must be a mesh (one object)");
-        tdb::run_queries(ctx(), 0, TDB_OP_DISTANCE, seg6, n, mesh->g, dist_out, nullptr, face_out);
+        need(out != nullptr, "null output handle");
+        need(n == 0 || q != nullptr, "null query array");
+        need(kind == TDB_QUERY_SEGMENTS || kind == TDB_QUERY_POINTS, "unknown query kind");
+        tdb::Ctx c = ctx();
+        auto* h = new tdb_queries_s();
+        h->q.device = t_device;
+        try {
+            tdb::queries_build(&h->q, q, n, kind == TDB_QUERY_SEGMENTS ? tdb::kQuerySegments : tdb::kQueryPoints,
+                               c.stream);
+        } catch (...) {
+            cudaFree(h->q.planes);
+            delete h;
+            throw;
+        }
+        *out = h;
     });
+}
+
+void tdb_queries_free(tdb_queries q) {
+    if (!q) return;
+    cudaSetDevice(q->q.device);
+    cudaFree(q->q.planes);
+    delete q;
+}
+
+int tdb_queries_mesh_distance(tdb_queries q, tdb_mesh mesh, double* dist_out, uint64_t* face_out) {
+    return guarded([&] {
+        need(q && mesh && (q->q.n == 0 || (dist_out && face_out)), "null argument");
+        need(mesh->g.n_obj == 1, "the argument must be a mesh (one object)");
+        tdb::run_queries(ctx(), TDB_OP_DISTANCE, q->q, mesh->g, dist_out, nullptr, face_out);
+    });
+}
+
+int tdb_queries_mesh_intersects(tdb_queries q, tdb_mesh mesh, uint8_t* hit_out, uint64_t* face_out) {
+    return guarded([&] {
+        need(q && mesh && (q->q.n == 0 || (hit_out && face_out)), "null argument");
+        need(q->q.kind == tdb::kQuerySegments, "intersects takes segment queries (intersects_mesh, kernels.hpp:80)");
+        need(mesh->g.n_obj == 1, "the argument must be a mesh (one object)");
+        tdb::run_queries(ctx(), TDB_OP_INTERSECTS, q->q, mesh->g, nullptr, hit_out, face_out);
+    });
+}
+
+static int one_shot_queries(const double* q, uint64_t n, int kind, int op, tdb_mesh mesh, double* dist,
+                            uint8_t* hit, uint64_t* face) {
+    tdb_queries qs = nullptr;
+    int rc = tdb_queries_upload(q, n, kind, &qs);
+    if (rc == TDB_OK)
+        rc = op == TDB_OP_DISTANCE ? tdb_queries_mesh_distance(qs, mesh, dist, face)
+                                   : tdb_queries_mesh_intersects(qs, mesh, hit, face);
+    const std::string err = t_err;
+    tdb_queries_free(qs);
+    t_err = err;
+    return rc;
+}
+
+int tdb_segments_mesh_distance(const double* seg6, uint64_t n, tdb_mesh mesh, double* dist_out, uint64_t* face_out) {
+    return one_shot_queries(seg6, n, TDB_QUERY_SEGMENTS, TDB_OP_DISTANCE, mesh, dist_out, nullptr, face_out);
 }
 
 int tdb_points_mesh_distance(const double* pt3, uint64_t n, tdb_mesh mesh, double* dist_out, uint64_t* face_out) {
-    return guarded([&] {
-        need(mesh && (n == 0 || (pt3 && dist_out && face_out)), "null argument");
-        need(mesh->g.n_obj == 1, "the argument must be a mesh (one object)");
-        tdb::run_queries(ctx(), 1, TDB_OP_DISTANCE, pt3, n, mesh->g, dist_out, nullptr, face_out);
-    });
+    return one_shot_queries(pt3, n, TDB_QUERY_POINTS, TDB_OP_DISTANCE, mesh, dist_out, nullptr, face_out);
 }
 
 int tdb_segments_mesh_intersects(const double* seg6, uint64_t n, tdb_mesh mesh, uint8_t* hit_out, uint64_t* face_out) {
-    return guarded([&] {
-        need(mesh && (n == 0 || (seg6 && hit_out && face_out)), "null argument");
-        need(mesh->g.n_obj == 1, "the argument must be a mesh (one object)");
-        tdb::run_queries(ctx(), 0, TDB_OP_INTERSECTS, seg6, n, mesh->g, nullptr, hit_out, face_out);
-    });
+    return one_shot_queries(seg6, n, TDB_QUERY_SEGMENTS, TDB_OP_INTERSECTS, mesh, nullptr, hit_out, face_out);
 }
 
 int tdb_mesh_volume(tdb_mesh m, uint64_t chunk_size, double* volume_out) {

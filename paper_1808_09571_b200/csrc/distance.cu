@@ -63,7 +63,7 @@ __device__ __forceinline__ double warp_min_nn(double x) {
 #define TDB_FILTER_MINB 3
 #endif
 __global__ void __launch_bounds__(kTile, TDB_FILTER_MINB) filter_kernel(DistArgs a) {
-    __shared__ alignas(128) double sm[2][NF * kSB];
+    __shared__ alignas(128) double sm[2][kFilterPlanes * kSB];
     __shared__ alignas(8) uint64_t bar[2];
     __shared__ double red[kTile / 32];
 
@@ -100,9 +100,9 @@ __global__ void __launch_bounds__(kTile, TDB_FILTER_MINB) filter_kernel(DistArgs
         const uint64_t f0 = b0 + (uint64_t)s * kSB;
         const int cnt = (int)min((uint64_t)kSB, b1 - f0);
         const uint32_t bytes = (uint32_t)(((cnt + 1) & ~1) * sizeof(double));
-        mbar_expect_tx(&bar[st], bytes * NF);
+        mbar_expect_tx(&bar[st], bytes * kFilterPlanes);
 #pragma unroll 1
-        for (int f = 0; f < NF; ++f) bulk_g2s(&sm[st][f * kSB], a.Bp + (uint64_t)f * a.Bn_pad + f0, bytes, &bar[st]);
+        for (int f = 0; f < kFilterPlanes; ++f) bulk_g2s(&sm[st][f * kSB], a.Bp + (uint64_t)f * a.Bn_pad + f0, bytes, &bar[st]);
     };
     if (threadIdx.x == 0) {
         issue(0);

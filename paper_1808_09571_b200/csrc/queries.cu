@@ -12,12 +12,20 @@
 //              face whose segment_triangle_intersect hits (every face is
 //              tested, degenerate ones through the exact predicate)
 //
-// Layout: queries are uploaded per call into SoA planes; a CTA holds 128
-// queries (one per thread) and streams a B chunk through shared memory with
-// TMA bulk copies. Filter values are high-word truncated squared distances
-// (fast_pair.cuh conventions); the exact pass re-evaluates, with the
-// bit-exact reference primitives (exact.cuh), every (query, face) whose
-// filter value lies inside the query's band.
+// Layout: a query set lives in HBM as SoA planes (uploaded once, reusable);
+// a CTA holds 128 queries (one per thread) and streams the mesh through
+// shared memory with TMA bulk copies. Filter values are high-word truncated
+// squared distances (fast_pair.cuh conventions); the exact pass re-evaluates,
+// with the bit-exact reference primitives (exact.cuh), every (query, face)
+// whose filter value lies inside the query's band.
+//
+// Two distance paths:
+//   * fused (the mesh fits one work chunk, e.g. the paper's 500-face ore):
+//     one kernel — filter over the mesh, the query's band from its own
+//     minimum, an exact rescan of the in-band faces, the band check — every
+//     answer final inside the CTA;
+//   * chunked (large meshes): filter -> per-query band -> flagged items ->
+//     exact rescans (as distance.cu).
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -31,7 +39,6 @@ namespace tdb {
 namespace {
 
 constexpr unsigned long long kNone = ~0ull;
-enum { QK_SEG = 0, QK_POINT = 1 };
 
 struct QArgs {
     const double* Q;  // query planes: 6 (segments: p0 xyz, p1 xyz) or 3 (points), stride Qpad
@@ -43,13 +50,72 @@ struct QArgs {
     unsigned long long* qmin;
 };
 
+// ---- TMA-staged streaming of B faces [b0, b1) through 2 SMEM stages ------
+// `g` counts sub-tiles across calls so the mbarrier phases stay consistent
+// when one kernel streams the same range several times.
+template <int NP>
+struct Stream {
+    double (*sm)[NP * kSB];
+    uint64_t* bar;
+    const int* plane;
+    uint32_t g = 0;
+
+    __device__ void init() {
+        if (threadIdx.x == 0) {
+            mbar_init(&bar[0], 1);
+            mbar_init(&bar[1], 1);
+            mbar_fence_init();
+        }
+        __syncthreads();
+    }
+
+    __device__ void issue(const double* Bp, uint64_t pad, uint64_t b0, uint64_t b1, uint32_t s) {
+        const int st = (g + s) & 1;
+        const uint64_t f0 = b0 + (uint64_t)s * kSB;
+        const int cnt = (int)min((uint64_t)kSB, b1 - f0);
+        const uint32_t bytes = (uint32_t)(((cnt + 1) & ~1) * sizeof(double));
+        mbar_expect_tx(&bar[st], bytes * NP);
+#pragma unroll 1
+        for (int f = 0; f < NP; ++f) bulk_g2s(&sm[st][f * kSB], Bp + (uint64_t)plane[f] * pad + f0, bytes, &bar[st]);
+    }
+
+    // fn(sb, cnt, f0) per staged sub-tile; must be called by every thread
+    template <class F>
+    __device__ void run(const double* Bp, uint64_t pad, uint64_t b0, uint64_t b1, F&& fn) {
+        const uint32_t nsub = (uint32_t)((b1 - b0 + kSB - 1) / kSB);
+        if (threadIdx.x == 0) {
+            if (nsub > 0) issue(Bp, pad, b0, b1, 0);
+            if (nsub > 1) issue(Bp, pad, b0, b1, 1);
+        }
+#pragma unroll 1
+        for (uint32_t s = 0; s < nsub; ++s) {
+            const int st = (g + s) & 1;
+            mbar_wait(&bar[st], ((g + s) >> 1) & 1);
+            const uint64_t f0 = b0 + (uint64_t)s * kSB;
+            fn(sm[st], (int)min((uint64_t)kSB, b1 - f0), f0);
+            __syncthreads();
+            if (threadIdx.x == 0 && s + 2 < nsub) issue(Bp, pad, b0, b1, s + 2);
+        }
+        g += nsub;
+    }
+};
+
+__device__ __constant__ int kDistPlaneIds[kFilterPlanes] = {0,  1,  2,  3,  4,  5,  6,  7,  8,  9,  10, 11,
+                                                             12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22, 23,
+                                                             24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34};
+constexpr int kHitPlanes = 20;  // V (9), N (3), C, DEG, face AABB lo/hi (6)
+__device__ __constant__ int kHitPlaneIds[kHitPlanes] = {0,   1,   2,       3,       4,       5,       6,
+                                                         7,   8,   F_N,     F_N + 1, F_N + 2, F_C,     F_DEG,
+                                                         F_LO, F_LO + 1, F_LO + 2, F_HI, F_HI + 1, F_HI + 2};
+enum { HP_N = 9, HP_C = 12, HP_DEG = 13, HP_LO = 14, HP_HI = 17 };
+
 // ---- filter values -----------------------------------------------------------
 // point P vs face B: vertex/face projection + the three clamped point/edge
 // distances.
 template <class P>
 __device__ __forceinline__ int pt_d2(double px, double py, double pz, const P& bt) {
     const double qx = px - bt(F_V), qy = py - bt(F_V + 1), qz = pz - bt(F_V + 2);
-    int best = kInfHi, hmin = kInfHi;
+    int best = kInfHi, hmin;
     {
         const double nb[3] = {bt(F_N), bt(F_N + 1), bt(F_N + 2)};
         const double ub[3] = {bt(F_U), bt(F_U + 1), bt(F_U + 2)};
@@ -73,7 +139,7 @@ __device__ __forceinline__ int pt_d2(double px, double py, double pz, const P& b
 // and the three clamped segment/edge distances (Ericson, as in pair_d2).
 template <class P>
 __device__ __forceinline__ int seg_d2(const double p0[3], const double d[3], double Ld, double ILd, const P& bt) {
-    int best = kInfHi, hmin = kInfHi;
+    int best = kInfHi, hmin;
     double w[3][3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -126,7 +192,7 @@ __device__ __forceinline__ int seg_d2(const double p0[3], const double d[3], dou
 }
 
 struct QueryRegs {
-    double p0[3], d[3], Ld, ILd;
+    double p0[3], p1[3], d[3], Ld, ILd;
     bool point;  // a point query, or a zero-length segment (kernels.cpp:388)
 };
 
@@ -134,17 +200,17 @@ __device__ __forceinline__ QueryRegs load_query(const QArgs& a, uint64_t q) {
     QueryRegs r;
 #pragma unroll
     for (int k = 0; k < 3; ++k) r.p0[k] = __ldg(a.Q + (uint64_t)k * a.Qpad + q);
-    if (a.kind == QK_SEG) {
-        double p1[3];
+    if (a.kind == kQuerySegments) {
 #pragma unroll
-        for (int k = 0; k < 3; ++k) p1[k] = __ldg(a.Q + (uint64_t)(3 + k) * a.Qpad + q);
-        r.point = p1[0] == r.p0[0] && p1[1] == r.p0[1] && p1[2] == r.p0[2];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) r.d[k] = p1[k] - r.p0[k];
+        for (int k = 0; k < 3; ++k) r.p1[k] = __ldg(a.Q + (uint64_t)(3 + k) * a.Qpad + q);
+        r.point = r.p1[0] == r.p0[0] && r.p1[1] == r.p0[1] && r.p1[2] == r.p0[2];
     } else {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) r.p1[k] = r.p0[k];
         r.point = true;
-        r.d[0] = r.d[1] = r.d[2] = 0.0;
     }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) r.d[k] = r.p1[k] - r.p0[k];
     r.Ld = fma(r.d[0], r.d[0], fma(r.d[1], r.d[1], r.d[2] * r.d[2]));
     r.ILd = r.Ld > 0.0 ? 1.0 / r.Ld : 0.0;
     return r;
@@ -156,51 +222,102 @@ __device__ __forceinline__ double query_d2(const QueryRegs& Q, const P& bt) {
     return __hiloint2double(h, 0);
 }
 
+// the reference primitive for one (query, face): distance bits
+__device__ __forceinline__ unsigned long long exact_bits(const QueryRegs& Q, const double* sb, int j) {
+    const double* bv = sb + j;
+    const exact::tri t{{bv[0], bv[kSB], bv[2 * kSB]}, {bv[3 * kSB], bv[4 * kSB], bv[5 * kSB]},
+                       {bv[6 * kSB], bv[7 * kSB], bv[8 * kSB]}};
+    const exact::v3 p0{Q.p0[0], Q.p0[1], Q.p0[2]}, p1{Q.p1[0], Q.p1[1], Q.p1[2]};
+    const double d = Q.point ? exact::pt_tri(p0, t).d : exact::seg_tri(p0, p1, t).d;
+    return (unsigned long long)__double_as_longlong(d);
+}
+
+// eta of one query: max edge over B and the segment, max |coord| over both
+__device__ __forceinline__ double q_eta(const QueryRegs& Q, const double* Bs) {
+    double ext = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) ext = fmax(ext, fmax(fabs(Q.p0[k]), fabs(Q.p1[k])));
+    return kBandEdge * fmax(Bs[6], sqrt(Q.Ld)) + kBandAbs * fmax(Bs[7], ext);
+}
+
+// ---- fused path: the whole mesh is one chunk --------------------------------
+__global__ void __launch_bounds__(kTile, 3) q_fused_kernel(QArgs a, const double* Bs, double* out_d,
+                                                           unsigned long long* out_f, unsigned long long* ncand,
+                                                           unsigned long long* nrounds) {
+    __shared__ alignas(128) double sm[2][kFilterPlanes * kSB];
+    __shared__ alignas(8) uint64_t bar[2];
+    Stream<kFilterPlanes> S{sm, bar, kDistPlaneIds};
+    S.init();
+    const uint64_t qi = (uint64_t)blockIdx.x * kTile + threadIdx.x;
+    const bool active = qi < a.Qn;
+    const uint64_t q = min(qi, a.Qn - 1);
+    const QueryRegs Q = load_query(a, q);
+    double best = pos_inf();
+    S.run(a.Bp, a.Bn_pad, 0, a.Bn, [&](const double* sb, int cnt, uint64_t) {
+#pragma unroll 1
+        for (int j = 0; j < cnt; ++j) {
+            if (reinterpret_cast<const int*>(sb + F_DEG * kSB + j)[1] != 0) continue;  // degenerate face
+            best = min_nn(best, query_d2(Q, FaceRef{sb + j, (uint64_t)kSB}));
+        }
+    });
+    const double eta = q_eta(Q, Bs);
+    double band = active && best < pos_inf() ? sqrt(best) * (1.0 + kBandRel) + 2.0 * eta : -1.0;
+    unsigned long long D = kNone, P = kNone, cand = 0;
+    bool again = band >= 0.0;
+    int rounds = 0;
+    while (__syncthreads_or(again)) {  // exact rescan; repeats only when a band must widen
+        ++rounds;
+        const double b2 = again ? band * band * (1.0 + 4e-16) : -1.0;
+        if (again) D = P = kNone;
+        S.run(a.Bp, a.Bn_pad, 0, a.Bn, [&](const double* sb, int cnt, uint64_t f0) {
+#pragma unroll 1
+            for (int j = 0; j < cnt; ++j) {
+                if (reinterpret_cast<const int*>(sb + F_DEG * kSB + j)[1] != 0) continue;
+                if (b2 < 0.0) continue;
+                if (query_d2(Q, FaceRef{sb + j, (uint64_t)kSB}) > b2) continue;
+                ++cand;
+                const unsigned long long e = exact_bits(Q, sb, j);
+                if (e < D) D = e, P = f0 + j;  // ascending faces: strict < keeps the lowest index
+            }
+        });
+        if (again) {
+            if (D != kNone && __longlong_as_double((long long)D) > band - eta) {
+                band = __longlong_as_double((long long)D) * (1.0 + kBandRel) + 2.0 * eta;
+            } else {
+                again = false;
+            }
+        }
+        if (rounds >= 8) break;
+    }
+    if (active) {
+        out_d[q] = P == kNone ? pos_inf() : __longlong_as_double((long long)D);
+        out_f[q] = P;
+    }
+    if (cand) atomicAdd(ncand, cand);
+    if (threadIdx.x == 0) atomicMax(nrounds, (unsigned long long)rounds);
+}
+
+// ---- chunked path -------------------------------------------------------------
 __global__ void __launch_bounds__(kTile, 4) q_filter_kernel(QArgs a) {
-    __shared__ alignas(128) double sm[2][NF * kSB];
+    __shared__ alignas(128) double sm[2][kFilterPlanes * kSB];
     __shared__ alignas(8) uint64_t bar[2];
     __shared__ double red[kTile / 32];
+    Stream<kFilterPlanes> S{sm, bar, kDistPlaneIds};
+    S.init();
     const uint64_t item = blockIdx.x;
     const uint64_t tl = item / a.n_chunks, ch = item - tl * a.n_chunks;
     const uint64_t q = min(tl * kTile + threadIdx.x, a.Qn - 1);
     const bool active = tl * kTile + threadIdx.x < a.Qn;
     const QueryRegs Q = load_query(a, q);
     const uint64_t b0 = ch * a.chunk, b1 = min(a.Bn, b0 + a.chunk);
-    const int nsub = (int)((b1 - b0 + kSB - 1) / kSB);
-    if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        mbar_fence_init();
-    }
-    __syncthreads();
-    auto issue = [&](int s) {
-        const int st = s & 1;
-        const uint64_t f0 = b0 + (uint64_t)s * kSB;
-        const int cnt = (int)min((uint64_t)kSB, b1 - f0);
-        const uint32_t bytes = (uint32_t)(((cnt + 1) & ~1) * sizeof(double));
-        mbar_expect_tx(&bar[st], bytes * NF);
-#pragma unroll 1
-        for (int f = 0; f < NF; ++f) bulk_g2s(&sm[st][f * kSB], a.Bp + (uint64_t)f * a.Bn_pad + f0, bytes, &bar[st]);
-    };
-    if (threadIdx.x == 0) {
-        issue(0);
-        if (nsub > 1) issue(1);
-    }
     double best = pos_inf();
-#pragma unroll 1
-    for (int s = 0; s < nsub; ++s) {
-        const int st = s & 1;
-        mbar_wait(&bar[st], (uint32_t)((s >> 1) & 1));
-        const int cnt = (int)min((uint64_t)kSB, b1 - (b0 + (uint64_t)s * kSB));
-        const double* sb = sm[st];
+    S.run(a.Bp, a.Bn_pad, b0, b1, [&](const double* sb, int cnt, uint64_t) {
 #pragma unroll 1
         for (int j = 0; j < cnt; ++j) {
-            if (reinterpret_cast<const int*>(sb + F_DEG * kSB + j)[1] != 0) continue;  // degenerate face
+            if (reinterpret_cast<const int*>(sb + F_DEG * kSB + j)[1] != 0) continue;
             best = min_nn(best, query_d2(Q, FaceRef{sb + j, (uint64_t)kSB}));
         }
-        __syncthreads();
-        if (threadIdx.x == 0 && s + 2 < nsub) issue(s + 2);
-    }
+    });
     if (!active) best = pos_inf();
     if (active && best < pos_inf()) atomicMin(a.qmin + q, (unsigned long long)__double_as_longlong(best));
     double m = best;
@@ -216,14 +333,6 @@ __global__ void __launch_bounds__(kTile, 4) q_filter_kernel(QArgs a) {
     }
 }
 
-// eta of one query: max edge over B and the segment, max |coord| over both
-__device__ __forceinline__ double q_eta(const QArgs& a, uint64_t q, const double* Bs) {
-    const QueryRegs Q = load_query(a, q);
-    double ext = fmax(fabs(Q.p0[0]), fmax(fabs(Q.p0[1]), fabs(Q.p0[2])));
-    ext = fmax(ext, fmax(fabs(Q.p0[0] + Q.d[0]), fmax(fabs(Q.p0[1] + Q.d[1]), fabs(Q.p0[2] + Q.d[2]))));
-    return kBandEdge * fmax(Bs[6], sqrt(Q.Ld)) + kBandAbs * fmax(Bs[7], ext);
-}
-
 __global__ void q_band_kernel(QArgs a, const double* Bs, double* band2, double* band, unsigned long long* qD,
                               unsigned long long* qP) {
     const uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -235,7 +344,7 @@ __global__ void q_band_kernel(QArgs a, const double* Bs, double* band2, double* 
         band2[q] = band[q] = -1.0;
         return;
     }
-    const double b = sqrt(__longlong_as_double((long long)e)) * (1.0 + kBandRel) + 2.0 * q_eta(a, q, Bs);
+    const double b = sqrt(__longlong_as_double((long long)e)) * (1.0 + kBandRel) + 2.0 * q_eta(load_query(a, q), Bs);
     band[q] = b;
     band2[q] = b * b * (1.0 + 4e-16);
 }
@@ -251,52 +360,37 @@ __global__ void q_flag_kernel(QArgs a, uint64_t n_items, const double* band2, un
     if (bmax >= 0.0 && a.itemmin[item] <= bmax) list[atomicAdd(count, 1ull)] = item;
 }
 
-__device__ __forceinline__ exact::tri tri_at(const double* P, uint64_t pad, uint64_t i) {
-    double v[9];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) v[k] = __ldg(P + (uint64_t)(F_V + k) * pad + i);
-    return exact::tri{{v[0], v[1], v[2]}, {v[3], v[4], v[5]}, {v[6], v[7], v[8]}};
-}
-
-__global__ void __launch_bounds__(kTile) q_verify_kernel(QArgs a, const unsigned long long* list,
-                                                         const unsigned long long* count, int nsplit, int pass,
-                                                         const double* band2, unsigned long long* qD,
-                                                         unsigned long long* qP, unsigned long long* ncand) {
-    const uint64_t units = *count * (uint64_t)nsplit;
-    for (uint64_t w = blockIdx.x; w < units; w += gridDim.x) {
-        const uint64_t item = list[w / nsplit];
-        const int part = (int)(w % nsplit);
-        const uint64_t tl = item / a.n_chunks, ch = item - tl * a.n_chunks;
-        const uint64_t q = min(tl * kTile + threadIdx.x, a.Qn - 1);
-        const bool active = tl * kTile + threadIdx.x < a.Qn;
-        const QueryRegs Q = load_query(a, q);
-        const uint64_t c0 = ch * a.chunk, c1 = min(a.Bn, c0 + a.chunk);
-        const uint64_t len = (c1 - c0 + nsplit - 1) / nsplit;
-        const uint64_t b0 = c0 + part * len, b1 = min(c1, b0 + len);
-        const double b2 = active ? band2[q] : -1.0;
-        const exact::v3 p0{Q.p0[0], Q.p0[1], Q.p0[2]};
-        const exact::v3 p1{Q.p0[0] + Q.d[0], Q.p0[1] + Q.d[1], Q.p0[2] + Q.d[2]};
-        for (uint64_t j = b0; j < b1; ++j) {
-            if (__ldg(a.Bp + (uint64_t)F_DEG * a.Bn_pad + j) != 0.0) continue;
-            const double d2 = query_d2(Q, FaceRefLdg{a.Bp + j, a.Bn_pad});
-            if (d2 <= b2) {
-                const exact::tri t = tri_at(a.Bp, a.Bn_pad, j);
-                // the exact endpoints: p1 re-read (p0 + (p1 - p0) need not round-trip)
-                exact::v3 e1 = p0;
-                if (a.kind == QK_SEG)
-                    e1 = exact::v3{__ldg(a.Q + 3 * a.Qpad + q), __ldg(a.Q + 4 * a.Qpad + q), __ldg(a.Q + 5 * a.Qpad + q)};
-                const double dx = a.kind == QK_SEG ? exact::seg_tri(p0, e1, t).d : exact::pt_tri(p0, t).d;
-                const unsigned long long bits = (unsigned long long)__double_as_longlong(dx);
-                if (pass == 1) {
-                    atomicMin(qD + q, bits);
-                    atomicAdd(ncand, 1ull);
-                } else if (bits == qD[q]) {
-                    atomicMin(qP + q, (unsigned long long)j);
-                }
+// exact rescan of flagged items, TMA-staged like the filter
+__global__ void __launch_bounds__(kTile, 4) q_verify_kernel(QArgs a, const unsigned long long* list, int pass,
+                                                            const double* band2, unsigned long long* qD,
+                                                            unsigned long long* qP, unsigned long long* ncand) {
+    __shared__ alignas(128) double sm[2][kFilterPlanes * kSB];
+    __shared__ alignas(8) uint64_t bar[2];
+    Stream<kFilterPlanes> S{sm, bar, kDistPlaneIds};
+    S.init();
+    const uint64_t item = list[blockIdx.x];
+    const uint64_t tl = item / a.n_chunks, ch = item - tl * a.n_chunks;
+    const uint64_t q = min(tl * kTile + threadIdx.x, a.Qn - 1);
+    const bool active = tl * kTile + threadIdx.x < a.Qn;
+    const QueryRegs Q = load_query(a, q);
+    const uint64_t b0 = ch * a.chunk, b1 = min(a.Bn, b0 + a.chunk);
+    const double b2 = active ? band2[q] : -1.0;
+    unsigned long long cand = 0;
+    S.run(a.Bp, a.Bn_pad, b0, b1, [&](const double* sb, int cnt, uint64_t f0) {
+#pragma unroll 1
+        for (int j = 0; j < cnt; ++j) {
+            if (reinterpret_cast<const int*>(sb + F_DEG * kSB + j)[1] != 0) continue;
+            if (b2 < 0.0 || query_d2(Q, FaceRef{sb + j, (uint64_t)kSB}) > b2) continue;
+            const unsigned long long e = exact_bits(Q, sb, j);
+            if (pass == 1) {
+                atomicMin(qD + q, e);
+                ++cand;
+            } else if (e == qD[q]) {
+                atomicMin(qP + q, (unsigned long long)(f0 + j));
             }
         }
-        (void)p1;
-    }
+    });
+    if (cand) atomicAdd(ncand, cand);
 }
 
 __global__ void q_check_kernel(QArgs a, const double* Bs, double* band2, double* band, unsigned long long* qD,
@@ -308,7 +402,7 @@ __global__ void q_check_kernel(QArgs a, const double* Bs, double* band2, double*
         band2[q] = -1.0;
         return;
     }
-    const double eta = q_eta(a, q, Bs);
+    const double eta = q_eta(load_query(a, q), Bs);
     const unsigned long long d = qD[q];
     if (d != kNone && __longlong_as_double((long long)d) > b - eta) {
         const double nb = __longlong_as_double((long long)d) * (1.0 + kBandRel) + 2.0 * eta;
@@ -323,89 +417,72 @@ __global__ void q_check_kernel(QArgs a, const double* Bs, double* band2, double*
 }
 
 // ---- intersects -------------------------------------------------------------
+// Per (segment, face): (1) the segment's box vs the face's AABB plane,
+// expanded by tau; (2) both endpoints strictly on one side of the face plane
+// by tau; otherwise (3) the exact reference predicate. (1) and (2) only drop
+// pairs the reference cannot hit (intersects.cu header); degenerate faces
+// (n = 0, c = 0) always reach (3).
 __global__ void __launch_bounds__(kTile, 4) q_hit_kernel(QArgs a, const double* Bs, unsigned long long* qhit,
                                                          unsigned long long* nexact) {
-    __shared__ alignas(128) double sm[2][14 * kSB];
+    __shared__ alignas(128) double sm[2][kHitPlanes * kSB];
     __shared__ alignas(8) uint64_t bar[2];
-    const int planes[14] = {0, 1, 2, 3, 4, 5, 6, 7, 8, F_N, F_N + 1, F_N + 2, F_C, F_DEG};
+    Stream<kHitPlanes> S{sm, bar, kHitPlaneIds};
+    S.init();
     const uint64_t item = blockIdx.x;
     const uint64_t tl = item / a.n_chunks, ch = item - tl * a.n_chunks;
     const uint64_t q = min(tl * kTile + threadIdx.x, a.Qn - 1);
     const uint64_t b0 = ch * a.chunk, b1 = min(a.Bn, b0 + a.chunk);
-    double p0[3], p1[3];
+    double p0[3], p1[3], lo[3], hi[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         p0[k] = __ldg(a.Q + (uint64_t)k * a.Qpad + q);
         p1[k] = __ldg(a.Q + (uint64_t)(3 + k) * a.Qpad + q);
     }
-    // cull margin over the bounding box of B and this segment (intersects.cu)
     double diag2 = 0.0, ext = Bs[7];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        const double lo = fmin(Bs[k], fmin(p0[k], p1[k])), hi = fmax(Bs[3 + k], fmax(p0[k], p1[k]));
-        diag2 += (hi - lo) * (hi - lo);
+        const double l = fmin(Bs[k], fmin(p0[k], p1[k])), h = fmax(Bs[3 + k], fmax(p0[k], p1[k]));
+        diag2 += (h - l) * (h - l);
         ext = fmax(ext, fmax(fabs(p0[k]), fabs(p1[k])));
     }
     const double tau = kCullDiag * sqrt(diag2) + kCullAbs * ext;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = fmin(p0[k], p1[k]) - tau;
+        hi[k] = fmax(p0[k], p1[k]) + tau;
+    }
     bool live = tl * kTile + threadIdx.x < a.Qn && *(volatile unsigned long long*)(qhit + q) >= b0;
     if (!__syncthreads_or(live)) return;
-    const int nsub = (int)((b1 - b0 + kSB - 1) / kSB);
-    if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        mbar_fence_init();
-    }
-    __syncthreads();
-    auto issue = [&](int s) {
-        const int st = s & 1;
-        const uint64_t f0 = b0 + (uint64_t)s * kSB;
-        const int cnt = (int)min((uint64_t)kSB, b1 - f0);
-        const uint32_t bytes = (uint32_t)(((cnt + 1) & ~1) * sizeof(double));
-        mbar_expect_tx(&bar[st], bytes * 14);
-#pragma unroll 1
-        for (int f = 0; f < 14; ++f)
-            bulk_g2s(&sm[st][f * kSB], a.Bp + (uint64_t)planes[f] * a.Bn_pad + f0, bytes, &bar[st]);
-    };
-    if (threadIdx.x == 0) {
-        issue(0);
-        if (nsub > 1) issue(1);
-    }
     unsigned long long nex = 0;
     const exact::v3 e0{p0[0], p0[1], p0[2]}, e1{p1[0], p1[1], p1[2]};
-#pragma unroll 1
-    for (int s = 0; s < nsub; ++s) {
-        const int st = s & 1;
-        mbar_wait(&bar[st], (uint32_t)((s >> 1) & 1));
-        const uint64_t f0 = b0 + (uint64_t)s * kSB;
-        const int cnt = (int)min((uint64_t)kSB, b1 - f0);
-        const double* sb = sm[st];
+    S.run(a.Bp, a.Bn_pad, b0, b1, [&](const double* sb, int cnt, uint64_t f0) {
         if (live && *(volatile unsigned long long*)(qhit + q) < f0) live = false;
-        if (__syncthreads_or(live)) {
 #pragma unroll 1
-            for (int j = 0; j < cnt; ++j) {
-                if (!live) continue;
-                const double n0 = sb[9 * kSB + j], n1 = sb[10 * kSB + j], n2 = sb[11 * kSB + j], c = sb[12 * kSB + j];
-                const double h0 = fma(n0, p0[0], fma(n1, p0[1], fma(n2, p0[2], -c)));
-                const double h1 = fma(n0, p1[0], fma(n1, p1[1], fma(n2, p1[2], -c)));
-                const double q0 = fabs(h0) - tau, q1 = fabs(h1) - tau;
-                const bool apart = ((__double2hiint(h0) ^ __double2hiint(h1)) | __double2hiint(q0) |
-                                    __double2hiint(q1)) >= 0 &&
-                                   q0 != 0.0 && q1 != 0.0;
-                // degenerate faces have n = 0, c = 0: never culled, decided exactly
-                if (apart) continue;
-                ++nex;
-                const double* bv = sb + j;
-                const exact::tri t{{bv[0], bv[kSB], bv[2 * kSB]}, {bv[3 * kSB], bv[4 * kSB], bv[5 * kSB]},
-                                   {bv[6 * kSB], bv[7 * kSB], bv[8 * kSB]}};
-                if (exact::seg_tri_hit(e0, e1, t)) {
-                    atomicMin(qhit + q, (unsigned long long)(f0 + j));
-                    live = false;  // later faces only give larger indices
-                }
+        for (int j = 0; j < cnt; ++j) {
+            if (!live) continue;
+            bool apart = false;
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                apart |= (sb[(HP_LO + k) * kSB + j] > hi[k]) | (sb[(HP_HI + k) * kSB + j] < lo[k]);
+            if (apart) continue;
+            const double n0 = sb[HP_N * kSB + j], n1 = sb[(HP_N + 1) * kSB + j], n2 = sb[(HP_N + 2) * kSB + j],
+                         c = sb[HP_C * kSB + j];
+            const double h0 = fma(n0, p0[0], fma(n1, p0[1], fma(n2, p0[2], -c)));
+            const double h1 = fma(n0, p1[0], fma(n1, p1[1], fma(n2, p1[2], -c)));
+            const double q0 = fabs(h0) - tau, q1 = fabs(h1) - tau;
+            if (((__double2hiint(h0) ^ __double2hiint(h1)) | __double2hiint(q0) | __double2hiint(q1)) >= 0 &&
+                q0 != 0.0 && q1 != 0.0)
+                continue;
+            ++nex;
+            const double* bv = sb + j;
+            const exact::tri t{{bv[0], bv[kSB], bv[2 * kSB]}, {bv[3 * kSB], bv[4 * kSB], bv[5 * kSB]},
+                               {bv[6 * kSB], bv[7 * kSB], bv[8 * kSB]}};
+            if (exact::seg_tri_hit(e0, e1, t)) {
+                atomicMin(qhit + q, (unsigned long long)(f0 + j));
+                live = false;  // later faces only give larger indices
             }
         }
-        __syncthreads();
-        if (threadIdx.x == 0 && s + 2 < nsub) issue(s + 2);
-    }
+    });
     if (nex) atomicAdd(nexact, nex);
 }
 
@@ -419,50 +496,61 @@ __global__ void q_transpose_kernel(const double* __restrict__ in, uint64_t n, in
 
 }  // namespace
 
-void run_queries(const Ctx& cx, int kind, int op, const double* host_q, uint64_t n, const Geom& B, double* dist,
-                 uint8_t* hit, uint64_t* face) {
+void queries_build(QuerySet* qs, const double* host_q, uint64_t n, int kind, cudaStream_t st) {
+    qs->n = n;
+    qs->kind = kind;
+    qs->width = kind == kQuerySegments ? 6 : 3;
+    qs->pad = ((n + kPlanePad - 1) / kPlanePad) * kPlanePad;
+    CK(cudaMallocAsync(&qs->planes, std::max<uint64_t>(1, qs->pad * qs->width) * sizeof(double), st));
+    if (n) {
+        double* stage = nullptr;
+        CK(cudaMallocAsync(&stage, n * qs->width * sizeof(double), st));
+        CK(cudaMemcpyAsync(stage, host_q, n * qs->width * sizeof(double), cudaMemcpyHostToDevice, st));
+        q_transpose_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(stage, n, qs->width, qs->pad, qs->planes);
+        CK(cudaGetLastError());
+        CK(cudaFreeAsync(stage, st));
+    }
+    CK(cudaStreamSynchronize(st));
+}
+
+void run_queries(const Ctx& cx, int op, const QuerySet& qs, const Geom& B, double* dist, uint8_t* hit,
+                 uint64_t* face) {
     const cudaStream_t st = cx.stream;
     tdb_stats& S = *cx.stats;
     std::memset(&S, 0, sizeof S);
+    const uint64_t n = qs.n;
     for (uint64_t q = 0; q < n; ++q) {
         if (dist) dist[q] = pos_inf_h();
         if (hit) hit[q] = 0;
         face[q] = kNone;
     }
     if (n == 0 || B.n == 0) return;
-    const int width = kind == QK_SEG ? 6 : 3;
-    const uint64_t pad = ((n + kPlanePad - 1) / kPlanePad) * kPlanePad;
     const uint64_t tiles = (n + kTile - 1) / kTile;
-    const uint64_t chunk = pick_chunk(tiles, B.n, cx.sms, 16);
+    const bool fused = op == TDB_OP_DISTANCE && B.n <= kChunk && tiles >= (uint64_t)cx.sms * 2;
+    const uint64_t chunk = fused ? kChunk : pick_chunk(tiles, B.n, cx.sms, 16);
     const uint64_t n_chunks = (B.n + chunk - 1) / chunk;
     const uint64_t n_items = tiles * n_chunks;
     if (n_items > 0x7fffffffull) throw std::invalid_argument("queries: too many work items for one launch");
 
-    double *stage = nullptr, *Q = nullptr, *Bs = nullptr;
-    CK(cudaMallocAsync(&stage, n * width * sizeof(double), st));
-    CK(cudaMallocAsync(&Q, pad * width * sizeof(double), st));
-    CK(cudaMallocAsync(&Bs, kObjStats * sizeof(double), st));
-    CK(cudaMemcpyAsync(stage, host_q, n * width * sizeof(double), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(Bs, B.stats, kObjStats * sizeof(double), cudaMemcpyHostToDevice, st));
-    cudaEvent_t ev[4];
-    for (auto& e : ev) CK(cudaEventCreate(&e));
-    CK(cudaEventRecord(ev[0], st));
-    q_transpose_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(stage, n, width, pad, Q);
-    CK(cudaGetLastError());
-    QArgs a{Q, n, pad, kind, B.planes, B.n_pad, B.n, n_chunks, chunk, nullptr, nullptr};
-    std::vector<unsigned long long> hres(n);
-    uint64_t launches = 1, flagged = 0;
-    int rounds = 0;
-    unsigned long long hc[4] = {0, 0, 0, 0};
-    std::vector<void*> mem = {stage, Q, Bs};
+    std::vector<void*> mem;
     auto alloc = [&](size_t bytes) {
         void* p = nullptr;
         CK(cudaMallocAsync(&p, std::max<size_t>(1, bytes), st));
         mem.push_back(p);
         return p;
     };
+    double* Bs = (double*)alloc(kObjStats * sizeof(double));
+    CK(cudaMemcpyAsync(Bs, B.stats, kObjStats * sizeof(double), cudaMemcpyHostToDevice, st));
     unsigned long long* ctr = (unsigned long long*)alloc(4 * sizeof(unsigned long long));
     CK(cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), st));
+    cudaEvent_t ev[4];
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(ev[0], st));
+    QArgs a{qs.planes, n, qs.pad, qs.kind, B.planes, B.n_pad, B.n, n_chunks, chunk, nullptr, nullptr};
+    std::vector<unsigned long long> hres(n), hd;
+    uint64_t launches = 0, flagged = 0;
+    int rounds = 0;
+    unsigned long long hc[4] = {0, 0, 0, 0};
     if (op == TDB_OP_INTERSECTS) {
         unsigned long long* qhit = (unsigned long long*)alloc(n * sizeof(unsigned long long));
         CK(cudaMemsetAsync(qhit, 0xff, n * sizeof(unsigned long long), st));
@@ -472,9 +560,21 @@ void run_queries(const Ctx& cx, int kind, int op, const double* host_q, uint64_t
         CK(cudaEventRecord(ev[2], st));
         CK(cudaMemcpyAsync(hres.data(), qhit, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, st));
-        launches += 1;
+        launches = 1;
         rounds = 1;
         S.exact_pairs = hc[0];
+    } else if (fused) {
+        double* od = (double*)alloc(n * sizeof(double));
+        unsigned long long* of = (unsigned long long*)alloc(n * sizeof(unsigned long long));
+        q_fused_kernel<<<(unsigned)tiles, kTile, 0, st>>>(a, Bs, od, of, ctr, ctr + 1);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(ev[1], st));
+        CK(cudaEventRecord(ev[2], st));
+        hd.resize(n);
+        CK(cudaMemcpyAsync(hd.data(), od, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hres.data(), of, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, st));
+        launches = 1;
     } else {
         a.itemmin = (double*)alloc(n_items * sizeof(double));
         a.qmin = (unsigned long long*)alloc(n * sizeof(unsigned long long));
@@ -490,34 +590,34 @@ void run_queries(const Ctx& cx, int kind, int op, const double* host_q, uint64_t
         const unsigned qb = (unsigned)((n + 255) / 256);
         q_band_kernel<<<qb, 256, 0, st>>>(a, Bs, band2, band, qD, qP);
         CK(cudaGetLastError());
-        launches += 2;
+        launches = 2;
         for (;;) {
             ++rounds;
-            CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
-            CK(cudaMemsetAsync(ctr + 2, 0, sizeof(unsigned long long), st));
-            q_flag_kernel<<<(unsigned)((n_items + 255) / 256), 256, 0, st>>>(a, n_items, band2, list, ctr);
+            CK(cudaMemsetAsync(ctr + 2, 0, 2 * sizeof(unsigned long long), st));  // flagged, retry
+            q_flag_kernel<<<(unsigned)((n_items + 255) / 256), 256, 0, st>>>(a, n_items, band2, list, ctr + 2);
             CK(cudaGetLastError());
-            for (int pass = 1; pass <= 2; ++pass) {
-                q_verify_kernel<<<(unsigned)(cx.sms * 8), kTile, 0, st>>>(a, list, ctr, 4, pass, band2, qD, qP,
-                                                                          ctr + 1);
-                CK(cudaGetLastError());
+            unsigned long long nflag = 0;
+            CK(cudaMemcpyAsync(&nflag, ctr + 2, sizeof nflag, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            flagged += nflag;
+            if (nflag) {
+                for (int pass = 1; pass <= 2; ++pass) {
+                    q_verify_kernel<<<(unsigned)nflag, kTile, 0, st>>>(a, list, pass, band2, qD, qP, ctr);
+                    CK(cudaGetLastError());
+                }
             }
-            q_check_kernel<<<qb, 256, 0, st>>>(a, Bs, band2, band, qD, qP, ctr + 2);
+            q_check_kernel<<<qb, 256, 0, st>>>(a, Bs, band2, band, qD, qP, ctr + 3);
             CK(cudaGetLastError());
             launches += 4;
             CK(cudaMemcpyAsync(hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
-            flagged += hc[0];
-            if (hc[2] == 0 || rounds >= 8) break;
+            if (hc[3] == 0 || rounds >= 8) break;
+            CK(cudaMemsetAsync(ctr + 3, 0, sizeof(unsigned long long), st));
         }
         CK(cudaEventRecord(ev[2], st));
-        std::vector<unsigned long long> hd(n);
+        hd.resize(n);
         CK(cudaMemcpyAsync(hd.data(), qD, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(hres.data(), qP, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        for (uint64_t q = 0; q < n; ++q)
-            if (hres[q] != kNone) std::memcpy(&dist[q], &hd[q], sizeof(double));
-        S.candidates = hc[1];
     }
     CK(cudaEventRecord(ev[3], st));
     for (void* p : mem) CK(cudaFreeAsync(p, st));
@@ -525,6 +625,7 @@ void run_queries(const Ctx& cx, int kind, int op, const double* host_q, uint64_t
     for (uint64_t q = 0; q < n; ++q) {
         face[q] = hres[q];
         if (hit) hit[q] = hres[q] != kNone;
+        if (dist && hres[q] != kNone) std::memcpy(&dist[q], &hd[q], sizeof(double));
     }
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
@@ -538,8 +639,9 @@ void run_queries(const Ctx& cx, int kind, int op, const double* host_q, uint64_t
     S.pairs_evaluated = n * B.n;
     S.items = n_items;
     S.items_flagged = flagged;
+    if (op == TDB_OP_DISTANCE) S.candidates = hc[0];
     S.kernels = launches;
-    S.rounds = rounds;
+    S.rounds = fused ? (int)hc[1] : rounds;
 }
 
 }  // namespace tdb

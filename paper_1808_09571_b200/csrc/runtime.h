@@ -90,11 +90,22 @@ void run_pairs_filter(const Ctx& cx, const Geom& A, const Geom& B, double* d2);
 
 double fp64_peak(const Ctx& cx, double* ms);
 
-// Segment (kind 0) / point (kind 1) queries against mesh B, per query:
-// distance_to_mesh (op TDB_OP_DISTANCE: dist + lowest face) or
-// intersects_mesh (TDB_OP_INTERSECTS, segments: hit + lowest hit face).
-void run_queries(const Ctx& cx, int kind, int op, const double* host_q, uint64_t n, const Geom& B, double* dist,
-                 uint8_t* hit, uint64_t* face);
+// A device-resident set of segment or point queries (SoA planes).
+constexpr int kQuerySegments = 0, kQueryPoints = 1;
+struct QuerySet {
+    int device = 0;
+    int kind = kQuerySegments;
+    int width = 6;  // doubles per query
+    uint64_t n = 0, pad = 0;
+    double* planes = nullptr;  // width x pad
+};
+void queries_build(QuerySet* qs, const double* host_q, uint64_t n, int kind, cudaStream_t st);
+
+// Queries against mesh B, per query: distance_to_mesh (op TDB_OP_DISTANCE:
+// dist + lowest face) or intersects_mesh (TDB_OP_INTERSECTS, segments: hit +
+// lowest hit face).
+void run_queries(const Ctx& cx, int op, const QuerySet& qs, const Geom& B, double* dist, uint8_t* hit,
+                 uint64_t* face);
 
 // mesh_volume (kernels.cpp:27-46) with the reference's fixed chunk tree.
 double run_volume(const Ctx& cx, const Geom& g, uint64_t chunk);

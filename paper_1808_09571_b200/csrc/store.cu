@@ -90,7 +90,11 @@ __global__ void prep_kernel(const double* __restrict__ aos, uint64_t n, uint64_t
         }
         p[F_C * n_pad] = c;
         p[F_DEG * n_pad] = deg ? 1.0 : 0.0;
-        p[F_SPARE * n_pad] = 0.0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            p[(F_LO + k) * n_pad] = fmin(v[k], fmin(v[3 + k], v[6 + k]));
+            p[(F_HI + k) * n_pad] = fmax(v[k], fmax(v[3 + k], v[6 + k]));
+        }
     }
 
     // ---- per-object statistics, warp-aggregated when the warp is one object

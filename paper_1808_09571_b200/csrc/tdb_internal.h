@@ -21,9 +21,11 @@ enum Field : int {
     F_U = 28,    // dual basis: u(P) = U.(P - V0)
     F_W = 31,    //             v(P) = W.(P - V0)
     F_DEG = 34,  // 1.0 when degenerate (geometry.hpp:75, evaluated exactly)
-    F_SPARE = 35,
-    NF = 36
+    F_LO = 35,   // face AABB lo xyz
+    F_HI = 38,   // face AABB hi xyz
+    NF = 41
 };
+constexpr int kFilterPlanes = F_DEG + 1;  // planes the distance filters stage (V .. DEG)
 
 // A-side work tile: up to kTile consecutive faces of one object.
 struct Tile {

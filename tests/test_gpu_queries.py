@@ -59,6 +59,29 @@ def test_paper_scale_drills_vs_oracle():
     assert 0 < h.sum() < len(h)
 
 
+def test_fused_and_chunked_paths_agree_resident():
+    """>= 2 x SMs tiles with a one-chunk mesh take the fused kernel; a larger
+    mesh takes the chunked filter/verify path; both match the oracle."""
+    drills = T.drills(60_000, 7)
+    q = T.Queries(drills)
+    small, big = T.ore_body(1000), T.ore_body(20_000)  # 1,280 (fused) / 20,480 faces (chunked)
+    for ore in (small, big):
+        d, f = T.queries_mesh_distance(q, ore)
+        st = T.last_stats()
+        od, of = O.segments_mesh_distance(drills, ore)
+        assert np.array_equal(bits(d), bits(od)) and np.array_equal(f, of)
+        assert st["pairs"] == len(drills) * len(ore)
+        h, hf = T.queries_mesh_intersects(q, ore)
+        oh, ohf = O.segments_mesh_intersects(drills, ore)
+        assert np.array_equal(h, oh) and np.array_equal(hf, ohf)
+    pts = T.Queries(drills[:, :3].copy(), T.QUERY_POINTS)
+    d, f = T.queries_mesh_distance(pts, small)
+    od, of = O.points_mesh_distance(drills[:, :3].copy(), small)
+    assert np.array_equal(bits(d), bits(od)) and np.array_equal(f, of)
+    with pytest.raises(ValueError):
+        T.queries_mesh_intersects(pts, small)  # intersects takes segments
+
+
 def test_queries_with_degenerate_faces_and_ties():
     s = T.unit_sphere(80)
     mesh = np.concatenate([s[:10], np.tile([[0, 0, 0, 1, 1, 1, 2, 2, 2]], (3, 1)), s[:10], s[10:]])  # dups + slivers
