@@ -39,6 +39,7 @@ namespace tdb {
 namespace {
 
 constexpr unsigned long long kNone = ~0ull;
+constexpr int kCand = 8;  // per-query candidate list of the fused kernel
 
 struct QArgs {
     const double* Q;  // query planes: 6 (segments: p0 xyz, p1 xyz) or 3 (points), stride Qpad
@@ -248,24 +249,77 @@ __global__ void __launch_bounds__(kTile, 3) q_fused_kernel(QArgs a, const double
     __shared__ alignas(8) uint64_t bar[2];
     Stream<kFilterPlanes> S{sm, bar, kDistPlaneIds};
     S.init();
-    const uint64_t qi = (uint64_t)blockIdx.x * kTile + threadIdx.x;
+    // per-thread candidate list (SMEM, column per thread): faces whose filter
+    // value lies inside the band of the running minimum
+    __shared__ double cd[kCand][kTile];
+    __shared__ uint32_t cj[kCand][kTile];
+    const int tx = threadIdx.x;
+    const uint64_t qi = (uint64_t)blockIdx.x * kTile + tx;
     const bool active = qi < a.Qn;
     const uint64_t q = min(qi, a.Qn - 1);
     const QueryRegs Q = load_query(a, q);
-    double best = pos_inf();
-    S.run(a.Bp, a.Bn_pad, 0, a.Bn, [&](const double* sb, int cnt, uint64_t) {
+    const double eta = q_eta(Q, Bs);
+    auto band_of = [&](double m2) { return sqrt(m2) * (1.0 + kBandRel) + 2.0 * eta; };
+    double best = pos_inf(), cut2 = pos_inf(), evicted = pos_inf();
+    int nc = 0;
+    S.run(a.Bp, a.Bn_pad, 0, a.Bn, [&](const double* sb, int cnt, uint64_t f0) {
 #pragma unroll 1
         for (int j = 0; j < cnt; ++j) {
             if (reinterpret_cast<const int*>(sb + F_DEG * kSB + j)[1] != 0) continue;  // degenerate face
-            best = min_nn(best, query_d2(Q, FaceRef{sb + j, (uint64_t)kSB}));
+            const double d2 = query_d2(Q, FaceRef{sb + j, (uint64_t)kSB});
+            if (d2 < best) {  // new minimum: tighten the cut, drop what fell out of it
+                best = d2;
+                const double b = band_of(best);
+                cut2 = b * b * (1.0 + 4e-16);
+                int w = 0;
+                for (int k = 0; k < nc; ++k)
+                    if (cd[k][tx] <= cut2) cd[w][tx] = cd[k][tx], cj[w][tx] = cj[k][tx], ++w;
+                nc = w;
+            }
+            if (d2 <= cut2) {
+                if (nc < kCand) {
+                    cd[nc][tx] = d2, cj[nc][tx] = (uint32_t)(f0 + j), ++nc;
+                } else {  // full: keep the kCand smallest, remember the best one dropped
+                    int worst = 0;
+                    for (int k = 1; k < kCand; ++k)
+                        if (cd[k][tx] > cd[worst][tx]) worst = k;
+                    if (d2 < cd[worst][tx]) {
+                        evicted = fmin(evicted, cd[worst][tx]);
+                        cd[worst][tx] = d2, cj[worst][tx] = (uint32_t)(f0 + j);
+                    } else {
+                        evicted = fmin(evicted, d2);
+                    }
+                }
+            }
         }
     });
-    const double eta = q_eta(Q, Bs);
-    double band = active && best < pos_inf() ? sqrt(best) * (1.0 + kBandRel) + 2.0 * eta : -1.0;
+    double band = active && best < pos_inf() ? band_of(best) : -1.0;
     unsigned long long D = kNone, P = kNone, cand = 0;
-    bool again = band >= 0.0;
-    int rounds = 0;
-    while (__syncthreads_or(again)) {  // exact rescan; repeats only when a band must widen
+    bool again = false;
+    if (band >= 0.0) {  // exact composition on the listed candidates, lanes in lockstep
+        const double b2 = band * band * (1.0 + 4e-16);
+        for (int k = 0; k < nc; ++k) {
+            if (cd[k][tx] > b2) continue;
+            ++cand;
+            const uint64_t j = cj[k][tx];
+            const exact::tri t = [&] {
+                double v[9];
+#pragma unroll
+                for (int c = 0; c < 9; ++c) v[c] = __ldg(a.Bp + (uint64_t)(F_V + c) * a.Bn_pad + j);
+                return exact::tri{{v[0], v[1], v[2]}, {v[3], v[4], v[5]}, {v[6], v[7], v[8]}};
+            }();
+            const exact::v3 p0{Q.p0[0], Q.p0[1], Q.p0[2]}, p1{Q.p1[0], Q.p1[1], Q.p1[2]};
+            const double dx = Q.point ? exact::pt_tri(p0, t).d : exact::seg_tri(p0, p1, t).d;
+            const unsigned long long e = (unsigned long long)__double_as_longlong(dx);
+            if (e < D || (e == D && j < P)) D = e, P = j;
+        }
+        // complete only if nothing in the band was dropped and the band holds
+        again = evicted <= b2 || D == kNone || __longlong_as_double((long long)D) > band - eta;
+        if (again && D != kNone && __longlong_as_double((long long)D) > band - eta)
+            band = __longlong_as_double((long long)D) * (1.0 + kBandRel) + 2.0 * eta;
+    }
+    int rounds = 1;
+    while (__syncthreads_or(again)) {  // fallback exact rescan (list overflow or a widened band)
         ++rounds;
         const double b2 = again ? band * band * (1.0 + 4e-16) : -1.0;
         if (again) D = P = kNone;
