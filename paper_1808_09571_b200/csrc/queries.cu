@@ -540,6 +540,17 @@ __global__ void __launch_bounds__(kTile, 4) q_hit_kernel(QArgs a, const double* 
     if (nex) atomicAdd(nexact, nex);
 }
 
+// final per-query outputs: distance (+inf when no face qualified) and hit
+__global__ void q_finalize_kernel(uint64_t n, const unsigned long long* __restrict__ rD,
+                                  const unsigned long long* __restrict__ rP, double* __restrict__ dist,
+                                  uint8_t* __restrict__ hit) {
+    const uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const bool found = rP[q] != kNone;
+    if (dist) dist[q] = found && rD ? __longlong_as_double((long long)rD[q]) : pos_inf();
+    if (hit) hit[q] = found ? 1 : 0;
+}
+
 // queries (host AoS, width 6 or 3) -> SoA planes
 __global__ void q_transpose_kernel(const double* __restrict__ in, uint64_t n, int width, uint64_t pad,
                                    double* __restrict__ out) {
@@ -573,12 +584,15 @@ void run_queries(const Ctx& cx, int op, const QuerySet& qs, const Geom& B, doubl
     tdb_stats& S = *cx.stats;
     std::memset(&S, 0, sizeof S);
     const uint64_t n = qs.n;
-    for (uint64_t q = 0; q < n; ++q) {
-        if (dist) dist[q] = pos_inf_h();
-        if (hit) hit[q] = 0;
-        face[q] = kNone;
+    if (n == 0) return;
+    if (B.n == 0) {
+        for (uint64_t q = 0; q < n; ++q) {
+            if (dist) dist[q] = pos_inf_h();
+            if (hit) hit[q] = 0;
+            face[q] = kNone;
+        }
+        return;
     }
-    if (n == 0 || B.n == 0) return;
     const uint64_t tiles = (n + kTile - 1) / kTile;
     const bool fused = op == TDB_OP_DISTANCE && B.n <= kChunk && tiles >= (uint64_t)cx.sms * 2;
     const uint64_t chunk = fused ? kChunk : pick_chunk(tiles, B.n, cx.sms, 16);
@@ -597,52 +611,42 @@ void run_queries(const Ctx& cx, int op, const QuerySet& qs, const Geom& B, doubl
     CK(cudaMemcpyAsync(Bs, B.stats, kObjStats * sizeof(double), cudaMemcpyHostToDevice, st));
     unsigned long long* ctr = (unsigned long long*)alloc(4 * sizeof(unsigned long long));
     CK(cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), st));
+    // results: exact distance bits / face (or lowest hit face), finalized on the device
+    unsigned long long* rD = (unsigned long long*)alloc(n * sizeof(unsigned long long));
+    unsigned long long* rP = (unsigned long long*)alloc(n * sizeof(unsigned long long));
     cudaEvent_t ev[4];
     for (auto& e : ev) CK(cudaEventCreate(&e));
     CK(cudaEventRecord(ev[0], st));
     QArgs a{qs.planes, n, qs.pad, qs.kind, B.planes, B.n_pad, B.n, n_chunks, chunk, nullptr, nullptr};
-    std::vector<unsigned long long> hres(n), hd;
     uint64_t launches = 0, flagged = 0;
     int rounds = 0;
     unsigned long long hc[4] = {0, 0, 0, 0};
     if (op == TDB_OP_INTERSECTS) {
-        unsigned long long* qhit = (unsigned long long*)alloc(n * sizeof(unsigned long long));
-        CK(cudaMemsetAsync(qhit, 0xff, n * sizeof(unsigned long long), st));
-        q_hit_kernel<<<(unsigned)n_items, kTile, 0, st>>>(a, Bs, qhit, ctr);
+        CK(cudaMemsetAsync(rP, 0xff, n * sizeof(unsigned long long), st));
+        q_hit_kernel<<<(unsigned)n_items, kTile, 0, st>>>(a, Bs, rP, ctr);
         CK(cudaGetLastError());
         CK(cudaEventRecord(ev[1], st));
         CK(cudaEventRecord(ev[2], st));
-        CK(cudaMemcpyAsync(hres.data(), qhit, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, st));
         launches = 1;
         rounds = 1;
-        S.exact_pairs = hc[0];
     } else if (fused) {
-        double* od = (double*)alloc(n * sizeof(double));
-        unsigned long long* of = (unsigned long long*)alloc(n * sizeof(unsigned long long));
-        q_fused_kernel<<<(unsigned)tiles, kTile, 0, st>>>(a, Bs, od, of, ctr, ctr + 1);
+        q_fused_kernel<<<(unsigned)tiles, kTile, 0, st>>>(a, Bs, (double*)rD, rP, ctr, ctr + 1);
         CK(cudaGetLastError());
         CK(cudaEventRecord(ev[1], st));
         CK(cudaEventRecord(ev[2], st));
-        hd.resize(n);
-        CK(cudaMemcpyAsync(hd.data(), od, n * sizeof(double), cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(hres.data(), of, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, st));
         launches = 1;
     } else {
         a.itemmin = (double*)alloc(n_items * sizeof(double));
         a.qmin = (unsigned long long*)alloc(n * sizeof(unsigned long long));
         double* band2 = (double*)alloc(n * sizeof(double));
         double* band = (double*)alloc(n * sizeof(double));
-        unsigned long long* qD = (unsigned long long*)alloc(n * sizeof(unsigned long long));
-        unsigned long long* qP = (unsigned long long*)alloc(n * sizeof(unsigned long long));
         unsigned long long* list = (unsigned long long*)alloc(n_items * sizeof(unsigned long long));
         CK(cudaMemsetAsync(a.qmin, 0xff, n * sizeof(unsigned long long), st));
         q_filter_kernel<<<(unsigned)n_items, kTile, 0, st>>>(a);
         CK(cudaGetLastError());
         CK(cudaEventRecord(ev[1], st));
         const unsigned qb = (unsigned)((n + 255) / 256);
-        q_band_kernel<<<qb, 256, 0, st>>>(a, Bs, band2, band, qD, qP);
+        q_band_kernel<<<qb, 256, 0, st>>>(a, Bs, band2, band, rD, rP);
         CK(cudaGetLastError());
         launches = 2;
         for (;;) {
@@ -656,31 +660,33 @@ void run_queries(const Ctx& cx, int op, const QuerySet& qs, const Geom& B, doubl
             flagged += nflag;
             if (nflag) {
                 for (int pass = 1; pass <= 2; ++pass) {
-                    q_verify_kernel<<<(unsigned)nflag, kTile, 0, st>>>(a, list, pass, band2, qD, qP, ctr);
+                    q_verify_kernel<<<(unsigned)nflag, kTile, 0, st>>>(a, list, pass, band2, rD, rP, ctr);
                     CK(cudaGetLastError());
                 }
             }
-            q_check_kernel<<<qb, 256, 0, st>>>(a, Bs, band2, band, qD, qP, ctr + 3);
+            q_check_kernel<<<qb, 256, 0, st>>>(a, Bs, band2, band, rD, rP, ctr + 3);
             CK(cudaGetLastError());
             launches += 4;
             CK(cudaMemcpyAsync(hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
             if (hc[3] == 0 || rounds >= 8) break;
-            CK(cudaMemsetAsync(ctr + 3, 0, sizeof(unsigned long long), st));
         }
         CK(cudaEventRecord(ev[2], st));
-        hd.resize(n);
-        CK(cudaMemcpyAsync(hd.data(), qD, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(hres.data(), qP, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     }
+    // distances as doubles (+inf when no face qualified), hits as bytes
+    double* od = dist ? (double*)alloc(n * sizeof(double)) : nullptr;
+    uint8_t* oh = hit ? (uint8_t*)alloc(n) : nullptr;
+    q_finalize_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, op == TDB_OP_DISTANCE ? rD : nullptr, rP, od,
+                                                                  oh);
+    CK(cudaGetLastError());
+    ++launches;
+    if (od) CK(cudaMemcpyAsync(dist, od, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (oh) CK(cudaMemcpyAsync(hit, oh, n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(face, rP, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, st));
     CK(cudaEventRecord(ev[3], st));
     for (void* p : mem) CK(cudaFreeAsync(p, st));
     CK(cudaStreamSynchronize(st));
-    for (uint64_t q = 0; q < n; ++q) {
-        face[q] = hres[q];
-        if (hit) hit[q] = hres[q] != kNone;
-        if (dist && hres[q] != kNone) std::memcpy(&dist[q], &hd[q], sizeof(double));
-    }
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
     S.ms_filter = ms;
@@ -694,6 +700,7 @@ void run_queries(const Ctx& cx, int op, const QuerySet& qs, const Geom& B, doubl
     S.items = n_items;
     S.items_flagged = flagged;
     if (op == TDB_OP_DISTANCE) S.candidates = hc[0];
+    else S.exact_pairs = hc[0];
     S.kernels = launches;
     S.rounds = fused ? (int)hc[1] : rounds;
 }
