@@ -83,6 +83,12 @@ void ensure_device() {
     if (!g_streams[dev]) {
         CK(cudaStreamCreateWithFlags(&g_streams[dev], cudaStreamNonBlocking));
         g_sms[dev] = prop.multiProcessorCount;
+        // keep per-call scratch (cudaMallocAsync) cached in the device pool
+        // instead of returning it to the OS at every synchronize
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+        uint64_t keep = UINT64_MAX;
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     }
     t_device = dev;
 }
