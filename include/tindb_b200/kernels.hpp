@@ -11,9 +11,11 @@
 // * eval_mesh_mesh — the branch batch.cpp:49 (eval_distance) and :62
 //   (eval_intersects) lack today; returns nullopt for other pairings so the
 //   reference's dispatch continues unchanged.
-// * run_batch_b200 — run_batch (batch.hpp:49-51) with the whole Mesh column
-//   evaluated in one device launch against a Mesh literal; every other
-//   pairing is delegated to the reference run_batch in record order.
+// * run_batch_b200 — run_batch (batch.hpp:49-51) against a Mesh literal with
+//   the Mesh records (triangle pairs), the Segment / 2-point LineString
+//   records and the Point records (distance_to_mesh / intersects_mesh, the
+//   paper's drill workload) each evaluated as one device column; every other
+//   pairing is delegated to the reference run_batch, in record order.
 //
 // Error behaviour mirrors the reference: invalid input throws
 // std::invalid_argument (kernels.cpp:403), device failures throw
@@ -147,9 +149,56 @@ inline std::vector<KernelResult> run_batch_b200(BatchOp op, const std::vector<st
         return run_batch(op, records, argument, cfg);
 
     std::vector<KernelResult> out(records.size());
-    std::vector<std::size_t> mesh_rows, other_rows;
-    for (std::size_t i = 0; i < records.size(); ++i)
-        (kind_of(records[i].geometry) == GeometryKind::Mesh ? mesh_rows : other_rows).push_back(i);
+    std::vector<std::size_t> mesh_rows, seg_rows, pt_rows, other_rows;
+    for (std::size_t i = 0; i < records.size(); ++i) {
+        const GeometryKind k = kind_of(records[i].geometry);
+        if (k == GeometryKind::Mesh) mesh_rows.push_back(i);
+        else if (k == GeometryKind::Segment) seg_rows.push_back(i);  // incl. 2-point line strings
+        else if (k == GeometryKind::Point && op == BatchOp::Distance) pt_rows.push_back(i);
+        else other_rows.push_back(i);
+    }
+    // Segment / Point x Mesh (batch.cpp:37-40, :58): distance_to_mesh /
+    // intersects_mesh per record, the whole column in one device call
+    if (!seg_rows.empty() || !pt_rows.empty()) {
+        DeviceMesh lit(std::get<TriangleMesh>(*argument));
+        auto run_queries = [&](const std::vector<std::size_t>& rows, int kind) {
+            if (rows.empty()) return;
+            const int width = kind == TDB_QUERY_SEGMENTS ? 6 : 3;
+            std::vector<double> q(width * rows.size());
+            for (std::size_t k = 0; k < rows.size(); ++k) {
+                const Geometry& g = records[rows[k]].geometry;
+                if (kind == TDB_QUERY_SEGMENTS) {
+                    const LineSegment s = segment_view(g);
+                    const double v[6] = {s.p0.x, s.p0.y, s.p0.z, s.p1.x, s.p1.y, s.p1.z};
+                    std::copy(v, v + 6, q.begin() + 6 * k);
+                } else {
+                    const Point3& p = std::get<Point3>(g);
+                    q[3 * k] = p.x, q[3 * k + 1] = p.y, q[3 * k + 2] = p.z;
+                }
+            }
+            tdb_queries qs = nullptr;
+            check(tdb_queries_upload(q.data(), rows.size(), kind, &qs));
+            struct FreeQ {
+                tdb_queries q;
+                ~FreeQ() { tdb_queries_free(q); }
+            } gq{qs};
+            std::vector<double> dist(rows.size());
+            std::vector<std::uint8_t> hit(rows.size());
+            std::vector<std::uint64_t> face(rows.size());
+            if (op == BatchOp::Distance)
+                check(tdb_queries_mesh_distance(qs, lit.handle(), dist.data(), face.data()));
+            else
+                check(tdb_queries_mesh_intersects(qs, lit.handle(), hit.data(), face.data()));
+            for (std::size_t k = 0; k < rows.size(); ++k) {
+                KernelResult& r = out[rows[k]];
+                r.record_id = records[rows[k]].id;
+                if (op == BatchOp::Distance) r.value = dist[k];
+                else r.value = hit[k] != 0;
+            }
+        };
+        run_queries(seg_rows, TDB_QUERY_SEGMENTS);
+        run_queries(pt_rows, TDB_QUERY_POINTS);
+    }
 
     if (!other_rows.empty()) {  // reference dispatch for every other pairing
         std::vector<store::GeometryRecord> rest;

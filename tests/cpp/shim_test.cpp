@@ -81,6 +81,19 @@ int main() {
     recs.push_back({13, Geometry{shifted(s, -3.0, 1.0, 0, 0.2)}});
     recs.push_back({14, Geometry{Point3{0, 0, 5}}});
     recs.push_back({15, Geometry{LineString{{{0, 0, 0}, {1, 0, 0}, {1, 1, 0}}}}});
+    recs.push_back({16, Geometry{LineSegment{{-2, -2, -2}, {2, 2, 2}}}});        // pierces the sphere
+    recs.push_back({17, Geometry{LineSegment{{0.1, 0.1, 0.1}, {0.1, 0.1, 0.1}}}});  // zero length
+    recs.push_back({18, Geometry{LineString{{{1.5, 0, 0}, {2, 0, 0}}}}});       // 2-point line string
+    recs.push_back({19, Geometry{Point3{0.2, 0.1, 0.3}}});
+    {  // a drill column in the sphere's frame
+        bench::DatasetSpec spec;
+        spec.segment_count = 300;
+        for (const LineSegment& d : bench::make_drills(spec)) {
+            const Point3 a{d.p0.x / 400.0 - 1.25, d.p0.y / 400.0 - 1.25, d.p0.z / 200.0 + 1.0};
+            const Point3 b{d.p1.x / 400.0 - 1.25, d.p1.y / 400.0 - 1.25, d.p1.z / 200.0 + 1.0};
+            recs.push_back({100 + (std::int64_t)recs.size(), Geometry{LineSegment{a, b}}});
+        }
+    }
     const std::optional<Geometry> lit = Geometry{s};
     for (K::BatchOp op : {K::BatchOp::Distance, K::BatchOp::Intersects}) {
         auto got = K::b200::run_batch_b200(op, recs, lit, cfg);
