@@ -498,6 +498,8 @@ def main():
     h2d = d2h = 0
     e2e_pairs = 0
     barrier()
+    clocks_e2e = ClockSampler(local)
+    clocks_e2e.start()
     t0 = time.perf_counter()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
@@ -510,6 +512,7 @@ def main():
     e3.record(stream)
     barrier()
     wall_e2e = time.perf_counter() - t0
+    clk_e2e = clocks_e2e.stop()
     ms_e2e = max_over_ranks(max(e2.elapsed_time(e3), wall_e2e * 1e3))
     e2e_value = max_over_ranks(float(e2e_pairs)) * world / (ms_e2e * 1e-3)
 
@@ -564,7 +567,8 @@ def main():
                        "l2": "inputs larger than L2 (B / table stores of 288 B per face in HBM)"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d // max(1, e2e_steps),
                     "d2h_bytes_per_step": d2h // max(1, e2e_steps), "steps": e2e_steps},
-            "roofline": roofline, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": kernels,
+            "roofline": roofline, "cpu_baseline": cpu, "clocks": clk, "clocks_e2e": clk_e2e,
+            "gpu_launches": kernels,
             "result": {"best_value_seen": best[0], "pair": best[1]},
         })
         print(json.dumps(out), flush=True)
