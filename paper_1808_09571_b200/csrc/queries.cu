@@ -553,10 +553,16 @@ __global__ void q_finalize_kernel(uint64_t n, const unsigned long long* __restri
 
 // queries (host AoS, width 6 or 3) -> SoA planes
 __global__ void q_transpose_kernel(const double* __restrict__ in, uint64_t n, int width, uint64_t pad,
-                                   double* __restrict__ out) {
+                                   double* __restrict__ out, unsigned long long* __restrict__ nonfinite) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    for (int k = 0; k < width; ++k) out[(uint64_t)k * pad + i] = in[(uint64_t)width * i + k];
+    bool bad = false;
+    for (int k = 0; k < width; ++k) {
+        const double x = in[(uint64_t)width * i + k];
+        bad |= !isfinite(x);
+        out[(uint64_t)k * pad + i] = x;
+    }
+    if (bad) atomicAdd(nonfinite, 1ull);
 }
 
 }  // namespace
@@ -567,15 +573,25 @@ void queries_build(QuerySet* qs, const double* host_q, uint64_t n, int kind, cud
     qs->width = kind == kQuerySegments ? 6 : 3;
     qs->pad = ((n + kPlanePad - 1) / kPlanePad) * kPlanePad;
     CK(cudaMallocAsync(&qs->planes, std::max<uint64_t>(1, qs->pad * qs->width) * sizeof(double), st));
+    unsigned long long bad = 0;
     if (n) {
         double* stage = nullptr;
+        unsigned long long* nbad = nullptr;
         CK(cudaMallocAsync(&stage, n * qs->width * sizeof(double), st));
+        CK(cudaMallocAsync(&nbad, sizeof(unsigned long long), st));
+        CK(cudaMemsetAsync(nbad, 0, sizeof(unsigned long long), st));
         CK(cudaMemcpyAsync(stage, host_q, n * qs->width * sizeof(double), cudaMemcpyHostToDevice, st));
-        q_transpose_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(stage, n, qs->width, qs->pad, qs->planes);
+        q_transpose_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(stage, n, qs->width, qs->pad, qs->planes,
+                                                                       nbad);
         CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(&bad, nbad, sizeof bad, cudaMemcpyDeviceToHost, st));
         CK(cudaFreeAsync(stage, st));
+        CK(cudaFreeAsync(nbad, st));
     }
     CK(cudaStreamSynchronize(st));
+    if (bad)
+        throw std::invalid_argument(std::to_string(bad) +
+                                    " quer(ies) with non-finite coordinates (geometry.hpp:16-18 requires finite)");
 }
 
 void run_queries(const Ctx& cx, int op, const QuerySet& qs, const Geom& B, double* dist, uint8_t* hit,

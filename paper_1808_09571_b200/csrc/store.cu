@@ -133,6 +133,13 @@ __global__ void prep_kernel(const double* __restrict__ aos, uint64_t n, uint64_t
     }
     const unsigned dm = __ballot_sync(mask, live && deg);
     if ((threadIdx.x & 31) == 0 && dm) atomicAdd(n_deg, (unsigned long long)__popc(dm));
+    // non-finite coordinates (the reference rejects them at construction,
+    // geometry.hpp:16-18): counted in n_deg[1], the upload then fails
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) bad |= !isfinite(v[k]);
+    const unsigned bm = __ballot_sync(mask, live && bad);
+    if ((threadIdx.x & 31) == 0 && bm) atomicAdd(n_deg + 1, (unsigned long long)__popc(bm));
 }
 
 __global__ void stats_init_kernel(unsigned long long* stats, uint64_t n_obj) {
@@ -221,8 +228,8 @@ void geom_build(Geom* g, const double* host_tri9, uint64_t n, const uint64_t* ho
     unsigned long long* ustats = nullptr;
     unsigned long long* ndeg = nullptr;
     CK(cudaMallocAsync(&ustats, std::max<uint64_t>(1, n_obj) * kObjStats * sizeof(unsigned long long), st));
-    CK(cudaMallocAsync(&ndeg, sizeof(unsigned long long), st));
-    CK(cudaMemsetAsync(ndeg, 0, sizeof(unsigned long long), st));
+    CK(cudaMallocAsync(&ndeg, 2 * sizeof(unsigned long long), st));  // degenerate, non-finite
+    CK(cudaMemsetAsync(ndeg, 0, 2 * sizeof(unsigned long long), st));
     CK(cudaMemsetAsync(g->planes, 0, (size_t)NF * g->n_pad * sizeof(double), st));
 
     if (n) CK(cudaMemcpyAsync(staging, host_tri9, 9 * n * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -250,8 +257,8 @@ void geom_build(Geom* g, const double* host_tri9, uint64_t n, const uint64_t* ho
         stats_final_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(ustats, g->d_obj_stats, m);
         CK(cudaGetLastError());
     }
-    unsigned long long nd = 0;
-    CK(cudaMemcpyAsync(&nd, ndeg, sizeof nd, cudaMemcpyDeviceToHost, st));
+    unsigned long long nd2[2] = {0, 0};
+    CK(cudaMemcpyAsync(nd2, ndeg, sizeof nd2, cudaMemcpyDeviceToHost, st));
     // overall AABB / scale (for the single-object case this is the object)
     std::vector<double> os(std::max<uint64_t>(1, n_obj) * kObjStats, 0.0);
     if (n_obj) CK(cudaMemcpyAsync(os.data(), g->d_obj_stats, n_obj * kObjStats * sizeof(double),
@@ -260,7 +267,10 @@ void geom_build(Geom* g, const double* host_tri9, uint64_t n, const uint64_t* ho
     CK(cudaFreeAsync(ustats, st));
     CK(cudaFreeAsync(ndeg, st));
     CK(cudaStreamSynchronize(st));
-    g->n_degenerate = nd;
+    if (nd2[1])
+        throw std::invalid_argument(std::to_string(nd2[1]) +
+                                    " face(s) with non-finite coordinates (geometry.hpp:16-18 requires finite)");
+    g->n_degenerate = nd2[0];
     double agg[kObjStats] = {pos_inf_h(), pos_inf_h(), pos_inf_h(), -pos_inf_h(), -pos_inf_h(), -pos_inf_h(), 0.0, 0.0};
     for (uint64_t o = 0; o < n_obj; ++o) {
         if (g->h_off[o + 1] == g->h_off[o]) continue;
