@@ -76,7 +76,8 @@ typedef struct {
     uint64_t exact_pairs;   /* intersects: pairs that reached the exact predicate */
     uint64_t kernels;       /* kernel launches in the call */
     uint64_t pairs_evaluated; /* pairs run through the per-pair filter (== pairs in FULL mode) */
-    int32_t rounds;         /* exact-pass rounds (>= 1; > 1 when a band was widened) */
+    uint64_t near_degenerate; /* exact-pass pairs flagged near-degenerate (tdb_last_near_degenerate) */
+    int32_t rounds;       /* exact-pass rounds (>= 1; > 1 when a band was widened) */
     int32_t _pad;
 } tdb_stats;
 
@@ -94,6 +95,13 @@ int tdb_set_stream(void* cuda_stream); /* thread-local launch stream (NULL = lib
 int tdb_set_mode(int mode);           /* thread-local TDB_MODE_* */
 const char* tdb_last_error(void);
 int tdb_last_stats(tdb_stats* out);
+/* Near-degenerate pairs met by the exact pass of the last call on this thread
+ * (SPEC north star: "near-degenerate pairs logged"): a pair whose triangle
+ * (or segment/triangle) is within 1e3 ulps of degenerate or of parallel.
+ * Writes up to `cap` (object, pair) entries — object = A object / table row /
+ * query index, pair = i*|B|+j / face index — as 2*cap uint64 values, and the
+ * total count (which may exceed the 1024 entries kept) to *count_out. */
+int tdb_last_near_degenerate(uint64_t* obj_pair_out, uint64_t cap, uint64_t* count_out);
 int tdb_device_count(void);
 
 /* ---- device geometry store (replaces the CPU mesh store, store_types.hpp:14-32) */

@@ -70,6 +70,7 @@ class Stats(ct.Structure):
         ("exact_pairs", ct.c_uint64),
         ("kernels", ct.c_uint64),
         ("pairs_evaluated", ct.c_uint64),
+        ("near_degenerate", ct.c_uint64),
         ("rounds", ct.c_int32),
         ("_pad", ct.c_int32),
     ]
@@ -85,6 +86,7 @@ _SIGS = [
     ("tdb_set_mode", ct.c_int, [ct.c_int]),
     ("tdb_last_error", ct.c_char_p, []),
     ("tdb_last_stats", ct.c_int, [ct.POINTER(Stats)]),
+    ("tdb_last_near_degenerate", ct.c_int, [_U64, ct.c_uint64, _U64]),
     ("tdb_device_count", ct.c_int, []),
     ("tdb_mesh_upload", ct.c_int, [_D, ct.c_uint64, ct.POINTER(ct.c_void_p)]),
     ("tdb_table_upload", ct.c_int, [_D, _U64, ct.c_uint64, ct.POINTER(ct.c_void_p)]),
@@ -186,6 +188,21 @@ def last_stats() -> dict:
     s = Stats()
     _check(lib().tdb_last_stats(ct.byref(s)))
     return s.as_dict()
+
+
+NEAR_LOG_CAP = 1024  # kNearLogCap (exact.cuh): entries kept per call
+
+
+def last_near_degenerate(cap: int = NEAR_LOG_CAP):
+    """(count, entries[k, 2]) of the near-degenerate pairs the exact pass met
+    in the last call on this thread: (object, pair) per entry (object = A
+    object / table row / query; pair = i*|B|+j / face index). `count` may
+    exceed the entries kept (1024)."""
+    buf = np.zeros((max(cap, 0), 2), np.uint64)
+    cnt = np.zeros(1, np.uint64)
+    _check(lib().tdb_last_near_degenerate(buf.ctypes.data_as(_U64), cap, cnt.ctypes.data_as(_U64)))
+    n = int(cnt[0])
+    return n, buf[: min(n, cap, NEAR_LOG_CAP)]
 
 
 class _Geom:

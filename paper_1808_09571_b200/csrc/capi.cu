@@ -33,6 +33,7 @@ thread_local bool t_stream_set = false;
 thread_local int t_mode = TDB_MODE_FULL;
 thread_local int t_device = -1;
 thread_local tdb_stats t_stats{};
+thread_local tdb::NearHost t_near;
 
 std::mutex g_mu;
 std::vector<cudaStream_t> g_streams;  // library stream per device
@@ -100,6 +101,9 @@ tdb::Ctx ctx() {
     c.mode = t_mode;
     c.sms = g_sms[t_device];
     c.stats = &t_stats;
+    t_near.count = 0;
+    t_near.entries.clear();
+    c.near = &t_near;
     return c;
 }
 
@@ -195,6 +199,14 @@ int tdb_set_mode(int mode) {
 }
 
 const char* tdb_last_error(void) { return t_err.c_str(); }
+
+int tdb_last_near_degenerate(uint64_t* obj_pair_out, uint64_t cap, uint64_t* count_out) {
+    if (!count_out || (cap && !obj_pair_out)) return fail(TDB_E_ARG, "null output");
+    *count_out = t_near.count;
+    const uint64_t n = std::min<uint64_t>(cap, t_near.entries.size() / 2);
+    if (n) std::memcpy(obj_pair_out, t_near.entries.data(), 2 * n * sizeof(uint64_t));
+    return TDB_OK;
+}
 
 int tdb_last_stats(tdb_stats* out) {
     if (!out) return fail(TDB_E_ARG, "null stats");

@@ -195,6 +195,7 @@ struct VerifyArgs {
     unsigned long long* objD;
     unsigned long long* objP;
     unsigned long long* ncand;
+    NearLog near;
 };
 
 __device__ __forceinline__ exact::tri load_tri(const double* P, uint64_t pad, uint64_t i) {
@@ -228,11 +229,13 @@ __global__ void __launch_bounds__(kTile) verify_kernel(VerifyArgs v) {
             if (__ldg(a.Bp + (uint64_t)F_DEG * a.Bn_pad + j) != 0.0) continue;
             const double d2 = pair_d2(A, FaceRefLdg{a.Bp + j, a.Bn_pad}, a.Ap + row, a.An_pad);
             if (active && d2 <= b2) {
-                const exact::res x = exact::tri_tri(load_tri(a.Ap, a.An_pad, row), load_tri(a.Bp, a.Bn_pad, j));
+                const exact::tri ta = load_tri(a.Ap, a.An_pad, row), tb = load_tri(a.Bp, a.Bn_pad, j);
+                const exact::res x = exact::tri_tri(ta, tb);
                 const unsigned long long bits = (unsigned long long)__double_as_longlong(x.d);
                 if (v.pass == 1) {
                     atomicMin(v.objD + o, bits);
                     atomicAdd(v.ncand, 1ull);
+                    if (exact::near_degenerate_pair(ta, tb)) near_log(v.near, a.obj0 + o, i_loc * a.Bn + j);
                 } else if (bits == v.objD[o]) {
                     atomicMin(v.objP + o, i_loc * a.Bn + j);
                 }
@@ -364,6 +367,8 @@ void run_distance(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, u
     CK(cudaMemcpyAsync(Bstats, B.stats, kObjStats * sizeof(double), cudaMemcpyHostToDevice, st));
 
     EventPair ev;
+    NearDev near;
+    near.alloc(st);
     CK(cudaEventRecord(ev.e[0], st));
     uint64_t launches = 0;
     unsigned long long *perm = nullptr, *lb2 = nullptr;
@@ -412,7 +417,8 @@ void run_distance(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, u
             FlagArgs{A.d_tiles, sel.tile0, n_chunks, n_items, sel.obj0, itemmin, band2, list, ctr});
         CK(cudaGetLastError());
         for (int pass = 1; pass <= 2; ++pass) {
-            verify_kernel<<<vgrid, kTile, 0, st>>>(VerifyArgs{da, list, ctr, nsplit, pass, band2, objD, objP, ctr + 1});
+            verify_kernel<<<vgrid, kTile, 0, st>>>(
+                VerifyArgs{da, list, ctr, nsplit, pass, band2, objD, objP, ctr + 1, near.log});
             CK(cudaGetLastError());
         }
         check_kernel<<<ob, 256, 0, st>>>(CheckArgs{nobj, sel.obj0, A.d_obj_stats, Bstats, band2, band, objD, objP, ctr + 2});
@@ -468,6 +474,8 @@ void run_distance(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, u
     S.kernels = launches;
     S.pairs_evaluated = h_ctr[3];
     S.rounds = rounds;
+    near.fetch(st, cx.near);
+    S.near_degenerate = cx.near->count;
 }
 
 }  // namespace tdb

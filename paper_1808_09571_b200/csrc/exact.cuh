@@ -16,6 +16,8 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdint>
+
 namespace tdb {
 namespace exact {
 
@@ -269,5 +271,55 @@ static __device__ __noinline__ bool tri_tri_hit(const tri& a, const tri& b) {
     return seg_tri_hit(b.v0, b.v1, a) || seg_tri_hit(b.v1, b.v2, a) || seg_tri_hit(b.v2, b.v0, a);
 }
 
+// ---- near-degenerate detection (logging only; never changes a result) -----
+// A pair is near-degenerate when one of the reference's decision thresholds
+// is within a factor kNearFactor of deciding it the other way:
+//   * a triangle's norm2((v1-v0) x (v2-v0)) in (1e-30, 1e-30 * f^2]
+//     (geometry.hpp:58,75: skipped below);
+//   * a directed edge's pierce denominator |(d x e1).e0| in
+//     (1e-12 s, 1e-12 s f] with s = |d||e0||e1| (kernels.cpp:243-244:
+//     treated as parallel below, solved above).
+constexpr double kNearFactor = 1e3;
+
+__device__ __forceinline__ bool near_area(const tri& t) {
+    const v3 n = cross(sub(t.v1, t.v0), sub(t.v2, t.v0));
+    const double a2 = dot(n, n);
+    return a2 > kDegenArea2 && a2 <= kDegenArea2 * kNearFactor * kNearFactor;
+}
+
+__device__ __forceinline__ bool near_parallel(v3 p0, v3 p1, const tri& t) {
+    const v3 d = sub(p1, p0), e0 = sub(t.v1, t.v0), e1 = sub(t.v2, t.v0);
+    const double den = fabs(dot(cross(d, e1), e0));
+    const double lim = __dmul_rn(kPierceEps, __dmul_rn(__dmul_rn(norm(d), norm(e0)), norm(e1)));
+    return den > lim && den <= lim * kNearFactor;
+}
+
+static __device__ __noinline__ bool near_degenerate_pair(const tri& a, const tri& b) {
+    if (near_area(a) || near_area(b)) return true;
+    return near_parallel(a.v0, a.v1, b) || near_parallel(a.v1, a.v2, b) || near_parallel(a.v2, a.v0, b) ||
+           near_parallel(b.v0, b.v1, a) || near_parallel(b.v1, b.v2, a) || near_parallel(b.v2, b.v0, a);
+}
+
+static __device__ __noinline__ bool near_degenerate_seg(v3 p0, v3 p1, const tri& t) {
+    return near_area(t) || near_parallel(p0, p1, t);
+}
+
 }  // namespace exact
+
+// Per-call log of near-degenerate pairs (north star: "near-degenerate pairs
+// logged"): a count and the first kNearLogCap (object, pair) entries.
+constexpr uint32_t kNearLogCap = 1024;
+struct NearLog {
+    unsigned long long* count;
+    unsigned long long* entries;  // 2 per entry: object, pair
+};
+
+__device__ __forceinline__ void near_log(const NearLog& L, unsigned long long obj, unsigned long long pair) {
+    if (!L.count) return;
+    const unsigned long long k = atomicAdd(L.count, 1ull);
+    if (k < kNearLogCap) {
+        L.entries[2 * k] = obj;
+        L.entries[2 * k + 1] = pair;
+    }
+}
 }  // namespace tdb

@@ -63,6 +63,7 @@ struct HitArgs {
     // CULL mode (null in FULL): per-tile and per-chunk AABBs
     const double* tile_aabb;
     const double* chunk_aabb;
+    NearLog near;
 };
 
 __device__ __forceinline__ exact::tri load_tri(const double* P, uint64_t pad, uint64_t i) {
@@ -83,7 +84,8 @@ __device__ __forceinline__ bool separated(double h0, double h1, double h2, doubl
 
 // Second plane test + exact reference predicate (rare path, out of line).
 static __device__ __noinline__ bool slow_pair(const double* Ap, uint64_t An_pad, uint64_t row, const double* sb,
-                                              int j, double tau) {
+                                              int j, double tau, const NearLog& near, unsigned long long obj,
+                                              unsigned long long pair) {
     double av[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) av[k] = __ldg(Ap + (uint64_t)(F_V + k) * An_pad + row);
@@ -97,6 +99,7 @@ static __device__ __noinline__ bool slow_pair(const double* Ap, uint64_t An_pad,
     const exact::tri ta{{av[0], av[1], av[2]}, {av[3], av[4], av[5]}, {av[6], av[7], av[8]}};
     const exact::tri tb{{bv[0], bv[kSBH], bv[2 * kSBH]}, {bv[3 * kSBH], bv[4 * kSBH], bv[5 * kSBH]},
                         {bv[6 * kSBH], bv[7 * kSBH], bv[8 * kSBH]}};
+    if (exact::near_degenerate_pair(ta, tb)) near_log(near, obj, pair);
     return exact::tri_tri_hit(ta, tb);
 }
 
@@ -222,7 +225,7 @@ __global__ void __launch_bounds__(32 * kWarps) hit_kernel(HitArgs a) {
                     const int r = __ffs(need) - 1;
                     need &= need - 1;
                     ++nex;
-                    if (slow_pair(a.Ap, a.An_pad, rowv[r], sb, j, tau)) {
+                    if (slow_pair(a.Ap, a.An_pad, rowv[r], sb, j, tau, a.near, a.obj0 + o, row_pmin(r, f0 + j))) {
                         atomicMin(a.objhit + o, row_pmin(r, f0 + j));
                         live &= ~(1u << r);  // later j of this row only give larger p
                     }
@@ -266,6 +269,8 @@ void run_intersects(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit,
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     CK(cudaEventCreate(&e2));
+    NearDev near;
+    near.alloc(st);
     double* caabb = nullptr;
     if (cx.mode == TDB_MODE_CULL) {
         CK(cudaMallocAsync(&caabb, n_chunks * 6 * sizeof(double), st));
@@ -276,7 +281,7 @@ void run_intersects(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit,
                                                                   sel.row_lo, sel.row_hi, B.planes, B.n_pad, B.n,
                                                                   n_chunks, chunk, sel.obj0, A.d_obj_stats, Bstats,
                                                                   objhit, nex, caabb ? A.d_tile_aabb : nullptr,
-                                                                  caabb});
+                                                                  caabb, near.log});
     CK(cudaGetLastError());
     CK(cudaEventRecord(e1, st));
     std::vector<unsigned long long> hp(nobj);
@@ -313,6 +318,8 @@ void run_intersects(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit,
     S.pairs_evaluated = pairs;  // covered (early exit and culls are not subtracted)
     S.kernels = 1;
     S.rounds = 1;
+    near.fetch(st, cx.near);
+    S.near_degenerate = cx.near->count;
 }
 
 }  // namespace tdb

@@ -244,7 +244,7 @@ __device__ __forceinline__ double q_eta(const QueryRegs& Q, const double* Bs) {
 // ---- fused path: the whole mesh is one chunk --------------------------------
 __global__ void __launch_bounds__(kTile, 3) q_fused_kernel(QArgs a, const double* Bs, double* out_d,
                                                            unsigned long long* out_f, unsigned long long* ncand,
-                                                           unsigned long long* nrounds) {
+                                                           unsigned long long* nrounds, NearLog near) {
     __shared__ alignas(128) double sm[2][kFilterPlanes * kSB];
     __shared__ alignas(8) uint64_t bar[2];
     Stream<kFilterPlanes> S{sm, bar, kDistPlaneIds};
@@ -312,6 +312,7 @@ __global__ void __launch_bounds__(kTile, 3) q_fused_kernel(QArgs a, const double
             const double dx = Q.point ? exact::pt_tri(p0, t).d : exact::seg_tri(p0, p1, t).d;
             const unsigned long long e = (unsigned long long)__double_as_longlong(dx);
             if (e < D || (e == D && j < P)) D = e, P = j;
+            if (Q.point ? exact::near_area(t) : exact::near_degenerate_seg(p0, p1, t)) near_log(near, q, j);
         }
         // complete only if nothing in the band was dropped and the band holds
         again = evicted <= b2 || D == kNone || __longlong_as_double((long long)D) > band - eta;
@@ -417,7 +418,8 @@ __global__ void q_flag_kernel(QArgs a, uint64_t n_items, const double* band2, un
 // exact rescan of flagged items, TMA-staged like the filter
 __global__ void __launch_bounds__(kTile, 4) q_verify_kernel(QArgs a, const unsigned long long* list, int pass,
                                                             const double* band2, unsigned long long* qD,
-                                                            unsigned long long* qP, unsigned long long* ncand) {
+                                                            unsigned long long* qP, unsigned long long* ncand,
+                                                            NearLog near) {
     __shared__ alignas(128) double sm[2][kFilterPlanes * kSB];
     __shared__ alignas(8) uint64_t bar[2];
     Stream<kFilterPlanes> S{sm, bar, kDistPlaneIds};
@@ -439,6 +441,11 @@ __global__ void __launch_bounds__(kTile, 4) q_verify_kernel(QArgs a, const unsig
             if (pass == 1) {
                 atomicMin(qD + q, e);
                 ++cand;
+                const double* bv = sb + j;
+                const exact::tri t{{bv[0], bv[kSB], bv[2 * kSB]}, {bv[3 * kSB], bv[4 * kSB], bv[5 * kSB]},
+                                   {bv[6 * kSB], bv[7 * kSB], bv[8 * kSB]}};
+                const exact::v3 p0{Q.p0[0], Q.p0[1], Q.p0[2]}, p1{Q.p1[0], Q.p1[1], Q.p1[2]};
+                if (Q.point ? exact::near_area(t) : exact::near_degenerate_seg(p0, p1, t)) near_log(near, q, f0 + j);
             } else if (e == qD[q]) {
                 atomicMin(qP + q, (unsigned long long)(f0 + j));
             }
@@ -477,7 +484,7 @@ __global__ void q_check_kernel(QArgs a, const double* Bs, double* band2, double*
 // pairs the reference cannot hit (intersects.cu header); degenerate faces
 // (n = 0, c = 0) always reach (3).
 __global__ void __launch_bounds__(kTile, 4) q_hit_kernel(QArgs a, const double* Bs, unsigned long long* qhit,
-                                                         unsigned long long* nexact) {
+                                                         unsigned long long* nexact, NearLog near) {
     __shared__ alignas(128) double sm[2][kHitPlanes * kSB];
     __shared__ alignas(8) uint64_t bar[2];
     Stream<kHitPlanes> S{sm, bar, kHitPlaneIds};
@@ -531,6 +538,7 @@ __global__ void __launch_bounds__(kTile, 4) q_hit_kernel(QArgs a, const double* 
             const double* bv = sb + j;
             const exact::tri t{{bv[0], bv[kSB], bv[2 * kSB]}, {bv[3 * kSB], bv[4 * kSB], bv[5 * kSB]},
                                {bv[6 * kSB], bv[7 * kSB], bv[8 * kSB]}};
+            if (exact::near_degenerate_seg(e0, e1, t)) near_log(near, q, f0 + j);
             if (exact::seg_tri_hit(e0, e1, t)) {
                 atomicMin(qhit + q, (unsigned long long)(f0 + j));
                 live = false;  // later faces only give larger indices
@@ -630,6 +638,8 @@ void run_queries(const Ctx& cx, int op, const QuerySet& qs, const Geom& B, doubl
     // results: exact distance bits / face (or lowest hit face), finalized on the device
     unsigned long long* rD = (unsigned long long*)alloc(n * sizeof(unsigned long long));
     unsigned long long* rP = (unsigned long long*)alloc(n * sizeof(unsigned long long));
+    NearDev near;
+    near.alloc(st);
     cudaEvent_t ev[4];
     for (auto& e : ev) CK(cudaEventCreate(&e));
     CK(cudaEventRecord(ev[0], st));
@@ -639,14 +649,14 @@ void run_queries(const Ctx& cx, int op, const QuerySet& qs, const Geom& B, doubl
     unsigned long long hc[4] = {0, 0, 0, 0};
     if (op == TDB_OP_INTERSECTS) {
         CK(cudaMemsetAsync(rP, 0xff, n * sizeof(unsigned long long), st));
-        q_hit_kernel<<<(unsigned)n_items, kTile, 0, st>>>(a, Bs, rP, ctr);
+        q_hit_kernel<<<(unsigned)n_items, kTile, 0, st>>>(a, Bs, rP, ctr, near.log);
         CK(cudaGetLastError());
         CK(cudaEventRecord(ev[1], st));
         CK(cudaEventRecord(ev[2], st));
         launches = 1;
         rounds = 1;
     } else if (fused) {
-        q_fused_kernel<<<(unsigned)tiles, kTile, 0, st>>>(a, Bs, (double*)rD, rP, ctr, ctr + 1);
+        q_fused_kernel<<<(unsigned)tiles, kTile, 0, st>>>(a, Bs, (double*)rD, rP, ctr, ctr + 1, near.log);
         CK(cudaGetLastError());
         CK(cudaEventRecord(ev[1], st));
         CK(cudaEventRecord(ev[2], st));
@@ -676,7 +686,7 @@ void run_queries(const Ctx& cx, int op, const QuerySet& qs, const Geom& B, doubl
             flagged += nflag;
             if (nflag) {
                 for (int pass = 1; pass <= 2; ++pass) {
-                    q_verify_kernel<<<(unsigned)nflag, kTile, 0, st>>>(a, list, pass, band2, rD, rP, ctr);
+                    q_verify_kernel<<<(unsigned)nflag, kTile, 0, st>>>(a, list, pass, band2, rD, rP, ctr, near.log);
                     CK(cudaGetLastError());
                 }
             }
@@ -719,6 +729,8 @@ void run_queries(const Ctx& cx, int op, const QuerySet& qs, const Geom& B, doubl
     else S.exact_pairs = hc[0];
     S.kernels = launches;
     S.rounds = fused ? (int)hc[1] : rounds;
+    near.fetch(st, cx.near);
+    S.near_degenerate = cx.near->count;
 }
 
 }  // namespace tdb

@@ -3,12 +3,14 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <limits>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
+#include "exact.cuh"
 #include "fast_pair.cuh"
 #include "tdb_internal.h"
 #include "tindb_b200.h"
@@ -49,12 +51,54 @@ void geom_release(Geom* g);
 // AABBs (lo xyz, hi xyz) of the uniform face chunks [c*len, (c+1)*len) of g.
 void chunk_aabbs(const Geom& g, uint64_t len, double* out, cudaStream_t st);
 
+// Near-degenerate log of the last call (host side, per thread).
+struct NearHost {
+    uint64_t count = 0;
+    std::vector<uint64_t> entries;  // (object, pair) pairs, at most kNearLogCap
+};
+
 // Per-call execution context.
 struct Ctx {
     cudaStream_t stream;
     int mode;
     int sms;
     tdb_stats* stats;
+    NearHost* near;
+};
+
+// Device side of the near-degenerate log for one call.
+struct NearDev {
+    NearLog log{nullptr, nullptr};
+    cudaStream_t stream = nullptr;
+    NearDev() = default;
+    NearDev(const NearDev&) = delete;
+    NearDev& operator=(const NearDev&) = delete;
+    ~NearDev() {  // error paths: release without throwing
+        if (log.count) cudaFreeAsync(log.count, stream);
+        if (log.entries) cudaFreeAsync(log.entries, stream);
+    }
+    void alloc(cudaStream_t st) {
+        stream = st;
+        CK(cudaMallocAsync(&log.count, sizeof(unsigned long long), st));
+        CK(cudaMallocAsync(&log.entries, 2 * kNearLogCap * sizeof(unsigned long long), st));
+        CK(cudaMemsetAsync(log.count, 0, sizeof(unsigned long long), st));
+    }
+    // after the call's final synchronize
+    void fetch(cudaStream_t st, NearHost* h) {
+        unsigned long long c = 0;
+        CK(cudaMemcpyAsync(&c, log.count, sizeof c, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        h->count = c;
+        h->entries.assign(2 * std::min<uint64_t>(c, kNearLogCap), 0);
+        if (!h->entries.empty())
+            CK(cudaMemcpyAsync(h->entries.data(), log.entries, h->entries.size() * sizeof(uint64_t),
+                               cudaMemcpyDeviceToHost, st));
+        CK(cudaFreeAsync(log.count, st));
+        log.count = nullptr;
+        CK(cudaFreeAsync(log.entries, st));
+        log.entries = nullptr;
+        CK(cudaStreamSynchronize(st));
+    }
 };
 
 // A-side selection: tiles [tile0, tile1) of A, rows restricted to
