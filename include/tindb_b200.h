@@ -39,6 +39,7 @@ extern "C" {
 #define TDB_E_ARG (-1)   /* bad argument (maps to std::invalid_argument) */
 #define TDB_E_CUDA (-2)  /* CUDA / device failure (maps to std::runtime_error) */
 #define TDB_E_NOMEM (-3) /* device allocation failed */
+#define TDB_E_PARSE (-4) /* malformed WKT: tindb::WktParseError (wkt.hpp:13); last_error = its what() */
 
 typedef struct tdb_geom_s* tdb_mesh;  /* device-resident triangle soup (1 object) */
 typedef struct tdb_geom_s* tdb_table; /* many objects: CSR face offsets + AABB headers */
@@ -110,6 +111,21 @@ int tdb_mesh_upload(const double* tri9, uint64_t n_tris, tdb_mesh* out);
  * entries (CSR), face_offsets[0] == 0. */
 int tdb_table_upload(const double* tri9, const uint64_t* face_offsets, uint64_t n_objects,
                      tdb_table* out);
+/* ---- device geometry loader (replaces tindb::parse_wkt, wkt.hpp:35, and the
+ * TriangleMesh it builds; load_wkt_file / load_csv_text's WKT column,
+ * store.hpp:62-71). The text is parsed in HBM; coordinates are bit-identical
+ * to std::from_chars (wkt.cpp:84-95); POLYHEDRALSURFACE patches are
+ * fan-triangulated as wkt.cpp:134-138. A literal the reference rejects
+ * returns TDB_E_PARSE with the reference's WktParseError what() in
+ * tdb_last_error() and its byte position in *err_pos (relative to the
+ * literal); POINT / LINESTRING literals are not meshes (TDB_E_PARSE, pos 0). */
+int tdb_mesh_from_wkt(const char* text, uint64_t len, tdb_mesh* out, uint64_t* err_pos);
+/* n_lit literals text[lit_off[i], lit_off[i+1]) -> one table object each;
+ * *err_literal names the first rejected literal. */
+int tdb_table_from_wkt(const char* text, const uint64_t* lit_off, uint64_t n_lit, tdb_table* out,
+                       uint64_t* err_literal, uint64_t* err_pos);
+/* The store's faces back as host AoS, 9 doubles per face in face order. */
+int tdb_geom_download(tdb_mesh g, double* tri9_out);
 int tdb_geom_info(tdb_mesh g, uint64_t* n_tris, uint64_t* n_objects, uint64_t* n_degenerate,
                   double* aabb6);
 void tdb_mesh_free(tdb_mesh m);

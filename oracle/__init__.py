@@ -109,6 +109,11 @@ def _load_ref():
     L.ref_mesh_volume.restype = ct.c_double
     L.ref_unit_cube.argtypes = [_D]
     L.ref_unit_cube.restype = ct.c_uint64
+    L.ref_parse_wkt.argtypes = [ct.c_char_p, ct.c_uint64, ct.POINTER(ct.c_int), _D, ct.c_uint64, _U64,
+                                ct.POINTER(ct.c_int), ct.c_char_p, ct.c_uint64, _U64]
+    L.ref_parse_wkt.restype = ct.c_int
+    L.ref_serialize_mesh.argtypes = [_D, ct.c_uint64, ct.c_char_p, ct.c_uint64]
+    L.ref_serialize_mesh.restype = ct.c_uint64
     return L
 
 
@@ -313,3 +318,50 @@ def ref_unit_cube():
     out = np.empty((12, 9), np.float64)
     REF.ref_unit_cube(_dp(out))
     return out
+
+
+class RefWktError(ValueError):
+    """tindb::WktParseError raised by the reference parser (wkt.hpp:13)."""
+
+    def __init__(self, what, position):
+        super().__init__(what)
+        self.what = what
+        self.position = position
+
+
+REF_KINDS = {0: "point", 1: "segment", 2: "linestring", 3: "mesh"}
+
+
+def ref_parse_wkt(text):
+    """The reference parse_wkt (wkt.cpp:188): (kind, coords, mesh_source) or
+    raises RefWktError(what, position). Mesh coords are (n, 9)."""
+    raw = text.encode() if isinstance(text, str) else bytes(text)
+    kind, src, n = ct.c_int(0), ct.c_int(0), ct.c_uint64(0)
+    pos = ct.c_uint64(0)
+    err = ct.create_string_buffer(512)
+    cap = 9 * (raw.count(b",") + 4)  # >= 9 doubles per point listed
+    out = np.empty(cap, np.float64)
+    rc = REF.ref_parse_wkt(raw, len(raw), ct.byref(kind), _dp(out), cap, ct.byref(n), ct.byref(src), err, 512,
+                           ct.byref(pos))
+    if rc:
+        raise RefWktError(err.value.decode(), pos.value)
+    k = REF_KINDS[kind.value]
+    if k == "mesh":
+        return k, out[: 9 * n.value].reshape(-1, 9).copy(), ("tin", "polyhedralsurface")[src.value]
+    return k, out[: 3 * n.value].reshape(-1, 3).copy(), None
+
+
+def ref_serialize_mesh(tris, as_bytes=False):
+    """The reference serialize_wkt(TriangleMesh) text (canonical TIN Z)."""
+    t = _f64(tris).reshape(-1, 9)
+    n = REF.ref_serialize_mesh(_dp(t), len(t), None, 0)
+    buf = ct.create_string_buffer(n)
+    REF.ref_serialize_mesh(_dp(t), len(t), buf, n)
+    raw = buf.raw[:n]
+    return raw if as_bytes else raw.decode()
+
+
+def sha_f64(a):
+    """sha256 of a float64 array's bytes (golden fixture digests)."""
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a, np.float64).tobytes()).hexdigest()

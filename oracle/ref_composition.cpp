@@ -21,10 +21,16 @@
 //   mesh intersects = lowest hit p (mirrors intersects_mesh, kernels.cpp:407)
 // Row parallelism uses the reference's own for_each_chunk
 // (executor.hpp:50-83) with chunk = 1 row.
+#include <cstdio>
+#include <cstring>
+#include <string_view>
+#include <variant>
+
 #include <tindb/dataset.hpp>
 #include <tindb/executor.hpp>
 #include <tindb/geometry.hpp>
 #include <tindb/kernels.hpp>
+#include <tindb/wkt.hpp>
 
 #include "support/fixtures.hpp"
 
@@ -322,6 +328,52 @@ double ref_mesh_volume(const double* t9, std::uint64_t n, std::uint64_t chunk, i
     const double v = K::mesh_volume(m, cfg, closed_out ? &closed : nullptr);
     if (closed_out) *closed_out = closed ? 1 : 0;
     return v;
+}
+
+// wkt.cpp:188 parse_wkt. Returns 0 and the geometry (kind 0 point, 1
+// segment, 2 linestring, 3 mesh; coordinates in `out`, *n_out points or
+// triangles; *src_out the MeshSource) or 1 with the WktParseError's what()
+// and position.
+int ref_parse_wkt(const char* text, std::uint64_t len, int* kind_out, double* out, std::uint64_t cap,
+                  std::uint64_t* n_out, int* src_out, char* err, std::uint64_t errcap, std::uint64_t* pos_out) {
+    try {
+        const tindb::Geometry g = tindb::parse_wkt(std::string_view(text, len));
+        *n_out = 0;
+        if (auto* p = std::get_if<Point3>(&g)) {
+            *kind_out = 0;
+            *n_out = 1;
+            if (cap >= 3) std::memcpy(out, p, sizeof *p);
+        } else if (auto* sg = std::get_if<LineSegment>(&g)) {
+            *kind_out = 1;
+            *n_out = 2;
+            if (cap >= 6) std::memcpy(out, sg, sizeof *sg);
+        } else if (auto* ls = std::get_if<tindb::LineString>(&g)) {
+            *kind_out = 2;
+            *n_out = ls->points.size();
+            if (cap >= 3 * ls->points.size()) std::memcpy(out, ls->points.data(), ls->points.size() * sizeof(Point3));
+        } else if (auto* m = std::get_if<TriangleMesh>(&g)) {
+            *kind_out = 3;
+            *n_out = m->triangles.size();
+            if (src_out) *src_out = (int)m->source_kind;
+            if (cap >= 9 * m->triangles.size())
+                std::memcpy(out, m->triangles.data(), m->triangles.size() * sizeof(Triangle));
+        }
+        return 0;
+    } catch (const tindb::WktParseError& e) {
+        std::snprintf(err, errcap, "%s", e.what());
+        *pos_out = e.position();
+        return 1;
+    }
+}
+
+// wkt.cpp serialize_wkt(TriangleMesh): canonical TIN Z text, shortest
+// round-trip numbers. Returns the text length (writes when it fits).
+std::uint64_t ref_serialize_mesh(const double* t9, std::uint64_t n, char* out, std::uint64_t cap) {
+    TriangleMesh m;
+    m.triangles = load_mesh(t9, n);
+    const std::string s = tindb::serialize_wkt(m);
+    if (out && cap >= s.size()) std::memcpy(out, s.data(), s.size());
+    return s.size();
 }
 
 }  // extern "C"

@@ -25,7 +25,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libtindb_b200.so")
 
-TDB_OK, TDB_E_ARG, TDB_E_CUDA, TDB_E_NOMEM = 0, -1, -2, -3
+TDB_OK, TDB_E_ARG, TDB_E_CUDA, TDB_E_NOMEM, TDB_E_PARSE = 0, -1, -2, -3, -4
 OP_DISTANCE, OP_INTERSECTS = 1, 2
 MODE_FULL, MODE_CULL = 0, 1
 U64_MAX = (1 << 64) - 1
@@ -91,6 +91,9 @@ _SIGS = [
     ("tdb_mesh_upload", ct.c_int, [_D, ct.c_uint64, ct.POINTER(ct.c_void_p)]),
     ("tdb_table_upload", ct.c_int, [_D, _U64, ct.c_uint64, ct.POINTER(ct.c_void_p)]),
     ("tdb_geom_info", ct.c_int, [ct.c_void_p, _U64, _U64, _U64, _D]),
+    ("tdb_mesh_from_wkt", ct.c_int, [ct.c_char_p, ct.c_uint64, ct.POINTER(ct.c_void_p), _U64]),
+    ("tdb_table_from_wkt", ct.c_int, [ct.c_char_p, _U64, ct.c_uint64, ct.POINTER(ct.c_void_p), _U64, _U64]),
+    ("tdb_geom_download", ct.c_int, [ct.c_void_p, _D]),
     ("tdb_mesh_free", None, [ct.c_void_p]),
     ("tdb_table_free", None, [ct.c_void_p]),
     ("tdb_mesh_mesh_distance", ct.c_int, [ct.c_void_p, ct.c_void_p, ct.POINTER(DistOut)]),
@@ -221,6 +224,13 @@ class _Geom:
         _check(lib().tdb_geom_info(self._h, ct.byref(n), ct.byref(no), ct.byref(nd), box))
         return {"faces": n.value, "objects": no.value, "degenerate": nd.value, "aabb": list(box)}
 
+    def download(self) -> np.ndarray:
+        """The stored faces as (n, 9) float64, face order (the AoS the store was built from)."""
+        n = self.info()["faces"]
+        out = np.empty((n, 9), np.float64)
+        _check(lib().tdb_geom_download(self._h, _dp(out)))
+        return out
+
     def free(self):
         if self._h is not None and self._h.value:
             lib().tdb_mesh_free(self._h)
@@ -255,6 +265,57 @@ class Table(_Geom):
         super().__init__(h.value)
         self.objects = len(off) - 1
         self.ids = list(ids) if ids is not None else list(range(1, self.objects + 1))
+
+
+class WktParseError(ValueError):
+    """tindb::WktParseError (wkt.hpp:13-23): the reference's what() and 0-based
+    byte `position` within the literal; `literal` indexes the rejected literal
+    of a multi-literal load."""
+
+    def __init__(self, what: str, position: int, literal: int = 0):
+        super().__init__(what)
+        self.what = what
+        self.position = position
+        self.literal = literal
+
+
+def _wkt_bytes(text) -> bytes:
+    return text.encode() if isinstance(text, str) else bytes(text)
+
+
+def mesh_from_wkt(text) -> Mesh:
+    """parse_wkt (wkt.hpp:35) of a TIN Z / POLYHEDRALSURFACE Z literal, parsed
+    on the device straight into the store (bit-identical coordinates)."""
+    raw = _wkt_bytes(text)
+    h, pos = ct.c_void_p(), ct.c_uint64(0)
+    rc = lib().tdb_mesh_from_wkt(raw, len(raw), ct.byref(h), ct.byref(pos))
+    if rc == TDB_E_PARSE:
+        raise WktParseError(lib().tdb_last_error().decode(), pos.value, 0)
+    _check(rc)
+    m = Mesh.__new__(Mesh)
+    _Geom.__init__(m, h.value)
+    m.faces = m.info()["faces"]
+    return m
+
+
+def table_from_wkt(literals: Sequence, ids: Optional[Sequence[int]] = None) -> Table:
+    """A mesh column from WKT literals (load_csv_text's WKT field,
+    store.cpp:71-122), all parsed in one device pass; object i = literal i."""
+    raws = [_wkt_bytes(x) for x in literals]
+    off = np.zeros(len(raws) + 1, np.uint64)
+    off[1:] = np.cumsum([len(r) for r in raws], dtype=np.uint64)
+    blob = b"".join(raws)
+    h, lit, pos = ct.c_void_p(), ct.c_uint64(0), ct.c_uint64(0)
+    rc = lib().tdb_table_from_wkt(blob, off.ctypes.data_as(_U64), len(raws), ct.byref(h), ct.byref(lit),
+                                  ct.byref(pos))
+    if rc == TDB_E_PARSE:
+        raise WktParseError(lib().tdb_last_error().decode(), pos.value, lit.value)
+    _check(rc)
+    t = Table.__new__(Table)
+    _Geom.__init__(t, h.value)
+    t.objects = len(raws)
+    t.ids = list(ids) if ids is not None else list(range(1, t.objects + 1))
+    return t
 
 
 @dataclass

@@ -34,6 +34,7 @@ thread_local int t_mode = TDB_MODE_FULL;
 thread_local int t_device = -1;
 thread_local tdb_stats t_stats{};
 thread_local tdb::NearHost t_near;
+thread_local uint64_t t_wkt_literal = 0, t_wkt_pos = 0;
 
 std::mutex g_mu;
 std::vector<cudaStream_t> g_streams;  // library stream per device
@@ -50,6 +51,10 @@ int guarded(F&& f) {
         f();
         t_err.clear();
         return TDB_OK;
+    } catch (const tdb::WktError& e) {
+        t_wkt_literal = e.literal;
+        t_wkt_pos = e.position;
+        return fail(TDB_E_PARSE, e.what());
     } catch (const std::invalid_argument& e) {
         return fail(TDB_E_ARG, e.what());
     } catch (const std::bad_alloc& e) {
@@ -225,6 +230,44 @@ int tdb_table_upload(const double* tri9, const uint64_t* off, uint64_t n_obj, td
     return guarded([&] {
         need(off != nullptr, "null face offsets");
         upload(tri9, off[n_obj], off, n_obj, out);
+    });
+}
+
+int tdb_mesh_from_wkt(const char* text, uint64_t len, tdb_mesh* out, uint64_t* err_pos) {
+    const uint64_t off[2] = {0, len};
+    return tdb_table_from_wkt(text, off, 1, out, nullptr, err_pos);
+}
+
+int tdb_table_from_wkt(const char* text, const uint64_t* lit_off, uint64_t n_lit, tdb_table* out,
+                       uint64_t* err_literal, uint64_t* err_pos) {
+    const int rc = guarded([&] {
+        need(out != nullptr, "null output handle");
+        need(lit_off != nullptr && (text != nullptr || lit_off[n_lit] == 0), "null WKT text or offsets");
+        need(lit_off[0] == 0, "literal offsets must start at 0");
+        tdb::Ctx c = ctx();
+        auto* h = new tdb_geom_s();
+        h->g.device = t_device;
+        try {
+            tdb::wkt_build(&h->g, text, lit_off, n_lit, c.stream);
+        } catch (...) {
+            tdb::geom_release(&h->g);
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+    if (rc == TDB_E_PARSE) {
+        if (err_literal) *err_literal = t_wkt_literal;
+        if (err_pos) *err_pos = t_wkt_pos;
+    }
+    return rc;
+}
+
+int tdb_geom_download(tdb_mesh g, double* tri9_out) {
+    return guarded([&] {
+        need(g != nullptr, "null handle");
+        need(tri9_out != nullptr || g->g.n == 0, "null output");
+        tdb::geom_download(g->g, tri9_out, ctx().stream);
     });
 }
 

@@ -29,6 +29,14 @@ struct CudaError : std::runtime_error {
                                    __FILE__ + ":" + std::to_string(__LINE__) + ")");          \
     } while (0)
 
+// A rejected WKT literal: the reference's WktParseError (wkt.hpp:13-23)
+// what() and position, plus the literal's index in a multi-literal load.
+struct WktError : std::invalid_argument {
+    uint64_t literal, position;
+    WktError(const std::string& what, uint64_t lit, uint64_t pos)
+        : std::invalid_argument(what), literal(lit), position(pos) {}
+};
+
 inline double pos_inf_h() { return std::numeric_limits<double>::infinity(); }
 
 struct Geom {
@@ -45,9 +53,15 @@ struct Geom {
     double stats[kObjStats] = {};      // aggregate: aabb lo/hi, max edge, max |coord|
 };
 
-void geom_build(Geom* g, const double* host_tri9, uint64_t n, const uint64_t* host_off,
-                uint64_t n_obj, cudaStream_t st);
+// tri9: 9 doubles per face (AoS), on the host unless tri9_on_device
+void geom_build(Geom* g, const double* tri9, uint64_t n, const uint64_t* host_off, uint64_t n_obj,
+                cudaStream_t st, bool tri9_on_device = false);
 void geom_release(Geom* g);
+// WKT literals text[lit_off[i], lit_off[i+1]) (TIN Z / POLYHEDRALSURFACE Z),
+// parsed on the device into g, one object per literal (csrc/wkt.cu).
+void wkt_build(Geom* g, const char* text, const uint64_t* lit_off, uint64_t n_lit, cudaStream_t st);
+// g's faces back to host AoS (9 doubles per face).
+void geom_download(const Geom& g, double* host_tri9, cudaStream_t st);
 // AABBs (lo xyz, hi xyz) of the uniform face chunks [c*len, (c+1)*len) of g.
 void chunk_aabbs(const Geom& g, uint64_t len, double* out, cudaStream_t st);
 

@@ -195,7 +195,7 @@ __global__ void range_aabb_kernel(const double* __restrict__ planes, uint64_t n,
 }  // namespace
 
 void geom_build(Geom* g, const double* host_tri9, uint64_t n, const uint64_t* host_off,
-                uint64_t n_obj, cudaStream_t st) {
+                uint64_t n_obj, cudaStream_t st, bool tri9_on_device) {
     g->n = n;
     g->n_obj = n_obj;
     g->n_pad = ((n + 1 + kPlanePad - 1) / kPlanePad) * kPlanePad;
@@ -219,7 +219,7 @@ void geom_build(Geom* g, const double* host_tri9, uint64_t n, const uint64_t* ho
     g->n_chunks = (n + kChunk - 1) / kChunk;
 
     double* staging = nullptr;
-    CK(cudaMallocAsync(&staging, std::max<uint64_t>(1, 9 * n) * sizeof(double), st));
+    if (!tri9_on_device) CK(cudaMallocAsync(&staging, std::max<uint64_t>(1, 9 * n) * sizeof(double), st));
     CK(cudaMallocAsync(&g->planes, (size_t)NF * g->n_pad * sizeof(double), st));
     CK(cudaMallocAsync(&g->d_off, (n_obj + 1) * sizeof(uint64_t), st));
     CK(cudaMallocAsync(&g->d_tiles, std::max<size_t>(1, g->h_tiles.size()) * sizeof(Tile), st));
@@ -232,7 +232,9 @@ void geom_build(Geom* g, const double* host_tri9, uint64_t n, const uint64_t* ho
     CK(cudaMemsetAsync(ndeg, 0, 2 * sizeof(unsigned long long), st));
     CK(cudaMemsetAsync(g->planes, 0, (size_t)NF * g->n_pad * sizeof(double), st));
 
-    if (n) CK(cudaMemcpyAsync(staging, host_tri9, 9 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (n && !tri9_on_device)
+        CK(cudaMemcpyAsync(staging, host_tri9, 9 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+    const double* src = tri9_on_device ? host_tri9 : staging;
     CK(cudaMemcpyAsync(g->d_off, g->h_off.data(), (n_obj + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
     if (!g->h_tiles.empty())
         CK(cudaMemcpyAsync(g->d_tiles, g->h_tiles.data(), g->h_tiles.size() * sizeof(Tile),
@@ -243,7 +245,7 @@ void geom_build(Geom* g, const double* host_tri9, uint64_t n, const uint64_t* ho
         CK(cudaGetLastError());
     }
     if (n) {
-        prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(staging, n, g->n_pad, g->d_off, n_obj,
+        prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, n, g->n_pad, g->d_off, n_obj,
                                                                 g->planes, ustats, ndeg);
         CK(cudaGetLastError());
         if (!g->h_tiles.empty()) {
@@ -263,7 +265,7 @@ void geom_build(Geom* g, const double* host_tri9, uint64_t n, const uint64_t* ho
     std::vector<double> os(std::max<uint64_t>(1, n_obj) * kObjStats, 0.0);
     if (n_obj) CK(cudaMemcpyAsync(os.data(), g->d_obj_stats, n_obj * kObjStats * sizeof(double),
                                   cudaMemcpyDeviceToHost, st));
-    CK(cudaFreeAsync(staging, st));
+    if (staging) CK(cudaFreeAsync(staging, st));
     CK(cudaFreeAsync(ustats, st));
     CK(cudaFreeAsync(ndeg, st));
     CK(cudaStreamSynchronize(st));

@@ -176,6 +176,156 @@ def sha(a):
     return hashlib.sha256(np.ascontiguousarray(a, np.float64).tobytes()).hexdigest()
 
 
+def _fmt_num(rng, v):
+    """One coordinate in a random textual form that still means exactly v
+    (or, for the 'lossy' forms, a nearby decimal the reference rounds)."""
+    k = rng.integers(0, 10)
+    if k == 0:
+        return repr(float(v))
+    if k == 1:
+        return "%.17g" % v
+    if k == 2:
+        return "%.17E" % v
+    if k == 3:
+        return "%.6e" % v                        # lossy, short
+    if k == 4:
+        return "%.3f" % v                        # lossy, fixed
+    if k == 5:
+        s = "%.25f" % v                          # long fixed
+        return s
+    if k == 6:
+        s = repr(float(v))
+        return ("00" + s) if not s.startswith("-") else "-00" + s[1:]   # leading zeros
+    if k == 7:
+        return "%.40e" % v                       # 41 significant digits (beyond 19)
+    if k == 8:
+        s = "%.3f" % v
+        return s.rstrip("0") if "." in s else s   # "1." style trailing point
+    return "%.0f." % v if abs(v) < 1e15 else repr(float(v))
+
+
+def _ws(rng, allow_empty=True):
+    opts = [" ", "  ", "\t", "\n", "\r\n", " \t "] + ([""] * 3 if allow_empty else [])
+    return opts[rng.integers(0, len(opts))]
+
+
+def _surface_text(rng, kw, rings):
+    """TIN Z / POLYHEDRALSURFACE Z text of closed rings (lists of 3-tuples),
+    with random spacing and number forms (only where the grammar allows)."""
+    parts = []
+    for ring in rings:
+        pts = []
+        for p in ring:
+            a, b, c = (_fmt_num(rng, x) for x in p)
+            pts.append(a + _ws(rng, False) + b + _ws(rng, False) + c)
+        pts.append(pts[0])  # the closure repeats the first point's text
+        sep = [_ws(rng) + "," + _ws(rng) for _ in pts[1:]]
+        body = pts[0] + "".join(s + q for s, q in zip(sep, pts[1:]))
+        parts.append("(" + _ws(rng) + "(" + _ws(rng) + body + _ws(rng) + ")" + _ws(rng) + ")")
+    body = (_ws(rng) + "," + _ws(rng)).join(parts)
+    return kw + _ws(rng, False) + "Z" + _ws(rng) + "(" + _ws(rng) + body + _ws(rng) + ")" + _ws(rng)
+
+
+def wkt_cases():
+    """WKT literals and what the reference's parse_wkt makes of them."""
+    rng = np.random.default_rng(1808)
+    texts = {}
+    # reference unit tests (test_geometry.cpp:110-205)
+    texts["tin_two_patches"] = "TIN Z (((0 0 0, 1 0 0, 0 1 0, 0 0 0)), ((0 0 1, 1 0 1, 0 1 1, 0 0 1)))"
+    texts["tin_non_triangular"] = "TIN Z (((0 0 0, 1 0 0, 1 1 0, 0 1 0, 0 0 0)))"
+    texts["poly_quad_fan"] = "POLYHEDRALSURFACE Z (((0 0 0, 1 0 0, 1 1 0, 0 1 0, 0 0 0)))"
+    texts["unclosed_ring"] = "TIN Z (((0 0 0, 1 0 0, 0 1 0, 5 5 5)))"
+    texts["short_ring"] = "TIN Z (((0 0 0, 1 0 0, 0 0 0)))"
+    texts["no_z"] = "TIN (((0 0 0, 1 0 0, 0 1 0, 0 0 0)))"
+    texts["zm"] = "TIN ZM (((0 0 0 1, 1 0 0 1, 0 1 0 1, 0 0 0 1)))"
+    texts["m"] = "TIN M (((0 0 0, 1 0 0, 0 1 0, 0 0 0)))"
+    texts["two_d"] = "TIN Z (((0 0, 1 0, 0 1, 0 0)))"
+    texts["nan"] = "TIN Z (((0 0 nan, 1 0 0, 0 1 0, 0 0 0)))"
+    texts["inf"] = "TIN Z (((inf 0 0, 1 0 0, 0 1 0, 0 0 0)))"
+    texts["minus_inf"] = "TIN Z (((0 -inf 0, 1 0 0, 0 1 0, 0 0 0)))"
+    texts["overflow"] = "TIN Z (((0 0 1e999, 1 0 0, 0 1 0, 0 0 0)))"
+    texts["underflow"] = "TIN Z (((0 0 1e-400, 1 0 0, 0 1 0, 0 0 0)))"
+    texts["trailing"] = "TIN Z (((0 0 0, 1 0 0, 0 1 0, 0 0 0))) x"
+    texts["unknown_tag"] = "CIRCLE Z (0 0 0)"
+    texts["empty"] = ""
+    texts["blank"] = "  \n\t "
+    texts["point"] = "POINT Z (1 2 3)"
+    texts["linestring"] = "LINESTRING Z (0 0 0, 1 1 1)"
+    texts["incomplete_triple"] = "TIN Z (((0 0 0, 1, 0 1 0, 0 0 0)))"
+    texts["plus_sign"] = "TIN Z (((+1 0 0, 1 0 0, 0 1 0, +1 0 0)))"
+    texts["garbage_number"] = "TIN Z (((0 0 0, 1 0 0, 0 1 x, 0 0 0)))"
+    texts["interior_ring"] = "POLYHEDRALSURFACE Z (((0 0 0, 4 0 0, 4 4 0, 0 0 0), (1 1 0, 2 1 0, 2 2 0, 1 1 0)))"
+    texts["missing_close"] = "TIN Z (((0 0 0, 1 0 0, 0 1 0, 0 0 0))"
+    texts["extra_close"] = "TIN Z (((0 0 0, 1 0 0, 0 1 0, 0 0 0))))"
+    texts["empty_surface"] = "TIN Z ()"
+    texts["header_only"] = "TIN Z"
+    texts["empty_patch"] = "TIN Z (())"
+    texts["four_coords"] = "TIN Z (((0 0 0 0, 1 0 0, 0 1 0, 0 0 0)))"
+    texts["missing_comma"] = "TIN Z (((0 0 0 1 0 0, 0 1 0, 0 0 0)))"
+    texts["double_comma"] = "TIN Z (((0 0 0,, 1 0 0, 0 1 0, 0 0 0)))"
+    texts["patch_no_comma"] = "TIN Z (((0 0 0, 1 0 0, 0 1 0, 0 0 0)) ((0 0 1, 1 0 1, 0 1 1, 0 0 1)))"
+    texts["bad_exponent"] = "TIN Z (((0 0 1e, 1 0 0, 0 1 0, 0 0 1e)))"
+    texts["dot_alone"] = "TIN Z (((0 0 ., 1 0 0, 0 1 0, 0 0 0)))"
+    texts["nul_byte"] = "TIN Z (((0 0 0, 1 0\x00 0, 0 1 0, 0 0 0)))"
+    texts["utf8"] = "TIN Z (((0 0 0, 1 0 0, 0 1 0, 0 0 0)))\u00a0"
+    # accepted oddities of the from_chars grammar
+    texts["juxtaposed"] = "TIN Z (((0-1 2, 1.5.5 -.25, 0 1 0, 0-1 2)))"
+    texts["no_spaces"] = "tin z(((0 0 0,1 0 0,0 1 0,0 0 0)),((0 0 1,1 0 1,0 1 1,0 0 1)))"
+    texts["case_mix"] = "  PolyhedralSurface   z\n(((0 0 0,\t1 0 0,1 1 0,0 1 0,0 0 0)))\n"
+    texts["exp_forms"] = "TIN Z (((1E2 1e+2 1e-2, 1. .5 -.5, 0e0 -0 00012, 1E2 1e+2 1e-2)))"
+    texts["minus_zero_closure"] = "TIN Z (((0 0 0, 1 0 0, 0 1 0, -0 -0.0 0e5)))"
+    # generated meshes with random spacing and number forms
+    tris = O.ref_random_triangles(77, 200, -1000.0, 1000.0)
+    texts["soup_tin"] = _surface_text(rng, "TIN", [t.reshape(3, 3) for t in tris])
+    polys = []
+    for n in rng.integers(3, 11, 60):
+        ang = np.sort(rng.uniform(0, 2 * np.pi, n))
+        c = rng.uniform(-50, 50, 3)
+        polys.append([c + [5 * np.cos(a), 5 * np.sin(a), rng.uniform(-1, 1)] for a in ang])
+    texts["soup_poly"] = _surface_text(rng, "POLYHEDRALSURFACE", polys)
+    texts["sphere_canonical"] = O.ref_serialize_mesh(O.ref_unit_sphere(1000))
+    # hard decimals: exact halfway points between neighbouring doubles (hundreds
+    # of digits), subnormals, near DBL_MAX
+    from decimal import Decimal, getcontext
+    getcontext().prec = 2000
+    hard = []
+    for _ in range(40):
+        x = float(rng.uniform(-1e3, 1e3)) * 10.0 ** int(rng.integers(-300, 300))
+        y = np.nextafter(x, np.inf)
+        mid = (Decimal(x) + Decimal(float(y))) / 2
+        hard.append(format(mid, "f") if abs(x) > 1e-5 and abs(x) < 1e20 else format(mid, "e"))
+    hard += ["4.9406564584124654e-324", "2.4703282292062328e-324", "1.7976931348623157e308",
+             "2.2250738585072011e-308", "9007199254740993", "0." + "0" * 320 + "123"]
+    hard_tris = []
+    for i in range(0, len(hard) - 2, 3):
+        a = [hard[i], hard[i + 1], hard[i + 2]]
+        hard_tris.append("((%s %s %s, 1 0 0, 0 1 0, %s %s %s))" % (*a, *a))
+    texts["hard_numbers"] = "TIN Z (" + ", ".join(hard_tris) + ")"
+    # an error deep inside a long literal
+    big = O.ref_serialize_mesh(O.ref_unit_sphere(1000))
+    cut = big.rfind("((", 0, len(big) * 2 // 3)
+    texts["deep_unclosed"] = big[:cut] + "((0 0 0, 1 0 0, 0 1 0, 0 0 1))" + big[cut + len("(("):].split("))", 1)[1]
+
+    out = {}
+    for name, t in texts.items():
+        try:
+            kind, c, src = O.ref_parse_wkt(t)
+            rec = {"text": t, "ok": True, "kind": kind}
+            if kind == "mesh":
+                rec.update(faces=len(c), sha=sha(c), source=src)
+        except O.RefWktError as e:
+            rec = {"text": t, "ok": False, "what": e.what, "position": e.position}
+        out[name] = rec
+    return out
+
+
+def main_wkt():
+    cases = wkt_cases()
+    with open(os.path.join(OUT, "wkt_cases.json"), "w") as f:
+        json.dump(cases, f, indent=0, sort_keys=True)
+    print("wkt cases:", len(cases), "accepted:", sum(c["ok"] for c in cases.values()))
+
+
 def main():
     assert O.REF is not None, "build oracle/_ref first (make -C oracle)"
     # random pairs on [-1,1]^3 (fixtures.cpp:89 random_triangle)
@@ -238,4 +388,8 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["wkt"]:
+        main_wkt()
+    else:
+        main()
+        main_wkt()
