@@ -71,8 +71,8 @@ void run_pairs(const Ctx& cx, const double* a9, const double* b9, uint64_t n, do
     uint8_t* dh = nullptr;
     CK(cudaMallocAsync(&da, 9 * n * sizeof(double), st));
     CK(cudaMallocAsync(&db, 9 * n * sizeof(double), st));
-    CK(cudaMemcpyAsync(da, a9, 9 * n * sizeof(double), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(db, b9, 9 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+    h2d(da, a9, 9 * n * sizeof(double), st);
+    h2d(db, b9, 9 * n * sizeof(double), st);
     if (dist) CK(cudaMallocAsync(&dd, n * sizeof(double), st));
     if (hit) CK(cudaMallocAsync(&dh, n, st));
     pairs_kernel<<<(unsigned)std::min<uint64_t>((n + 127) / 128, 148 * 16), 128, 0, st>>>(da, db, n, dd, dh);

@@ -588,7 +588,7 @@ void queries_build(QuerySet* qs, const double* host_q, uint64_t n, int kind, cud
         CK(cudaMallocAsync(&stage, n * qs->width * sizeof(double), st));
         CK(cudaMallocAsync(&nbad, sizeof(unsigned long long), st));
         CK(cudaMemsetAsync(nbad, 0, sizeof(unsigned long long), st));
-        CK(cudaMemcpyAsync(stage, host_q, n * qs->width * sizeof(double), cudaMemcpyHostToDevice, st));
+        h2d(stage, host_q, n * qs->width * sizeof(double), st);
         q_transpose_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(stage, n, qs->width, qs->pad, qs->planes,
                                                                        nbad);
         CK(cudaGetLastError());
@@ -706,11 +706,11 @@ void run_queries(const Ctx& cx, int op, const QuerySet& qs, const Geom& B, doubl
                                                                   oh);
     CK(cudaGetLastError());
     ++launches;
-    if (od) CK(cudaMemcpyAsync(dist, od, n * sizeof(double), cudaMemcpyDeviceToHost, st));
-    if (oh) CK(cudaMemcpyAsync(hit, oh, n, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(face, rP, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, st));
     CK(cudaEventRecord(ev[3], st));
+    if (od) d2h(dist, od, n * sizeof(double), st);
+    if (oh) d2h(hit, oh, n, st);
+    d2h(face, rP, n * sizeof(uint64_t), st);
+    CK(cudaMemcpyAsync(hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, st));
     for (void* p : mem) CK(cudaFreeAsync(p, st));
     CK(cudaStreamSynchronize(st));
     float ms = 0;

@@ -57,6 +57,11 @@ struct Geom {
 void geom_build(Geom* g, const double* tri9, uint64_t n, const uint64_t* host_off, uint64_t n_obj,
                 cudaStream_t st, bool tri9_on_device = false);
 void geom_release(Geom* g);
+// Caller (pageable) buffers <-> device through pinned staging (host_copy.cpp).
+// h2d is stream-ordered (returns once the source was read); d2h returns
+// with the data in dst.
+void h2d(void* dst, const void* src, size_t n, cudaStream_t st);
+void d2h(void* dst, const void* src, size_t n, cudaStream_t st);
 // WKT literals text[lit_off[i], lit_off[i+1]) (TIN Z / POLYHEDRALSURFACE Z),
 // parsed on the device into g, one object per literal (csrc/wkt.cu).
 void wkt_build(Geom* g, const char* text, const uint64_t* lit_off, uint64_t n_lit, cudaStream_t st);

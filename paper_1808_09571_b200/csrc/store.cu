@@ -233,7 +233,7 @@ void geom_build(Geom* g, const double* host_tri9, uint64_t n, const uint64_t* ho
     CK(cudaMemsetAsync(g->planes, 0, (size_t)NF * g->n_pad * sizeof(double), st));
 
     if (n && !tri9_on_device)
-        CK(cudaMemcpyAsync(staging, host_tri9, 9 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+        h2d(staging, host_tri9, 9 * n * sizeof(double), st);
     const double* src = tri9_on_device ? host_tri9 : staging;
     CK(cudaMemcpyAsync(g->d_off, g->h_off.data(), (n_obj + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
     if (!g->h_tiles.empty())

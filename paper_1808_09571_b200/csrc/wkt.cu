@@ -69,28 +69,78 @@ struct LexArgs {
     unsigned int* n_slow;
     uint32_t* lit_tok0;
     unsigned long long* err_byte;
+    uint8_t* span_multi;  // pass 0 -> 1: the span has a run with several numbers
 };
 
-template <int PASS>
-__global__ void lex_kernel(LexArgs a) {
-    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const uint64_t i0 = t * kSpan;
-    if (i0 >= a.n) return;
-    const uint64_t i1 = min(a.n, i0 + kSpan);
-    int64_t lo = 0, hi = a.n_lit;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (a.bb[mid] <= i0) lo = mid + 1;
-        else hi = mid;
+constexpr int kLexThreads = 256;
+constexpr int kLexChunk = kLexThreads * kSpan;  // bytes per CTA
+constexpr int kLexHalo = 512;                   // run look-ahead kept in SMEM
+constexpr int kTextPad = 16;                    // bytes before text[0] in the device copy
+
+// Shared view of a CTA's text window: bytes [c0 - kTextPad, c0 + kLexChunk +
+// kLexHalo) in SMEM, the rest read from global memory.
+struct Window {
+    const char* sm;
+    const char* text;
+    uint64_t c0, end;
+    __device__ __forceinline__ const char* at(uint64_t i) const {
+        return i < end ? sm + kTextPad + (i - c0) : text + i;
     }
-    int64_t j = lo - 1;
-    const uint32_t tok0 = PASS ? a.cnt_tok[t] : 0, num0 = PASS ? a.cnt_num[t] : 0;
+    __device__ __forceinline__ bool in(uint64_t i) const { return i <= end; }
+};
+
+// Emit (PASS 1) or count (PASS 0) the number(s) of run [p, r) whose first
+// token / number indices are tok / num; returns the number count, or -1 on
+// a lexical error (PASS 0 records it).
+template <int PASS>
+__device__ int lex_run(const LexArgs& a, const Window& w, uint64_t p, uint64_t r, uint32_t tok, uint32_t num) {
+    const bool smem = w.in(r);
+    int cnt = 0;
+    while (p < r) {  // from_chars maximal munch, number after number
+        const num::Scan s = smem ? num::parse_number<PASS == 1>(w.at(p), w.at(r))
+                                 : num::parse_number<PASS == 1>(a.text + p, a.text + r);
+        if (s.status == num::kNoMatch || s.status == num::kRange) {
+            if (!PASS) atomicMin(a.err_byte, (unsigned long long)p);
+            return -1;
+        }
+        if (PASS) {
+            a.tok[tok + cnt] = T_NUM;
+            a.tok_num[tok + cnt] = num + cnt;
+            if (s.status == num::kOk) {
+                a.nums[num + cnt] = s.value;
+            } else {
+                const unsigned int q = atomicAdd(a.n_slow, 1u);
+                a.slow[q] = num + cnt;
+                a.slow_pos[q] = p;
+                a.slow_len[q] = s.len;
+            }
+        }
+        ++cnt;
+        p += s.len;
+    }
+    return cnt;
+}
+
+constexpr int kMaxRuns = kSpan / 2;  // runs are separated by at least one byte
+
+// Byte-by-byte lexing of one span (the reference order of work); used for
+// spans where a run holds several numbers ("1-2"), which pass 0 flags.
+template <int PASS>
+__device__ void lex_span_serial(const LexArgs& a, const Window& w, uint64_t i0, uint64_t i1, int64_t j,
+                                uint32_t tok0, uint32_t num0, uint32_t* ntok_out, uint32_t* nnum_out) {
+    uint64_t cur_bb = j >= 0 ? a.bb[j] : 0, cur_be = j >= 0 ? a.be[j] : 0;
+    uint64_t next_bb = j + 1 < (int64_t)a.n_lit ? a.bb[j + 1] : ~0ull;
     uint32_t ntok = 0, nnum = 0;
     for (uint64_t i = i0; i < i1; ++i) {
-        while (j + 1 < (int64_t)a.n_lit && a.bb[j + 1] <= i) ++j;
-        if (j < 0 || i >= a.be[j]) continue;
-        if (PASS && i == a.bb[j]) a.lit_tok0[j] = tok0 + ntok;
-        const unsigned char c = (unsigned char)a.text[i];
+        while (i >= next_bb) {
+            ++j;
+            cur_bb = next_bb;
+            cur_be = a.be[j];
+            next_bb = j + 1 < (int64_t)a.n_lit ? a.bb[j + 1] : ~0ull;
+        }
+        if (j < 0 || i >= cur_be) continue;
+        if (PASS && i == cur_bb) a.lit_tok0[j] = tok0 + ntok;
+        const unsigned char c = (unsigned char)*w.at(i);
         if (ws_byte(c)) continue;
         if (c == '(' || c == ')' || c == ',') {
             if (PASS) {
@@ -104,37 +154,130 @@ __global__ void lex_kernel(LexArgs a) {
             if (!PASS) atomicMin(a.err_byte, (unsigned long long)i);
             continue;
         }
-        if (i > a.bb[j] && num_byte((unsigned char)a.text[i - 1])) continue;  // run owned upstream
-        uint64_t r = i;
-        while (r < a.be[j] && num_byte((unsigned char)a.text[r])) ++r;
-        uint64_t p = i;
-        while (p < r) {  // from_chars maximal munch, number after number
-            const num::Scan s = num::parse_number(a.text + p, a.text + r);
-            if (s.status == num::kNoMatch || s.status == num::kRange) {
-                if (!PASS) atomicMin(a.err_byte, (unsigned long long)p);
-                break;
+        if (i > cur_bb && num_byte((unsigned char)*w.at(i - 1))) continue;  // run owned upstream
+        uint64_t r = i + 1;
+        while (r < cur_be && num_byte((unsigned char)*w.at(r))) ++r;
+        const int c2 = lex_run<PASS>(a, w, i, r, tok0 + ntok, num0 + nnum);
+        if (c2 > 0) ntok += c2, nnum += c2;
+    }
+    *ntok_out = ntok;
+    *nnum_out = nnum;
+}
+
+// One CTA stages its 8 KB of text (+ halo, + the byte before) in SMEM with
+// 16-byte loads. Each thread owns a 32-byte span and works in two phases so
+// the lanes of a warp stay converged:
+//   A. classify the span's bytes: structural tokens (written in pass 1), and
+//      the extent of each run of number characters starting in the span;
+//   B. parse the runs in lockstep (run k of every lane together).
+// Token indices in phase A assume one number per run; pass 0 flags the spans
+// where a run holds several ("1-2"), and pass 1 lexes those byte by byte.
+template <int PASS>
+__global__ void __launch_bounds__(kLexThreads) lex_kernel(LexArgs a) {
+    __shared__ alignas(16) char sm[kTextPad + kLexChunk + kLexHalo];
+    const uint64_t c0 = (uint64_t)blockIdx.x * kLexChunk;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(a.text + c0 - kTextPad);
+        uint4* dst = reinterpret_cast<uint4*>(sm);
+        for (int k = threadIdx.x; k < (kTextPad + kLexChunk + kLexHalo) / 16; k += kLexThreads) dst[k] = src[k];
+    }
+    __syncthreads();
+    const Window w{sm, a.text, c0, c0 + kLexChunk + kLexHalo};
+    const uint64_t t = (uint64_t)blockIdx.x * kLexThreads + threadIdx.x;
+    const uint64_t i0 = t * kSpan;
+    if (i0 >= a.n) return;
+    const uint64_t i1 = min(a.n, i0 + kSpan);
+    int64_t lo = 0, hi = a.n_lit;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (a.bb[mid] <= i0) lo = mid + 1;
+        else hi = mid;
+    }
+    const int64_t j0 = lo - 1;
+    const uint32_t tok0 = PASS ? a.cnt_tok[t] : 0, num0 = PASS ? a.cnt_num[t] : 0;
+    if (PASS && a.span_multi[t]) {
+        uint32_t nt, nn;
+        lex_span_serial<PASS>(a, w, i0, i1, j0, tok0, num0, &nt, &nn);
+        return;
+    }
+
+    // ---- phase A
+    uint8_t rs[kMaxRuns];   // run start, offset from i0
+    uint8_t rb[kMaxRuns];   // structural tokens before the run
+    uint16_t re[kMaxRuns];  // run end, offset from i0; 0xffff: still open at i1
+    uint64_t open_be = 0;   // body end bounding the open run
+    int nr = 0;
+    uint32_t nstruct = 0;
+    bool open = false;
+    {
+        int64_t j = j0;
+        uint64_t cur_bb = j >= 0 ? a.bb[j] : 0, cur_be = j >= 0 ? a.be[j] : 0;
+        uint64_t next_bb = j + 1 < (int64_t)a.n_lit ? a.bb[j + 1] : ~0ull;
+        for (uint64_t i = i0; i < i1; ++i) {
+            while (i >= next_bb) {
+                if (open) re[nr - 1] = (uint16_t)(i - i0), open = false;
+                ++j;
+                cur_bb = next_bb;
+                cur_be = a.be[j];
+                next_bb = j + 1 < (int64_t)a.n_lit ? a.bb[j + 1] : ~0ull;
             }
-            if (PASS) {
-                const uint32_t k = num0 + nnum;
-                a.tok[tok0 + ntok] = T_NUM;
-                a.tok_num[tok0 + ntok] = k;
-                if (s.status == num::kOk) {
-                    a.nums[k] = s.value;
-                } else {
-                    const unsigned int q = atomicAdd(a.n_slow, 1u);
-                    a.slow[q] = k;
-                    a.slow_pos[q] = p;
-                    a.slow_len[q] = s.len;
+            if (j < 0 || i >= cur_be) {
+                if (open) re[nr - 1] = (uint16_t)(i - i0), open = false;
+                continue;
+            }
+            if (PASS && i == cur_bb) a.lit_tok0[j] = tok0 + nstruct + nr;
+            const unsigned char c = (unsigned char)sm[kTextPad + (i - c0)];
+            const bool nb = num_byte(c);
+            if (open) {
+                if (nb) continue;
+                re[nr - 1] = (uint16_t)(i - i0);
+                open = false;
+            }
+            if (ws_byte(c)) continue;
+            if (c == '(' || c == ')' || c == ',') {
+                if (PASS) {
+                    const uint32_t k = tok0 + nstruct + nr;
+                    a.tok[k] = c == '(' ? T_LP : c == ')' ? T_RP : T_CM;
+                    a.tok_num[k] = num0 + nr;
                 }
+                ++nstruct;
+                continue;
             }
-            ++ntok;
-            ++nnum;
-            p += s.len;
+            if (!nb) {
+                if (!PASS) atomicMin(a.err_byte, (unsigned long long)i);
+                continue;
+            }
+            if (i > cur_bb && num_byte((unsigned char)sm[kTextPad + (i - c0) - 1])) continue;  // owned upstream
+            rs[nr] = (uint8_t)(i - i0);
+            rb[nr] = (uint8_t)nstruct;
+            re[nr] = 0xffff;
+            ++nr;
+            open = true;
+            open_be = cur_be;
         }
     }
+
+    // ---- phase B
+    uint32_t nnum = 0;
+    bool multi = false;
+    for (int k = 0; k < nr; ++k) {
+        const uint64_t p = i0 + rs[k];
+        uint64_t r;
+        if (re[k] != 0xffff) {
+            r = i0 + re[k];
+        } else {
+            r = i1;
+            while (r < open_be && num_byte((unsigned char)*w.at(r))) ++r;
+        }
+        const int c = lex_run<PASS>(a, w, p, r, tok0 + rb[k] + nnum, num0 + nnum);
+        if (c < 0) continue;
+        multi |= c != 1;
+        nnum += (uint32_t)c;
+    }
     if (!PASS) {
-        a.cnt_tok[t] = ntok;
+        a.cnt_tok[t] = nstruct + nnum;
         a.cnt_num[t] = nnum;
+        a.span_multi[t] = multi;
     }
 }
 
@@ -519,11 +662,14 @@ void parse_batch(const char* text, const uint64_t* lit_off, uint64_t L0, uint64_
         if (bb[i] == be[i]) throw_literal(text, lit_off, L, "empty body");
     }
     Frees fr{st, {}};
-    char* d_text = fr.take(dnew<char>(n, st));
+    char* d_text_buf = fr.take(dnew<char>(kTextPad + n + kLexChunk + kLexHalo + 16, st));
+    char* d_text = d_text_buf + kTextPad;
+    CK(cudaMemsetAsync(d_text_buf, 0, kTextPad, st));
+    CK(cudaMemsetAsync(d_text + n, 0, kLexChunk + kLexHalo + 16, st));
     uint64_t* d_bb = fr.take(dnew<uint64_t>(n_lit, st));
     uint64_t* d_be = fr.take(dnew<uint64_t>(n_lit, st));
     uint8_t* d_kind = fr.take(dnew<uint8_t>(n_lit, st));
-    CK(cudaMemcpyAsync(d_text, text + base, n, cudaMemcpyHostToDevice, st));
+    h2d(d_text, text + base, n, st);
     CK(cudaMemcpyAsync(d_bb, bb.data(), n_lit * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d_be, be.data(), n_lit * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d_kind, kind.data(), n_lit, cudaMemcpyHostToDevice, st));
@@ -548,8 +694,9 @@ void parse_batch(const char* text, const uint64_t* lit_off, uint64_t L0, uint64_
     a.n_slow = err_lit + 1;
     a.cnt_tok = cnt;
     a.cnt_num = cnt + nthr + 1;
-    const unsigned lex_blocks = (unsigned)((nthr + 255) / 256);
-    lex_kernel<0><<<lex_blocks, 256, 0, st>>>(a);
+    a.span_multi = fr.take(dnew<uint8_t>(nthr, st));
+    const unsigned lex_blocks = (unsigned)((nthr + kLexThreads - 1) / kLexThreads);
+    lex_kernel<0><<<lex_blocks, kLexThreads, 0, st>>>(a);
     CK(cudaGetLastError());
     const int items = (int)(nthr + 1);
     for (int h = 0; h < 2; ++h)
@@ -587,7 +734,7 @@ void parse_batch(const char* text, const uint64_t* lit_off, uint64_t L0, uint64_
     a.slow_pos = slow_pos;
     a.slow_len = slow_len;
     a.lit_tok0 = lit_tok0;
-    lex_kernel<1><<<lex_blocks, 256, 0, st>>>(a);
+    lex_kernel<1><<<lex_blocks, kLexThreads, 0, st>>>(a);
     CK(cudaGetLastError());
     if (NN) {
         slow_number_kernel<<<(unsigned)((NN + 127) / 128), 128, 0, st>>>(d_text, slow, slow_pos, slow_len, err_lit + 1,
@@ -732,7 +879,14 @@ void geom_download(const Geom& g, double* host_tri9, cudaStream_t st) {
     double* d = dnew<double>(9 * g.n, st);
     download_kernel<<<(unsigned)((g.n + 255) / 256), 256, 0, st>>>(g.planes, g.n, g.n_pad, d);
     cudaError_t e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaMemcpyAsync(host_tri9, d, 9 * g.n * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) {
+        try {
+            d2h(host_tri9, d, 9 * g.n * sizeof(double), st);
+        } catch (...) {
+            cudaFreeAsync(d, st);
+            throw;
+        }
+    }
     cudaFreeAsync(d, st);
     CK(e);
     CK(cudaStreamSynchronize(st));

@@ -116,6 +116,9 @@ TDB_NUM_FN bool eisel_lemire(uint64_t w, int q, uint64_t& bits) {
 }
 
 // Fast tier over [s, end): syntax, 19-digit mantissa, Eisel-Lemire.
+// kValue = false scans the syntax only (token counting): the status is then
+// kOk for every in-range number, kRange only for the gross range cases.
+template <bool kValue = true>
 TDB_NUM_FN Scan parse_number(const char* s, const char* end) {
     const char* p = s;
     const bool neg = p < end && *p == '-';
@@ -177,6 +180,7 @@ TDB_NUM_FN Scan parse_number(const char* s, const char* end) {
     const long long top = e10 + nd - 1;
     if (top >= 309) return Scan{kRange, len, 0.0};   // >= 1e309 > DBL_MAX
     if (top < -325) return Scan{kRange, len, 0.0};   // < 1e-325 < 2^-1075: rounds to 0
+    if (!kValue) return Scan{kOk, len, 0.0};
     uint64_t b;
     if (eisel_lemire(w, (int)e10, b)) {
         if (trunc) {
