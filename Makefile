@@ -48,6 +48,29 @@ shimtest: $(LIB) oracle
 	    -Wl,-rpath,'$$ORIGIN/../oracle/_ref' -Wl,-rpath,'$$ORIGIN/../$(PKG)'; \
 	else echo "shimtest: $(REF) absent; keeping prebuilt $(BUILD)/shim_test"; fi
 
+# The SQL route: the reference engine (engine.cpp, unmodified, force-including
+# tests/cpp/engine_route.hpp) over the device shim, against the unmodified
+# reference engine in oracle/_ref. Test-only binary; needs /root/reference.
+ENGINE_SRCS := kernels batch wkt store sql_parser closure
+enginetest: $(LIB) oracle
+	@if [ -d "$(REF)/include" ]; then \
+	  mkdir -p $(BUILD)/engine && \
+	  for f in $(ENGINE_SRCS); do \
+	    $(CXX) -std=c++20 -O2 -DNDEBUG -ffp-contract=off -fPIC -I$(REF)/include -c $(REF)/src/$$f.cpp \
+	      -o $(BUILD)/engine/$$f.o || exit 1; done && \
+	  $(CXX) -std=c++20 -O2 -DNDEBUG -ffp-contract=off -I$(REF)/include -Iinclude \
+	    -include tests/cpp/engine_route.hpp -c $(REF)/src/engine.cpp -o $(BUILD)/engine/engine_routed.o && \
+	  $(CXX) -std=c++20 -O2 -ffp-contract=off -I$(REF)/include -Iinclude -Itests/cpp \
+	    -DENGINE_SIDE=engine_dev -DENGINE_SIDE_DEVICE -c tests/cpp/engine_side.cpp -o $(BUILD)/engine/side_dev.o && \
+	  $(CXX) -std=c++20 -O2 -DNDEBUG -ffp-contract=off -Dtindb=tindb_ref -I$(REF)/include \
+	    -include tests/cpp/engine_route_a17.hpp -c $(REF)/src/engine.cpp -o $(BUILD)/engine/engine_a17.o && \
+	  $(CXX) -std=c++20 -O2 -ffp-contract=off -Dtindb=tindb_ref -I$(REF)/include -Itests/cpp \
+	    -DENGINE_SIDE=engine_ref -c tests/cpp/engine_side.cpp -o $(BUILD)/engine/side_ref.o && \
+	  $(CXX) -std=c++20 -O2 -Itests/cpp tests/cpp/engine_test.cpp $(BUILD)/engine/*.o -o $(BUILD)/engine_test \
+	    -Loracle/_ref -ltindb_ref -L$(PKG) -ltindb_b200 -pthread \
+	    -Wl,-rpath,'$$ORIGIN/../oracle/_ref' -Wl,-rpath,'$$ORIGIN/../$(PKG)'; \
+	else echo "enginetest: $(REF) absent; keeping prebuilt $(BUILD)/engine_test"; fi
+
 sass: $(LIB)
 	cuobjdump -sass $(LIB) > $(BUILD)/libtindb_b200.sass
 
@@ -55,4 +78,4 @@ clean:
 	rm -rf $(BUILD) $(LIB)
 	$(MAKE) -C oracle clean
 
-.PHONY: all lib oracle sass clean shimtest
+.PHONY: enginetest all lib oracle sass clean shimtest

@@ -28,8 +28,12 @@
 #include <tindb/kernels.hpp>
 #include <tindb/store_types.hpp>
 
+#include <algorithm>
 #include <cstdint>
 #include <limits>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -139,104 +143,195 @@ inline std::optional<KernelValue> eval_mesh_mesh(BatchOp op, const Geometry& rec
     return std::nullopt;
 }
 
-// run_batch (batch.hpp:49-51) with the Mesh column on the device: one upload
-// of the column (CSR face offsets + per-object AABB headers), one launch.
+// Device copies of one record column's geometry, split by kind: the Mesh
+// records as a device table (CSR faces + per-object AABB headers), the
+// Segment records (incl. 2-point line strings) and the Point records as
+// device query sets; `other_rows` go to the reference dispatch.
+struct DeviceColumns {
+    tdb_table meshes = nullptr;
+    tdb_queries segments = nullptr, points = nullptr;
+    std::vector<std::size_t> mesh_rows, seg_rows, pt_rows, other_rows;
+
+    DeviceColumns() = default;
+    DeviceColumns(const DeviceColumns&) = delete;
+    DeviceColumns& operator=(const DeviceColumns&) = delete;
+    ~DeviceColumns() {
+        tdb_table_free(meshes);
+        tdb_queries_free(segments);
+        tdb_queries_free(points);
+    }
+
+    explicit DeviceColumns(const std::vector<store::GeometryRecord>& records) {
+        for (std::size_t i = 0; i < records.size(); ++i) {
+            const GeometryKind k = kind_of(records[i].geometry);
+            if (k == GeometryKind::Mesh) mesh_rows.push_back(i);
+            else if (k == GeometryKind::Segment) seg_rows.push_back(i);
+            else if (k == GeometryKind::Point) pt_rows.push_back(i);
+            else other_rows.push_back(i);
+        }
+        try {
+            if (!mesh_rows.empty()) {
+                std::vector<std::uint64_t> off(mesh_rows.size() + 1, 0);
+                for (std::size_t k = 0; k < mesh_rows.size(); ++k)
+                    off[k + 1] = off[k] + std::get<TriangleMesh>(records[mesh_rows[k]].geometry).triangles.size();
+                std::vector<double> faces(9 * off.back());
+                for (std::size_t k = 0; k < mesh_rows.size(); ++k) {
+                    const auto& m = std::get<TriangleMesh>(records[mesh_rows[k]].geometry);
+                    std::copy(faces_of(m), faces_of(m) + 9 * m.triangles.size(), faces.begin() + 9 * off[k]);
+                }
+                check(tdb_table_upload(faces.data(), off.data(), mesh_rows.size(), &meshes));
+            }
+            if (!seg_rows.empty()) {
+                std::vector<double> q(6 * seg_rows.size());
+                for (std::size_t k = 0; k < seg_rows.size(); ++k) {
+                    const LineSegment s = segment_view(records[seg_rows[k]].geometry);
+                    const double v[6] = {s.p0.x, s.p0.y, s.p0.z, s.p1.x, s.p1.y, s.p1.z};
+                    std::copy(v, v + 6, q.begin() + 6 * k);
+                }
+                check(tdb_queries_upload(q.data(), seg_rows.size(), TDB_QUERY_SEGMENTS, &segments));
+            }
+            if (!pt_rows.empty()) {
+                std::vector<double> q(3 * pt_rows.size());
+                for (std::size_t k = 0; k < pt_rows.size(); ++k) {
+                    const Point3& p = std::get<Point3>(records[pt_rows[k]].geometry);
+                    q[3 * k] = p.x, q[3 * k + 1] = p.y, q[3 * k + 2] = p.z;
+                }
+                check(tdb_queries_upload(q.data(), pt_rows.size(), TDB_QUERY_POINTS, &points));
+            }
+        } catch (...) {
+            tdb_table_free(meshes);
+            tdb_queries_free(segments);
+            tdb_queries_free(points);
+            throw;
+        }
+    }
+};
+
+// Device columns per TableSnapshot. Snapshots are immutable once Ready
+// (store_types.hpp:21-32) and a reload publishes a new snapshot
+// (store.cpp:162-167), so a snapshot's device copy stays valid for its
+// whole life. Entries are keyed by the snapshot's control block
+// (owner_less on a weak_ptr: an address can never be reused while the key
+// lives) and released once the snapshot is gone.
+class SnapshotCache {
+  public:
+    std::shared_ptr<const DeviceColumns> columns(const store::TableSnapshot& snap) {
+        std::lock_guard<std::mutex> g(mu_);
+        for (auto it = map_.begin(); it != map_.end();) it = it->first.expired() ? map_.erase(it) : std::next(it);
+        const Key key(snap);
+        auto it = map_.find(key);
+        if (it != map_.end()) {
+            ++hits_;
+            return it->second;
+        }
+        auto cols = std::make_shared<const DeviceColumns>(snap->records);
+        map_.emplace(key, cols);
+        ++builds_;
+        return cols;
+    }
+    std::size_t size() {
+        std::lock_guard<std::mutex> g(mu_);
+        return map_.size();
+    }
+    std::size_t hits() const { return hits_; }
+    std::size_t builds() const { return builds_; }
+    void clear() {
+        std::lock_guard<std::mutex> g(mu_);
+        map_.clear();
+    }
+
+  private:
+    using Key = std::weak_ptr<const store::GeometryTable>;
+    std::mutex mu_;
+    std::map<Key, std::shared_ptr<const DeviceColumns>, std::owner_less<Key>> map_;
+    std::size_t hits_ = 0, builds_ = 0;
+};
+
+inline SnapshotCache& default_cache() {
+    static SnapshotCache cache;
+    return cache;
+}
+
+// run_batch over device columns: the Mesh records against a Mesh literal
+// (triangle pairs, one table launch), Segment / Point records against it
+// (distance_to_mesh / intersects_mesh, batch.cpp:37-40,:58, one query-set
+// launch each); every other pairing through the reference run_batch. Results
+// in record order, as batch.hpp:49-51.
+inline std::vector<KernelResult> run_batch_columns(BatchOp op, const std::vector<store::GeometryRecord>& records,
+                                                   const DeviceColumns& cols, const Geometry& literal,
+                                                   const ExecutorConfig& cfg) {
+    std::vector<KernelResult> out(records.size());
+    std::vector<std::size_t> ref_rows = cols.other_rows;
+    if (op == BatchOp::Intersects)  // Point x Mesh has no intersects (batch.cpp:53-63)
+        ref_rows.insert(ref_rows.end(), cols.pt_rows.begin(), cols.pt_rows.end());
+    std::sort(ref_rows.begin(), ref_rows.end());
+    if (!ref_rows.empty()) {
+        std::vector<store::GeometryRecord> rest;
+        rest.reserve(ref_rows.size());
+        for (std::size_t i : ref_rows) rest.push_back(records[i]);
+        std::vector<KernelResult> r = run_batch(op, rest, literal, cfg);
+        for (std::size_t k = 0; k < ref_rows.size(); ++k) out[ref_rows[k]] = std::move(r[k]);
+    }
+    const bool need_lit = cols.meshes || cols.segments || (cols.points && op == BatchOp::Distance);
+    if (!need_lit) return out;
+    DeviceMesh lit(std::get<TriangleMesh>(literal));
+    auto put = [&](const std::vector<std::size_t>& rows, const std::vector<double>& dist,
+                   const std::vector<std::uint8_t>& hit) {
+        for (std::size_t k = 0; k < rows.size(); ++k) {
+            KernelResult& r = out[rows[k]];
+            r.record_id = records[rows[k]].id;
+            if (op == BatchOp::Distance) r.value = dist[k];
+            else r.value = hit[k] != 0;
+        }
+    };
+    auto queries = [&](tdb_queries qs, const std::vector<std::size_t>& rows) {
+        std::vector<double> dist(rows.size());
+        std::vector<std::uint8_t> hit(rows.size());
+        std::vector<std::uint64_t> face(rows.size());
+        if (op == BatchOp::Distance) check(tdb_queries_mesh_distance(qs, lit.handle(), dist.data(), face.data()));
+        else check(tdb_queries_mesh_intersects(qs, lit.handle(), hit.data(), face.data()));
+        put(rows, dist, hit);
+    };
+    if (cols.segments) queries(cols.segments, cols.seg_rows);
+    if (cols.points && op == BatchOp::Distance) queries(cols.points, cols.pt_rows);
+    if (cols.meshes) {
+        std::vector<double> dist(cols.mesh_rows.size());
+        std::vector<std::uint8_t> hit(cols.mesh_rows.size());
+        if (op == BatchOp::Distance)
+            check(tdb_table_eval(TDB_OP_DISTANCE, cols.meshes, lit.handle(), dist.data(), nullptr, nullptr));
+        else
+            check(tdb_table_eval(TDB_OP_INTERSECTS, cols.meshes, lit.handle(), nullptr, hit.data(), nullptr));
+        put(cols.mesh_rows, dist, hit);
+    }
+    return out;
+}
+
+inline bool device_pairing(BatchOp op, const std::optional<Geometry>& argument) {
+    return argument && kind_of(*argument) == GeometryKind::Mesh &&
+           (op == BatchOp::Distance || op == BatchOp::Intersects);
+}
+
+// run_batch (batch.hpp:49-51) for a record column: the column is uploaded
+// for this call only.
 inline std::vector<KernelResult> run_batch_b200(BatchOp op, const std::vector<store::GeometryRecord>& records,
                                                 const std::optional<Geometry>& argument,
                                                 const ExecutorConfig& cfg) {
-    const bool mesh_arg = argument && kind_of(*argument) == GeometryKind::Mesh;
-    if (!mesh_arg || (op != BatchOp::Distance && op != BatchOp::Intersects))
-        return run_batch(op, records, argument, cfg);
+    if (!device_pairing(op, argument)) return run_batch(op, records, argument, cfg);
+    const DeviceColumns cols(records);
+    return run_batch_columns(op, records, cols, *argument, cfg);
+}
 
-    std::vector<KernelResult> out(records.size());
-    std::vector<std::size_t> mesh_rows, seg_rows, pt_rows, other_rows;
-    for (std::size_t i = 0; i < records.size(); ++i) {
-        const GeometryKind k = kind_of(records[i].geometry);
-        if (k == GeometryKind::Mesh) mesh_rows.push_back(i);
-        else if (k == GeometryKind::Segment) seg_rows.push_back(i);  // incl. 2-point line strings
-        else if (k == GeometryKind::Point && op == BatchOp::Distance) pt_rows.push_back(i);
-        else other_rows.push_back(i);
-    }
-    // Segment / Point x Mesh (batch.cpp:37-40, :58): distance_to_mesh /
-    // intersects_mesh per record, the whole column in one device call
-    if (!seg_rows.empty() || !pt_rows.empty()) {
-        DeviceMesh lit(std::get<TriangleMesh>(*argument));
-        auto run_queries = [&](const std::vector<std::size_t>& rows, int kind) {
-            if (rows.empty()) return;
-            const int width = kind == TDB_QUERY_SEGMENTS ? 6 : 3;
-            std::vector<double> q(width * rows.size());
-            for (std::size_t k = 0; k < rows.size(); ++k) {
-                const Geometry& g = records[rows[k]].geometry;
-                if (kind == TDB_QUERY_SEGMENTS) {
-                    const LineSegment s = segment_view(g);
-                    const double v[6] = {s.p0.x, s.p0.y, s.p0.z, s.p1.x, s.p1.y, s.p1.z};
-                    std::copy(v, v + 6, q.begin() + 6 * k);
-                } else {
-                    const Point3& p = std::get<Point3>(g);
-                    q[3 * k] = p.x, q[3 * k + 1] = p.y, q[3 * k + 2] = p.z;
-                }
-            }
-            tdb_queries qs = nullptr;
-            check(tdb_queries_upload(q.data(), rows.size(), kind, &qs));
-            struct FreeQ {
-                tdb_queries q;
-                ~FreeQ() { tdb_queries_free(q); }
-            } gq{qs};
-            std::vector<double> dist(rows.size());
-            std::vector<std::uint8_t> hit(rows.size());
-            std::vector<std::uint64_t> face(rows.size());
-            if (op == BatchOp::Distance)
-                check(tdb_queries_mesh_distance(qs, lit.handle(), dist.data(), face.data()));
-            else
-                check(tdb_queries_mesh_intersects(qs, lit.handle(), hit.data(), face.data()));
-            for (std::size_t k = 0; k < rows.size(); ++k) {
-                KernelResult& r = out[rows[k]];
-                r.record_id = records[rows[k]].id;
-                if (op == BatchOp::Distance) r.value = dist[k];
-                else r.value = hit[k] != 0;
-            }
-        };
-        run_queries(seg_rows, TDB_QUERY_SEGMENTS);
-        run_queries(pt_rows, TDB_QUERY_POINTS);
-    }
-
-    if (!other_rows.empty()) {  // reference dispatch for every other pairing
-        std::vector<store::GeometryRecord> rest;
-        rest.reserve(other_rows.size());
-        for (std::size_t i : other_rows) rest.push_back(records[i]);
-        std::vector<KernelResult> r = run_batch(op, rest, argument, cfg);
-        for (std::size_t k = 0; k < other_rows.size(); ++k) out[other_rows[k]] = std::move(r[k]);
-    }
-    if (mesh_rows.empty()) return out;
-
-    std::vector<std::uint64_t> off(mesh_rows.size() + 1, 0);
-    for (std::size_t k = 0; k < mesh_rows.size(); ++k)
-        off[k + 1] = off[k] + std::get<TriangleMesh>(records[mesh_rows[k]].geometry).triangles.size();
-    std::vector<double> faces(9 * off.back());
-    for (std::size_t k = 0; k < mesh_rows.size(); ++k) {
-        const auto& m = std::get<TriangleMesh>(records[mesh_rows[k]].geometry);
-        std::copy(faces_of(m), faces_of(m) + 9 * m.triangles.size(), faces.begin() + 9 * off[k]);
-    }
-    tdb_table t = nullptr;
-    check(tdb_table_upload(faces.data(), off.data(), mesh_rows.size(), &t));
-    struct Free {
-        tdb_table t;
-        ~Free() { tdb_table_free(t); }
-    } guard{t};
-    DeviceMesh lit(std::get<TriangleMesh>(*argument));
-    std::vector<double> dist(mesh_rows.size());
-    std::vector<std::uint8_t> hit(mesh_rows.size());
-    if (op == BatchOp::Distance)
-        check(tdb_table_eval(TDB_OP_DISTANCE, t, lit.handle(), dist.data(), nullptr, nullptr));
-    else
-        check(tdb_table_eval(TDB_OP_INTERSECTS, t, lit.handle(), nullptr, hit.data(), nullptr));
-    for (std::size_t k = 0; k < mesh_rows.size(); ++k) {
-        KernelResult& r = out[mesh_rows[k]];
-        r.record_id = records[mesh_rows[k]].id;
-        if (op == BatchOp::Distance) r.value = dist[k];
-        else r.value = hit[k] != 0;
-    }
-    return out;
+// run_batch for a table snapshot, the call engine.cpp:203 makes
+// (kernels::run_batch(op, snapshot->records, argument, cfg)): the
+// snapshot's device columns are built once and reused by every later
+// statement on the same snapshot.
+inline std::vector<KernelResult> run_batch_b200(BatchOp op, const store::TableSnapshot& snapshot,
+                                                const std::optional<Geometry>& argument,
+                                                const ExecutorConfig& cfg,
+                                                SnapshotCache& cache = default_cache()) {
+    if (!device_pairing(op, argument)) return run_batch(op, snapshot->records, argument, cfg);
+    const std::shared_ptr<const DeviceColumns> cols = cache.columns(snapshot);
+    return run_batch_columns(op, snapshot->records, *cols, *argument, cfg);
 }
 
 }  // namespace tindb::kernels::b200

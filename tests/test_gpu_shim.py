@@ -18,3 +18,16 @@ def test_cpp_shim_against_reference_dispatch():
     r = subprocess.run([BIN], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "SHIM OK" in r.stdout
+
+
+ENGINE = os.path.join(ROOT, "build", "engine_test")
+
+
+@pytest.mark.skipif(not os.path.exists(ENGINE), reason="build/engine_test not built (needs /root/reference)")
+def test_sql_route_through_reference_engine():
+    """SQL statements through the reference engine with
+    run_batch routed to the device give the reference's rendered text cell
+    for cell, and the snapshot's device columns are built once."""
+    r = subprocess.run([ENGINE], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "ENGINE OK" in r.stdout
