@@ -165,6 +165,13 @@ int tdb_queries_upload(const double* q, uint64_t n, int kind, tdb_queries* out);
 void tdb_queries_free(tdb_queries q);
 int tdb_queries_mesh_distance(tdb_queries q, tdb_mesh mesh, double* dist_out, uint64_t* face_out);
 int tdb_queries_mesh_intersects(tdb_queries q, tdb_mesh mesh, uint8_t* hit_out, uint64_t* face_out);
+/* run_batch with a Segment / Point literal over a mesh column (batch.cpp:44-48
+ * eval_distance Mesh x Segment|Point, :59 eval_intersects Mesh x Segment):
+ * per record distance_to_mesh(literal, record) / intersects_mesh(literal,
+ * record); literal = 6 doubles (TDB_QUERY_SEGMENTS) or 3 (TDB_QUERY_POINTS,
+ * distance only). face_out = lowest (hit) face within the record. */
+int tdb_literal_table_eval(int op, int literal_kind, const double* literal, tdb_table records, double* dist_out,
+                           uint8_t* hit_out, uint64_t* face_out);
 /* one-shot forms: upload the host queries, evaluate, free */
 int tdb_segments_mesh_distance(const double* seg6, uint64_t n, tdb_mesh mesh, double* dist_out,
                                uint64_t* face_out);
@@ -179,6 +186,9 @@ uint64_t tdb_gen_drills(uint64_t seed, uint64_t count, int style, double* out6);
  * (0 = ExecutorConfig default 4096; the chunk tree fixes the summation order,
  * executor.hpp:20-49). */
 int tdb_mesh_volume(tdb_mesh m, uint64_t chunk_size, double* volume_out);
+/* run_batch(Volume, records) over a mesh column (batch.cpp:23-29): one
+ * volume per object, each with its own chunk tree (volume_out: n_objects). */
+int tdb_table_volume(tdb_table t, uint64_t chunk_size, double* volume_out);
 
 /* ---- one-shot host-buffer entry points (upload + evaluate + free) -------- */
 int tdb_distance_host(const double* a9, uint64_t n, const double* b9, uint64_t m,

@@ -306,9 +306,77 @@ inline std::vector<KernelResult> run_batch_columns(BatchOp op, const std::vector
     return out;
 }
 
-inline bool device_pairing(BatchOp op, const std::optional<Geometry>& argument) {
-    return argument && kind_of(*argument) == GeometryKind::Mesh &&
-           (op == BatchOp::Distance || op == BatchOp::Intersects);
+// Volume over the Mesh records (batch.cpp:23-29, permissive policy: the
+// Strict policy's watertightness check stays on the reference path), and a
+// Segment / Point literal against the Mesh records (batch.cpp:44-48, :59).
+inline std::vector<KernelResult> run_batch_mesh_column(BatchOp op, const std::vector<store::GeometryRecord>& records,
+                                                       const DeviceColumns& cols,
+                                                       const std::optional<Geometry>& argument,
+                                                       const ExecutorConfig& cfg) {
+    std::vector<KernelResult> out(records.size());
+    std::vector<std::size_t> ref_rows = cols.other_rows;
+    ref_rows.insert(ref_rows.end(), cols.seg_rows.begin(), cols.seg_rows.end());
+    ref_rows.insert(ref_rows.end(), cols.pt_rows.begin(), cols.pt_rows.end());
+    std::sort(ref_rows.begin(), ref_rows.end());
+    if (!ref_rows.empty()) {
+        std::vector<store::GeometryRecord> rest;
+        rest.reserve(ref_rows.size());
+        for (std::size_t i : ref_rows) rest.push_back(records[i]);
+        std::vector<KernelResult> r = run_batch(op, rest, argument, cfg);
+        for (std::size_t k = 0; k < ref_rows.size(); ++k) out[ref_rows[k]] = std::move(r[k]);
+    }
+    if (!cols.meshes) return out;
+    const std::size_t n = cols.mesh_rows.size();
+    std::vector<double> dist(n);
+    std::vector<std::uint8_t> hit(n);
+    if (op == BatchOp::Volume) {
+        check(tdb_table_volume(cols.meshes, cfg.chunk_size, dist.data()));
+    } else {
+        const Geometry& g = *argument;
+        double lit[6];
+        int kind;
+        if (kind_of(g) == GeometryKind::Point) {
+            const Point3& p = std::get<Point3>(g);
+            lit[0] = p.x, lit[1] = p.y, lit[2] = p.z;
+            kind = TDB_QUERY_POINTS;
+        } else {
+            const LineSegment s = segment_view(g);
+            const double v[6] = {s.p0.x, s.p0.y, s.p0.z, s.p1.x, s.p1.y, s.p1.z};
+            std::copy(v, v + 6, lit);
+            kind = TDB_QUERY_SEGMENTS;
+        }
+        std::vector<std::uint64_t> face(n);
+        check(tdb_literal_table_eval(op == BatchOp::Distance ? TDB_OP_DISTANCE : TDB_OP_INTERSECTS, kind, lit,
+                                     cols.meshes, op == BatchOp::Distance ? dist.data() : nullptr,
+                                     op == BatchOp::Intersects ? hit.data() : nullptr, face.data()));
+    }
+    for (std::size_t k = 0; k < n; ++k) {
+        KernelResult& r = out[cols.mesh_rows[k]];
+        r.record_id = records[cols.mesh_rows[k]].id;
+        if (op == BatchOp::Intersects) r.value = hit[k] != 0;
+        else r.value = dist[k];
+    }
+    return out;
+}
+
+// Which device path a run_batch call takes: 1 = a Mesh literal (every
+// record kind against the mesh), 2 = the Mesh records against a Segment /
+// Point literal or Volume; 0 = the reference dispatch.
+inline int device_route(BatchOp op, const std::optional<Geometry>& argument, const ExecutorConfig& cfg) {
+    if (op == BatchOp::Volume) return cfg.volume_policy == VolumePolicy::Permissive ? 2 : 0;
+    if (!argument) return 0;
+    const GeometryKind k = kind_of(*argument);
+    if (k == GeometryKind::Mesh) return 1;
+    if (k == GeometryKind::Segment) return 2;
+    if (k == GeometryKind::Point && op == BatchOp::Distance) return 2;
+    return 0;
+}
+
+inline std::vector<KernelResult> run_batch_routed(BatchOp op, const std::vector<store::GeometryRecord>& records,
+                                                  const DeviceColumns& cols, const std::optional<Geometry>& argument,
+                                                  const ExecutorConfig& cfg, int route) {
+    if (route == 1) return run_batch_columns(op, records, cols, *argument, cfg);
+    return run_batch_mesh_column(op, records, cols, argument, cfg);
 }
 
 // run_batch (batch.hpp:49-51) for a record column: the column is uploaded
@@ -316,9 +384,10 @@ inline bool device_pairing(BatchOp op, const std::optional<Geometry>& argument) 
 inline std::vector<KernelResult> run_batch_b200(BatchOp op, const std::vector<store::GeometryRecord>& records,
                                                 const std::optional<Geometry>& argument,
                                                 const ExecutorConfig& cfg) {
-    if (!device_pairing(op, argument)) return run_batch(op, records, argument, cfg);
+    const int route = device_route(op, argument, cfg);
+    if (!route) return run_batch(op, records, argument, cfg);
     const DeviceColumns cols(records);
-    return run_batch_columns(op, records, cols, *argument, cfg);
+    return run_batch_routed(op, records, cols, argument, cfg, route);
 }
 
 // run_batch for a table snapshot, the call engine.cpp:203 makes
@@ -329,9 +398,10 @@ inline std::vector<KernelResult> run_batch_b200(BatchOp op, const store::TableSn
                                                 const std::optional<Geometry>& argument,
                                                 const ExecutorConfig& cfg,
                                                 SnapshotCache& cache = default_cache()) {
-    if (!device_pairing(op, argument)) return run_batch(op, snapshot->records, argument, cfg);
+    const int route = device_route(op, argument, cfg);
+    if (!route) return run_batch(op, snapshot->records, argument, cfg);
     const std::shared_ptr<const DeviceColumns> cols = cache.columns(snapshot);
-    return run_batch_columns(op, snapshot->records, *cols, *argument, cfg);
+    return run_batch_routed(op, snapshot->records, *cols, argument, cfg, route);
 }
 
 }  // namespace tindb::kernels::b200

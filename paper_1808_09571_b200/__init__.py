@@ -115,6 +115,8 @@ _SIGS = [
     ("tdb_gen_terrain", ct.c_uint64, [ct.c_uint32, ct.c_uint32, ct.c_double, ct.c_uint64, _D]),
     ("tdb_fp64_peak", ct.c_int, [_D, _D]),
     ("tdb_mesh_volume", ct.c_int, [ct.c_void_p, ct.c_uint64, _D]),
+    ("tdb_table_volume", ct.c_int, [ct.c_void_p, ct.c_uint64, _D]),
+    ("tdb_literal_table_eval", ct.c_int, [ct.c_int, ct.c_int, _D, ct.c_void_p, _D, _U8, _U64]),
     ("tdb_segments_mesh_distance", ct.c_int, [_D, ct.c_uint64, ct.c_void_p, _D, _U64]),
     ("tdb_points_mesh_distance", ct.c_int, [_D, ct.c_uint64, ct.c_void_p, _D, _U64]),
     ("tdb_segments_mesh_intersects", ct.c_int, [_D, ct.c_uint64, ct.c_void_p, _U8, _U64]),
@@ -545,6 +547,14 @@ def mesh_volume(mesh, chunk_size: int = 4096) -> float:
     return v.value
 
 
+def table_volume(table: Table, chunk_size: int = 4096) -> np.ndarray:
+    """run_batch(Volume) over a mesh column: mesh_volume per object, each with
+    its own chunk tree (batch.cpp:23-29), bit for bit."""
+    out = np.empty(table.objects, np.float64)
+    _check(lib().tdb_table_volume(table.handle, chunk_size, _dp(out)))
+    return out
+
+
 # ---- mesh generators (host; bit-identical to dataset.cpp) -------------------
 def unit_sphere(face_target: int) -> np.ndarray:
     n = lib().tdb_gen_unit_sphere(face_target, None)
@@ -581,3 +591,22 @@ def fp64_peak() -> tuple:
     tf, ms = ct.c_double(), ct.c_double()
     _check(lib().tdb_fp64_peak(ct.byref(tf), ct.byref(ms)))
     return tf.value, ms.value
+
+
+def literal_table_eval(op: int, literal, table: Table):
+    """run_batch with a segment (6 doubles) or point (3) literal over a mesh
+    column: per record distance_to_mesh / intersects_mesh (batch.cpp:44-48,
+    :59). Returns (dist or hit, face) per record; face = U64_MAX when none."""
+    lit = np.ascontiguousarray(literal, dtype=np.float64).reshape(-1)
+    kind = {6: QUERY_SEGMENTS, 3: QUERY_POINTS}.get(lit.size)
+    if kind is None:
+        raise ValueError("a literal is a segment (6 doubles) or a point (3)")
+    face = np.empty(table.objects, np.uint64)
+    if op == OP_DISTANCE:
+        d = np.empty(table.objects, np.float64)
+        _check(lib().tdb_literal_table_eval(op, kind, _dp(lit), table.handle, _dp(d), None, face.ctypes.data_as(_U64)))
+        return d, face
+    h = np.empty(table.objects, np.uint8)
+    _check(lib().tdb_literal_table_eval(op, kind, _dp(lit), table.handle, None, h.ctypes.data_as(_U8),
+                                        face.ctypes.data_as(_U64)))
+    return h.astype(bool), face

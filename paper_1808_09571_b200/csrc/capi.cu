@@ -469,6 +469,28 @@ static int one_shot_queries(const double* q, uint64_t n, int kind, int op, tdb_m
     return rc;
 }
 
+int tdb_literal_table_eval(int op, int literal_kind, const double* literal, tdb_table records, double* dist_out,
+                           uint8_t* hit_out, uint64_t* face_out) {
+    return guarded([&] {
+        need(records != nullptr && literal != nullptr, "null argument");
+        need(op == TDB_OP_DISTANCE || op == TDB_OP_INTERSECTS, "unknown op");
+        need(literal_kind == TDB_QUERY_SEGMENTS || literal_kind == TDB_QUERY_POINTS, "unknown literal kind");
+        tdb::Ctx c = ctx();
+        tdb::QuerySet q1;
+        q1.device = t_device;
+        try {
+            tdb::queries_build(&q1, literal, 1, literal_kind == TDB_QUERY_SEGMENTS ? tdb::kQuerySegments
+                                                                                    : tdb::kQueryPoints,
+                               c.stream);
+            tdb::run_literal_table(c, op, q1, records->g, dist_out, hit_out, face_out);
+        } catch (...) {
+            cudaFree(q1.planes);
+            throw;
+        }
+        cudaFree(q1.planes);
+    });
+}
+
 int tdb_segments_mesh_distance(const double* seg6, uint64_t n, tdb_mesh mesh, double* dist_out, uint64_t* face_out) {
     return one_shot_queries(seg6, n, TDB_QUERY_SEGMENTS, TDB_OP_DISTANCE, mesh, dist_out, nullptr, face_out);
 }
@@ -486,6 +508,13 @@ int tdb_mesh_volume(tdb_mesh m, uint64_t chunk_size, double* volume_out) {
         need(m && volume_out, "null argument");
         need(m->g.n_obj == 1, "volume takes a mesh (one object)");
         *volume_out = tdb::run_volume(ctx(), m->g, chunk_size);
+    });
+}
+
+int tdb_table_volume(tdb_table t, uint64_t chunk_size, double* volume_out) {
+    return guarded([&] {
+        need(t != nullptr && (volume_out != nullptr || t->g.n_obj == 0), "null argument");
+        tdb::run_volume_table(ctx(), t->g, chunk_size, volume_out);
     });
 }
 

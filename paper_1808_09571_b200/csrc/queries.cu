@@ -733,4 +733,263 @@ void run_queries(const Ctx& cx, int op, const QuerySet& qs, const Geom& B, doubl
     S.near_degenerate = cx.near->count;
 }
 
+// ---- one literal against every object of a table ----------------------------
+// run_batch over Mesh records with a Segment / Point literal (batch.cpp:44-48,
+// :59): per record, distance_to_mesh(literal, record mesh) (lowest face on
+// ties, degenerate faces skipped, kernels.cpp:340-405) or intersects_mesh
+// (lowest hit face, kernels.cpp:407-432). One CTA per 128-face tile of the
+// table (tiles never straddle objects); the same filter -> band -> exact
+// re-evaluation as the query sets, with per-object bands and the object's
+// own AABB / scale header.
+namespace {
+
+__device__ __forceinline__ bool face_degenerate(const double* P, uint64_t pad, uint64_t f) {
+    return reinterpret_cast<const int*>(P + (uint64_t)F_DEG * pad + f)[1] != 0;
+}
+
+__device__ __forceinline__ exact::tri face_tri(const double* P, uint64_t pad, uint64_t f) {
+    double v[9];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) v[c] = __ldg(P + (uint64_t)(F_V + c) * pad + f);
+    return exact::tri{{v[0], v[1], v[2]}, {v[3], v[4], v[5]}, {v[6], v[7], v[8]}};
+}
+
+__global__ void __launch_bounds__(kTile) lt_filter_kernel(QArgs a, const Tile* tiles, const double* P, uint64_t pad,
+                                                          unsigned long long* objmin) {
+    __shared__ double red[kTile / 32];
+    const Tile T = tiles[blockIdx.x];
+    const QueryRegs Q = load_query(a, 0);
+    double d2 = pos_inf();
+    if (threadIdx.x < T.count) {
+        const uint64_t f = T.row0 + threadIdx.x;
+        if (!face_degenerate(P, pad, f)) d2 = query_d2(Q, FaceRefLdg{P + f, pad});
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d2 = min_nn(d2, __shfl_xor_sync(0xffffffffu, d2, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = d2;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double r = red[0];
+#pragma unroll
+        for (int w = 1; w < kTile / 32; ++w) r = min_nn(r, red[w]);
+        if (r < pos_inf()) atomicMin(objmin + T.obj, (unsigned long long)__double_as_longlong(r));
+    }
+}
+
+// per object: band from the filter minimum and the object's header
+__global__ void lt_band_kernel(QArgs a, uint64_t n_obj, const double* obj_stats, const unsigned long long* objmin,
+                               double* band2, double* band, unsigned long long* D, unsigned long long* Pf) {
+    const uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= n_obj) return;
+    D[o] = Pf[o] = kNone;
+    if (objmin[o] == kNone) {
+        band2[o] = band[o] = -1.0;
+        return;
+    }
+    const double b = sqrt(__longlong_as_double((long long)objmin[o])) * (1.0 + kBandRel) +
+                     2.0 * q_eta(load_query(a, 0), obj_stats + o * kObjStats);
+    band[o] = b;
+    band2[o] = b * b * (1.0 + 4e-16);
+}
+
+__global__ void __launch_bounds__(kTile) lt_verify_kernel(QArgs a, const Tile* tiles, const double* P, uint64_t pad,
+                                                          int pass, const double* band2, unsigned long long* D,
+                                                          unsigned long long* Pf, unsigned long long* ncand,
+                                                          NearLog near) {
+    const Tile T = tiles[blockIdx.x];
+    const double b2 = band2[T.obj];
+    if (b2 < 0.0 || threadIdx.x >= T.count) return;
+    const uint64_t f = T.row0 + threadIdx.x;
+    if (face_degenerate(P, pad, f)) return;
+    const QueryRegs Q = load_query(a, 0);
+    if (query_d2(Q, FaceRefLdg{P + f, pad}) > b2) return;
+    const exact::tri t = face_tri(P, pad, f);
+    const exact::v3 p0{Q.p0[0], Q.p0[1], Q.p0[2]}, p1{Q.p1[0], Q.p1[1], Q.p1[2]};
+    const double d = Q.point ? exact::pt_tri(p0, t).d : exact::seg_tri(p0, p1, t).d;
+    const unsigned long long e = (unsigned long long)__double_as_longlong(d);
+    if (pass == 1) {
+        atomicMin(D + T.obj, e);
+        atomicAdd(ncand, 1ull);
+        if (Q.point ? exact::near_area(t) : exact::near_degenerate_seg(p0, p1, t))
+            near_log(near, T.obj, f - T.obj_row0);
+    } else if (e == D[T.obj]) {
+        atomicMin(Pf + T.obj, (unsigned long long)(f - T.obj_row0));
+    }
+}
+
+__global__ void lt_check_kernel(QArgs a, uint64_t n_obj, const double* obj_stats, double* band2, double* band,
+                                unsigned long long* D, unsigned long long* Pf, unsigned long long* retry) {
+    const uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= n_obj) return;
+    const double b = band[o];
+    if (b < 0.0) {
+        band2[o] = -1.0;
+        return;
+    }
+    const double eta = q_eta(load_query(a, 0), obj_stats + o * kObjStats);
+    const unsigned long long d = D[o];
+    if (d != kNone && __longlong_as_double((long long)d) > b - eta) {
+        const double nb = __longlong_as_double((long long)d) * (1.0 + kBandRel) + 2.0 * eta;
+        band[o] = nb;
+        band2[o] = nb * nb * (1.0 + 4e-16);
+        D[o] = Pf[o] = kNone;
+        atomicAdd(retry, 1ull);
+    } else {
+        band2[o] = -1.0;
+    }
+}
+
+// intersects: the q_hit_kernel cull (face box vs segment box +- tau, both
+// endpoints strictly on one side of the face plane by tau), then the exact
+// predicate; a tile is skipped once its object has a lower hit
+__global__ void __launch_bounds__(kTile) lt_hit_kernel(QArgs a, const Tile* tiles, const double* P, uint64_t pad,
+                                                       const double* obj_stats, unsigned long long* hitf,
+                                                       unsigned long long* nexact, NearLog near) {
+    const Tile T = tiles[blockIdx.x];
+    const uint64_t rel0 = T.row0 - T.obj_row0;
+    if (*(volatile unsigned long long*)(hitf + T.obj) < rel0 || threadIdx.x >= T.count) return;
+    const uint64_t f = T.row0 + threadIdx.x;
+    double p0[3], p1[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        p0[k] = __ldg(a.Q + (uint64_t)k * a.Qpad);
+        p1[k] = __ldg(a.Q + (uint64_t)(3 + k) * a.Qpad);
+    }
+    const double* Bs = obj_stats + (uint64_t)T.obj * kObjStats;
+    double diag2 = 0.0, ext = Bs[7];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double l = fmin(Bs[k], fmin(p0[k], p1[k])), h = fmax(Bs[3 + k], fmax(p0[k], p1[k]));
+        diag2 += (h - l) * (h - l);
+        ext = fmax(ext, fmax(fabs(p0[k]), fabs(p1[k])));
+    }
+    const double tau = kCullDiag * sqrt(diag2) + kCullAbs * ext;
+    bool apart = false;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double lo = fmin(p0[k], p1[k]) - tau, hi = fmax(p0[k], p1[k]) + tau;
+        apart |= (__ldg(P + (uint64_t)(F_LO + k) * pad + f) > hi) | (__ldg(P + (uint64_t)(F_HI + k) * pad + f) < lo);
+    }
+    if (apart) return;
+    const double n0 = __ldg(P + (uint64_t)F_N * pad + f), n1 = __ldg(P + (uint64_t)(F_N + 1) * pad + f),
+                 n2 = __ldg(P + (uint64_t)(F_N + 2) * pad + f), c = __ldg(P + (uint64_t)F_C * pad + f);
+    const double h0 = fma(n0, p0[0], fma(n1, p0[1], fma(n2, p0[2], -c)));
+    const double h1 = fma(n0, p1[0], fma(n1, p1[1], fma(n2, p1[2], -c)));
+    const double q0 = fabs(h0) - tau, q1 = fabs(h1) - tau;
+    if (((__double2hiint(h0) ^ __double2hiint(h1)) | __double2hiint(q0) | __double2hiint(q1)) >= 0 && q0 != 0.0 &&
+        q1 != 0.0)
+        return;
+    atomicAdd(nexact, 1ull);
+    const exact::tri t = face_tri(P, pad, f);
+    const exact::v3 e0{p0[0], p0[1], p0[2]}, e1{p1[0], p1[1], p1[2]};
+    if (exact::near_degenerate_seg(e0, e1, t)) near_log(near, T.obj, f - T.obj_row0);
+    if (exact::seg_tri_hit(e0, e1, t)) atomicMin(hitf + T.obj, (unsigned long long)(f - T.obj_row0));
+}
+
+__global__ void lt_finalize_kernel(uint64_t n, const unsigned long long* D, const unsigned long long* Pf,
+                                   double* dist, uint8_t* hit) {
+    const uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= n) return;
+    if (dist) dist[o] = Pf[o] == kNone || !D ? pos_inf() : __longlong_as_double((long long)D[o]);
+    if (hit) hit[o] = Pf[o] != kNone;
+}
+
+}  // namespace
+
+void run_literal_table(const Ctx& cx, int op, const QuerySet& q1, const Geom& B, double* dist, uint8_t* hit,
+                       uint64_t* face) {
+    const cudaStream_t st = cx.stream;
+    tdb_stats& S = *cx.stats;
+    std::memset(&S, 0, sizeof S);
+    const uint64_t n_obj = B.n_obj, n_tiles = B.h_tiles.size();
+    if (q1.n != 1) throw std::invalid_argument("one literal query expected");
+    if (n_obj == 0) return;
+    if (op == TDB_OP_INTERSECTS && q1.kind != kQuerySegments)
+        throw std::invalid_argument("intersects takes a segment literal (batch.cpp:53-63)");
+    std::vector<void*> mem;
+    auto alloc = [&](size_t bytes) {
+        void* p = nullptr;
+        CK(cudaMallocAsync(&p, std::max<size_t>(1, bytes), st));
+        mem.push_back(p);
+        return p;
+    };
+    unsigned long long* ctr = (unsigned long long*)alloc(4 * sizeof(unsigned long long));
+    CK(cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), st));
+    unsigned long long* D = (unsigned long long*)alloc(n_obj * sizeof(unsigned long long));
+    unsigned long long* Pf = (unsigned long long*)alloc(n_obj * sizeof(unsigned long long));
+    NearDev near;
+    near.alloc(st);
+    QArgs a{q1.planes, 1, q1.pad, q1.kind, B.planes, B.n_pad, B.n, 1, B.n, nullptr, nullptr};
+    cudaEvent_t ev[2];
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(ev[0], st));
+    uint64_t launches = 0;
+    int rounds = 0;
+    if (n_tiles) {
+        if (op == TDB_OP_INTERSECTS) {
+            CK(cudaMemsetAsync(Pf, 0xff, n_obj * sizeof(unsigned long long), st));
+            lt_hit_kernel<<<(unsigned)n_tiles, kTile, 0, st>>>(a, B.d_tiles, B.planes, B.n_pad, B.d_obj_stats, Pf,
+                                                               ctr + 1, near.log);
+            CK(cudaGetLastError());
+            ++launches;
+        } else {
+            unsigned long long* objmin = (unsigned long long*)alloc(n_obj * sizeof(unsigned long long));
+            double* band2 = (double*)alloc(n_obj * sizeof(double));
+            double* band = (double*)alloc(n_obj * sizeof(double));
+            CK(cudaMemsetAsync(objmin, 0xff, n_obj * sizeof(unsigned long long), st));
+            const unsigned ob = (unsigned)((n_obj + 255) / 256);
+            lt_filter_kernel<<<(unsigned)n_tiles, kTile, 0, st>>>(a, B.d_tiles, B.planes, B.n_pad, objmin);
+            lt_band_kernel<<<ob, 256, 0, st>>>(a, n_obj, B.d_obj_stats, objmin, band2, band, D, Pf);
+            launches += 2;
+            for (rounds = 1; rounds <= 8; ++rounds) {
+                for (int pass = 1; pass <= 2; ++pass) {
+                    lt_verify_kernel<<<(unsigned)n_tiles, kTile, 0, st>>>(a, B.d_tiles, B.planes, B.n_pad, pass,
+                                                                          band2, D, Pf, ctr, near.log);
+                    ++launches;
+                }
+                CK(cudaMemsetAsync(ctr + 2, 0, sizeof(unsigned long long), st));
+                lt_check_kernel<<<ob, 256, 0, st>>>(a, n_obj, B.d_obj_stats, band2, band, D, Pf, ctr + 2);
+                ++launches;
+                CK(cudaGetLastError());
+                unsigned long long retry = 0;
+                CK(cudaMemcpyAsync(&retry, ctr + 2, sizeof retry, cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                if (!retry) break;
+            }
+        }
+    } else if (op == TDB_OP_INTERSECTS) {
+        CK(cudaMemsetAsync(Pf, 0xff, n_obj * sizeof(unsigned long long), st));
+    } else {
+        CK(cudaMemsetAsync(D, 0xff, n_obj * sizeof(unsigned long long), st));
+        CK(cudaMemsetAsync(Pf, 0xff, n_obj * sizeof(unsigned long long), st));
+    }
+    double* od = dist ? (double*)alloc(n_obj * sizeof(double)) : nullptr;
+    uint8_t* oh = hit ? (uint8_t*)alloc(n_obj) : nullptr;
+    lt_finalize_kernel<<<(unsigned)((n_obj + 255) / 256), 256, 0, st>>>(n_obj, op == TDB_OP_DISTANCE ? D : nullptr,
+                                                                        Pf, od, oh);
+    CK(cudaGetLastError());
+    ++launches;
+    CK(cudaEventRecord(ev[1], st));
+    if (od) d2h(dist, od, n_obj * sizeof(double), st);
+    if (oh) d2h(hit, oh, n_obj, st);
+    if (face) d2h(face, Pf, n_obj * sizeof(uint64_t), st);
+    unsigned long long hc[4] = {0, 0, 0, 0};
+    CK(cudaMemcpyAsync(hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, st));
+    for (void* p : mem) CK(cudaFreeAsync(p, st));
+    CK(cudaStreamSynchronize(st));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+    S.ms_total = ms;
+    for (auto& e : ev) CK(cudaEventDestroy(e));
+    S.pairs = B.n;
+    S.pairs_evaluated = B.n;
+    S.items = n_tiles;
+    S.candidates = hc[0];
+    S.exact_pairs = hc[1];
+    S.kernels = launches;
+    S.rounds = rounds ? rounds : 1;
+    near.fetch(st, cx.near);
+    S.near_degenerate = cx.near->count;
+}
+
 }  // namespace tdb

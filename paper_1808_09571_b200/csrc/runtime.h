@@ -170,7 +170,16 @@ void queries_build(QuerySet* qs, const double* host_q, uint64_t n, int kind, cud
 void run_queries(const Ctx& cx, int op, const QuerySet& qs, const Geom& B, double* dist, uint8_t* hit,
                  uint64_t* face);
 
+// One segment / point literal (q1.n == 1) against every object of table B
+// (run_batch with a Segment / Point argument over Mesh records): per object
+// distance_to_mesh (dist + lowest face) or intersects_mesh (hit + lowest hit
+// face); faces are object-relative.
+void run_literal_table(const Ctx& cx, int op, const QuerySet& q1, const Geom& B, double* dist, uint8_t* hit,
+                       uint64_t* face);
+
 // mesh_volume (kernels.cpp:27-46) with the reference's fixed chunk tree.
 double run_volume(const Ctx& cx, const Geom& g, uint64_t chunk);
+// ... for every object of a table (out: n_obj doubles)
+void run_volume_table(const Ctx& cx, const Geom& g, uint64_t chunk, double* out);
 
 }  // namespace tdb

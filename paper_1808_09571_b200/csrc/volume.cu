@@ -14,6 +14,7 @@
 // evaluated on the device.
 #include <algorithm>
 #include <cstring>
+#include <vector>
 
 #include "exact.cuh"
 #include "runtime.h"
@@ -56,7 +57,82 @@ __global__ void tree_sum_kernel(double* leaves, uint64_t size, double* out) {
     *out = leaves[0];
 }
 
+// per-object leaves: leaf k covers faces [lb[k], le[k])
+__global__ void leaf_sums_kernel(const double* __restrict__ P, uint64_t pad, const uint64_t* __restrict__ lb,
+                                 const uint64_t* __restrict__ le, uint64_t n_leaves, double* __restrict__ leaves) {
+    const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_leaves) return;
+    double acc = 0.0;
+    for (uint64_t i = lb[k]; i < le[k]; ++i) acc = __dadd_rn(acc, face_term(P, pad, i));
+    leaves[k] = acc;
+}
+
+// pairwise_tree_sum per object over its leaves [l0[o], l0[o+1])
+__global__ void object_trees_kernel(double* leaves, const uint64_t* __restrict__ l0, uint64_t n_obj,
+                                    double* __restrict__ out) {
+    const uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= n_obj) return;
+    double* L = leaves + l0[o];
+    uint64_t size = l0[o + 1] - l0[o];
+    if (size == 0) {
+        out[o] = 0.0;
+        return;
+    }
+    while (size > 1) {
+        uint64_t w = 0, i = 0;
+        for (; i + 1 < size; i += 2) L[w++] = __dadd_rn(L[i], L[i + 1]);
+        if (i < size) L[w++] = L[i];
+        size = w;
+    }
+    out[o] = L[0];
+}
+
 }  // namespace
+
+// mesh_volume of every object of a table (run_batch(Volume, ...) over a mesh
+// column, batch.cpp:23-29): each object gets its own chunk tree, exactly as
+// eval_volume calls mesh_volume per record with the caller's chunk_size.
+void run_volume_table(const Ctx& cx, const Geom& g, uint64_t chunk, double* out) {
+    const cudaStream_t st = cx.stream;
+    if (chunk == 0) chunk = 4096;
+    std::vector<uint64_t> lb, le, l0(g.n_obj + 1, 0);
+    for (uint64_t o = 0; o < g.n_obj; ++o) {
+        l0[o] = lb.size();
+        for (uint64_t b = g.h_off[o]; b < g.h_off[o + 1]; b += chunk) {
+            lb.push_back(b);
+            le.push_back(std::min(g.h_off[o + 1], b + chunk));
+        }
+    }
+    l0[g.n_obj] = lb.size();
+    const uint64_t nl = lb.size();
+    uint64_t *d_lb = nullptr, *d_le = nullptr, *d_l0 = nullptr;
+    double *leaves = nullptr, *d_out = nullptr;
+    CK(cudaMallocAsync(&d_lb, std::max<uint64_t>(1, nl) * sizeof(uint64_t), st));
+    CK(cudaMallocAsync(&d_le, std::max<uint64_t>(1, nl) * sizeof(uint64_t), st));
+    CK(cudaMallocAsync(&d_l0, (g.n_obj + 1) * sizeof(uint64_t), st));
+    CK(cudaMallocAsync(&leaves, std::max<uint64_t>(1, nl) * sizeof(double), st));
+    CK(cudaMallocAsync(&d_out, std::max<uint64_t>(1, g.n_obj) * sizeof(double), st));
+    h2d(d_lb, lb.data(), nl * sizeof(uint64_t), st);
+    h2d(d_le, le.data(), nl * sizeof(uint64_t), st);
+    h2d(d_l0, l0.data(), (g.n_obj + 1) * sizeof(uint64_t), st);
+    if (nl) {
+        leaf_sums_kernel<<<(unsigned)((nl + 127) / 128), 128, 0, st>>>(g.planes, g.n_pad, d_lb, d_le, nl, leaves);
+        CK(cudaGetLastError());
+    }
+    if (g.n_obj) {
+        object_trees_kernel<<<(unsigned)((g.n_obj + 127) / 128), 128, 0, st>>>(leaves, d_l0, g.n_obj, d_out);
+        CK(cudaGetLastError());
+        d2h(out, d_out, g.n_obj * sizeof(double), st);
+    }
+    CK(cudaFreeAsync(d_lb, st));
+    CK(cudaFreeAsync(d_le, st));
+    CK(cudaFreeAsync(d_l0, st));
+    CK(cudaFreeAsync(leaves, st));
+    CK(cudaFreeAsync(d_out, st));
+    CK(cudaStreamSynchronize(st));
+    std::memset(cx.stats, 0, sizeof *cx.stats);
+    cx.stats->kernels = (nl ? 1 : 0) + (g.n_obj ? 1 : 0);
+}
 
 double run_volume(const Ctx& cx, const Geom& g, uint64_t chunk) {
     const cudaStream_t st = cx.stream;

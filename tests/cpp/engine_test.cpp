@@ -70,6 +70,8 @@ int main() {
         "SELECT id, ST_3DDistance(geom, " + seg + ") FROM t",
         "SELECT id, ST_Volume(geom) FROM t",
         "SELECT id, ST_3DDistance(geom, " + lit + ") FROM t",
+        "SELECT id, ST_3DDistance(geom, ST_GeomFromText('POINT Z (50 50 50)')) FROM t",
+        "SELECT id FROM t WHERE ST_3DIntersects(" + seg + ", geom)",
     };
     const SideResult ref = engine_ref(csv, sqls);
     const SideResult dev = engine_dev(csv, sqls);
@@ -98,7 +100,7 @@ int main() {
                     a.notices.size(), a.error.empty() ? "" : (" error: " + a.error).c_str());
     }
     std::printf("device snapshot cache: builds=%zu hits=%zu\n", dev.cache_builds, dev.cache_hits);
-    if (dev.cache_builds != 1 || dev.cache_hits < 5) {
+    if (dev.cache_builds != 1 || dev.cache_hits < 9) {
         std::printf("unexpected cache use\n");
         ++bad;
     }
