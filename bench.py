@@ -11,8 +11,8 @@ A step is one pass of the hot path over one batch of A rows (default 65,536
 terrain rows x 1,310,720 ore faces = 8.6e10 pairs); 16 batches are the whole
 1M x 1M job, so the default --steps 16 times the full configuration. Under
 torchrun each rank takes its own batches (weak scaling); per-step answers are
-combined with an NCCL all_gather of 16 B per rank (the lexicographic
-(distance, pair) min).
+combined by NCCL MIN all-reduces (the distance, then the lowest pair among
+the ranks holding it: the lexicographic (distance, pair) min).
 
   value        pairs/s with the meshes resident in HBM (CUDA events on the
                launch stream, max over ranks)
@@ -464,7 +464,7 @@ def main():
         b = s * world + rank
         d, p = wl.run(T, b)
         st = T.last_stats()
-        d, p = shard.combine_min(d, p, device="cuda")  # NCCL all_gather, 16 B per rank
+        d, p = shard.combine_min(d, p, device="cuda")  # NCCL MIN all-reduce (distance, then pair)
         if record:
             results.append((d, p))
             k_ms.append(st["ms_filter"])

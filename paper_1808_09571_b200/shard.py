@@ -5,9 +5,12 @@ first mesh, or objects of a table) is split into contiguous shards and each
 rank evaluates its shard against the replicated B with no data-path
 collective. The only exchange is the final reduction of the per-rank answers:
 
-* distance   : lexicographic min of (distance, pair index) — an all_gather
-               of 16 B per rank (NCCL over NVLink on B200s, gloo on CPU);
-* intersects : min of the lowest hit pair index (UINT64_MAX = no hit);
+* distance   : lexicographic min of (distance, pair index) — a MIN
+               all-reduce of the distance (non-negative doubles order as their
+               int64 bits), then a MIN all-reduce of the pair among the ranks
+               holding that distance (NCCL over NVLink on B200s, gloo on CPU);
+* intersects : one MIN all-reduce of the lowest hit pair index (the OR of the
+               ranks' hits, keeping the reference's lowest-index winner);
 * table      : each rank owns a slice of records; slices are gathered.
 
 Pair indices are global (i * |B| + j) on every rank, so the reduced answer is
@@ -60,33 +63,40 @@ def lexmin(pairs: Sequence[Tuple[float, int]]) -> Tuple[float, int]:
     return best
 
 
-def _pack(d: float, p: int):
+I64_MAX = (1 << 63) - 1  # "no pair" inside the int64 reductions
+
+
+def _allreduce_min(value: int, group=None, device=None) -> int:
     import torch
-    return torch.tensor([np.float64(d).view(np.int64), np.uint64(p).view(np.int64)], dtype=torch.int64)
+    import torch.distributed as dist_
+
+    t = torch.tensor([value], dtype=torch.int64, device=device or "cpu")
+    dist_.all_reduce(t, op=dist_.ReduceOp.MIN, group=group)
+    return int(t.item())
 
 
 def combine_min(dist: float, pair: Optional[int], group=None, device=None) -> Tuple[float, int]:
     """All ranks get the lexicographic (distance, pair) min over ranks."""
-    import torch
     import torch.distributed as dist_
 
     p = U64_MAX if pair is None else int(pair)
     if not dist_.is_initialized() or dist_.get_world_size(group) == 1:
         return float(dist), p
-    t = _pack(dist, p).to(device or "cpu")
-    g = [torch.empty_like(t) for _ in range(dist_.get_world_size(group))]
-    dist_.all_gather(g, t, group=group)
-    vals = []
-    for x in g:
-        x = x.cpu().numpy()
-        vals.append((float(x[0:1].view(np.float64)[0]), int(x[1:2].view(np.uint64)[0])))
-    return lexmin(vals)
+    dbits = int(np.float64(dist).view(np.int64))  # >= 0 (or +inf): orders as the double
+    gbits = _allreduce_min(dbits, group, device)
+    mine = p if (dbits == gbits and pair is not None) else I64_MAX
+    gp = _allreduce_min(mine, group, device)
+    return float(np.int64(gbits).view(np.float64)), (U64_MAX if gp == I64_MAX else gp)
 
 
 def combine_hit(pair: Optional[int], group=None, device=None) -> Optional[int]:
-    """Lowest hit pair over ranks (None when no rank hit)."""
-    d, p = combine_min(0.0 if pair is not None else float("inf"), pair, group, device)
-    return None if p == U64_MAX else p
+    """Lowest hit pair over ranks (None when no rank hit): one MIN all-reduce."""
+    import torch.distributed as dist_
+
+    if not dist_.is_initialized() or dist_.get_world_size(group) == 1:
+        return pair
+    gp = _allreduce_min(I64_MAX if pair is None else int(pair), group, device)
+    return None if gp == I64_MAX else gp
 
 
 def gather_slices(local: np.ndarray, counts: Sequence[int], group=None, device=None) -> np.ndarray:
