@@ -138,10 +138,21 @@ struct Stage {
 
 thread_local Stage t_stage;
 
+// Page-locked (cudaHostAlloc / cudaHostRegister) host memory: the copy
+// engine reads it directly.
+bool pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 }  // namespace
 
 void h2d(void* dst, const void* src, size_t n, cudaStream_t st) {
-    if (n < kDirectBelow) {
+    if (n < kDirectBelow || pinned(src)) {
         if (n) CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st));
         return;
     }
@@ -158,7 +169,7 @@ void h2d(void* dst, const void* src, size_t n, cudaStream_t st) {
 }
 
 void d2h(void* dst, const void* src, size_t n, cudaStream_t st) {
-    if (n < kDirectBelow) {
+    if (n < kDirectBelow || pinned(dst)) {
         if (n) CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         return;

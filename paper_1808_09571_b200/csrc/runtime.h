@@ -57,9 +57,11 @@ struct Geom {
 void geom_build(Geom* g, const double* tri9, uint64_t n, const uint64_t* host_off, uint64_t n_obj,
                 cudaStream_t st, bool tri9_on_device = false);
 void geom_release(Geom* g);
-// Caller (pageable) buffers <-> device through pinned staging (host_copy.cpp).
-// h2d is stream-ordered (returns once the source was read); d2h returns
-// with the data in dst.
+// Caller buffers <-> device (host_copy.cu): large pageable buffers go through
+// pinned staging, page-locked ones straight to the copy engine. h2d is
+// stream-ordered; the source must stay valid until the stream has passed the
+// copy (every C-ABI call synchronises before it returns). d2h returns with
+// the data in dst.
 void h2d(void* dst, const void* src, size_t n, cudaStream_t st);
 void d2h(void* dst, const void* src, size_t n, cudaStream_t st);
 // WKT literals text[lit_off[i], lit_off[i+1]) (TIN Z / POLYHEDRALSURFACE Z),
