@@ -126,6 +126,8 @@ int tdb_table_from_wkt(const char* text, const uint64_t* lit_off, uint64_t n_lit
                        uint64_t* err_literal, uint64_t* err_pos);
 /* The store's faces back as host AoS, 9 doubles per face in face order. */
 int tdb_geom_download(tdb_mesh g, double* tri9_out);
+/* Its CSR face offsets (n_objects + 1 entries). */
+int tdb_geom_offsets(tdb_mesh g, uint64_t* off_out);
 int tdb_geom_info(tdb_mesh g, uint64_t* n_tris, uint64_t* n_objects, uint64_t* n_degenerate,
                   double* aabb6);
 void tdb_mesh_free(tdb_mesh m);

@@ -161,7 +161,11 @@ struct DeviceColumns {
         tdb_queries_free(points);
     }
 
-    explicit DeviceColumns(const std::vector<store::GeometryRecord>& records) {
+    // `meshes` (optional): the Mesh records already on the device as a table,
+    // one object per Mesh record in record order (the device loader's
+    // output); the columns take ownership.
+    explicit DeviceColumns(const std::vector<store::GeometryRecord>& records, tdb_table meshes_in = nullptr) {
+        meshes = meshes_in;
         for (std::size_t i = 0; i < records.size(); ++i) {
             const GeometryKind k = kind_of(records[i].geometry);
             if (k == GeometryKind::Mesh) mesh_rows.push_back(i);
@@ -170,7 +174,11 @@ struct DeviceColumns {
             else other_rows.push_back(i);
         }
         try {
-            if (!mesh_rows.empty()) {
+            if (meshes) {
+                std::uint64_t n_obj = 0;
+                check(tdb_geom_info(meshes, nullptr, &n_obj, nullptr, nullptr));
+                if (n_obj != mesh_rows.size()) throw std::invalid_argument("device mesh table does not match the records");
+            } else if (!mesh_rows.empty()) {
                 std::vector<std::uint64_t> off(mesh_rows.size() + 1, 0);
                 for (std::size_t k = 0; k < mesh_rows.size(); ++k)
                     off[k + 1] = off[k] + std::get<TriangleMesh>(records[mesh_rows[k]].geometry).triangles.size();
@@ -229,6 +237,14 @@ class SnapshotCache {
         ++builds_;
         return cols;
     }
+    // Seed the cache with columns built elsewhere for this snapshot (the
+    // device loader's table, store.hpp in this directory).
+    void adopt(const store::TableSnapshot& snap, std::shared_ptr<const DeviceColumns> cols) {
+        std::lock_guard<std::mutex> g(mu_);
+        map_[Key(snap)] = std::move(cols);
+        ++adopted_;
+    }
+    std::size_t adopted() const { return adopted_; }
     std::size_t size() {
         std::lock_guard<std::mutex> g(mu_);
         return map_.size();
@@ -244,7 +260,7 @@ class SnapshotCache {
     using Key = std::weak_ptr<const store::GeometryTable>;
     std::mutex mu_;
     std::map<Key, std::shared_ptr<const DeviceColumns>, std::owner_less<Key>> map_;
-    std::size_t hits_ = 0, builds_ = 0;
+    std::size_t hits_ = 0, builds_ = 0, adopted_ = 0;
 };
 
 inline SnapshotCache& default_cache() {

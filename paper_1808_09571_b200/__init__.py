@@ -94,6 +94,7 @@ _SIGS = [
     ("tdb_mesh_from_wkt", ct.c_int, [ct.c_char_p, ct.c_uint64, ct.POINTER(ct.c_void_p), _U64]),
     ("tdb_table_from_wkt", ct.c_int, [ct.c_char_p, _U64, ct.c_uint64, ct.POINTER(ct.c_void_p), _U64, _U64]),
     ("tdb_geom_download", ct.c_int, [ct.c_void_p, _D]),
+    ("tdb_geom_offsets", ct.c_int, [ct.c_void_p, _U64]),
     ("tdb_mesh_free", None, [ct.c_void_p]),
     ("tdb_table_free", None, [ct.c_void_p]),
     ("tdb_mesh_mesh_distance", ct.c_int, [ct.c_void_p, ct.c_void_p, ct.POINTER(DistOut)]),

@@ -263,6 +263,13 @@ int tdb_table_from_wkt(const char* text, const uint64_t* lit_off, uint64_t n_lit
     return rc;
 }
 
+int tdb_geom_offsets(tdb_mesh g, uint64_t* off_out) {
+    return guarded([&] {
+        need(g != nullptr && off_out != nullptr, "null argument");
+        std::memcpy(off_out, g->g.h_off.data(), (g->g.n_obj + 1) * sizeof(uint64_t));
+    });
+}
+
 int tdb_geom_download(tdb_mesh g, double* tri9_out) {
     return guarded([&] {
         need(g != nullptr, "null handle");

@@ -13,8 +13,11 @@ struct SideStatement {
 
 struct SideResult {
     std::vector<SideStatement> statements;
-    std::size_t cache_builds = 0, cache_hits = 0;
+    std::size_t cache_builds = 0, cache_hits = 0, cache_adopted = 0;
 };
+
+std::string engine_ref_load(const std::string& csv);
+std::string engine_dev_load(const std::string& csv);
 
 SideResult engine_ref(const std::string& csv, const std::vector<std::string>& sqls);
 SideResult engine_dev(const std::string& csv, const std::vector<std::string>& sqls);

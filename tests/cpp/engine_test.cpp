@@ -99,10 +99,32 @@ int main() {
         std::printf("statement %zu: %s, %zu rows, notices=%zu%s\n", s, a.tag.c_str(), a.rows.size(),
                     a.notices.size(), a.error.empty() ? "" : (" error: " + a.error).c_str());
     }
-    std::printf("device snapshot cache: builds=%zu hits=%zu\n", dev.cache_builds, dev.cache_hits);
-    if (dev.cache_builds != 1 || dev.cache_hits < 9) {
+    std::printf("device snapshot cache: adopted=%zu builds=%zu hits=%zu\n", dev.cache_adopted, dev.cache_builds,
+                dev.cache_hits);
+    if (dev.cache_adopted != 1 || dev.cache_builds != 0 || dev.cache_hits < 10) {
         std::printf("unexpected cache use\n");
         ++bad;
+    }
+    // the loader itself: the reference load_csv_text vs the device loader,
+    // on the table above and on CSVs that must fail at a given line
+    std::vector<std::string> csvs = {csv};
+    const std::string good_tin = "\"TIN Z (((0 0 0, 1 0 0, 0 1 0, 0 0 0)))\"";
+    csvs.push_back("id,geom\n1," + good_tin + "\n2,\"TIN Z (((0 0 0, 1 0 0, 0 1 0, 5 5 5)))\"\n3," + good_tin + "\n");
+    csvs.push_back("id,geom\n1," + good_tin + "\n2,POINT Z (1 2)\n3,\"TIN Z (((0 0 0)))\"\n");
+    csvs.push_back("1," + good_tin + "\n1," + good_tin + "\n");             // duplicate id
+    csvs.push_back("1," + good_tin + "\nx," + good_tin + "\n");             // bad id
+    csvs.push_back("1," + good_tin + "\n2,\"TIN Z (((0 0 0, 1 0 0\n");     // unterminated quote
+    csvs.push_back("1,\"TIN Z (((0 0 0, 1 0 0, 0 1 nan, 0 0 0)))\"\n2\n"); // device error before a host error
+    csvs.push_back("\r\n  \nid , WKT\r\n7 , \"POLYHEDRALSURFACE Z (((0 0 0, 1 0 0, 1 1 0, 0 1 0, 0 0 0)))\" \r\n"
+                   "8,\"LINESTRING Z (0 0 0, 1 1 1)\"\n9,\"TIN Z (((0 0 0, 1 0 0, 0.5 1e-20 0, 0 0 0)))\"\n");
+    csvs.push_back("");
+    for (std::size_t k = 0; k < csvs.size(); ++k) {
+        const std::string a = engine_ref_load(csvs[k]), b = engine_dev_load(csvs[k]);
+        std::printf("load %zu: %.100s\n", k, a.c_str());
+        if (a != b) {
+            std::printf("LOAD MISMATCH %zu:\n  ref %.300s\n  dev %.300s\n", k, a.c_str(), b.c_str());
+            ++bad;
+        }
     }
     if (bad) return 1;
     std::printf("ENGINE OK (%zu cells identical)\n", cells);
