@@ -7,6 +7,9 @@
 // boundary.
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -99,6 +102,13 @@ void ensure_device() {
     t_device = dev;
 }
 
+// The library's stream on `dev` (created by the first call on it): handle
+// frees are stream-ordered there, back into the device pool.
+cudaStream_t lib_stream(int dev) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return dev >= 0 && dev < (int)g_streams.size() ? g_streams[dev] : nullptr;
+}
+
 tdb::Ctx ctx() {
     ensure_device();
     tdb::Ctx c;
@@ -163,7 +173,7 @@ void upload(const double* tri9, uint64_t n, const uint64_t* off, uint64_t n_obj,
     try {
         tdb::geom_build(&h->g, tri9, n, off, n_obj, c.stream);
     } catch (...) {
-        tdb::geom_release(&h->g);
+        tdb::geom_release(&h->g, c.stream);
         delete h;
         throw;
     }
@@ -250,7 +260,7 @@ int tdb_table_from_wkt(const char* text, const uint64_t* lit_off, uint64_t n_lit
         try {
             tdb::wkt_build(&h->g, text, lit_off, n_lit, c.stream);
         } catch (...) {
-            tdb::geom_release(&h->g);
+            tdb::geom_release(&h->g, c.stream);
             delete h;
             throw;
         }
@@ -291,7 +301,7 @@ int tdb_geom_info(tdb_mesh g, uint64_t* n, uint64_t* n_obj, uint64_t* n_deg, dou
 void tdb_mesh_free(tdb_mesh m) {
     if (!m) return;
     cudaSetDevice(m->g.device);
-    tdb::geom_release(&m->g);
+    tdb::geom_release(&m->g, lib_stream(m->g.device));
     delete m;
 }
 
@@ -369,13 +379,21 @@ int tdb_table_eval(int op, tdb_table t, tdb_mesh lit, double* dist, uint8_t* hit
 }
 
 int tdb_distance_host(const double* a9, uint64_t n, const double* b9, uint64_t m, tdb_dist_out* out) {
+    static const bool trace = getenv("TDB_TRACE") != nullptr;
+    auto now = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    const double t0 = now();
     tdb_mesh a = nullptr, b = nullptr;
     int rc = tdb_mesh_upload(a9, n, &a);
+    const double t1 = now();
     if (rc == TDB_OK) rc = tdb_mesh_upload(b9, m, &b);
+    const double t2 = now();
     if (rc == TDB_OK) rc = tdb_mesh_mesh_distance(a, b, out);
+    const double t3 = now();
     const std::string err = t_err;
     tdb_mesh_free(a);
     tdb_mesh_free(b);
+    const double t4 = now();
+    if (trace) fprintf(stderr, "[tdb] distance_host upA %.2f upB %.2f eval %.2f free %.2f ms\n", t1 - t0, t2 - t1, t3 - t2, t4 - t3);
     t_err = err;
     return rc;
 }
@@ -431,7 +449,7 @@ int tdb_queries_upload(const double* q, uint64_t n, int kind, tdb_queries* out) 
             tdb::queries_build(&h->q, q, n, kind == TDB_QUERY_SEGMENTS ? tdb::kQuerySegments : tdb::kQueryPoints,
                                c.stream);
         } catch (...) {
-            cudaFree(h->q.planes);
+            cudaFreeAsync(h->q.planes, c.stream);
             delete h;
             throw;
         }
@@ -442,7 +460,7 @@ int tdb_queries_upload(const double* q, uint64_t n, int kind, tdb_queries* out) 
 void tdb_queries_free(tdb_queries q) {
     if (!q) return;
     cudaSetDevice(q->q.device);
-    cudaFree(q->q.planes);
+    cudaFreeAsync(q->q.planes, lib_stream(q->q.device));
     delete q;
 }
 
@@ -491,10 +509,10 @@ int tdb_literal_table_eval(int op, int literal_kind, const double* literal, tdb_
                                c.stream);
             tdb::run_literal_table(c, op, q1, records->g, dist_out, hit_out, face_out);
         } catch (...) {
-            cudaFree(q1.planes);
+            cudaFreeAsync(q1.planes, c.stream);
             throw;
         }
-        cudaFree(q1.planes);
+        cudaFreeAsync(q1.planes, c.stream);
     });
 }
 

@@ -115,8 +115,9 @@ __global__ void __launch_bounds__(kTile, TDB_FILTER_MINB) filter_kernel(DistArgs
         mbar_wait(&bar[st], (uint32_t)((s >> 1) & 1));
         const int cnt = (int)min((uint64_t)kSB, b1 - (b0 + (uint64_t)s * kSB));
         const double* sb = sm[st];
+        int j = 0;
 #pragma unroll 1
-        for (int j = 0; j < cnt; ++j) {
+        for (; j < cnt; ++j) {
             if (reinterpret_cast<const int*>(sb + F_DEG * kSB + j)[1] != 0) continue;  // uniform across the CTA
             best = min_nn(best, pair_d2(A, FaceRef{sb + j, (uint64_t)kSB}, a.Ap + row, a.An_pad));
         }

@@ -142,14 +142,16 @@ static __device__ __noinline__ bool pierce_slow(const double* ap, uint64_t as, c
     return edges_pierce(hb, ub, vb) || edges_pierce(ha, ua, va);
 }
 
-// clamp to [0,1] on the high word only (the low word is dropped: relative
-// truncation <= 2^-20). Used for the first parameter estimate, whose
-// precision is already bounded by rcp.approx.
+// clamp to [0,1] on the high word only. Used for the first parameter
+// estimate, whose precision is already bounded by rcp.approx.
 __device__ __forceinline__ double clamp01_hi(double x) {
-    return __hiloint2double(min(max(__double2hiint(x), 0), 0x3ff00000), 0);
+    // the low word is kept as is (no register move to zero it): x >= 1 lands
+    // in [1 - 2^-20, 1), x < 0 on a subnormal
+    return __hiloint2double(min(max(__double2hiint(x), 0), 0x3fefffff), __double2loint(x));
 }
 
 constexpr int kInfHi = 0x7ff00000;  // high word of +inf
+
 
 // Barycentric inside test u >= 0, v >= 0, u + v < 1 with one FP64 add: the
 // sum is non-negative when u, v are, so "< 1" is a high-word compare
@@ -208,6 +210,7 @@ __device__ __forceinline__ double pair_d2(const AFace& A, const P& bt, const dou
         const double ebx = bt(F_E + 3 * k), eby = bt(F_E + 3 * k + 1), ebz = bt(F_E + 3 * k + 2);
         const double Lb = bt(F_L + k), ILb = bt(F_IL + k);
         double fw = fma(ebx, w[0][0], fma(eby, w[0][1], ebz * w[0][2]));
+        int cand[3];
 #pragma unroll
         for (int j = 0; j < 3; ++j) {  // edge A_j->A_j+1 against edge B_k->B_k+1
             const double* ea = A.e + 3 * j;
@@ -223,11 +226,12 @@ __device__ __forceinline__ double pair_d2(const AFace& A, const P& bt, const dou
             const double dx = fma(s, ea[0], fma(-t, ebx, -w[j][0]));
             const double dy = fma(s, ea[1], fma(-t, eby, -w[j][1]));
             const double dz = fma(s, ea[2], fma(-t, ebz, -w[j][2]));
-            best = min(best, __double2hiint(fma(dx, dx, fma(dy, dy, dz * dz))));
+            cand[j] = __double2hiint(fma(dx, dx, fma(dy, dy, dz * dz)));
             cw_prev[j] = cw;
             bb_prev[j] = bb;
             fw = fw - bb;
         }
+        best = min(min(best, cand[0]), min(cand[1], cand[2]));  // VIMNMX3 pairs
     }
     // Both triangles straddle the other's plane: an edge may pierce a face.
     const bool sb = !(hb_or >= 0 || hb_and < 0);
@@ -239,5 +243,6 @@ __device__ __forceinline__ double pair_d2(const AFace& A, const P& bt, const dou
     if (sa && sb && pierce_slow(ap, as, bt.p, bt.stride)) best = 0;
     return __hiloint2double(best, 0);
 }
+
 
 }  // namespace tdb

@@ -56,7 +56,7 @@ struct Geom {
 // tri9: 9 doubles per face (AoS), on the host unless tri9_on_device
 void geom_build(Geom* g, const double* tri9, uint64_t n, const uint64_t* host_off, uint64_t n_obj,
                 cudaStream_t st, bool tri9_on_device = false);
-void geom_release(Geom* g);
+void geom_release(Geom* g, cudaStream_t st);
 // Caller buffers <-> device (host_copy.cu): large pageable buffers go through
 // pinned staging, page-locked ones straight to the copy engine. h2d is
 // stream-ordered; the source must stay valid until the stream has passed the

@@ -290,13 +290,17 @@ void chunk_aabbs(const Geom& g, uint64_t len, double* out, cudaStream_t st) {
     CK(cudaGetLastError());
 }
 
-void geom_release(Geom* g) {
+// Stream-ordered frees back into the device pool (the store was allocated
+// from it with cudaMallocAsync): a plain cudaFree hands the pages back to the
+// driver, and the next large upload then waits for them to be mapped again.
+// Every call that used the store has synchronized before it returns.
+void geom_release(Geom* g, cudaStream_t st) {
     if (!g) return;
-    cudaFree(g->planes);
-    cudaFree(g->d_off);
-    cudaFree(g->d_tiles);
-    cudaFree(g->d_obj_stats);
-    cudaFree(g->d_tile_aabb);
+    cudaFreeAsync(g->planes, st);
+    cudaFreeAsync(g->d_off, st);
+    cudaFreeAsync(g->d_tiles, st);
+    cudaFreeAsync(g->d_obj_stats, st);
+    cudaFreeAsync(g->d_tile_aabb, st);
     g->planes = nullptr;
 }
 
