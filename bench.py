@@ -433,9 +433,16 @@ def main():
     import paper_1808_09571_b200 as T
     from paper_1808_09571_b200 import shard
 
+    # one process per GPU; TDB_BENCH_BACKEND=gloo (with ranks sharing a GPU)
+    # only exercises the multi-rank plumbing on a one-GPU box
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("TDB_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     T.init(local)
     T.set_mode(T.MODE_CULL if args.mode == "cull" else T.MODE_FULL)
     stream = torch.cuda.current_stream()

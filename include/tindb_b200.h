@@ -192,6 +192,33 @@ int tdb_mesh_volume(tdb_mesh m, uint64_t chunk_size, double* volume_out);
  * volume per object, each with its own chunk tree (volume_out: n_objects). */
 int tdb_table_volume(tdb_table t, uint64_t chunk_size, double* volume_out);
 
+/* ---- device group: one process driving several B200s (SURVEY.md 8(b)
+ * "tdb_init(int n_gpus): NCCL comm + streams", 8(e)). One worker thread per
+ * device, one NCCL communicator per device (ncclCommInitAll). Geometry is
+ * replicated on every member; mesh x mesh splits a's rows into contiguous
+ * tile-aligned ranges, a table splits its objects into contiguous ranges of
+ * near-equal face count. The only exchange is an NCCL MIN all-reduce: the
+ * distance (its int64 bits), then the pair among the members holding it
+ * (lowest pair on ties); intersects: the lowest hit pair. Results are those
+ * of the single-device calls. Group calls are serialised per group. */
+typedef struct tdb_group_s* tdb_group;
+typedef struct tdb_gmesh_s* tdb_gmesh; /* a mesh or table replicated on the group */
+int tdb_group_create(int n_devices, const int* devices, tdb_group* out); /* devices NULL = 0..n-1 */
+void tdb_group_free(tdb_group g);
+int tdb_group_size(tdb_group g);
+int tdb_group_mesh_upload(tdb_group g, const double* tri9, uint64_t n_tris, tdb_gmesh* out);
+int tdb_group_table_upload(tdb_group g, const double* tri9, const uint64_t* face_offsets,
+                           uint64_t n_objects, tdb_gmesh* out);
+void tdb_gmesh_free(tdb_gmesh m);
+int tdb_group_mesh_mesh_distance(tdb_group g, tdb_gmesh a, tdb_gmesh b, tdb_dist_out* out);
+int tdb_group_mesh_mesh_intersects(tdb_group g, tdb_gmesh a, tdb_gmesh b, tdb_hit_out* out);
+/* run_batch(op, records, literal) with the records split over the group;
+ * outputs as tdb_table_eval (one slot per record, record order). */
+int tdb_group_table_eval(tdb_group g, int op, tdb_gmesh records, tdb_gmesh literal,
+                         double* dist_out, uint8_t* hit_out, uint64_t* pair_out);
+/* tdb_stats of member `member`'s share of the last group call */
+int tdb_group_last_stats(tdb_group g, int member, tdb_stats* out);
+
 /* ---- one-shot host-buffer entry points (upload + evaluate + free) -------- */
 int tdb_distance_host(const double* a9, uint64_t n, const double* b9, uint64_t m,
                       tdb_dist_out* out);

@@ -11,6 +11,8 @@
 // * eval_mesh_mesh — the branch batch.cpp:49 (eval_distance) and :62
 //   (eval_intersects) lack today; returns nullopt for other pairings so the
 //   reference's dispatch continues unchanged.
+// * DeviceGroup — the same operators over several devices of the box
+//   (tdb_group_*: rows split over the members, one NCCL MIN all-reduce).
 // * run_batch_b200 — run_batch (batch.hpp:49-51) against a Mesh literal with
 //   the Mesh records (triangle pairs), the Segment / 2-point LineString
 //   records and the Point records (distance_to_mesh / intersects_mesh, the
@@ -129,6 +131,75 @@ inline IntersectionResult mesh_mesh_intersects(const TriangleMesh& a, const Tria
                                                MeshPairInfo* info = nullptr) {
     DeviceMesh da(a), db(b);
     return mesh_mesh_intersects(da, db, info);
+}
+
+// Several devices from this process (tdb_group_*): geometry replicated on
+// every member, a's rows split over them, one NCCL MIN all-reduce. Same
+// results as the single-device calls.
+class DeviceGroup {
+  public:
+    // devices empty = 0 .. n-1 with n = tdb_device_count()
+    explicit DeviceGroup(std::vector<int> devices = {}) {
+        if (devices.empty())
+            for (int d = 0, n = tdb_device_count(); d < n; ++d) devices.push_back(d);
+        check(tdb_group_create(static_cast<int>(devices.size()), devices.data(), &g_));
+    }
+    ~DeviceGroup() { tdb_group_free(g_); }
+    DeviceGroup(const DeviceGroup&) = delete;
+    DeviceGroup& operator=(const DeviceGroup&) = delete;
+    tdb_group handle() const { return g_; }
+    int size() const { return tdb_group_size(g_); }
+
+  private:
+    tdb_group g_ = nullptr;
+};
+
+class GroupMesh {
+  public:
+    GroupMesh(const DeviceGroup& g, const TriangleMesh& m) {
+        check(tdb_group_mesh_upload(g.handle(), faces_of(m), m.triangles.size(), &h_));
+    }
+    ~GroupMesh() { tdb_gmesh_free(h_); }
+    GroupMesh(const GroupMesh&) = delete;
+    GroupMesh& operator=(const GroupMesh&) = delete;
+    tdb_gmesh handle() const { return h_; }
+
+  private:
+    tdb_gmesh h_ = nullptr;
+};
+
+inline DistanceResult mesh_mesh_distance(const DeviceGroup& g, const TriangleMesh& a, const TriangleMesh& b,
+                                         MeshPairInfo* info = nullptr) {
+    GroupMesh da(g, a), db(g, b);
+    tdb_dist_out o{};
+    check(tdb_group_mesh_mesh_distance(g.handle(), da.handle(), db.handle(), &o));
+    DistanceResult r;
+    r.distance = o.distance;
+    if (o.found) {
+        r.closest_on_a = {o.on_a[0], o.on_a[1], o.on_a[2]};
+        r.closest_on_b = {o.on_b[0], o.on_b[1], o.on_b[2]};
+        r.face_index = static_cast<std::size_t>(o.i);
+    }
+    if (info) {
+        *info = {};
+        if (o.found) info->pair_index = o.pair, info->face_a = o.i, info->face_b = o.j;
+    }
+    return r;
+}
+
+inline IntersectionResult mesh_mesh_intersects(const DeviceGroup& g, const TriangleMesh& a,
+                                               const TriangleMesh& b, MeshPairInfo* info = nullptr) {
+    GroupMesh da(g, a), db(g, b);
+    tdb_hit_out o{};
+    check(tdb_group_mesh_mesh_intersects(g.handle(), da.handle(), db.handle(), &o));
+    IntersectionResult r;
+    r.hit = o.hit != 0;
+    if (r.hit) r.face_index = static_cast<std::size_t>(o.i);
+    if (info) {
+        *info = {};
+        if (r.hit) info->pair_index = o.pair, info->face_a = o.i, info->face_b = o.j;
+    }
+    return r;
 }
 
 // The missing Mesh x Mesh branch of eval_distance / eval_intersects

@@ -126,6 +126,16 @@ _SIGS = [
     ("tdb_queries_free", None, [ct.c_void_p]),
     ("tdb_queries_mesh_distance", ct.c_int, [ct.c_void_p, ct.c_void_p, _D, _U64]),
     ("tdb_queries_mesh_intersects", ct.c_int, [ct.c_void_p, ct.c_void_p, _U8, _U64]),
+    ("tdb_group_create", ct.c_int, [ct.c_int, ct.POINTER(ct.c_int), ct.POINTER(ct.c_void_p)]),
+    ("tdb_group_free", None, [ct.c_void_p]),
+    ("tdb_group_size", ct.c_int, [ct.c_void_p]),
+    ("tdb_group_mesh_upload", ct.c_int, [ct.c_void_p, _D, ct.c_uint64, ct.POINTER(ct.c_void_p)]),
+    ("tdb_group_table_upload", ct.c_int, [ct.c_void_p, _D, _U64, ct.c_uint64, ct.POINTER(ct.c_void_p)]),
+    ("tdb_gmesh_free", None, [ct.c_void_p]),
+    ("tdb_group_mesh_mesh_distance", ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.POINTER(DistOut)]),
+    ("tdb_group_mesh_mesh_intersects", ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.POINTER(HitOut)]),
+    ("tdb_group_table_eval", ct.c_int, [ct.c_void_p, ct.c_int, ct.c_void_p, ct.c_void_p, _D, _U8, _U64]),
+    ("tdb_group_last_stats", ct.c_int, [ct.c_void_p, ct.c_int, ct.POINTER(Stats)]),
 ]
 EXPORTS = [s[0] for s in _SIGS]
 
@@ -611,3 +621,97 @@ def literal_table_eval(op: int, literal, table: Table):
     _check(lib().tdb_literal_table_eval(op, kind, _dp(lit), table.handle, None, h.ctypes.data_as(_U8),
                                         face.ctypes.data_as(_U64)))
     return h.astype(bool), face
+
+
+# --------------------------------------------------------------------------
+# device group: one process, several GPUs (include/tindb_b200.h tdb_group_*)
+# --------------------------------------------------------------------------
+class _GroupGeom:
+    def __init__(self, group, handle, faces, objects):
+        self.group, self._h, self.faces, self.objects = group, ct.c_void_p(handle), faces, objects
+
+    @property
+    def handle(self):
+        return self._h
+
+    def free(self):
+        if self._h is not None and self._h.value:
+            lib().tdb_gmesh_free(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Group:
+    """Several devices driven from this process: replicated geometry, A rows
+    (or table objects) split over the members, one NCCL MIN all-reduce."""
+
+    def __init__(self, devices: Union[int, Sequence[int]]):
+        devs = list(range(devices)) if isinstance(devices, int) else list(devices)
+        arr = (ct.c_int * len(devs))(*devs)
+        h = ct.c_void_p()
+        _check(lib().tdb_group_create(len(devs), arr, ct.byref(h)))
+        self._h, self.devices = h, devs
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __len__(self):
+        return lib().tdb_group_size(self._h)
+
+    def mesh(self, triangles) -> _GroupGeom:
+        t = _f64(triangles)
+        h = ct.c_void_p()
+        _check(lib().tdb_group_mesh_upload(self._h, _dp(t), len(t), ct.byref(h)))
+        return _GroupGeom(self, h.value, len(t), 1)
+
+    def table(self, triangles, face_offsets) -> _GroupGeom:
+        t = _f64(triangles)
+        off = np.ascontiguousarray(face_offsets, dtype=np.uint64)
+        h = ct.c_void_p()
+        _check(lib().tdb_group_table_upload(self._h, _dp(t), off.ctypes.data_as(_U64), len(off) - 1, ct.byref(h)))
+        return _GroupGeom(self, h.value, len(t), len(off) - 1)
+
+    def mesh_mesh_distance(self, a: _GroupGeom, b: _GroupGeom) -> DistanceResult:
+        o = DistOut()
+        _check(lib().tdb_group_mesh_mesh_distance(self._h, a.handle, b.handle, ct.byref(o)))
+        return _dist_result(o)
+
+    def mesh_mesh_intersects(self, a: _GroupGeom, b: _GroupGeom) -> IntersectionResult:
+        o = HitOut()
+        _check(lib().tdb_group_mesh_mesh_intersects(self._h, a.handle, b.handle, ct.byref(o)))
+        return _hit_result(o)
+
+    def table_eval(self, op: int, records: _GroupGeom, literal: _GroupGeom):
+        k = records.objects
+        pair = np.empty(k, np.uint64)
+        if op == OP_DISTANCE:
+            d = np.empty(k, np.float64)
+            _check(lib().tdb_group_table_eval(self._h, op, records.handle, literal.handle, _dp(d), None,
+                                              pair.ctypes.data_as(_U64)))
+            return d, pair
+        h = np.empty(k, np.uint8)
+        _check(lib().tdb_group_table_eval(self._h, op, records.handle, literal.handle, None,
+                                          h.ctypes.data_as(_U8), pair.ctypes.data_as(_U64)))
+        return h.astype(bool), pair
+
+    def last_stats(self, member: int) -> dict:
+        st = Stats()
+        _check(lib().tdb_group_last_stats(self._h, member, ct.byref(st)))
+        return st.as_dict()
+
+    def free(self):
+        if self._h is not None and self._h.value:
+            lib().tdb_group_free(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass

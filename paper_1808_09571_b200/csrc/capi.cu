@@ -182,6 +182,10 @@ void upload(const double* tri9, uint64_t n, const uint64_t* off, uint64_t n_obj,
 
 }  // namespace
 
+cudaStream_t tdb::call_stream() { return ctx().stream; }
+
+int tdb::set_error(int rc, const std::string& msg) { return rc == TDB_OK ? (t_err.clear(), rc) : fail(rc, msg); }
+
 extern "C" {
 
 int tdb_init(int device) {

@@ -57,6 +57,10 @@ struct Geom {
 void geom_build(Geom* g, const double* tri9, uint64_t n, const uint64_t* host_off, uint64_t n_obj,
                 cudaStream_t st, bool tri9_on_device = false);
 void geom_release(Geom* g, cudaStream_t st);
+// capi.cu: the calling thread's launch stream (binding its device), and
+// "set tdb_last_error() and return rc" for code outside capi.cu (group.cu)
+cudaStream_t call_stream();
+int set_error(int rc, const std::string& msg);
 // Caller buffers <-> device (host_copy.cu): large pageable buffers go through
 // pinned staging, page-locked ones straight to the copy engine. h2d is
 // stream-ordered; the source must stay valid until the stream has passed the

@@ -67,6 +67,21 @@ int main() {
         if (h.hit) EXPECT(info.pair_index && *info.pair_index == hp);
     }
 
+    // the same through a device group (every device of the box)
+    {
+        K::b200::DeviceGroup g;
+        for (const TriangleMesh* b : {&far, &cross}) {
+            K::b200::MeshPairInfo i1, i2;
+            K::DistanceResult r1 = K::b200::mesh_mesh_distance(s, *b, cfg, &i1);
+            K::DistanceResult r2 = K::b200::mesh_mesh_distance(g, s, *b, &i2);
+            EXPECT(same_bits(r1.distance, r2.distance) && i1.pair_index == i2.pair_index);
+            EXPECT(same_bits(r1.closest_on_b.y, r2.closest_on_b.y));
+            K::IntersectionResult h1 = K::b200::mesh_mesh_intersects(s, *b, cfg, &i1);
+            K::IntersectionResult h2 = K::b200::mesh_mesh_intersects(g, s, *b, &i2);
+            EXPECT(h1.hit == h2.hit && i1.pair_index == i2.pair_index);
+        }
+    }
+
     // the missing batch.cpp:49/:62 branch
     EXPECT(!K::b200::eval_mesh_mesh(K::BatchOp::Distance, Geometry{LineSegment{{0, 0, 0}, {1, 1, 1}}},
                                     Geometry{s}, cfg));

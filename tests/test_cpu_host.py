@@ -79,6 +79,8 @@ def test_compute_fails_loudly_without_device():
         T.Mesh(a)
     with pytest.raises(T.TdbError):
         T.distance_host(a, a)
+    with pytest.raises(T.TdbError):
+        T.Group(1)  # no device: no NCCL group, no fallback
 
 
 def test_bad_arguments_rejected_before_device():
