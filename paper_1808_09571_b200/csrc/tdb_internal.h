@@ -52,7 +52,13 @@ constexpr int kObjStats = 8;
 // intersects plane cull margin:
 //   tau   = kCullDiag * diag(AABB(A obj u B)) + kCullAbs * max |coord|
 constexpr double kBandRel = 4e-6;
-constexpr double kBandEdge = 1e-7;
+// kBandEdge: the filter's first parameter s0 comes from rcp.approx (about
+// 2^-20 relative). Ericson's refinement (t for s0, then s for t) damps that by
+// cos^2(theta), but when two edges pass within d << |E| of each other the
+// distance error is first order: <= 0.38 * 1.2e-6 * |E| ~ 4.6e-7 |E| (4.0e-7
+// |E| seen in tests/test_gpu_bounds.py over 2M adversarial pairs). 4e-6 keeps
+// a ~9x margin; the band only widens by a few 1e-6 of an edge.
+constexpr double kBandEdge = 4e-6;
 constexpr double kBandAbs = 1e-12;
 constexpr double kCullDiag = 1e-10;
 constexpr double kCullAbs = 1e-13;

@@ -1,0 +1,152 @@
+"""The two engineering bounds of the fast paths, stressed at scale on the
+device (DESIGN.md section 7 names them as validated, not proven):
+
+* the distance filter's error |d~ - d| <= eta (+ the 2^-20 high-word
+  truncation), where d is the reference composition (tdb_pairs_distance,
+  bit-identical to the reference, tests/test_gpu_parity.py) — the invariant
+  the exact pass's band relies on (distance.cu, tdb_internal.h);
+* the intersects plane cull's margin tau: a table of one-face records
+  against a one-face literal runs the production hit_kernel (cull, then the
+  exact predicate for survivors); every boolean must equal the exact
+  predicate evaluated on every pair (tdb_pairs_intersects).
+
+Inputs are seeded adversarial families: near-parallel edge pairs at graded
+angles and separations, near-coplanar and grazing placements, slivers and
+needles (aspect ratios to 1e6), near-contact clusters, each under random
+rigid motions at scales 1e-3..1e3 and offsets up to 1e6.
+"""
+import numpy as np
+import pytest
+
+import paper_1808_09571_b200 as T
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def device():
+    T.init(0)
+    yield
+
+
+def _rots(rng, n):
+    q, r = np.linalg.qr(rng.normal(size=(n, 3, 3)))
+    return q * np.sign(np.diagonal(r, axis1=1, axis2=2))[:, None, :]
+
+
+def _place(tri, R, t, s):
+    v = tri.reshape(-1, 3, 3)
+    return (np.einsum("nij,nkj->nki", R, v) * s[:, None, None] + t[:, None, :]).reshape(-1, 9)
+
+
+def adversarial_pairs(seed, n):
+    rng = np.random.default_rng(seed)
+    k = n // 5
+    out_a, out_b = [], []
+    # 1. near-parallel edge pairs: a's edge v0v1 on the x axis, b's edge tilted by ang, lifted by sep
+    ang = 10.0 ** rng.uniform(-16, -1, k) * rng.choice([-1, 1], k)
+    sep = np.where(rng.random(k) < 0.2, 0.0, 10.0 ** rng.uniform(-14, 0, k))
+    x0 = rng.uniform(-0.5, 1.5, k)
+    a = np.tile([0, 0, 0, 1, 0, 0, 0.5, -1, -0.3], (k, 1)).astype(float)
+    a[:, 6:9] += rng.normal(scale=0.3, size=(k, 3))
+    b = np.stack([x0, sep, np.zeros(k), x0 + 1, sep + ang, np.zeros(k),
+                  x0 + rng.uniform(-1, 1, k), sep + rng.uniform(0.2, 1, k), rng.uniform(-0.5, 0.5, k)], 1)
+    out_a.append(a), out_b.append(b)
+    # 2. near-coplanar: b in a's plane up to a tilt, overlapping or grazing
+    a = rng.uniform(-1, 1, (k, 9))
+    a[:, 2::3] = 0.0
+    b = rng.uniform(-1, 1, (k, 9))
+    b[:, 2::3] = 10.0 ** rng.uniform(-15, -2, (k, 1)) * rng.normal(size=(k, 3))
+    out_a.append(a), out_b.append(b)
+    # 3. slivers and needles (aspect ratio up to 1e6) near a random triangle
+    a = rng.uniform(-1, 1, (k, 9))
+    p = rng.uniform(-1, 1, (k, 3))
+    d = rng.normal(size=(k, 3))
+    w = 10.0 ** rng.uniform(-6, 0, (k, 1)) * rng.normal(size=(k, 3))
+    b = np.concatenate([p, p + d, p + 0.5 * d + w], 1)
+    out_a.append(a), out_b.append(b)
+    # 4. vertex / edge contact: b's vertex placed at a point of a (edge or interior) plus a tiny offset
+    a = rng.uniform(-1, 1, (k, 9))
+    u, v = rng.random(k), rng.random(k)
+    on_edge = rng.random(k) < 0.5
+    v = np.where(on_edge, 0.0, v * (1 - u))
+    q = a[:, 0:3] + u[:, None] * (a[:, 3:6] - a[:, 0:3]) + v[:, None] * (a[:, 6:9] - a[:, 0:3])
+    q += 10.0 ** rng.uniform(-15, -3, (k, 1)) * rng.normal(size=(k, 3))
+    b = np.concatenate([q, q + rng.normal(size=(k, 3)), q + rng.normal(size=(k, 3))], 1)
+    out_a.append(a), out_b.append(b)
+    # 5. near-contact clusters of random triangles
+    m = n - 4 * k
+    a = rng.uniform(-1, 1, (m, 9))
+    b = rng.uniform(-1, 1, (m, 9)) * 0.3 + np.tile(a.reshape(m, 3, 3).mean(1) + rng.normal(scale=0.05, size=(m, 3)), 3)
+    out_a.append(a), out_b.append(b)
+    a, b = np.concatenate(out_a), np.concatenate(out_b)
+    # random rigid motion, scale, offset (shared by both triangles of a pair)
+    N = len(a)
+    R = _rots(rng, N)
+    s = 10.0 ** rng.integers(-3, 4, N).astype(float)
+    t = np.where(rng.random((N, 1)) < 0.3, rng.uniform(-1, 1, (N, 3)) * 1e6, rng.uniform(-3, 3, (N, 3)))
+    return _place(a, R, t, s), _place(b, R, t, s)
+
+
+@pytest.mark.parametrize("seed", [11, 12])
+def test_filter_error_within_eta_at_scale(seed):
+    a, b = adversarial_pairs(seed, 1_000_000)
+    ref = T.pairs_distance(a, b)
+    d2 = T.pairs_filter(a, b)
+    fin = np.isfinite(ref)
+    assert np.array_equal(np.isfinite(d2), fin)  # same degenerate skips
+    assert fin.mean() > 0.9
+    dt, r = np.sqrt(d2[fin]), ref[fin]
+    A, B = a[fin].reshape(-1, 3, 3), b[fin].reshape(-1, 3, 3)
+    edge = np.maximum(np.linalg.norm(A - np.roll(A, -1, 1), axis=2).max(1),
+                      np.linalg.norm(B - np.roll(B, -1, 1), axis=2).max(1))
+    scale = np.maximum(np.abs(A).max((1, 2)), np.abs(B).max((1, 2)))
+    eta = 4e-6 * edge + 1e-12 * scale        # tdb_internal.h kBandEdge, kBandAbs
+    tol = eta + 1e-6 * r                     # + the 2^-20 high-word truncation of d~^2
+    ratio = np.abs(dt - r) / tol
+    worst = int(np.argmax(ratio))
+    print(f"seed {seed}: {fin.sum()} pairs, max |d~-d|/tol = {ratio[worst]:.3g}")
+    assert ratio[worst] <= 1.0, (ratio[worst], A[worst].ravel(), B[worst].ravel(), r[worst], dt[worst])
+
+
+@pytest.mark.parametrize("seed", [21, 22])
+def test_intersects_cull_margin_at_scale(seed):
+    """hit_kernel (plane cull + exact survivors) == the exact predicate on
+    every pair: 400k one-face records around one literal face."""
+    rng = np.random.default_rng(seed)
+    lit = np.array([[0, 0, 0, 1, 0, 0, 0, 1, 0]], float)
+    n = 400_000
+    k = n // 4
+    # grazing: b crosses or just misses a's plane / edges by 10^-15..10^-3
+    g = 10.0 ** rng.uniform(-15, -3, (k, 1)) * rng.choice([-1, 1], (k, 1))
+    p = rng.uniform(-0.2, 1.2, (k, 3))
+    p[:, 2] = 0
+    b1 = np.concatenate([p + [0, 0, 1], p + g * [0, 0, 1] + rng.normal(scale=0.3, size=(k, 3)) * [1, 1, 0],
+                         p + [0.1, 0.2, 0] + g * [0, 0, 1]], 1)
+    # edge-on: b's edge runs through a's edges at tiny offsets
+    q = rng.uniform(-0.2, 1.2, (k, 3)) * [1, 1, 0]
+    e = 10.0 ** rng.uniform(-15, -3, (k, 1)) * rng.normal(size=(k, 3))
+    b2 = np.concatenate([q + e, q + [0, 0, 1] + e, q + rng.normal(size=(k, 3))], 1)
+    # near-coplanar overlaps
+    b3 = rng.uniform(-0.5, 1.5, (k, 9))
+    b3[:, 2::3] = 10.0 ** rng.uniform(-15, -6, (k, 1)) * rng.normal(size=(k, 3))
+    # vertex touches: one vertex of b on a (interior / edge) +- tiny
+    u, v = rng.random(n - 3 * k), rng.random(n - 3 * k)
+    v = v * (1 - u)
+    c = np.stack([u, v, 10.0 ** rng.uniform(-15, -3, len(u)) * rng.choice([-1, 1], len(u))], 1)
+    b4 = np.concatenate([c, c + rng.normal(size=c.shape) + [0, 0, 1], c + rng.normal(size=c.shape) + [0, 0, 1]], 1)
+    recs = np.concatenate([b1, b2, b3, b4])
+    # shared random rigid motion / scale / offset for literal and every record (the cull's tau
+    # scales with the object AABB and |coord|)
+    R = _rots(rng, 1)[0]
+    s = 10.0 ** rng.integers(-2, 3)
+    t = rng.uniform(-1, 1, 3) * (1e6 if seed % 2 else 3.0)
+    place = lambda m: ((m.reshape(-1, 3) @ R.T) * s + t).reshape(-1, 9)
+    lit_p, recs_p = place(lit), place(recs)
+    off = np.arange(n + 1, dtype=np.uint64)
+    hit, hp = T.table_eval(T.OP_INTERSECTS, T.Table(recs_p, off), T.Mesh(lit_p))
+    exact = T.pairs_intersects(recs_p, np.repeat(lit_p, n, 0))
+    print(f"seed {seed}: {n} pairs, {exact.sum()} hits")
+    assert 0 < exact.sum() < n
+    assert np.array_equal(hit, exact), np.flatnonzero(hit != exact)[:10]
+    assert (hp[hit] == 0).all() and (hp[~hit] == np.iinfo(np.uint64).max).all()
