@@ -150,3 +150,41 @@ def test_intersects_cull_margin_at_scale(seed):
     assert 0 < exact.sum() < n
     assert np.array_equal(hit, exact), np.flatnonzero(hit != exact)[:10]
     assert (hp[hit] == 0).all() and (hp[~hit] == np.iinfo(np.uint64).max).all()
+
+
+@pytest.mark.parametrize("seed", [31, 32])
+def test_segment_queries_near_edges_bit_exact(seed):
+    """distance_to_mesh for segments passing within 1e-14..1e-3 of a mesh
+    edge (shared by two faces: exact ties and near ties), through the fused
+    query kernel's candidate lists and band, against the pinned oracle."""
+    import os
+
+    import oracle as O
+    from conftest import bits
+
+    rng = np.random.default_rng(seed)
+    m = T.unit_sphere(2000)                                # 2,048 faces, shared edges
+    m = (m.reshape(-1, 3) * 10.0 ** rng.uniform(-2, 2) + rng.uniform(-1, 1, 3) * 1e4).reshape(-1, 9)
+    n = 100_000
+    tri = m[rng.integers(0, len(m), n)].reshape(-1, 3, 3)
+    j = rng.integers(0, 3, n)
+    e0 = tri[np.arange(n), j]
+    e1 = tri[np.arange(n), (j + 1) % 3]
+    L = np.linalg.norm(e1 - e0, axis=1, keepdims=True)
+    p = e0 + rng.uniform(-0.1, 1.1, (n, 1)) * (e1 - e0)
+    ed = (e1 - e0) / L
+    dirn = rng.normal(size=(n, 3))
+    dirn -= (dirn * ed).sum(1, keepdims=True) * ed * rng.uniform(0.0, 1.0, (n, 1))  # from crossing to near-parallel
+    dirn /= np.linalg.norm(dirn, axis=1, keepdims=True)
+    off = np.cross(ed, dirn)
+    off /= np.linalg.norm(off, axis=1, keepdims=True) + 1e-300
+    c = p + off * (10.0 ** rng.uniform(-14, -3, (n, 1))) * L * rng.choice([-1, 1], (n, 1))
+    h = rng.uniform(0.05, 1.0, (n, 1)) * L
+    segs = np.concatenate([c - h * dirn, c + h * dirn], 1)
+    dd, ff = T.segments_mesh_distance(segs, m)
+    rd, rf = O.segments_mesh_distance(segs, m, threads=os.cpu_count())
+    bad = np.flatnonzero((bits(dd) != bits(rd)) | (ff != rf))
+    assert len(bad) == 0, (len(bad), bad[:5], dd[bad[:5]], rd[bad[:5]], ff[bad[:5]], rf[bad[:5]])
+    hh, hf = T.segments_mesh_intersects(segs, m)
+    rh, rhf = O.segments_mesh_intersects(segs, m, threads=os.cpu_count())
+    assert np.array_equal(hh.astype(bool), rh.astype(bool)) and np.array_equal(hf, rhf)
