@@ -208,10 +208,16 @@ __device__ __forceinline__ exact::tri load_tri(const double* P, uint64_t pad, ui
 
 __global__ void __launch_bounds__(kTile) verify_kernel(VerifyArgs v) {
     const DistArgs& a = v.d;
-    const uint64_t units = *v.count * (uint64_t)v.nsplit;
+    // split each flagged item's B range into nsplit parts, more when few
+    // items are flagged so the grid stays busy (both passes see the same
+    // count, hence the same split)
+    const uint64_t count = *v.count;
+    if (count == 0) return;
+    const uint64_t nsplit = max((uint64_t)v.nsplit, min((uint64_t)a.chunk, (gridDim.x + count - 1) / count));
+    const uint64_t units = count * nsplit;
     for (uint64_t w = blockIdx.x; w < units; w += gridDim.x) {
-        const uint64_t item = v.list[w / v.nsplit];
-        const int part = (int)(w % v.nsplit);
+        const uint64_t item = v.list[w / nsplit];
+        const uint64_t part = w % nsplit;
         const uint64_t tl = item / a.n_chunks, ch = item - tl * a.n_chunks;
         const Tile T = a.tiles[a.tile0 + tl];
         const uint32_t r = min(threadIdx.x, T.count - 1);
@@ -221,8 +227,8 @@ __global__ void __launch_bounds__(kTile) verify_kernel(VerifyArgs v) {
         AFace A;
         load_aface(A, FaceRefLdg{a.Ap + row, a.An_pad});
         const uint64_t c0 = ch * a.chunk, c1 = min(a.Bn, c0 + a.chunk);
-        const uint64_t len = (c1 - c0 + v.nsplit - 1) / v.nsplit;
-        const uint64_t b0 = c0 + part * len, b1 = min(c1, b0 + len);
+        const uint64_t len = (c1 - c0 + nsplit - 1) / nsplit;
+        const uint64_t b0 = min(c1, c0 + part * len), b1 = min(c1, b0 + len);
         const uint64_t o = T.obj - a.obj0;
         const double b2 = v.band2[o];
         const uint64_t i_loc = row - T.obj_row0;
@@ -283,14 +289,37 @@ __global__ void check_kernel(CheckArgs a) {
     }
 }
 
+// The winner's witness points: exact::tri_tri with its six directed-edge
+// seg_tri calls on six lanes, then the same first-strict-minimum scan in the
+// same order (so the same candidate wins as in the sequential composition).
 __global__ void witness_kernel(const double* Ap, uint64_t An_pad, uint64_t obj_row0, const double* Bp,
                                uint64_t Bn_pad, uint64_t Bn, const unsigned long long* objP, double* out) {
+    __shared__ exact::res c[6];
     const unsigned long long p = *objP;
     if (p == kNone) return;
     const uint64_t i = obj_row0 + p / Bn, j = p % Bn;
-    const exact::res x = exact::tri_tri(load_tri(Ap, An_pad, i), load_tri(Bp, Bn_pad, j));
-    out[0] = x.a.x, out[1] = x.a.y, out[2] = x.a.z;
-    out[3] = x.b.x, out[4] = x.b.y, out[5] = x.b.z;
+    const exact::tri a = load_tri(Ap, An_pad, i), b = load_tri(Bp, Bn_pad, j);
+    const int k = threadIdx.x;
+    if (k < 6) {
+        const exact::tri& s = k < 3 ? a : b;
+        const exact::tri& o = k < 3 ? b : a;
+        const exact::v3 e0 = k % 3 == 0 ? s.v0 : k % 3 == 1 ? s.v1 : s.v2;
+        const exact::v3 e1 = k % 3 == 0 ? s.v1 : k % 3 == 1 ? s.v2 : s.v0;
+        c[k] = exact::seg_tri(e0, e1, o);
+    }
+    __syncthreads();
+    if (k != 0 || exact::degenerate(a) || exact::degenerate(b)) return;
+    exact::res best;
+    best.d = pos_inf();
+    best.a = best.b = exact::mk(0.0, 0.0, 0.0);
+    for (int q = 0; q < 6; ++q)
+        if (c[q].d < best.d) {
+            best.d = c[q].d;
+            best.a = q < 3 ? c[q].a : c[q].b;
+            best.b = q < 3 ? c[q].b : c[q].a;
+        }
+    out[0] = best.a.x, out[1] = best.a.y, out[2] = best.a.z;
+    out[3] = best.b.x, out[4] = best.b.y, out[5] = best.b.z;
 }
 
 // CULL: squared AABB distance between each item's A tile and B chunk (a lower
@@ -321,6 +350,8 @@ T* dalloc(size_t n, cudaStream_t st) {
     return p;
 }
 
+// Per-thread timing events (created once: cudaEventCreate per call costs
+// more than a small call's kernels).
 struct EventPair {
     cudaEvent_t e[4];
     EventPair() {
@@ -330,6 +361,39 @@ struct EventPair {
         for (auto& x : e) cudaEventDestroy(x);
     }
 };
+
+EventPair& thread_events() {
+    thread_local EventPair ev;
+    return ev;
+}
+
+// Device scratch of one call, one allocation. The result block (objD, objP,
+// the witness, the counters, the near-degenerate log) is contiguous so one
+// copy per round brings everything the host needs back.
+struct DistScratch {
+    unsigned long long* objD;  // result block begins here
+    unsigned long long* objP;
+    double* wit;
+    unsigned long long* ctr;   // flagged, candidates, retry, pairs evaluated
+    unsigned long long* near_count;
+    unsigned long long* near_entries;
+    size_t result_bytes;       // objD .. near_entries end
+    double* itemmin;
+    unsigned long long* objmin;
+    double* band2;
+    double* band;
+    unsigned long long* list;
+    void* base;
+};
+
+__global__ void dist_init_kernel(unsigned long long* objmin, uint64_t nobj, unsigned long long* ctr, double* wit,
+                                 unsigned long long* near_count) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nobj) objmin[i] = kNone;
+    if (i < 4) ctr[i] = 0;
+    if (i < 6) wit[i] = 0.0;
+    if (i == 0) *near_count = 0;
+}
 
 }  // namespace
 
@@ -352,26 +416,49 @@ void run_distance(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, u
     if (n_items == 0) return;
 
     const Geom& A = *sel.A;
-    double* itemmin = dalloc<double>(n_items, st);
-    unsigned long long* objmin = dalloc<unsigned long long>(nobj, st);
-    double* band2 = dalloc<double>(nobj, st);
-    double* band = dalloc<double>(nobj, st);
-    unsigned long long* objD = dalloc<unsigned long long>(nobj, st);
-    unsigned long long* objP = dalloc<unsigned long long>(nobj, st);
-    unsigned long long* list = dalloc<unsigned long long>(n_items, st);
-    unsigned long long* ctr = dalloc<unsigned long long>(4, st);  // flagged, cand, retry
-    double* Bstats = dalloc<double>(kObjStats, st);
-    double* wit = dalloc<double>(6, st);
-    CK(cudaMemsetAsync(objmin, 0xff, nobj * sizeof(unsigned long long), st));
-    CK(cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), st));
-    CK(cudaMemsetAsync(wit, 0, 6 * sizeof(double), st));
-    CK(cudaMemcpyAsync(Bstats, B.stats, kObjStats * sizeof(double), cudaMemcpyHostToDevice, st));
+    // ---- scratch layout (256-byte aligned pieces), one cudaMallocAsync
+    DistScratch sc{};
+    size_t off = 0;
+    auto piece = [&](size_t bytes) {
+        const size_t o = off;
+        off = (off + std::max<size_t>(bytes, 8) + 255) & ~size_t(255);
+        return o;
+    };
+    const size_t o_D = piece(nobj * 8), o_P = piece(nobj * 8), o_w = piece(6 * 8), o_c = piece(4 * 8),
+                 o_nc = piece(8), o_ne = piece(2 * kNearLogCap * 8);
+    const size_t result_end = off;
+    const size_t o_im = piece(n_items * 8), o_om = piece(nobj * 8), o_b2 = piece(nobj * 8), o_b = piece(nobj * 8),
+                 o_l = piece(n_items * 8);
+    char* base = dalloc<char>(off, st);
+    sc.base = base;
+    sc.objD = (unsigned long long*)(base + o_D);
+    sc.objP = (unsigned long long*)(base + o_P);
+    sc.wit = (double*)(base + o_w);
+    sc.ctr = (unsigned long long*)(base + o_c);
+    sc.near_count = (unsigned long long*)(base + o_nc);
+    sc.near_entries = (unsigned long long*)(base + o_ne);
+    sc.result_bytes = result_end;
+    sc.itemmin = (double*)(base + o_im);
+    sc.objmin = (unsigned long long*)(base + o_om);
+    sc.band2 = (double*)(base + o_b2);
+    sc.band = (double*)(base + o_b);
+    sc.list = (unsigned long long*)(base + o_l);
+    unsigned long long* const ctr = sc.ctr;
+    const NearLog nlog{sc.near_count, sc.near_entries};
+    // B's aggregate statistics: its one object's device header (a mesh), else a copy
+    double* Bstats = B.n_obj == 1 ? B.d_obj_stats : nullptr;
+    double* Bstats_copy = nullptr;
+    if (!Bstats) {
+        Bstats = Bstats_copy = dalloc<double>(kObjStats, st);
+        CK(cudaMemcpyAsync(Bstats, B.stats, kObjStats * sizeof(double), cudaMemcpyHostToDevice, st));
+    }
+    dist_init_kernel<<<(unsigned)((std::max<uint64_t>(nobj, 8) + 255) / 256), 256, 0, st>>>(sc.objmin, nobj, ctr,
+                                                                                           sc.wit, sc.near_count);
+    CK(cudaGetLastError());
 
-    EventPair ev;
-    NearDev near;
-    near.alloc(st);
+    EventPair& ev = thread_events();
     CK(cudaEventRecord(ev.e[0], st));
-    uint64_t launches = 0;
+    uint64_t launches = 1;
     unsigned long long *perm = nullptr, *lb2 = nullptr;
     void* cull_mem[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     if (cx.mode == TDB_MODE_CULL) {
@@ -394,59 +481,62 @@ void run_distance(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, u
         launches += 3;
     }
     DistArgs da{A.planes, A.n_pad, A.d_tiles, sel.tile0, sel.row_lo, sel.row_hi, B.planes, B.n_pad, B.n,
-                n_chunks, chunk, sel.obj0, itemmin, objmin, perm, lb2, ctr + 3};
+                n_chunks, chunk, sel.obj0, sc.itemmin, sc.objmin, perm, lb2, ctr + 3};
     filter_kernel<<<(unsigned)n_items, kTile, 0, st>>>(da);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ev.e[1], st));
     ++launches;
 
     const unsigned ob = (unsigned)((nobj + 255) / 256);
-    band_kernel<<<ob, 256, 0, st>>>(BandArgs{objmin, A.d_obj_stats, Bstats, sel.obj0, nobj, band2, band, objD, objP});
+    band_kernel<<<ob, 256, 0, st>>>(BandArgs{sc.objmin, A.d_obj_stats, Bstats, sel.obj0, nobj, sc.band2, sc.band,
+                                             sc.objD, sc.objP});
     CK(cudaGetLastError());
     ++launches;
 
     const int nsplit = 16;
     const unsigned vgrid = (unsigned)(cx.sms * 8);
+    const bool want_witness = witness6 && nobj == 1;
+    // host copy of the result block (pinned per thread, grown on demand)
+    thread_local std::vector<unsigned long long> hres;
+    hres.resize(sc.result_bytes / 8);
+    unsigned long long* h_ctr = hres.data() + o_c / 8;
     int rounds = 0;
-    unsigned long long h_ctr[4] = {0, 0, 0, 0};
     unsigned long long flagged_total = 0;
     for (;;) {
         ++rounds;
         CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));          // flagged count
         CK(cudaMemsetAsync(ctr + 2, 0, sizeof(unsigned long long), st));      // retry count
         flag_kernel<<<(unsigned)((n_items + 255) / 256), 256, 0, st>>>(
-            FlagArgs{A.d_tiles, sel.tile0, n_chunks, n_items, sel.obj0, itemmin, band2, list, ctr});
+            FlagArgs{A.d_tiles, sel.tile0, n_chunks, n_items, sel.obj0, sc.itemmin, sc.band2, sc.list, ctr});
         CK(cudaGetLastError());
         for (int pass = 1; pass <= 2; ++pass) {
             verify_kernel<<<vgrid, kTile, 0, st>>>(
-                VerifyArgs{da, list, ctr, nsplit, pass, band2, objD, objP, ctr + 1, near.log});
+                VerifyArgs{da, sc.list, ctr, nsplit, pass, sc.band2, sc.objD, sc.objP, ctr + 1, nlog});
             CK(cudaGetLastError());
         }
-        check_kernel<<<ob, 256, 0, st>>>(CheckArgs{nobj, sel.obj0, A.d_obj_stats, Bstats, band2, band, objD, objP, ctr + 2});
+        check_kernel<<<ob, 256, 0, st>>>(CheckArgs{nobj, sel.obj0, A.d_obj_stats, Bstats, sc.band2, sc.band,
+                                                   sc.objD, sc.objP, ctr + 2});
         CK(cudaGetLastError());
         launches += 4;
-        CK(cudaMemcpyAsync(h_ctr, ctr, sizeof h_ctr, cudaMemcpyDeviceToHost, st));
+        if (want_witness) {  // for this round's winner; recomputed if the band widens
+            const Tile& t0 = A.h_tiles[sel.tile0];
+            witness_kernel<<<1, 32, 0, st>>>(A.planes, A.n_pad, t0.obj_row0, B.planes, B.n_pad, B.n, sc.objP,
+                                             sc.wit);
+            CK(cudaGetLastError());
+            ++launches;
+        }
+        CK(cudaMemcpyAsync(hres.data(), base, sc.result_bytes, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         flagged_total += h_ctr[0];
         if (h_ctr[2] == 0 || rounds >= 8) break;
     }
     CK(cudaEventRecord(ev.e[2], st));
-    if (witness6 && nobj == 1) {
-        const Tile& t0 = A.h_tiles[sel.tile0];
-        witness_kernel<<<1, 1, 0, st>>>(A.planes, A.n_pad, t0.obj_row0, B.planes, B.n_pad, B.n, objP, wit);
-        CK(cudaGetLastError());
-        ++launches;
-    }
-    std::vector<unsigned long long> hD(nobj), hP(nobj);
-    CK(cudaMemcpyAsync(hD.data(), objD, nobj * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(hP.data(), objP, nobj * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    if (witness6) CK(cudaMemcpyAsync(witness6, wit, 6 * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaEventRecord(ev.e[3], st));
-    for (void* p : {(void*)itemmin, (void*)objmin, (void*)band2, (void*)band, (void*)objD, (void*)objP,
-                    (void*)list, (void*)ctr, (void*)Bstats, (void*)wit, (void*)perm, (void*)lb2, cull_mem[0],
-                    cull_mem[1], cull_mem[2], cull_mem[3]})
+    CK(cudaFreeAsync(base, st));
+    for (void* p : {(void*)Bstats_copy, (void*)perm, (void*)lb2, cull_mem[0], cull_mem[1], cull_mem[2], cull_mem[3]})
         if (p) CK(cudaFreeAsync(p, st));
-    CK(cudaStreamSynchronize(st));
+    const unsigned long long* hD = hres.data() + o_D / 8;
+    const unsigned long long* hP = hres.data() + o_P / 8;
     for (uint64_t o = 0; o < nobj; ++o) {
         if (hP[o] != kNone) {
             double d;
@@ -455,6 +545,8 @@ void run_distance(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, u
             pair[o] = hP[o];
         }
     }
+    if (want_witness) std::memcpy(witness6, hres.data() + o_w / 8, 6 * sizeof(double));
+    CK(cudaEventSynchronize(ev.e[3]));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, ev.e[0], ev.e[1]));
     S.ms_filter = ms;
@@ -475,8 +567,11 @@ void run_distance(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, u
     S.kernels = launches;
     S.pairs_evaluated = h_ctr[3];
     S.rounds = rounds;
-    near.fetch(st, cx.near);
-    S.near_degenerate = cx.near->count;
+    // near-degenerate log: came back with the result block
+    const unsigned long long nc = hres[o_nc / 8];
+    cx.near->count = nc;
+    cx.near->entries.assign(hres.data() + o_ne / 8, hres.data() + o_ne / 8 + 2 * std::min<uint64_t>(nc, kNearLogCap));
+    S.near_degenerate = nc;
 }
 
 }  // namespace tdb

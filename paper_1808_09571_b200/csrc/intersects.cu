@@ -245,7 +245,7 @@ void run_intersects(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit,
     const uint64_t nobj = sel.obj1 - sel.obj0;
     const uint64_t ntiles = sel.tile1 - sel.tile0;
     const uint64_t groups = (ntiles + kWarps - 1) / kWarps;
-    const uint64_t chunk = pick_chunk(groups, B.n, cx.sms, 12);
+    const uint64_t chunk = pick_chunk(groups, B.n, cx.sms, 12, 256);
     const uint64_t n_chunks = (B.n + chunk - 1) / chunk;
     const uint64_t n_items = groups * n_chunks;
     tdb_stats& S = *cx.stats;

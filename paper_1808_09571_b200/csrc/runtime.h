@@ -137,10 +137,13 @@ struct ASel {
 // CTA units against nB faces: kChunk, halved (down to 256, a multiple of the
 // TMA sub-tiles) until there are >= `waves` CTAs per SM, so small problems
 // still fill all SMs.
-inline uint64_t pick_chunk(uint64_t a_units, uint64_t nB, int sms, int waves) {
+// B-chunk length: halve from kChunk (down to `floor`, the kernel's staged
+// sub-tile) until a launch has `waves` CTAs per SM, so small problems still
+// spread over every SM (latency of small calls, the serving path).
+inline uint64_t pick_chunk(uint64_t a_units, uint64_t nB, int sms, int waves, uint64_t floor = kSB) {
     uint64_t chunk = kChunk;
     const uint64_t target = (uint64_t)sms * (uint64_t)waves;
-    while (chunk > 256 && a_units * ((nB + chunk - 1) / chunk) < target) chunk >>= 1;
+    while (chunk > floor && a_units * ((nB + chunk - 1) / chunk) < target) chunk >>= 1;
     return chunk;
 }
 
