@@ -397,8 +397,56 @@ __global__ void dist_init_kernel(unsigned long long* objmin, uint64_t nobj, unsi
 
 }  // namespace
 
+namespace {
+void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, uint64_t* pair,
+                        double* witness6);
+}  // namespace
+
 void run_distance(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, uint64_t* pair,
                   double* witness6) {
+    const uint64_t ntiles = sel.tile1 - sel.tile0;
+    const uint64_t chunk = pick_chunk(ntiles, B.n, cx.sms, 12);
+    const uint64_t n_chunks = (B.n + chunk - 1) / chunk;
+    if (ntiles * n_chunks <= max_items() || ntiles <= 1) return run_distance_batch(cx, sel, B, dist, pair, witness6);
+    // too many items for one launch: tile batches, merged per object
+    const uint64_t nobj = sel.obj1 - sel.obj0;
+    for (uint64_t o = 0; o < nobj; ++o) dist[o] = pos_inf_h(), pair[o] = kNone;
+    if (witness6) std::fill(witness6, witness6 + 6, 0.0);
+    tdb_stats tot{};
+    NearHost near_all;
+    const uint64_t per = std::max<uint64_t>(1, max_items() / n_chunks);
+    for (const ASel& b : tile_batches(sel, per)) {
+        const uint64_t k = b.obj1 - b.obj0;
+        std::vector<double> d(k), w6(6);
+        std::vector<uint64_t> p(k);
+        run_distance_batch(cx, b, B, d.data(), p.data(), witness6 ? w6.data() : nullptr);
+        for (uint64_t o = 0; o < k; ++o) {
+            const uint64_t g = b.obj0 - sel.obj0 + o;
+            if (p[o] != kNone && (d[o] < dist[g] || (d[o] == dist[g] && p[o] < pair[g]))) {
+                dist[g] = d[o];
+                pair[g] = p[o];
+                if (witness6 && nobj == 1) std::copy(w6.begin(), w6.end(), witness6);
+            }
+        }
+        const tdb_stats& s = *cx.stats;
+        tot.ms_total += s.ms_total, tot.ms_filter += s.ms_filter, tot.ms_verify += s.ms_verify;
+        tot.pairs += s.pairs, tot.items += s.items, tot.items_flagged += s.items_flagged;
+        tot.candidates += s.candidates, tot.kernels += s.kernels, tot.pairs_evaluated += s.pairs_evaluated;
+        tot.near_degenerate += s.near_degenerate;
+        tot.rounds = std::max(tot.rounds, s.rounds);
+        near_all.count += cx.near->count;
+        for (size_t e = 0; e < cx.near->entries.size() && near_all.entries.size() < 2 * kNearLogCap; e += 2) {
+            near_all.entries.push_back(cx.near->entries[e]);
+            near_all.entries.push_back(cx.near->entries[e + 1]);
+        }
+    }
+    *cx.stats = tot;
+    *cx.near = near_all;
+}
+
+namespace {
+void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, uint64_t* pair,
+                        double* witness6) {
     const cudaStream_t st = cx.stream;
     const uint64_t nobj = sel.obj1 - sel.obj0;
     const uint64_t ntiles = sel.tile1 - sel.tile0;
@@ -573,5 +621,7 @@ void run_distance(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, u
     cx.near->entries.assign(hres.data() + o_ne / 8, hres.data() + o_ne / 8 + 2 * std::min<uint64_t>(nc, kNearLogCap));
     S.near_degenerate = nc;
 }
+
+}  // namespace
 
 }  // namespace tdb

@@ -240,7 +240,56 @@ __global__ void __launch_bounds__(32 * kWarps) hit_kernel(HitArgs a) {
 
 }  // namespace
 
+namespace {
+void run_intersects_batch(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit, uint64_t* pair);
+}  // namespace
+
 void run_intersects(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit, uint64_t* pair) {
+    const uint64_t ntiles = sel.tile1 - sel.tile0;
+    const uint64_t groups = (ntiles + kWarps - 1) / kWarps;
+    const uint64_t chunk = pick_chunk(groups, B.n, cx.sms, 12, 256);
+    const uint64_t n_chunks = (B.n + chunk - 1) / chunk;
+    if (groups * n_chunks <= max_items() || groups <= 1) return run_intersects_batch(cx, sel, B, hit, pair);
+    // too many items for one launch: tile batches in row order, lowest hit per object
+    const uint64_t nobj = sel.obj1 - sel.obj0;
+    for (uint64_t o = 0; o < nobj; ++o) {
+        if (hit) hit[o] = 0;
+        pair[o] = kNone;
+    }
+    tdb_stats tot{};
+    NearHost near_all;
+    const uint64_t per = std::max<uint64_t>(1, max_items() / n_chunks) * kWarps;
+    for (const ASel& b : tile_batches(sel, per)) {
+        if (nobj == 1 && pair[0] != kNone) break;  // a later batch only holds higher pairs
+        const uint64_t k = b.obj1 - b.obj0;
+        std::vector<uint8_t> h(k);
+        std::vector<uint64_t> p(k);
+        run_intersects_batch(cx, b, B, h.data(), p.data());
+        for (uint64_t o = 0; o < k; ++o) {
+            const uint64_t g = b.obj0 - sel.obj0 + o;
+            if (h[o] && p[o] < pair[g]) {
+                pair[g] = p[o];
+                if (hit) hit[g] = 1;
+            }
+        }
+        const tdb_stats& s = *cx.stats;
+        tot.ms_total += s.ms_total, tot.ms_filter += s.ms_filter, tot.ms_verify += s.ms_verify;
+        tot.pairs += s.pairs, tot.items += s.items, tot.items_flagged += s.items_flagged;
+        tot.candidates += s.candidates, tot.exact_pairs += s.exact_pairs, tot.kernels += s.kernels;
+        tot.pairs_evaluated += s.pairs_evaluated, tot.near_degenerate += s.near_degenerate;
+        tot.rounds = std::max(tot.rounds, s.rounds);
+        near_all.count += cx.near->count;
+        for (size_t e = 0; e < cx.near->entries.size() && near_all.entries.size() < 2 * kNearLogCap; e += 2) {
+            near_all.entries.push_back(cx.near->entries[e]);
+            near_all.entries.push_back(cx.near->entries[e + 1]);
+        }
+    }
+    *cx.stats = tot;
+    *cx.near = near_all;
+}
+
+namespace {
+void run_intersects_batch(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit, uint64_t* pair) {
     const cudaStream_t st = cx.stream;
     const uint64_t nobj = sel.obj1 - sel.obj0;
     const uint64_t ntiles = sel.tile1 - sel.tile0;
@@ -255,7 +304,6 @@ void run_intersects(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit,
         pair[o] = kNone;
     }
     if (nobj == 0 || n_items == 0) return;
-    if (n_items > 0x7fffffffull) throw std::invalid_argument("intersects: too many work items for one launch");
     const Geom& A = *sel.A;
     unsigned long long *objhit = nullptr, *nex = nullptr;
     double* Bstats = nullptr;
@@ -321,5 +369,7 @@ void run_intersects(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit,
     near.fetch(st, cx.near);
     S.near_degenerate = cx.near->count;
 }
+
+}  // namespace
 
 }  // namespace tdb

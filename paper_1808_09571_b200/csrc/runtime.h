@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <limits>
 #include <stdexcept>
@@ -133,10 +134,6 @@ struct ASel {
     uint64_t tile0, tile1, row_lo, row_hi, obj0, obj1;
 };
 
-// B-chunk length (faces per work item) for a launch of `a_units` A-side
-// CTA units against nB faces: kChunk, halved (down to 256, a multiple of the
-// TMA sub-tiles) until there are >= `waves` CTAs per SM, so small problems
-// still fill all SMs.
 // B-chunk length: halve from kChunk (down to `floor`, the kernel's staged
 // sub-tile) until a launch has `waves` CTAs per SM, so small problems still
 // spread over every SM (latency of small calls, the serving path).
@@ -145,6 +142,35 @@ inline uint64_t pick_chunk(uint64_t a_units, uint64_t nB, int sms, int waves, ui
     const uint64_t target = (uint64_t)sms * (uint64_t)waves;
     while (chunk > floor && a_units * ((nB + chunk - 1) / chunk) < target) chunk >>= 1;
     return chunk;
+}
+
+// Work items (A tile x B chunk) one launch may carry: the per-item arrays
+// cost 16 B each (2^27 items = 2 GB), and grids stay below 2^31 blocks.
+// Larger selections run as consecutive tile batches whose per-object answers
+// are merged (lexicographic (distance, pair); lowest hit pair). The
+// TDB_MAX_ITEMS environment variable lowers the cap (tests).
+inline uint64_t max_items() {
+    static const uint64_t cap = [] {
+        const char* e = getenv("TDB_MAX_ITEMS");
+        const unsigned long long v = e ? strtoull(e, nullptr, 10) : 0;
+        return v ? (uint64_t)v : (uint64_t)1 << 27;
+    }();
+    return cap;
+}
+
+// The selection split into batches of at most max_tiles A tiles (objects may
+// straddle two batches; obj0/obj1 narrowed to each batch's tiles).
+inline std::vector<ASel> tile_batches(const ASel& sel, uint64_t max_tiles) {
+    std::vector<ASel> out;
+    for (uint64_t t = sel.tile0; t < sel.tile1; t += max_tiles) {
+        ASel b = sel;
+        b.tile0 = t;
+        b.tile1 = std::min(sel.tile1, t + max_tiles);
+        b.obj0 = sel.A->h_tiles[b.tile0].obj;
+        b.obj1 = (uint64_t)sel.A->h_tiles[b.tile1 - 1].obj + 1;
+        out.push_back(b);
+    }
+    return out;
 }
 
 // Distance over an A selection against mesh B. Outputs per object (host):

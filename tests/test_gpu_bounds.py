@@ -188,3 +188,51 @@ def test_segment_queries_near_edges_bit_exact(seed):
     hh, hf = T.segments_mesh_intersects(segs, m)
     rh, rhf = O.segments_mesh_intersects(segs, m, threads=os.cpu_count())
     assert np.array_equal(hh.astype(bool), rh.astype(bool)) and np.array_equal(hf, rhf)
+
+
+_BATCH_SCRIPT = r"""
+import sys
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + '/tests')
+import numpy as np
+import oracle as O
+import paper_1808_09571_b200 as T
+from conftest import bits, GOLDEN
+T.init(0)
+z = np.load(GOLDEN + '/meshes.npz'); cases = {}
+for k in z.files:
+    name, f = k.split('/'); cases.setdefault(name, {})[f] = z[k]
+for name, c in cases.items():
+    r = T.mesh_mesh_distance(c['a'], c['b'])
+    assert bits(r.distance) == bits(c['dist']), name
+    assert (r.pair_index if r.pair_index is not None else O.U64_MAX) == int(c['pair']), name
+    if r.pair_index is not None:
+        assert np.array_equal(bits(np.array(r.closest_on_b)), bits(c['on_b'])), name
+    h = T.mesh_mesh_intersects(c['a'], c['b'])
+    assert h.hit == bool(c['hit']) and (h.pair_index if h.hit else O.U64_MAX) == int(c['hit_pair']), name
+t = dict(np.load(GOLDEN + '/table.npz'))
+tab, q = T.Table(t['table'], t['offsets']), T.Mesh(t['query'])
+d, dp = T.table_eval(T.OP_DISTANCE, tab, q)
+assert np.array_equal(bits(d), bits(t['dist'])) and np.array_equal(dp, t['dist_pair'])
+hh, hp = T.table_eval(T.OP_INTERSECTS, tab, q)
+assert np.array_equal(hh, t['hit'].astype(bool)) and np.array_equal(hp, t['hit_pair'])
+s = T.unit_sphere(10_000)
+r = T.mesh_mesh_distance(np.concatenate([T.translate(s, 0, 0, 9.0), s]), T.translate(s, 2.5, 0, 0))
+assert r.distance == 0.5 and r.pair_index == O.mesh_mesh_distance(np.concatenate([T.translate(s, 0, 0, 9.0), s]), T.translate(s, 2.5, 0, 0))[1]
+assert T.last_stats()['kernels'] > 20  # really split into batches
+print('BATCHES OK')
+"""
+
+
+def test_item_cap_splits_into_batches_bit_exact():
+    """With the per-launch item cap forced down (TDB_MAX_ITEMS), every call
+    runs as several tile batches; merged answers must equal the golden ones."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    env = dict(os.environ, TDB_MAX_ITEMS="7")
+    out = subprocess.run([sys.executable, "-c", _BATCH_SCRIPT, ROOT], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert "BATCHES OK" in out.stdout, out.stdout + out.stderr
