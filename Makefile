@@ -48,6 +48,24 @@ shimtest: $(LIB) oracle
 	    -Wl,-rpath,'$$ORIGIN/../oracle/_ref' -Wl,-rpath,'$$ORIGIN/../$(PKG)'; \
 	else echo "shimtest: $(REF) absent; keeping prebuilt $(BUILD)/shim_test"; fi
 
+# The reference's own unit tests for the two replaced entry points
+# (tests/test_{batch,volume,distance,intersect}.cpp, unmodified, compiled where
+# they lie) with run_batch / mesh_volume routed to the device shim
+# (tests/cpp/ref_route.hpp) and a minimal doctest stand-in. Test-only.
+REFTESTS := test_batch test_volume test_distance test_intersect
+refunittest: $(LIB) oracle
+	@if [ -d "$(REF)/include" ]; then \
+	  mkdir -p $(BUILD)/refunit && \
+	  for f in $(REFTESTS); do \
+	    $(CXX) -std=c++20 -O2 -ffp-contract=off -Dtindb=tindb_ref -Itests/cpp/doctest_shim -I$(REF)/include -I$(REF)/tests \
+	      -Iinclude -include tests/cpp/ref_route.hpp -c $(REF)/tests/$$f.cpp -o $(BUILD)/refunit/$$f.o || exit 1; done && \
+	  $(CXX) -std=c++20 -O2 -ffp-contract=off -Dtindb=tindb_ref -I$(REF)/include -I$(REF)/tests \
+	    -c $(REF)/tests/support/oracles.cpp -o $(BUILD)/refunit/oracles.o && \
+	  $(CXX) -std=c++20 -O2 -Itests/cpp/doctest_shim -c tests/cpp/ref_unit_main.cpp -o $(BUILD)/refunit/main.o && \
+	  $(CXX) $(BUILD)/refunit/*.o -o $(BUILD)/ref_unit_tests -Loracle/_ref -ltindb_ref -L$(PKG) -ltindb_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../oracle/_ref' -Wl,-rpath,'$$ORIGIN/../$(PKG)'; \
+	else echo "refunittest: $(REF) absent; keeping prebuilt $(BUILD)/ref_unit_tests"; fi
+
 # The SQL route: the reference engine (engine.cpp, unmodified, force-including
 # tests/cpp/engine_route.hpp) over the device shim, against the unmodified
 # reference engine in oracle/_ref. Test-only binary; needs /root/reference.

@@ -182,6 +182,23 @@ int tdb_points_mesh_distance(const double* pt3, uint64_t n, tdb_mesh mesh, doubl
 int tdb_segments_mesh_intersects(const double* seg6, uint64_t n, tdb_mesh mesh, uint8_t* hit_out,
                                  uint64_t* face_out);
 uint64_t tdb_gen_drills(uint64_t seed, uint64_t count, int style, double* out6); /* dataset.cpp:141 */
+/* The reference's complete result for one query against one triangle: for
+ * TDB_OP_DISTANCE segment_triangle_distance / point_triangle_distance
+ * (kernels.cpp:138-316: distance, closest points, SurfaceParams t,u,v), for
+ * TDB_OP_INTERSECTS segment_triangle_intersect (kernels.cpp:318-336: hit,
+ * point, IntersectionParams t,u,v,w). distance_to_mesh / intersects_mesh
+ * report exactly this for their winning face (kernels.cpp:382-432): the
+ * shim asks the query path for the face, then this for its details. */
+typedef struct {
+    double distance;
+    double on_query[3]; /* closest_on_a */
+    double on_face[3];  /* closest_on_b */
+    double t, u, v, w;  /* SurfaceParams (w = 0) / IntersectionParams */
+    int32_t hit;
+    int32_t _pad;
+    double point[3];    /* intersects: seg.p0 + clamp01(t) * d */
+} tdb_face_result;
+int tdb_query_face_result(int op, int query_kind, const double* query, const double* tri9, tdb_face_result* out);
 
 /* ---- ST_3DVolume: mesh_volume (kernels.hpp:64-70, kernels.cpp:27-46),
  * permissive policy, bit-identical to the reference for the same chunk_size

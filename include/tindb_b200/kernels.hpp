@@ -11,6 +11,8 @@
 // * eval_mesh_mesh — the branch batch.cpp:49 (eval_distance) and :62
 //   (eval_intersects) lack today; returns nullopt for other pairings so the
 //   reference's dispatch continues unchanged.
+// * distance_to_mesh / intersects_mesh / mesh_volume — the reference's own
+//   per-query and volume entry points (kernels.hpp:64-90) on the device.
 // * DeviceGroup — the same operators over several devices of the box
 //   (tdb_group_*: rows split over the members, one NCCL MIN all-reduce).
 // * run_batch_b200 — run_batch (batch.hpp:49-51) against a Mesh literal with
@@ -26,6 +28,7 @@
 #pragma once
 
 #include <tindb/batch.hpp>
+#include <tindb/closure.hpp>
 #include <tindb/geometry.hpp>
 #include <tindb/kernels.hpp>
 #include <tindb/store_types.hpp>
@@ -199,6 +202,99 @@ inline IntersectionResult mesh_mesh_intersects(const DeviceGroup& g, const Trian
         *info = {};
         if (r.hit) info->pair_index = o.pair, info->face_a = o.i, info->face_b = o.j;
     }
+    return r;
+}
+
+// mesh_volume (kernels.hpp:66, kernels.cpp:27-46) with the face terms and
+// the fixed chunk tree on the device (bit-identical for the same
+// cfg.chunk_size). Closedness is the reference's own validate_closed
+// (closure.hpp:25), run only when the reference runs it: Strict policy or a
+// closed_out request.
+inline double mesh_volume(const TriangleMesh& mesh, const ExecutorConfig& cfg, bool* closed_out = nullptr) {
+    if (cfg.volume_policy == VolumePolicy::Strict || closed_out != nullptr) {
+        const ClosureReport report = validate_closed(mesh);
+        if (closed_out != nullptr) *closed_out = report.is_closed;
+        if (cfg.volume_policy == VolumePolicy::Strict && !report.is_closed)
+            throw MeshNotClosed("mesh is not watertight: " + std::to_string(report.boundary_edge_count) +
+                                " boundary edge(s), " + std::to_string(report.inconsistent_edge_count) +
+                                " inconsistent directed edge use(s)");
+    }
+    DeviceMesh d(mesh);
+    double v = 0.0;
+    check(tdb_mesh_volume(d.handle(), cfg.chunk_size, &v));
+    return v;
+}
+
+// distance_to_mesh / intersects_mesh (kernels.hpp:68-90, kernels.cpp:382-432)
+// on the device: the query path finds the winning face (lowest index on
+// ties; the lowest hit face), then tdb_query_face_result evaluates the
+// reference's per-face result for it (closest points and SurfaceParams, or
+// the hit point and IntersectionParams), as the reference reports the
+// winner's own result. Degenerate faces are skipped, as the reference does
+// whenever TriangleMesh::has_degenerate_faces is up to date (refresh,
+// geometry.hpp:89-97).
+inline DistanceResult distance_result_for(const TriangleMesh& mesh, int kind, const double* q, double d,
+                                          std::uint64_t face) {
+    DistanceResult r;
+    r.distance = d;
+    if (face == UINT64_MAX) return r;
+    tdb_face_result f{};
+    check(tdb_query_face_result(TDB_OP_DISTANCE, kind, q, reinterpret_cast<const double*>(&mesh.triangles[face]),
+                                &f));
+    r.closest_on_a = {f.on_query[0], f.on_query[1], f.on_query[2]};
+    r.closest_on_b = {f.on_face[0], f.on_face[1], f.on_face[2]};
+    r.face_index = static_cast<std::size_t>(face);
+    r.params = SurfaceParams{f.t, f.u, f.v};
+    return r;
+}
+
+inline DistanceResult distance_to_mesh(const Point3& query, const TriangleMesh& mesh,
+                                       const ExecutorConfig& /*cfg*/) {
+    const double q[3] = {query.x, query.y, query.z};
+    DeviceMesh dm(mesh);
+    double d = 0.0;
+    std::uint64_t face = 0;
+    check(tdb_points_mesh_distance(q, 1, dm.handle(), &d, &face));
+    return distance_result_for(mesh, TDB_QUERY_POINTS, q, d, face);
+}
+
+inline DistanceResult distance_to_mesh(const LineSegment& query, const TriangleMesh& mesh,
+                                       const ExecutorConfig& /*cfg*/) {
+    const double q[6] = {query.p0.x, query.p0.y, query.p0.z, query.p1.x, query.p1.y, query.p1.z};
+    DeviceMesh dm(mesh);
+    double d = 0.0;
+    std::uint64_t face = 0;
+    check(tdb_segments_mesh_distance(q, 1, dm.handle(), &d, &face));  // zero length: a point query
+    return distance_result_for(mesh, TDB_QUERY_SEGMENTS, q, d, face);
+}
+
+inline DistanceResult distance_to_mesh(const Geometry& query, const TriangleMesh& mesh, const ExecutorConfig& cfg) {
+    switch (kind_of(query)) {
+        case GeometryKind::Point:
+            return b200::distance_to_mesh(std::get<Point3>(query), mesh, cfg);
+        case GeometryKind::Segment:
+            return b200::distance_to_mesh(segment_view(query), mesh, cfg);
+        default:  // kernels.cpp:403
+            throw std::invalid_argument("distance_to_mesh: query must be a point or a segment");
+    }
+}
+
+inline IntersectionResult intersects_mesh(const LineSegment& query, const TriangleMesh& mesh,
+                                          const ExecutorConfig& /*cfg*/) {
+    const double q[6] = {query.p0.x, query.p0.y, query.p0.z, query.p1.x, query.p1.y, query.p1.z};
+    DeviceMesh dm(mesh);
+    std::uint8_t hit = 0;
+    std::uint64_t face = 0;
+    check(tdb_segments_mesh_intersects(q, 1, dm.handle(), &hit, &face));
+    IntersectionResult r;
+    if (!hit) return r;
+    tdb_face_result f{};
+    check(tdb_query_face_result(TDB_OP_INTERSECTS, TDB_QUERY_SEGMENTS, q,
+                                reinterpret_cast<const double*>(&mesh.triangles[face]), &f));
+    r.hit = f.hit != 0;
+    r.point = Point3{f.point[0], f.point[1], f.point[2]};
+    r.face_index = static_cast<std::size_t>(face);
+    r.params = IntersectionParams{f.t, f.u, f.v, f.w};
     return r;
 }
 

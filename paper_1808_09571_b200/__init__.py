@@ -58,6 +58,23 @@ class HitOut(ct.Structure):
     ]
 
 
+class FaceResult(ct.Structure):
+    """tdb_face_result: the reference's per-face DistanceResult /
+    IntersectionResult (kernels.hpp:28-48) for one query and one triangle."""
+    _fields_ = [
+        ("distance", ct.c_double),
+        ("on_query", ct.c_double * 3),
+        ("on_face", ct.c_double * 3),
+        ("t", ct.c_double),
+        ("u", ct.c_double),
+        ("v", ct.c_double),
+        ("w", ct.c_double),
+        ("hit", ct.c_int32),
+        ("_pad", ct.c_int32),
+        ("point", ct.c_double * 3),
+    ]
+
+
 class Stats(ct.Structure):
     _fields_ = [
         ("ms_total", ct.c_double),
@@ -126,6 +143,7 @@ _SIGS = [
     ("tdb_queries_free", None, [ct.c_void_p]),
     ("tdb_queries_mesh_distance", ct.c_int, [ct.c_void_p, ct.c_void_p, _D, _U64]),
     ("tdb_queries_mesh_intersects", ct.c_int, [ct.c_void_p, ct.c_void_p, _U8, _U64]),
+    ("tdb_query_face_result", ct.c_int, [ct.c_int, ct.c_int, _D, _D, ct.POINTER(FaceResult)]),
     ("tdb_group_create", ct.c_int, [ct.c_int, ct.POINTER(ct.c_int), ct.POINTER(ct.c_void_p)]),
     ("tdb_group_free", None, [ct.c_void_p]),
     ("tdb_group_size", ct.c_int, [ct.c_void_p]),
@@ -540,6 +558,20 @@ def segments_mesh_intersects(segments, mesh):
     _check(lib().tdb_segments_mesh_intersects(_dp(s), len(s), m.handle, h.ctypes.data_as(_U8),
                                               f.ctypes.data_as(_U64)))
     return h.astype(bool), f
+
+
+def query_face_result(op: int, query, tri) -> FaceResult:
+    """The reference's full per-face result (closest points + params, or hit
+    point + params) for one segment (6 doubles) or point (3) and one
+    triangle (9), evaluated on the device."""
+    q = np.ascontiguousarray(query, dtype=np.float64).ravel()
+    t = np.ascontiguousarray(tri, dtype=np.float64).ravel()
+    if t.size != 9 or q.size not in (3, 6):
+        raise ValueError("query is 3 or 6 doubles, the triangle 9")
+    o = FaceResult()
+    _check(lib().tdb_query_face_result(op, QUERY_POINTS if q.size == 3 else QUERY_SEGMENTS, _dp(q), _dp(t),
+                                       ct.byref(o)))
+    return o
 
 
 def drills(count: int, seed: int = 42, style: int = 0) -> np.ndarray:

@@ -441,6 +441,16 @@ int tdb_pairs_filter(const double* a9, const double* b9, uint64_t n, double* d2)
     return rc;
 }
 
+int tdb_query_face_result(int op, int kind, const double* q, const double* tri9, tdb_face_result* out) {
+    return guarded([&] {
+        need(q && tri9 && out, "null argument");
+        need(op == TDB_OP_DISTANCE || op == TDB_OP_INTERSECTS, "unknown op");
+        need(kind == TDB_QUERY_SEGMENTS || kind == TDB_QUERY_POINTS, "unknown query kind");
+        need(!(op == TDB_OP_INTERSECTS && kind == TDB_QUERY_POINTS), "intersects takes a segment");
+        tdb::run_face_result(ctx(), op, kind == TDB_QUERY_POINTS, q, tri9, out);
+    });
+}
+
 int tdb_queries_upload(const double* q, uint64_t n, int kind, tdb_queries* out) {
     return guarded([&] {
         need(out != nullptr, "null output handle");

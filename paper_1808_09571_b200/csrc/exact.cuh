@@ -69,6 +69,12 @@ struct res {
     v3 a, b;
 };
 
+// kernels::SurfaceParams (kernels.hpp:22-26), reported only when asked for
+// (the per-face detail of distance_to_mesh); the hot exact passes pass null.
+struct prm {
+    double t, u, v;
+};
+
 // kernels.cpp:54-60
 __device__ __forceinline__ res witness(v3 on_a, v3 on_b) {
     res r;
@@ -79,7 +85,7 @@ __device__ __forceinline__ res witness(v3 on_a, v3 on_b) {
 }
 
 // kernels.cpp:72-116
-static __device__ __noinline__ res seg_seg(v3 a0, v3 a1, v3 b0, v3 b1) {
+static __device__ __noinline__ res seg_seg(v3 a0, v3 a1, v3 b0, v3 b1, prm* pp = nullptr) {
     const v3 d1 = sub(a1, a0), d2 = sub(b1, b0), r = sub(a0, b0);
     const double aa = dot(d1, d1), ee = dot(d2, d2), f = dot(d2, r);
     double s = 0.0, t = 0.0;
@@ -104,6 +110,7 @@ static __device__ __noinline__ res seg_seg(v3 a0, v3 a1, v3 b0, v3 b1) {
             }
         }
     }
+    if (pp) *pp = prm{s, t, 0.0};  // kernels.cpp:110-114
     return witness(add(a0, scl(d1, s)), add(b0, scl(d2, t)));
 }
 
@@ -117,7 +124,7 @@ __device__ __forceinline__ res pt_seg(v3 p, v3 s0, v3 s1) {
 }
 
 // kernels.cpp:138-227 (degenerate fallback :127-134)
-static __device__ __noinline__ res pt_tri(v3 p, const tri& tr) {
+static __device__ __noinline__ res pt_tri(v3 p, const tri& tr, prm* pp = nullptr) {
     const v3 e0 = sub(tr.v1, tr.v0), e1 = sub(tr.v2, tr.v0), df = sub(tr.v0, p);
     const double a00 = dot(e0, e0), a01 = dot(e0, e1), a11 = dot(e1, e1);
     const double b0 = dot(df, e0), b1 = dot(df, e1);
@@ -129,6 +136,7 @@ static __device__ __noinline__ res pt_tri(v3 p, const tri& tr) {
         c = pt_seg(p, tr.v1, tr.v2);
         if (c.d < best.d) best = c;
         best.a = p;
+        if (pp) *pp = prm{0.0, 0.0, 0.0};  // kernels.cpp:154
         return best;
     }
     double s = __dsub_rn(__dmul_rn(a01, b1), __dmul_rn(a11, b0));
@@ -180,6 +188,7 @@ static __device__ __noinline__ res pt_tri(v3 p, const tri& tr) {
         }
         t = __dsub_rn(1.0, s);
     }
+    if (pp) *pp = prm{0.0, clamp_unit(s), clamp_unit(t)};  // kernels.cpp:221-225
     return witness(p, add(add(tr.v0, scl(e0, s)), scl(e1, t)));
 }
 
@@ -205,27 +214,34 @@ __device__ __forceinline__ pierce_t pierce(v3 e0, v3 e1, v3 d, v3 w) {
 }
 
 // kernels.cpp:256-316
-static __device__ __noinline__ res seg_tri(v3 p0, v3 p1, const tri& tr) {
-    if (same(p0, p1)) return pt_tri(p0, tr);
+static __device__ __noinline__ res seg_tri(v3 p0, v3 p1, const tri& tr, prm* pp = nullptr) {
+    if (same(p0, p1)) return pt_tri(p0, tr, pp);
     const v3 d = sub(p1, p0), e0 = sub(tr.v1, tr.v0), e1 = sub(tr.v2, tr.v0);
     if (!degenerate(tr)) {
         const pierce_t x = pierce(e0, e1, d, sub(p0, tr.v0));
-        if (x.ok && x.u >= 0.0 && x.v >= 0.0 && __dadd_rn(x.u, x.v) <= 1.0 && x.t >= 0.0 && x.t <= 1.0)
+        if (x.ok && x.u >= 0.0 && x.v >= 0.0 && __dadd_rn(x.u, x.v) <= 1.0 && x.t >= 0.0 && x.t <= 1.0) {
+            if (pp) *pp = prm{x.t, x.u, x.v};  // kernels.cpp:276
             return witness(add(p0, scl(d, x.t)), add(add(tr.v0, scl(e0, x.u)), scl(e1, x.v)));
+        }
     }
     res best;
     best.d = __longlong_as_double(0x7ff0000000000000LL);
     best.a = best.b = mk(0.0, 0.0, 0.0);
-    res c = seg_seg(p0, p1, tr.v0, tr.v1);
-    if (c.d < best.d) best = c;
-    c = seg_seg(p0, p1, tr.v0, tr.v2);
-    if (c.d < best.d) best = c;
-    c = seg_seg(p0, p1, tr.v1, tr.v2);
-    if (c.d < best.d) best = c;
-    c = pt_tri(p0, tr);
-    if (c.d < best.d) best = c;
-    c = pt_tri(p1, tr);
-    if (c.d < best.d) best = c;
+    prm q{0.0, 0.0, 0.0}, bp{0.0, 0.0, 0.0};
+    prm* const qp = pp ? &q : nullptr;
+    // edges v0v1, v0v2, v1v2 with (u, v) = (u0 + s du, v0 + s dv) (kernels.cpp:289-303)
+    const double u0[3] = {0.0, 0.0, 1.0}, du[3] = {1.0, 0.0, -1.0}, dv[3] = {0.0, 1.0, 1.0};
+    res c = seg_seg(p0, p1, tr.v0, tr.v1, qp);
+    if (c.d < best.d) best = c, bp = prm{q.t, __dadd_rn(u0[0], __dmul_rn(q.u, du[0])), __dadd_rn(0.0, __dmul_rn(q.u, dv[0]))};
+    c = seg_seg(p0, p1, tr.v0, tr.v2, qp);
+    if (c.d < best.d) best = c, bp = prm{q.t, __dadd_rn(u0[1], __dmul_rn(q.u, du[1])), __dadd_rn(0.0, __dmul_rn(q.u, dv[1]))};
+    c = seg_seg(p0, p1, tr.v1, tr.v2, qp);
+    if (c.d < best.d) best = c, bp = prm{q.t, __dadd_rn(u0[2], __dmul_rn(q.u, du[2])), __dadd_rn(0.0, __dmul_rn(q.u, dv[2]))};
+    c = pt_tri(p0, tr, qp);
+    if (c.d < best.d) best = c, bp = prm{0.0, q.u, q.v};  // kernels.cpp:307-314: t = endpoint index
+    c = pt_tri(p1, tr, qp);
+    if (c.d < best.d) best = c, bp = prm{1.0, q.u, q.v};
+    if (pp) *pp = bp;
     return best;
 }
 

@@ -992,4 +992,60 @@ void run_literal_table(const Ctx& cx, int op, const QuerySet& q1, const Geom& B,
     S.near_degenerate = cx.near->count;
 }
 
+namespace {
+
+struct FaceIn {
+    double q[6];
+    double t9[9];
+    int op, point;
+};
+
+// The reference's per-face result for one query (kernels.cpp:256-336 with
+// their SurfaceParams / IntersectionParams), one thread.
+__global__ void face_result_kernel(FaceIn in, tdb_face_result* out) {
+    const exact::tri t{{in.t9[0], in.t9[1], in.t9[2]}, {in.t9[3], in.t9[4], in.t9[5]}, {in.t9[6], in.t9[7], in.t9[8]}};
+    const exact::v3 p0{in.q[0], in.q[1], in.q[2]};
+    const exact::v3 p1 = in.point ? p0 : exact::v3{in.q[3], in.q[4], in.q[5]};
+    tdb_face_result r{};
+    if (in.op == TDB_OP_DISTANCE) {
+        exact::prm pr{0.0, 0.0, 0.0};
+        const exact::res x = in.point ? exact::pt_tri(p0, t, &pr) : exact::seg_tri(p0, p1, t, &pr);
+        r.distance = x.d;
+        r.on_query[0] = x.a.x, r.on_query[1] = x.a.y, r.on_query[2] = x.a.z;
+        r.on_face[0] = x.b.x, r.on_face[1] = x.b.y, r.on_face[2] = x.b.z;
+        r.t = pr.t, r.u = pr.u, r.v = pr.v;
+    } else {  // segment_triangle_intersect (kernels.cpp:318-336)
+        const exact::v3 d = exact::sub(p1, p0);
+        const exact::pierce_t x = exact::pierce(exact::sub(t.v1, t.v0), exact::sub(t.v2, t.v0), d, exact::sub(p0, t.v0));
+        const double sl = exact::kSlack;
+        if (x.ok && !(x.t < -sl || x.t > 1.0 + sl) && !(x.u < -sl || x.v < -sl || __dadd_rn(x.u, x.v) > 1.0 + sl)) {
+            r.hit = 1;
+            const exact::v3 pt = exact::add(p0, exact::scl(d, exact::clamp_unit(x.t)));
+            r.point[0] = pt.x, r.point[1] = pt.y, r.point[2] = pt.z;
+            r.t = x.t, r.u = x.u, r.v = x.v, r.w = __dsub_rn(__dsub_rn(1.0, x.u), x.v);
+        }
+    }
+    *out = r;
+}
+
+}  // namespace
+
+void run_face_result(const Ctx& cx, int op, int point, const double* q, const double* tri9, tdb_face_result* out) {
+    FaceIn in{};
+    std::copy(q, q + (point ? 3 : 6), in.q);
+    std::copy(tri9, tri9 + 9, in.t9);
+    in.op = op;
+    in.point = point;
+    tdb_face_result* d = nullptr;
+    CK(cudaMallocAsync(&d, sizeof *d, cx.stream));
+    face_result_kernel<<<1, 1, 0, cx.stream>>>(in, d);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, d, sizeof *out, cudaMemcpyDeviceToHost, cx.stream));
+    CK(cudaFreeAsync(d, cx.stream));
+    CK(cudaStreamSynchronize(cx.stream));
+    std::memset(cx.stats, 0, sizeof *cx.stats);
+    cx.stats->kernels = 1;
+    cx.stats->pairs = 1;
+}
+
 }  // namespace tdb

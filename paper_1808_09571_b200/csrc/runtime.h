@@ -209,6 +209,8 @@ void run_queries(const Ctx& cx, int op, const QuerySet& qs, const Geom& B, doubl
 // (run_batch with a Segment / Point argument over Mesh records): per object
 // distance_to_mesh (dist + lowest face) or intersects_mesh (hit + lowest hit
 // face); faces are object-relative.
+// The reference's full per-face result of one query against one triangle.
+void run_face_result(const Ctx& cx, int op, int point, const double* q, const double* tri9, tdb_face_result* out);
 void run_literal_table(const Ctx& cx, int op, const QuerySet& q1, const Geom& B, double* dist, uint8_t* hit,
                        uint64_t* face);
 

@@ -141,6 +141,56 @@ int main() {
             }
         }
     }
+    // distance_to_mesh / intersects_mesh: every field of the reference's
+    // result (distance, face, closest points, params; hit, point, params),
+    // bit for bit, over segments and points near a sphere mesh (with
+    // crossings, grazing and zero-length segments)
+    {
+        const TriangleMesh m = shifted(bench::unit_sphere(2000), 0.25, -0.5, 0.125);
+        std::uint64_t st = 12345;
+        auto rnd = [&st] {  // xorshift in [-1.5, 1.5)
+            st ^= st << 13, st ^= st >> 7, st ^= st << 17;
+            return (double)(st >> 11) * 0x1.0p-53 * 3.0 - 1.5;
+        };
+        int hits = 0;
+        for (int k = 0; k < 400; ++k) {
+            const Point3 p0{rnd(), rnd(), rnd()};
+            const Point3 p1 = k % 10 == 0 ? p0 : Point3{rnd(), rnd(), rnd()};
+            const LineSegment seg{p0, p1};
+            auto cmp = [&](const K::DistanceResult& a, const K::DistanceResult& b) {
+                EXPECT(same_bits(a.distance, b.distance) && a.face_index == b.face_index);
+                EXPECT(same_bits(a.closest_on_a.x, b.closest_on_a.x) && same_bits(a.closest_on_a.y, b.closest_on_a.y) &&
+                       same_bits(a.closest_on_a.z, b.closest_on_a.z));
+                EXPECT(same_bits(a.closest_on_b.x, b.closest_on_b.x) && same_bits(a.closest_on_b.y, b.closest_on_b.y) &&
+                       same_bits(a.closest_on_b.z, b.closest_on_b.z));
+                EXPECT(a.params.has_value() == b.params.has_value());
+                if (a.params && b.params)
+                    EXPECT(same_bits(a.params->t, b.params->t) && same_bits(a.params->u, b.params->u) &&
+                           same_bits(a.params->v, b.params->v));
+            };
+            cmp(K::b200::distance_to_mesh(seg, m, cfg), K::distance_to_mesh(seg, m, cfg));
+            cmp(K::b200::distance_to_mesh(p0, m, cfg), K::distance_to_mesh(p0, m, cfg));
+            const K::IntersectionResult hd = K::b200::intersects_mesh(seg, m, cfg);
+            const K::IntersectionResult hr = K::intersects_mesh(seg, m, cfg);
+            EXPECT(hd.hit == hr.hit && hd.face_index == hr.face_index && hd.point.has_value() == hr.point.has_value());
+            if (hd.point && hr.point)
+                EXPECT(same_bits(hd.point->x, hr.point->x) && same_bits(hd.point->y, hr.point->y) &&
+                       same_bits(hd.point->z, hr.point->z));
+            if (hd.params && hr.params)
+                EXPECT(same_bits(hd.params->t, hr.params->t) && same_bits(hd.params->u, hr.params->u) &&
+                       same_bits(hd.params->v, hr.params->v) && same_bits(hd.params->w, hr.params->w));
+            hits += hr.hit;
+        }
+        EXPECT(hits > 20 && hits < 380);
+        bool threw = false;
+        try {
+            K::b200::distance_to_mesh(Geometry{m}, m, cfg);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        EXPECT(threw);
+    }
+
     if (fails == 0) std::printf("SHIM OK\n");
     return fails ? 1 : 0;
 }
