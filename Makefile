@@ -49,10 +49,10 @@ shimtest: $(LIB) oracle
 	else echo "shimtest: $(REF) absent; keeping prebuilt $(BUILD)/shim_test"; fi
 
 # The reference's own unit tests for the two replaced entry points
-# (tests/test_{batch,volume,distance,intersect}.cpp, unmodified, compiled where
+# (tests/test_{batch,volume,distance,intersect,geometry,store}.cpp, unmodified, compiled where
 # they lie) with run_batch / mesh_volume routed to the device shim
 # (tests/cpp/ref_route.hpp) and a minimal doctest stand-in. Test-only.
-REFTESTS := test_batch test_volume test_distance test_intersect
+REFTESTS := test_batch test_volume test_distance test_intersect test_geometry test_store
 refunittest: $(LIB) oracle
 	@if [ -d "$(REF)/include" ]; then \
 	  mkdir -p $(BUILD)/refunit && \

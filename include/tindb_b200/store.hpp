@@ -23,6 +23,7 @@
 #include <memory>
 #include <sstream>
 #include <string>
+#include <string_view>
 #include <unordered_set>
 #include <utility>
 #include <vector>
@@ -280,3 +281,41 @@ inline TableSnapshot register_table_b200(Catalog& catalog, LoadedTable&& loaded,
 }
 
 }  // namespace tindb::store::b200
+
+namespace tindb::b200 {
+
+// parse_wkt (wkt.hpp:35, wkt.cpp:188) with mesh literals (TIN Z /
+// POLYHEDRALSURFACE Z) parsed on the device; other literals (a few bytes)
+// go to the reference parser. A rejected mesh literal raises the
+// reference's WktParseError: same message, same byte position.
+inline Geometry parse_wkt(std::string_view text) {
+    const int kind = store::b200::detail::mesh_keyword(std::string(text));
+    if (kind < 0) return ::tindb::parse_wkt(text);
+    tdb_mesh m = nullptr;
+    std::uint64_t pos = 0;
+    const int rc = tdb_mesh_from_wkt(text.data(), text.size(), &m, &pos);
+    if (rc == TDB_E_PARSE) {
+        std::string what = tdb_last_error();  // the reference's what(): "<message> at position <pos>"
+        const std::string tail = " at position " + std::to_string(pos);
+        if (what.size() >= tail.size() && what.compare(what.size() - tail.size(), tail.size(), tail) == 0)
+            what.resize(what.size() - tail.size());
+        throw WktParseError(what, static_cast<std::size_t>(pos));
+    }
+    kernels::b200::check(rc);
+    TriangleMesh mesh;
+    try {
+        std::uint64_t n = 0;
+        kernels::b200::check(tdb_geom_info(m, &n, nullptr, nullptr, nullptr));
+        mesh.triangles.resize(n);
+        kernels::b200::check(tdb_geom_download(m, reinterpret_cast<double*>(mesh.triangles.data())));
+    } catch (...) {
+        tdb_mesh_free(m);
+        throw;
+    }
+    tdb_mesh_free(m);
+    mesh.source_kind = kind == 0 ? MeshSource::Tin : MeshSource::PolyhedralSurface;
+    mesh.refresh_degeneracy_flag();
+    return Geometry{std::move(mesh)};
+}
+
+}  // namespace tindb::b200

@@ -34,6 +34,13 @@ class Approx {
     double eps_ = static_cast<double>(std::numeric_limits<float>::epsilon()) * 100;
 };
 
+// CHECK_THROWS_WITH_AS(expr, Contains("text"), Type)
+struct Contains {
+    std::string s;
+    explicit Contains(const char* x) : s(x) {}
+    bool operator()(const std::string& what) const { return what.find(s) != std::string::npos; }
+};
+
 namespace detail {
 struct Case {
     const char* name;
@@ -94,6 +101,18 @@ inline int run_all() {
 #define REQUIRE(...) ::doctest::detail::check(static_cast<bool>(__VA_ARGS__), #__VA_ARGS__, __FILE__, __LINE__, true)
 #define FAIL(msg) ::doctest::detail::check(false, msg, __FILE__, __LINE__, true)
 #define CAPTURE(x) ((void)0)
+#define CHECK_THROWS_WITH_AS(expr, matcher, ...)                                                           \
+    do {                                                                                                   \
+        bool ok_ = false;                                                                                  \
+        try {                                                                                              \
+            (void)(expr);                                                                                  \
+        } catch (const __VA_ARGS__& e_) {                                                                  \
+            ok_ = (matcher)(e_.what());                                                                    \
+        } catch (...) {                                                                                    \
+        }                                                                                                  \
+        ::doctest::detail::check(ok_, "throws " #__VA_ARGS__ " with " #matcher ": " #expr, __FILE__, __LINE__, \
+                                 false);                                                                   \
+    } while (0)
 #define CHECK_THROWS_AS(expr, ...)                                                                         \
     do {                                                                                                   \
         bool thrown_ = false;                                                                              \

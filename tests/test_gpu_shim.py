@@ -39,11 +39,12 @@ REFUNIT = os.path.join(ROOT, "build", "ref_unit_tests")
 @pytest.mark.skipif(not os.path.exists(REFUNIT), reason="build/ref_unit_tests not built (needs /root/reference)")
 def test_reference_unit_tests_on_the_device_engine():
     """The reference's own unit tests for the replaced entry points
-    (tests/test_batch.cpp, test_volume.cpp, test_distance.cpp and
-    test_intersect.cpp, unmodified) with run_batch, mesh_volume,
-    distance_to_mesh and intersects_mesh routed to the device shim: every
-    case passes (the primitive-level cases in those files run the
-    reference's own primitives)."""
+    (tests/test_batch.cpp, test_volume.cpp, test_distance.cpp,
+    test_intersect.cpp, test_geometry.cpp, test_store.cpp, unmodified) with
+    run_batch, mesh_volume, distance_to_mesh, intersects_mesh, parse_wkt and
+    the table loaders routed to the device shim: every case passes (the
+    primitive-level cases in those files run the reference's own
+    primitives)."""
     r = subprocess.run([REFUNIT], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert "52 test cases, 0 failed" in r.stdout, r.stdout
+    assert "90 test cases, 0 failed" in r.stdout, r.stdout
