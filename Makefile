@@ -49,10 +49,12 @@ shimtest: $(LIB) oracle
 	else echo "shimtest: $(REF) absent; keeping prebuilt $(BUILD)/shim_test"; fi
 
 # The reference's own unit tests for the two replaced entry points
-# (tests/test_{batch,volume,distance,intersect,geometry,store}.cpp, unmodified, compiled where
+# (tests/test_{batch,volume,distance,intersect,geometry,store,sqlfe}.cpp, unmodified, compiled where
 # they lie) with run_batch / mesh_volume routed to the device shim
-# (tests/cpp/ref_route.hpp) and a minimal doctest stand-in. Test-only.
-REFTESTS := test_batch test_volume test_distance test_intersect test_geometry test_store
+# (tests/cpp/ref_route.hpp; test_sqlfe through the reference engine.cpp with
+# engine.cpp:203 routed, tests/cpp/engine_route.hpp) and a minimal doctest
+# stand-in. Test-only.
+REFTESTS := test_batch test_volume test_distance test_intersect test_geometry test_store test_sqlfe
 refunittest: $(LIB) oracle
 	@if [ -d "$(REF)/include" ]; then \
 	  mkdir -p $(BUILD)/refunit && \
@@ -61,6 +63,8 @@ refunittest: $(LIB) oracle
 	      -Iinclude -include tests/cpp/ref_route.hpp -c $(REF)/tests/$$f.cpp -o $(BUILD)/refunit/$$f.o || exit 1; done && \
 	  $(CXX) -std=c++20 -O2 -ffp-contract=off -Dtindb=tindb_ref -I$(REF)/include -I$(REF)/tests \
 	    -c $(REF)/tests/support/oracles.cpp -o $(BUILD)/refunit/oracles.o && \
+	  $(CXX) -std=c++20 -O2 -DNDEBUG -ffp-contract=off -Dtindb=tindb_ref -I$(REF)/include -Iinclude \
+	    -include tests/cpp/engine_route.hpp -c $(REF)/src/engine.cpp -o $(BUILD)/refunit/engine_routed.o && \
 	  $(CXX) -std=c++20 -O2 -Itests/cpp/doctest_shim -c tests/cpp/ref_unit_main.cpp -o $(BUILD)/refunit/main.o && \
 	  $(CXX) $(BUILD)/refunit/*.o -o $(BUILD)/ref_unit_tests -Loracle/_ref -ltindb_ref -L$(PKG) -ltindb_b200 \
 	    -Wl,-rpath,'$$ORIGIN/../oracle/_ref' -Wl,-rpath,'$$ORIGIN/../$(PKG)'; \

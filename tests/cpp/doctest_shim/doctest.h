@@ -11,6 +11,7 @@
 #include <functional>
 #include <limits>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 namespace doctest {
@@ -68,6 +69,20 @@ inline bool check(bool ok, const char* expr, const char* file, int line, bool re
     }
     return ok;
 }
+// FAIL(part, part, ...): report the concatenated message, abort the test case
+inline void append(std::string& out, const std::string& v) { out += v; }
+inline void append(std::string& out, const char* v) { out += v; }
+template <class T>
+inline void append(std::string& out, const T& v) {
+    out += std::to_string(v);
+}
+template <class... T>
+[[noreturn]] inline void fail_with(const char* file, int line, const T&... parts) {
+    std::string m;
+    (append(m, parts), ...);
+    check(false, m.c_str(), file, line, true);
+    throw RequireFailed{};
+}
 inline int run_all() {
     int failed_cases = 0;
     for (const Case& c : registry()) {
@@ -99,7 +114,7 @@ inline int run_all() {
 #define CHECK(...) ::doctest::detail::check(static_cast<bool>(__VA_ARGS__), #__VA_ARGS__, __FILE__, __LINE__, false)
 #define CHECK_FALSE(...) ::doctest::detail::check(!(__VA_ARGS__), "!(" #__VA_ARGS__ ")", __FILE__, __LINE__, false)
 #define REQUIRE(...) ::doctest::detail::check(static_cast<bool>(__VA_ARGS__), #__VA_ARGS__, __FILE__, __LINE__, true)
-#define FAIL(msg) ::doctest::detail::check(false, msg, __FILE__, __LINE__, true)
+#define FAIL(...) ::doctest::detail::fail_with(__FILE__, __LINE__, __VA_ARGS__)
 #define CAPTURE(x) ((void)0)
 #define CHECK_THROWS_WITH_AS(expr, matcher, ...)                                                           \
     do {                                                                                                   \

@@ -40,11 +40,12 @@ REFUNIT = os.path.join(ROOT, "build", "ref_unit_tests")
 def test_reference_unit_tests_on_the_device_engine():
     """The reference's own unit tests for the replaced entry points
     (tests/test_batch.cpp, test_volume.cpp, test_distance.cpp,
-    test_intersect.cpp, test_geometry.cpp, test_store.cpp, unmodified) with
-    run_batch, mesh_volume, distance_to_mesh, intersects_mesh, parse_wkt and
-    the table loaders routed to the device shim: every case passes (the
+    test_intersect.cpp, test_geometry.cpp, test_store.cpp, test_sqlfe.cpp,
+    unmodified) with run_batch (also inside the reference engine, for
+    test_sqlfe), mesh_volume, distance_to_mesh, intersects_mesh, parse_wkt
+    and the table loaders routed to the device shim: every case passes (the
     primitive-level cases in those files run the reference's own
     primitives)."""
     r = subprocess.run([REFUNIT], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert "90 test cases, 0 failed" in r.stdout, r.stdout
+    assert "113 test cases, 0 failed" in r.stdout, r.stdout
