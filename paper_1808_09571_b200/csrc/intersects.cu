@@ -29,6 +29,7 @@
 // its first hit; an object whose AABB header is separated from B's by more
 // than tau is skipped whole.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <vector>
 
@@ -64,6 +65,10 @@ struct HitArgs {
     const double* tile_aabb;
     const double* chunk_aabb;
     NearLog near;
+    // FP32 pre-cull: B's vertices relative to its origin (9 float planes),
+    // the origin, and a bound on |v - origin| over B
+    const float* Bf;
+    double ox, oy, oz, RB;
 };
 
 __device__ __forceinline__ exact::tri load_tri(const double* P, uint64_t pad, uint64_t i) {
@@ -71,6 +76,19 @@ __device__ __forceinline__ exact::tri load_tri(const double* P, uint64_t pad, ui
 #pragma unroll
     for (int k = 0; k < 9; ++k) v[k] = __ldg(P + (uint64_t)(F_V + k) * pad + i);
     return exact::tri{{v[0], v[1], v[2]}, {v[3], v[4], v[5]}, {v[6], v[7], v[8]}};
+}
+
+// FP32 pre-cull: the same separation test on h32 = n32 . (v - O) - c32 with
+// |h32 - h| <= 6 * 2^-24 * (|v - O| + |c|) (roundings of n, v - O, c and
+// three FMAs), so tau32 = kCull32 * (RB + |c|) + tau implies the FP64 test
+// separates too: the pre-cull never drops a pair the FP64 test keeps.
+constexpr double kCull32 = 1e-6;
+
+// all three h on one side, beyond tau: min > tau or max < -tau. (A NaN h
+// needs an infinite input; the caller sets tau = +inf whenever FP32 could
+// overflow, and then nothing is separated here.)
+__device__ __forceinline__ bool separated32(float h0, float h1, float h2, float tau) {
+    return fminf(fminf(h0, h1), h2) > tau || fmaxf(fmaxf(h0, h1), h2) < -tau;
 }
 
 // all three |h| > tau with one common sign
@@ -105,6 +123,7 @@ static __device__ __noinline__ bool slow_pair(const double* Ap, uint64_t An_pad,
 
 __global__ void __launch_bounds__(32 * kWarps) hit_kernel(HitArgs a) {
     __shared__ alignas(128) double sm[2][kHitPlanes * kSBH];
+    __shared__ alignas(128) float smf[2][9 * kSBH];
     __shared__ alignas(8) uint64_t bar[2];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -154,6 +173,17 @@ __global__ void __launch_bounds__(32 * kWarps) hit_kernel(HitArgs a) {
         for (int k = 0; k < 3; ++k) an[r][k] = __ldg(a.Ap + (uint64_t)(F_N + k) * a.An_pad + row);
         ac[r] = __ldg(a.Ap + (uint64_t)F_C * a.An_pad + row);
     }
+    // the rows' planes in B's FP32 frame: h = n . (v - O) - (c - n . O)
+    float an32[kRows][3], ac32[kRows], tau32[kRows];
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+        const double cB = fma(-an[r][0], a.ox, fma(-an[r][1], a.oy, fma(-an[r][2], a.oz, ac[r])));
+#pragma unroll
+        for (int k = 0; k < 3; ++k) an32[r][k] = __double2float_rn(an[r][k]);
+        ac32[r] = __double2float_rn(cB);
+        const double t32 = kCull32 * (a.RB + fabs(cB)) + tau;
+        tau32[r] = a.RB + fabs(cB) < 1e30 ? __double2float_ru(t32) : __int_as_float(0x7f800000);  // +inf: no FP32 cull
+    }
     const uint64_t Bn = a.Bn;
     auto row_pmin = [&](int r, uint64_t f0) { return (rowv[r] - T.obj_row0) * Bn + f0; };
     {  // a lower pair of this object already hit: nothing here can lower it
@@ -179,10 +209,13 @@ __global__ void __launch_bounds__(32 * kWarps) hit_kernel(HitArgs a) {
         const uint64_t f0 = b0 + (uint64_t)s * kSBH;
         const int cnt = (int)min((uint64_t)kSBH, b1 - f0);
         const uint32_t bytes = (uint32_t)(((cnt + 1) & ~1) * sizeof(double));
-        mbar_expect_tx(&bar[st], bytes * kHitPlanes);
+        const uint32_t fbytes = (uint32_t)(((cnt + 3) & ~3) * sizeof(float));
+        mbar_expect_tx(&bar[st], bytes * kHitPlanes + fbytes * 9);
 #pragma unroll 1
         for (int f = 0; f < kHitPlanes; ++f)
             bulk_g2s(&sm[st][f * kSBH], a.Bp + (uint64_t)kHitPlaneOf[f] * a.Bn_pad + f0, bytes, &bar[st]);
+#pragma unroll 1
+        for (int f = 0; f < 9; ++f) bulk_g2s(&smf[st][f * kSBH], a.Bf + (uint64_t)f * a.Bn_pad + f0, fbytes, &bar[st]);
     };
     if (threadIdx.x == 0) {
         issue(0);
@@ -205,25 +238,38 @@ __global__ void __launch_bounds__(32 * kWarps) hit_kernel(HitArgs a) {
             }
         }
         if (__any_sync(0xffffffffu, live != 0)) {
+            const float* fb = smf[st];
+            const int* degw = reinterpret_cast<const int*>(sb + HS_DEG * kSBH) + 1;  // high words
 #pragma unroll 1
             for (int j = 0; j < cnt; ++j) {
-                if (reinterpret_cast<const int*>(sb + HS_DEG * kSBH + j)[1] != 0) continue;  // uniform
-                const double* bv = sb + HS_V * kSBH + j;
-                const double x0 = bv[0], y0 = bv[kSBH], z0 = bv[2 * kSBH];
-                const double x1 = bv[3 * kSBH], y1 = bv[4 * kSBH], z1 = bv[5 * kSBH];
-                const double x2 = bv[6 * kSBH], y2 = bv[7 * kSBH], z2 = bv[8 * kSBH];
+                if (degw[2 * j] != 0) continue;  // uniform
+                const float* fv = fb + j;
+                const float X0 = fv[0], Y0 = fv[kSBH], Z0 = fv[2 * kSBH];
+                const float X1 = fv[3 * kSBH], Y1 = fv[4 * kSBH], Z1 = fv[5 * kSBH];
+                const float X2 = fv[6 * kSBH], Y2 = fv[7 * kSBH], Z2 = fv[8 * kSBH];
+                bool sep[kRows];
+#pragma unroll
+                for (int r = 0; r < kRows; ++r) {  // FP32 pre-cull
+                    const float h0 = fmaf(an32[r][0], X0, fmaf(an32[r][1], Y0, fmaf(an32[r][2], Z0, -ac32[r])));
+                    const float h1 = fmaf(an32[r][0], X1, fmaf(an32[r][1], Y1, fmaf(an32[r][2], Z1, -ac32[r])));
+                    const float h2 = fmaf(an32[r][0], X2, fmaf(an32[r][1], Y2, fmaf(an32[r][2], Z2, -ac32[r])));
+                    sep[r] = separated32(h0, h1, h2, tau32[r]);
+                }
+                if (sep[0] & sep[1] & sep[2] & sep[3]) continue;  // the common case: all four culled
                 unsigned need = 0;
 #pragma unroll
-                for (int r = 0; r < kRows; ++r) {
-                    const double h0 = fma(an[r][0], x0, fma(an[r][1], y0, fma(an[r][2], z0, -ac[r])));
-                    const double h1 = fma(an[r][0], x1, fma(an[r][1], y1, fma(an[r][2], z1, -ac[r])));
-                    const double h2 = fma(an[r][0], x2, fma(an[r][1], y2, fma(an[r][2], z2, -ac[r])));
-                    need |= separated(h0, h1, h2, tau) ? 0u : 1u << r;
-                }
+                for (int r = 0; r < kRows; ++r) need |= sep[r] ? 0u : 1u << r;
                 need &= live;
-                while (need) {  // rare: second plane + exact predicate
+                while (need) {  // rare: FP64 plane test, second plane, exact predicate
                     const int r = __ffs(need) - 1;
                     need &= need - 1;
+                    const double* bv = sb + HS_V * kSBH + j;
+                    const double h0 = fma(an[r][0], bv[0], fma(an[r][1], bv[kSBH], fma(an[r][2], bv[2 * kSBH], -ac[r])));
+                    const double h1 =
+                        fma(an[r][0], bv[3 * kSBH], fma(an[r][1], bv[4 * kSBH], fma(an[r][2], bv[5 * kSBH], -ac[r])));
+                    const double h2 =
+                        fma(an[r][0], bv[6 * kSBH], fma(an[r][1], bv[7 * kSBH], fma(an[r][2], bv[8 * kSBH], -ac[r])));
+                    if (separated(h0, h1, h2, tau)) continue;
                     ++nex;
                     if (slow_pair(a.Ap, a.An_pad, rowv[r], sb, j, tau, a.near, a.obj0 + o, row_pmin(r, f0 + j))) {
                         atomicMin(a.objhit + o, row_pmin(r, f0 + j));
@@ -324,12 +370,17 @@ void run_intersects_batch(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t
         CK(cudaMallocAsync(&caabb, n_chunks * 6 * sizeof(double), st));
         chunk_aabbs(B, chunk, caabb, st);
     }
+    // |v - origin| over B <= the diagonal of B's AABB (the origin is a vertex of B)
+    double rb = 0.0;
+    for (int k = 0; k < 3; ++k) rb += (B.stats[3 + k] - B.stats[k]) * (B.stats[3 + k] - B.stats[k]);
+    rb = std::sqrt(rb) * (1.0 + 1e-12);
     CK(cudaEventRecord(e0, st));
     hit_kernel<<<(unsigned)n_items, 32 * kWarps, 0, st>>>(HitArgs{A.planes, A.n_pad, A.d_tiles, sel.tile0, ntiles,
                                                                   sel.row_lo, sel.row_hi, B.planes, B.n_pad, B.n,
                                                                   n_chunks, chunk, sel.obj0, A.d_obj_stats, Bstats,
                                                                   objhit, nex, caabb ? A.d_tile_aabb : nullptr,
-                                                                  caabb, near.log});
+                                                                  caabb, near.log, B.fplanes, B.origin[0],
+                                                                  B.origin[1], B.origin[2], rb});
     CK(cudaGetLastError());
     CK(cudaEventRecord(e1, st));
     std::vector<unsigned long long> hp(nobj);

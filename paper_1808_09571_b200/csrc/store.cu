@@ -6,6 +6,7 @@
 // tindb::TriangleMesh::triangles.data() (72 B per face); it is copied once
 // (H2D) into a staging buffer and transposed + enriched by prep_kernel.
 #include <algorithm>
+#include <cmath>
 #include <vector>
 
 #include "exact.cuh"
@@ -39,7 +40,8 @@ __device__ __forceinline__ uint32_t object_of(const uint64_t* off, uint64_t n_ob
 __global__ void prep_kernel(const double* __restrict__ aos, uint64_t n, uint64_t n_pad,
                             const uint64_t* __restrict__ off, uint64_t n_obj,
                             double* __restrict__ planes, unsigned long long* __restrict__ stats,
-                            unsigned long long* __restrict__ n_deg) {
+                            unsigned long long* __restrict__ n_deg, float* __restrict__ fplanes, double ox,
+                            double oy, double oz) {
     const uint64_t f = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool live = f < n;
     const uint64_t g = live ? f : (n ? n - 1 : 0);
@@ -95,6 +97,9 @@ __global__ void prep_kernel(const double* __restrict__ aos, uint64_t n, uint64_t
             p[(F_LO + k) * n_pad] = fmin(v[k], fmin(v[3 + k], v[6 + k]));
             p[(F_HI + k) * n_pad] = fmax(v[k], fmax(v[3 + k], v[6 + k]));
         }
+        const double o3[3] = {ox, oy, oz};
+#pragma unroll
+        for (int k = 0; k < 9; ++k) fplanes[(uint64_t)k * n_pad + f] = __double2float_rn(v[k] - o3[k % 3]);
     }
 
     // ---- per-object statistics, warp-aggregated when the warp is one object
@@ -231,6 +236,8 @@ void geom_build(Geom* g, const double* host_tri9, uint64_t n, const uint64_t* ho
     CK(cudaMallocAsync(&ndeg, 2 * sizeof(unsigned long long), st));  // degenerate, non-finite
     CK(cudaMemsetAsync(ndeg, 0, 2 * sizeof(unsigned long long), st));
     CK(cudaMemsetAsync(g->planes, 0, (size_t)NF * g->n_pad * sizeof(double), st));
+    CK(cudaMallocAsync(&g->fplanes, (size_t)9 * g->n_pad * sizeof(float), st));
+    CK(cudaMemsetAsync(g->fplanes, 0, (size_t)9 * g->n_pad * sizeof(float), st));
 
     if (n && !tri9_on_device)
         h2d(staging, host_tri9, 9 * n * sizeof(double), st);
@@ -245,8 +252,18 @@ void geom_build(Geom* g, const double* host_tri9, uint64_t n, const uint64_t* ho
         CK(cudaGetLastError());
     }
     if (n) {
-        prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, n, g->n_pad, g->d_off, n_obj,
-                                                                g->planes, ustats, ndeg);
+        // FP32 frame origin: the first vertex of face 0 (one small read; no reduction needed)
+        if (tri9_on_device) {
+            CK(cudaMemcpyAsync(g->origin, src, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        } else {
+            std::copy(host_tri9, host_tri9 + 3, g->origin);
+        }
+        for (double& x : g->origin)
+            if (!std::isfinite(x)) x = 0.0;  // rejected below (non-finite count)
+        prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, n, g->n_pad, g->d_off, n_obj, g->planes, ustats,
+                                                                ndeg, g->fplanes, g->origin[0], g->origin[1],
+                                                                g->origin[2]);
         CK(cudaGetLastError());
         if (!g->h_tiles.empty()) {
             range_aabb_kernel<<<(unsigned)g->h_tiles.size(), 128, 0, st>>>(g->planes, n, g->n_pad, g->d_tiles, 0,
@@ -301,7 +318,9 @@ void geom_release(Geom* g, cudaStream_t st) {
     cudaFreeAsync(g->d_tiles, st);
     cudaFreeAsync(g->d_obj_stats, st);
     cudaFreeAsync(g->d_tile_aabb, st);
+    cudaFreeAsync(g->fplanes, st);
     g->planes = nullptr;
+    g->fplanes = nullptr;
 }
 
 }  // namespace tdb

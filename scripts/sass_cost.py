@@ -17,7 +17,7 @@ for addr, txt in ins:
         lo = int(m.group(1), 16)
         reg = [t for a, t in ins if lo <= a <= addr]
         nfp = sum(1 for t in reg if re.match(r"(@!?U?P\d+\s+)?D(FMA|MUL|ADD)", t))
-        if nfp >= 100:
+        if nfp >= (int(sys.argv[3]) if len(sys.argv) > 3 else 100):
             cands.append((lo, addr, nfp, reg))
 inner = [c for c in cands if not any(o is not c and c[0] <= o[0] and o[1] <= c[1] for o in cands)]
 best = max(inner, key=lambda c: c[2])[3]
