@@ -121,7 +121,10 @@ static __device__ __noinline__ bool slow_pair(const double* Ap, uint64_t An_pad,
     return exact::tri_tri_hit(ta, tb);
 }
 
-__global__ void __launch_bounds__(32 * kWarps) hit_kernel(HitArgs a) {
+#ifndef TDB_HIT_MINB
+#define TDB_HIT_MINB 4  // 4 CTAs/SM (128 registers): 1.33e12 vs 1.14e12 pairs/s at 3 (scripts/variants_hit.sh)
+#endif
+__global__ void __launch_bounds__(32 * kWarps, TDB_HIT_MINB) hit_kernel(HitArgs a) {
     __shared__ alignas(128) double sm[2][kHitPlanes * kSBH];
     __shared__ alignas(128) float smf[2][9 * kSBH];
     __shared__ alignas(8) uint64_t bar[2];
