@@ -239,7 +239,8 @@ class QueryWorkload:
             k = int(np.argmin(d))
             return float(d[k]), int(f[k])
         h, f = T.queries_mesh_intersects(q, self.dB)
-        return (0.0, int(f[h].min())) if h.any() else (float("inf"), U64_MAX)
+        lowest = int(f.min())  # UINT64_MAX for the queries without a hit
+        return (0.0, lowest) if lowest != U64_MAX else (float("inf"), U64_MAX)
 
     def run_host(self, T, pinA, pinB, b):
         r0, r1 = self.batch(b)
@@ -553,9 +554,12 @@ def main():
     if wl.op == "distance" and wl.name != "paper":
         roofline["fp64_pipe_frac"] = FILTER_DP_INSTR * f_pairs / (f_ms * 1e-3) / (fp64_tf * 1e12 / 2)
         roofline["executed_fp64_tflops"] = FILTER_FLOPS * f_pairs / (f_ms * 1e-3) / 1e12
-    else:
-        roofline["note"] = ("culled pairs skip the W_i work (conservative separating-plane test, "
+    elif wl.op == "intersects":
+        roofline["note"] = ("culled pairs skip the W_i work (conservative FP32/FP64 separating-plane test, "
                             "DESIGN.md 4.3): frac > 1 is algorithmic, not hardware")
+    else:
+        roofline["note"] = ("segment x triangle: W = 473 flops/pair is the reference composition's count "
+                            "(SURVEY.md 8(a) A10); the FP64 filter needs fewer, so frac can exceed 1")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

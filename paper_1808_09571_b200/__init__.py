@@ -524,7 +524,7 @@ def queries_mesh_intersects(q: Queries, mesh):
     m = _as_mesh(mesh)
     h, f = np.empty(q.n, np.uint8), np.empty(q.n, np.uint64)
     _check(lib().tdb_queries_mesh_intersects(q.handle, m.handle, h.ctypes.data_as(_U8), f.ctypes.data_as(_U64)))
-    return h.astype(bool), f
+    return h.view(bool), f  # 0/1 bytes: a zero-copy bool view
 
 
 def segments_mesh_distance(segments, mesh):

@@ -242,7 +242,10 @@ __device__ __forceinline__ double q_eta(const QueryRegs& Q, const double* Bs) {
 }
 
 // ---- fused path: the whole mesh is one chunk --------------------------------
-__global__ void __launch_bounds__(kTile, 3) q_fused_kernel(QArgs a, const double* Bs, double* out_d,
+#ifndef TDB_QF_MINB
+#define TDB_QF_MINB 4  // 128 registers: 31.9 vs 34.9 ms at 3 on the paper workload (scripts/variants_q.sh)
+#endif
+__global__ void __launch_bounds__(kTile, TDB_QF_MINB) q_fused_kernel(QArgs a, const double* Bs, double* out_d,
                                                            unsigned long long* out_f, unsigned long long* ncand,
                                                            unsigned long long* nrounds, NearLog near) {
     __shared__ alignas(128) double sm[2][kFilterPlanes * kSB];
