@@ -38,6 +38,7 @@ thread_local int t_device = -1;
 thread_local tdb_stats t_stats{};
 thread_local tdb::NearHost t_near;
 thread_local uint64_t t_wkt_literal = 0, t_wkt_pos = 0;
+thread_local unsigned long long* t_shared_hit = nullptr;
 
 std::mutex g_mu;
 std::vector<cudaStream_t> g_streams;  // library stream per device
@@ -119,6 +120,7 @@ tdb::Ctx ctx() {
     t_near.count = 0;
     t_near.entries.clear();
     c.near = &t_near;
+    c.shared_hit = t_shared_hit;
     return c;
 }
 
@@ -183,6 +185,8 @@ void upload(const double* tri9, uint64_t n, const uint64_t* off, uint64_t n_obj,
 }  // namespace
 
 cudaStream_t tdb::call_stream() { return ctx().stream; }
+
+void tdb::set_shared_hit(unsigned long long* p) { t_shared_hit = p; }
 
 int tdb::set_error(int rc, const std::string& msg) { return rc == TDB_OK ? (t_err.clear(), rc) : fail(rc, msg); }
 

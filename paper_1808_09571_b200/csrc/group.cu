@@ -159,6 +159,11 @@ struct tdb_group_s {
     std::vector<ncclComm_t> comms;
     std::vector<int64_t*> scratch;  // one int64 per member for the all-reduces
     std::vector<tdb_stats> stats;   // per member, of the last group call
+    // intersects early exit across devices: one lowest-hit word on member 0's
+    // device, reached by the others through peer access (NVLink); off when a
+    // member cannot map it
+    unsigned long long* shared_hit = nullptr;
+    bool early_exit = false;
     Workers* workers = nullptr;
     std::mutex call_mu;             // one group call at a time (NCCL ordering)
 };
@@ -267,12 +272,29 @@ int tdb_group_create(int n_devices, const int* devices, tdb_group* out) {
         return tdb::set_error(TDB_E_CUDA, msg);
     }
     g->workers = new Workers(g->devices);
+    std::vector<int> peer_ok(n_devices, 0);
     const int rc = g->workers->run([&](int r) {
         return member_guard([&] {
             CK(cudaMalloc(&g->scratch[r], sizeof(int64_t)));
+            if (r == 0) {
+                CK(cudaMalloc(&g->shared_hit, sizeof(unsigned long long)));
+                peer_ok[r] = 1;
+            } else if (g->devices[r] == g->devices[0]) {
+                peer_ok[r] = 1;
+            } else {
+                int can = 0;
+                CK(cudaDeviceCanAccessPeer(&can, g->devices[r], g->devices[0]));
+                if (can) {
+                    const cudaError_t e = cudaDeviceEnablePeerAccess(g->devices[0], 0);
+                    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                    else CK(e);
+                }
+                peer_ok[r] = can;
+            }
             return TDB_OK;
         });
     });
+    g->early_exit = std::all_of(peer_ok.begin(), peer_ok.end(), [](int x) { return x != 0; });
     if (rc != TDB_OK) {
         const std::string err = tdb_last_error();
         tdb_group_free(g);
@@ -287,6 +309,7 @@ void tdb_group_free(tdb_group g) {
     if (g->workers)
         g->workers->run([&](int r) {
             if (g->scratch[r]) cudaFree(g->scratch[r]);
+            if (r == 0 && g->shared_hit) cudaFree(g->shared_hit);
             return TDB_OK;
         });
     delete g->workers;
@@ -356,9 +379,23 @@ int tdb_group_mesh_mesh_intersects(tdb_group g, tdb_gmesh a, tdb_gmesh b, tdb_hi
     const int world = (int)g->devices.size();
     std::vector<tdb_hit_out> part(world);
     std::vector<int64_t> gp(world);
+    if (g->early_exit) {  // reset the shared lowest-hit word before any member starts
+        const int irc = g->workers->run([&](int r) {
+            return member_guard([&] {
+                if (r == 0) {
+                    CK(cudaMemsetAsync(g->shared_hit, 0xff, sizeof(unsigned long long), tdb::call_stream()));
+                    CK(cudaStreamSynchronize(tdb::call_stream()));
+                }
+                return TDB_OK;
+            });
+        });
+        if (irc != TDB_OK) return irc;
+    }
     const int rc = g->workers->run([&](int r) {
         const auto [r0, r1] = row_shard(a->n, world, r);
+        tdb::set_shared_hit(g->early_exit ? g->shared_hit : nullptr);
         const int crc = tdb_mesh_mesh_intersects_rows(a->member[r], r0, r1, b->member[r], &part[r]);
+        tdb::set_shared_hit(nullptr);
         tdb_last_stats(&g->stats[r]);
         return member_guard([&] {
             gp[r] = allreduce_min(g, r, crc == TDB_OK && part[r].hit ? (int64_t)part[r].pair : kNone);

@@ -309,7 +309,10 @@ void run_intersects(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit,
     NearHost near_all;
     const uint64_t per = std::max<uint64_t>(1, max_items() / n_chunks) * kWarps;
     for (const ASel& b : tile_batches(sel, per)) {
-        if (nobj == 1 && pair[0] != kNone) break;  // a later batch only holds higher pairs
+        // a batch whose lowest pair is above the best hit so far cannot lower it
+        // (the hit may come from this selection's earlier batches or, through
+        // a device group's shared word, from another member)
+        if (nobj == 1 && pair[0] != kNone && pair[0] < std::max(sel.A->h_tiles[b.tile0].row0, sel.row_lo) * B.n) break;
         const uint64_t k = b.obj1 - b.obj0;
         std::vector<uint8_t> h(k);
         std::vector<uint64_t> p(k);
@@ -356,10 +359,16 @@ void run_intersects_batch(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t
     const Geom& A = *sel.A;
     unsigned long long *objhit = nullptr, *nex = nullptr;
     double* Bstats = nullptr;
-    CK(cudaMallocAsync(&objhit, nobj * sizeof(unsigned long long), st));
+    // a device group's shared lowest-hit word (initialised by the group) or our own
+    const bool shared = cx.shared_hit != nullptr && nobj == 1;
+    if (shared) {
+        objhit = cx.shared_hit;
+    } else {
+        CK(cudaMallocAsync(&objhit, nobj * sizeof(unsigned long long), st));
+        CK(cudaMemsetAsync(objhit, 0xff, nobj * sizeof(unsigned long long), st));
+    }
     CK(cudaMallocAsync(&nex, sizeof(unsigned long long), st));
     CK(cudaMallocAsync(&Bstats, kObjStats * sizeof(double), st));
-    CK(cudaMemsetAsync(objhit, 0xff, nobj * sizeof(unsigned long long), st));
     CK(cudaMemsetAsync(nex, 0, sizeof(unsigned long long), st));
     CK(cudaMemcpyAsync(Bstats, B.stats, kObjStats * sizeof(double), cudaMemcpyHostToDevice, st));
     cudaEvent_t e0, e1, e2;
@@ -391,7 +400,7 @@ void run_intersects_batch(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t
     CK(cudaMemcpyAsync(hp.data(), objhit, nobj * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&hn, nex, sizeof hn, cudaMemcpyDeviceToHost, st));
     CK(cudaEventRecord(e2, st));
-    CK(cudaFreeAsync(objhit, st));
+    if (!shared) CK(cudaFreeAsync(objhit, st));
     CK(cudaFreeAsync(nex, st));
     CK(cudaFreeAsync(Bstats, st));
     if (caabb) CK(cudaFreeAsync(caabb, st));

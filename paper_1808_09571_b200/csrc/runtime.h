@@ -65,6 +65,7 @@ void geom_release(Geom* g, cudaStream_t st);
 // capi.cu: the calling thread's launch stream (binding its device), and
 // "set tdb_last_error() and return rc" for code outside capi.cu (group.cu)
 cudaStream_t call_stream();
+void set_shared_hit(unsigned long long* p);  // this thread's Ctx::shared_hit
 int set_error(int rc, const std::string& msg);
 // Caller buffers <-> device (host_copy.cu): large pageable buffers go through
 // pinned staging, page-locked ones straight to the copy engine. h2d is
@@ -94,6 +95,10 @@ struct Ctx {
     int sms;
     tdb_stats* stats;
     NearHost* near;
+    // device groups (group.cu): a lowest-hit word shared by every member
+    // (peer memory over NVLink), so a hit on one device stops the others
+    // early; null outside group calls
+    unsigned long long* shared_hit = nullptr;
 };
 
 // Device side of the near-degenerate log for one call.

@@ -89,3 +89,18 @@ def test_group_rejects_bad_devices(monkeypatch):
     monkeypatch.setenv("TDB_GROUP_SHARED_DEVICES", "0")
     with pytest.raises(ValueError):
         T.Group([0, 0])
+
+
+def test_group_intersects_shared_early_exit_keeps_lowest_hit():
+    """Members share one lowest-hit word (intersects early exit across
+    devices): a hit found first by a member with higher rows must not stop
+    a member with lower rows from finding its lower hit."""
+    s = T.unit_sphere(10_000)
+    c = T.translate(s, 0.5, 0, 0)                       # hits
+    far = T.translate(s, 0, 0, 50.0)                    # no hits
+    for a in (np.concatenate([s, far, far, s]), np.concatenate([far, far, far, s]), np.concatenate([s, s, s, s])):
+        h = T.mesh_mesh_intersects(a, c)
+        for members in ([0], [0, 0], [0, 0, 0, 0], [0] * 8):
+            g = T.Group(members)
+            gh = g.mesh_mesh_intersects(g.mesh(a), g.mesh(c))
+            assert gh.hit == h.hit and gh.pair_index == h.pair_index, members
