@@ -350,22 +350,6 @@ T* dalloc(size_t n, cudaStream_t st) {
     return p;
 }
 
-// Per-thread timing events (created once: cudaEventCreate per call costs
-// more than a small call's kernels).
-struct EventPair {
-    cudaEvent_t e[4];
-    EventPair() {
-        for (auto& x : e) CK(cudaEventCreate(&x));
-    }
-    ~EventPair() {
-        for (auto& x : e) cudaEventDestroy(x);
-    }
-};
-
-EventPair& thread_events() {
-    thread_local EventPair ev;
-    return ev;
-}
 
 // Device scratch of one call, one allocation. The result block (objD, objP,
 // the witness, the counters, the near-degenerate log) is contiguous so one

@@ -371,10 +371,8 @@ void run_intersects_batch(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t
     CK(cudaMallocAsync(&Bstats, kObjStats * sizeof(double), st));
     CK(cudaMemsetAsync(nex, 0, sizeof(unsigned long long), st));
     CK(cudaMemcpyAsync(Bstats, B.stats, kObjStats * sizeof(double), cudaMemcpyHostToDevice, st));
-    cudaEvent_t e0, e1, e2;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    CK(cudaEventCreate(&e2));
+    EventPair& evs = thread_events();
+    cudaEvent_t e0 = evs.e[0], e1 = evs.e[1], e2 = evs.e[2];
     NearDev near;
     near.alloc(st);
     double* caabb = nullptr;
@@ -414,9 +412,6 @@ void run_intersects_batch(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t
     S.ms_filter = ms;
     CK(cudaEventElapsedTime(&ms, e0, e2));
     S.ms_total = ms;
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    cudaEventDestroy(e2);
     uint64_t pairs = 0;
     for (uint64_t t = sel.tile0; t < sel.tile1; ++t) {
         const Tile& T = A.h_tiles[t];

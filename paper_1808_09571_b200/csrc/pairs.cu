@@ -110,9 +110,8 @@ double fp64_peak(const Ctx& cx, double* ms_out) {
     double* out = nullptr;
     CK(cudaMallocAsync(&out, sizeof(double), st));
     const int blocks = cx.sms * 8, threads = 256, iters = 4096;
-    cudaEvent_t e0, e1;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
+    EventPair& evs = thread_events();
+    cudaEvent_t e0 = evs.e[0], e1 = evs.e[1];
     dfma_kernel<<<blocks, threads, 0, st>>>(out, 64, 0.999);  // warm-up
     CK(cudaEventRecord(e0, st));
     dfma_kernel<<<blocks, threads, 0, st>>>(out, iters, 0.999);
@@ -121,8 +120,6 @@ double fp64_peak(const Ctx& cx, double* ms_out) {
     CK(cudaStreamSynchronize(st));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, e0, e1));
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     CK(cudaFreeAsync(out, st));
     CK(cudaStreamSynchronize(st));
     if (ms_out) *ms_out = ms;

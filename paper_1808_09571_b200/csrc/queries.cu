@@ -643,8 +643,7 @@ void run_queries(const Ctx& cx, int op, const QuerySet& qs, const Geom& B, doubl
     unsigned long long* rP = (unsigned long long*)alloc(n * sizeof(unsigned long long));
     NearDev near;
     near.alloc(st);
-    cudaEvent_t ev[4];
-    for (auto& e : ev) CK(cudaEventCreate(&e));
+    cudaEvent_t* ev = thread_events().e;
     CK(cudaEventRecord(ev[0], st));
     QArgs a{qs.planes, n, qs.pad, qs.kind, B.planes, B.n_pad, B.n, n_chunks, chunk, nullptr, nullptr};
     uint64_t launches = 0, flagged = 0;
@@ -723,7 +722,6 @@ void run_queries(const Ctx& cx, int op, const QuerySet& qs, const Geom& B, doubl
     S.ms_verify = ms;
     CK(cudaEventElapsedTime(&ms, ev[0], ev[3]));
     S.ms_total = ms;
-    for (auto& e : ev) cudaEventDestroy(e);
     S.pairs = n * B.n;
     S.pairs_evaluated = n * B.n;
     S.items = n_items;
@@ -923,8 +921,7 @@ void run_literal_table(const Ctx& cx, int op, const QuerySet& q1, const Geom& B,
     NearDev near;
     near.alloc(st);
     QArgs a{q1.planes, 1, q1.pad, q1.kind, B.planes, B.n_pad, B.n, 1, B.n, nullptr, nullptr};
-    cudaEvent_t ev[2];
-    for (auto& e : ev) CK(cudaEventCreate(&e));
+    cudaEvent_t* ev = thread_events().e;
     CK(cudaEventRecord(ev[0], st));
     uint64_t launches = 0;
     int rounds = 0;
@@ -983,7 +980,6 @@ void run_literal_table(const Ctx& cx, int op, const QuerySet& q1, const Geom& B,
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
     S.ms_total = ms;
-    for (auto& e : ev) CK(cudaEventDestroy(e));
     S.pairs = B.n;
     S.pairs_evaluated = B.n;
     S.items = n_tiles;

@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstdint>
 #include <limits>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -100,6 +101,29 @@ struct Ctx {
     // early; null outside group calls
     unsigned long long* shared_hit = nullptr;
 };
+
+// Per-thread timing events, created once (cudaEventCreate per call costs
+// more than a small call's kernels, and nothing leaks on an error path).
+// A compute call records into e[0..3] and reads them before returning.
+struct EventPair {
+    cudaEvent_t e[4];
+    EventPair() {
+        for (auto& x : e) CK(cudaEventCreate(&x));
+    }
+    ~EventPair() {
+        for (auto& x : e) cudaEventDestroy(x);
+    }
+};
+
+// Events belong to a device: one set per (thread, current device).
+inline EventPair& thread_events() {
+    thread_local std::vector<std::unique_ptr<EventPair>> per_device;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if ((int)per_device.size() <= dev) per_device.resize(dev + 1);
+    if (!per_device[dev]) per_device[dev] = std::make_unique<EventPair>();
+    return *per_device[dev];
+}
 
 // Device side of the near-degenerate log for one call.
 struct NearDev {
