@@ -383,7 +383,8 @@ def run_reference(args, wl, rank, world):
     import paper_1808_09571_b200 as T
     wl.build(T, ref=True)
     threads = os.cpu_count() or 1
-    rows = max(1, args.ref_rows or max(1, wl.cpu_default_rows(threads) // 8))
+    # a whole number of rows per host thread (no idle threads in a step), ~3-4 s of CPU work per step
+    rows = args.ref_rows or max(threads, (wl.cpu_default_rows(threads) // 2) // threads * threads)
     for _ in range(args.warmup):
         wl.cpu_rate(rows, threads)
     total_pairs, total_t, kind, sample = 0.0, 0.0, "reference", ""
