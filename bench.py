@@ -565,7 +565,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        rows = args.cpu_rows or wl.cpu_default_rows(threads)
+        rows = args.cpu_rows or max(threads, wl.cpu_default_rows(threads) // threads * threads)  # whole rows per thread
         rate, dt, kind, sample = wl.cpu_rate(rows, threads)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind, "sample": f"{sample}, {dt:.1f} s"}
 
