@@ -7,9 +7,6 @@
 // boundary.
 #include <cuda_runtime.h>
 
-#include <chrono>
-#include <cstdio>
-#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -387,21 +384,13 @@ int tdb_table_eval(int op, tdb_table t, tdb_mesh lit, double* dist, uint8_t* hit
 }
 
 int tdb_distance_host(const double* a9, uint64_t n, const double* b9, uint64_t m, tdb_dist_out* out) {
-    static const bool trace = getenv("TDB_TRACE") != nullptr;
-    auto now = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
-    const double t0 = now();
     tdb_mesh a = nullptr, b = nullptr;
     int rc = tdb_mesh_upload(a9, n, &a);
-    const double t1 = now();
     if (rc == TDB_OK) rc = tdb_mesh_upload(b9, m, &b);
-    const double t2 = now();
     if (rc == TDB_OK) rc = tdb_mesh_mesh_distance(a, b, out);
-    const double t3 = now();
     const std::string err = t_err;
     tdb_mesh_free(a);
     tdb_mesh_free(b);
-    const double t4 = now();
-    if (trace) fprintf(stderr, "[tdb] distance_host upA %.2f upB %.2f eval %.2f free %.2f ms\n", t1 - t0, t2 - t1, t3 - t2, t4 - t3);
     t_err = err;
     return rc;
 }

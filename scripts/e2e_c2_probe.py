@@ -1,6 +1,5 @@
 """Break down the C2 e2e step (one-shot tdb_distance_host) against the resident step."""
-import os, sys, time
-os.environ["TDB_TRACE"] = "1"
+import sys, time
 sys.path.insert(0, '.')
 import numpy as np, torch
 import paper_1808_09571_b200 as T
@@ -24,8 +23,6 @@ for it in range(3):
     print(f"  upload A {1e3*(t2-t1):.1f}  upload B {1e3*(t3-t2):.1f}  eval {1e3*(t4-t3):.1f} (filter {s2['ms_filter']:.1f} total {s2['ms_total']:.1f})  free {1e3*(t5-t4):.1f}")
     print(f"  one-shot {1e3*(t6-t5):.1f} (filter {s3['ms_filter']:.1f} total {s3['ms_total']:.1f})")
     print("  ", {k: (s1[k], s2[k]) for k in s1 if s1[k] != s2[k]})
-import os
-os.environ["TDB_TRACE"] = "1"
 for it in range(4):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     r3 = T.distance_host(pA[it * R:(it + 1) * R], pB); t1 = time.perf_counter()
