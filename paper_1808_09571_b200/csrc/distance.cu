@@ -232,19 +232,46 @@ __global__ void __launch_bounds__(kTile) verify_kernel(VerifyArgs v) {
         const uint64_t o = T.obj - a.obj0;
         const double b2 = v.band2[o];
         const uint64_t i_loc = row - T.obj_row0;
-        for (uint64_t j = b0; j < b1; ++j) {
+        const int lane = threadIdx.x & 31;
+        for (uint64_t j = b0; j < b1; ++j) {  // uniform across the CTA
             if (__ldg(a.Bp + (uint64_t)F_DEG * a.Bn_pad + j) != 0.0) continue;
             const double d2 = pair_d2(A, FaceRefLdg{a.Bp + j, a.Bn_pad}, a.Ap + row, a.An_pad);
-            if (active && d2 <= b2) {
-                const exact::tri ta = load_tri(a.Ap, a.An_pad, row), tb = load_tri(a.Bp, a.Bn_pad, j);
-                const exact::res x = exact::tri_tri(ta, tb);
-                const unsigned long long bits = (unsigned long long)__double_as_longlong(x.d);
-                if (v.pass == 1) {
-                    atomicMin(v.objD + o, bits);
-                    atomicAdd(v.ncand, 1ull);
-                    if (exact::near_degenerate_pair(ta, tb)) near_log(v.near, a.obj0 + o, i_loc * a.Bn + j);
-                } else if (bits == v.objD[o]) {
-                    atomicMin(v.objP + o, i_loc * a.Bn + j);
+            unsigned m = __ballot_sync(0xffffffffu, active && d2 <= b2);
+            if (!m) continue;
+            // the warp evaluates its band pairs one at a time, the exact
+            // composition's six directed-edge seg_tri calls on six lanes
+            // (exact::tri_tri, both triangles non-degenerate here), then the
+            // same first-strict-minimum scan in the same order
+            const exact::tri tb = load_tri(a.Bp, a.Bn_pad, j);
+            while (m) {
+                const int src = __ffs(m) - 1;
+                m &= m - 1;
+                const uint64_t rc = __shfl_sync(0xffffffffu, row, src);
+                const exact::tri ta = load_tri(a.Ap, a.An_pad, rc);
+                double dk = pos_inf();
+                if (lane < 6) {
+                    const exact::tri& s = lane < 3 ? ta : tb;
+                    const exact::tri& t = lane < 3 ? tb : ta;
+                    const int e = lane % 3;
+                    const exact::v3 p0 = e == 0 ? s.v0 : e == 1 ? s.v1 : s.v2;
+                    const exact::v3 p1 = e == 0 ? s.v1 : e == 1 ? s.v2 : s.v0;
+                    dk = exact::seg_tri(p0, p1, t).d;
+                }
+                double x = pos_inf();
+#pragma unroll
+                for (int k = 0; k < 6; ++k) {
+                    const double c = __shfl_sync(0xffffffffu, dk, k);
+                    if (c < x) x = c;
+                }
+                if (lane == src) {
+                    const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+                    if (v.pass == 1) {
+                        atomicMin(v.objD + o, bits);
+                        atomicAdd(v.ncand, 1ull);
+                        if (exact::near_degenerate_pair(ta, tb)) near_log(v.near, a.obj0 + o, i_loc * a.Bn + j);
+                    } else if (bits == v.objD[o]) {
+                        atomicMin(v.objP + o, i_loc * a.Bn + j);
+                    }
                 }
             }
         }
