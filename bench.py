@@ -368,6 +368,16 @@ class ClockSampler:
                 "power_w_max": max(power), "samples": len(sm)}
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def base_line(args, wl, world, value, ms):
     return {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -567,7 +577,11 @@ def main():
         threads = os.cpu_count() or 1
         rows = args.cpu_rows or max(threads, wl.cpu_default_rows(threads) // threads * threads)  # whole rows per thread
         rate, dt, kind, sample = wl.cpu_rate(rows, threads)
-        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind, "sample": f"{sample}, {dt:.1f} s"}
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind, "sample": f"{sample}, {dt:.1f} s",
+               "cpu_model": cpu_model()}
+        # the single-core rate beside the all-core one (a one-thread sample of ~1-3 s)
+        r1, dt1, _, sample1 = wl.cpu_rate(max(1, rows // threads // 4), 1)
+        cpu["single_core"] = {"value": r1, "sample": f"{sample1}, {dt1:.1f} s"}
 
     if rank == 0:
         best = min(results) if results else (None, None)
