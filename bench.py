@@ -124,7 +124,8 @@ class MeshWorkload:
 
     def cpu_default_rows(self, threads):
         per_row = self.M / (1.0e6 if self.op == "distance" else 6.0e6)  # s per row on one core
-        return max(threads, int(10.0 * threads / max(per_row, 1e-6)))
+        # ~10-15 s of all-core work (R = 16 x nproc strided rows)
+        return max(threads, int(20.0 * threads / max(per_row, 1e-6)))
 
 
 class TableWorkload:
