@@ -1,3 +1,4 @@
+"""First-contact probe: FP64 peak, C2 distance at three row counts, C3 intersects (resident meshes)."""
 import time, sys, json
 sys.path.insert(0, '.')
 import numpy as np
