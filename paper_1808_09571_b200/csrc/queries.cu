@@ -266,10 +266,7 @@ __global__ void __launch_bounds__(kTile, TDB_QF_MINB) q_fused_kernel(QArgs a, co
     double best = pos_inf(), cut2 = pos_inf(), evicted = pos_inf();
     int nc = 0;
     S.run(a.Bp, a.Bn_pad, 0, a.Bn, [&](const double* sb, int cnt, uint64_t f0) {
-#pragma unroll 1
-        for (int j = 0; j < cnt; ++j) {
-            if (reinterpret_cast<const int*>(sb + F_DEG * kSB + j)[1] != 0) continue;  // degenerate face
-            const double d2 = query_d2(Q, FaceRef{sb + j, (uint64_t)kSB});
+        auto take = [&](double d2, int j) {  // candidate-list update for face f0 + j
             if (d2 < best) {  // new minimum: tighten the cut, drop what fell out of it
                 best = d2;
                 const double b = band_of(best);
@@ -294,7 +291,11 @@ __global__ void __launch_bounds__(kTile, TDB_QF_MINB) q_fused_kernel(QArgs a, co
                     }
                 }
             }
-        }
+        };
+        auto deg = [&](int j) { return reinterpret_cast<const int*>(sb + F_DEG * kSB + j)[1] != 0; };  // uniform
+#pragma unroll 1
+        for (int j = 0; j < cnt; ++j)
+            if (!deg(j)) take(query_d2(Q, FaceRef{sb + j, (uint64_t)kSB}), j);
     });
     double band = active && best < pos_inf() ? band_of(best) : -1.0;
     unsigned long long D = kNone, P = kNone, cand = 0;
