@@ -104,3 +104,16 @@ def test_group_intersects_shared_early_exit_keeps_lowest_hit():
             g = T.Group(members)
             gh = g.mesh_mesh_intersects(g.mesh(a), g.mesh(c))
             assert gh.hit == h.hit and gh.pair_index == h.pair_index, members
+
+
+def test_group_empty_and_single_face():
+    s = T.unit_sphere(80)
+    empty = np.zeros((0, 9))
+    for members in ([0], [0, 0, 0]):
+        g = T.Group(members)
+        r = g.mesh_mesh_distance(g.mesh(empty), g.mesh(s))
+        assert r.pair_index is None and r.distance == float("inf")
+        assert not g.mesh_mesh_intersects(g.mesh(s), g.mesh(empty)).hit
+        one = s[:1]
+        same_dist(g.mesh_mesh_distance(g.mesh(one), g.mesh(T.translate(s, 3, 0, 0))),
+                  T.mesh_mesh_distance(one, T.translate(s, 3, 0, 0)))
