@@ -216,8 +216,10 @@ int tdb_table_volume(tdb_table t, uint64_t chunk_size, double* volume_out);
  * tile-aligned ranges, a table splits its objects into contiguous ranges of
  * near-equal face count. The only exchange is an NCCL MIN all-reduce: the
  * distance (its int64 bits), then the pair among the members holding it
- * (lowest pair on ties); intersects: the lowest hit pair. Results are those
- * of the single-device calls. Group calls are serialised per group. */
+ * (lowest pair on ties); intersects: the lowest hit pair, with a shared
+ * lowest-hit word in peer memory so a hit on one device stops the work on
+ * the devices holding higher rows. Results are those of the single-device
+ * calls. Group calls are serialised per group. */
 typedef struct tdb_group_s* tdb_group;
 typedef struct tdb_gmesh_s* tdb_gmesh; /* a mesh or table replicated on the group */
 int tdb_group_create(int n_devices, const int* devices, tdb_group* out); /* devices NULL = 0..n-1 */
