@@ -37,7 +37,10 @@ struct Tile {
 
 constexpr int kTile = 128;          // A faces per CTA (one per thread)
 constexpr uint64_t kChunk = 8192;   // B faces per work item
-constexpr int kSB = 32;             // B faces per TMA-staged sub-tile
+#ifndef TDB_KSB
+#define TDB_KSB 32
+#endif
+constexpr int kSB = TDB_KSB;        // B faces per TMA-staged sub-tile
 constexpr int kPlanePad = 64;
 
 // per-object statistics (doubles): aabb lo xyz, hi xyz, max edge, max |coord|
