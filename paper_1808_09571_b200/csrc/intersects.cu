@@ -121,6 +121,13 @@ static __device__ __noinline__ bool slow_pair(const double* Ap, uint64_t An_pad,
     return exact::tri_tri_hit(ta, tb);
 }
 
+__global__ void hit_init_kernel(unsigned long long* objhit, uint64_t nobj, unsigned long long* nex,
+                                unsigned long long* near_count) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (objhit && i < nobj) objhit[i] = kNone;
+    if (i == 0) *nex = 0, *near_count = 0;
+}
+
 #ifndef TDB_HIT_MINB
 #define TDB_HIT_MINB 4  // 4 CTAs/SM (128 registers): 1.33e12 vs 1.14e12 pairs/s at 3 (scripts/variants_hit.sh)
 #endif
@@ -357,24 +364,37 @@ void run_intersects_batch(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t
     }
     if (nobj == 0 || n_items == 0) return;
     const Geom& A = *sel.A;
-    unsigned long long *objhit = nullptr, *nex = nullptr;
-    double* Bstats = nullptr;
+    // one scratch allocation; its head is the result block copied back in one
+    // piece: per-object lowest hit | exact-pair count | near-degenerate log
+    size_t off = 0;
+    auto piece = [&](size_t bytes) {
+        const size_t o = off;
+        off = (off + std::max<size_t>(bytes, 8) + 255) & ~size_t(255);
+        return o;
+    };
+    const size_t o_hit = piece(nobj * 8), o_nex = piece(8), o_nc = piece(8), o_ne = piece(2 * kNearLogCap * 8);
+    const size_t result_bytes = off;
+    char* base = nullptr;
+    CK(cudaMallocAsync(&base, off, st));
+    unsigned long long* nex = (unsigned long long*)(base + o_nex);
+    unsigned long long* near_count = (unsigned long long*)(base + o_nc);
+    const NearLog nlog{near_count, (unsigned long long*)(base + o_ne)};
     // a device group's shared lowest-hit word (initialised by the group) or our own
     const bool shared = cx.shared_hit != nullptr && nobj == 1;
-    if (shared) {
-        objhit = cx.shared_hit;
-    } else {
-        CK(cudaMallocAsync(&objhit, nobj * sizeof(unsigned long long), st));
-        CK(cudaMemsetAsync(objhit, 0xff, nobj * sizeof(unsigned long long), st));
+    unsigned long long* objhit = shared ? cx.shared_hit : (unsigned long long*)(base + o_hit);
+    hit_init_kernel<<<(unsigned)((std::max<uint64_t>(nobj, 1) + 255) / 256), 256, 0, st>>>(
+        shared ? nullptr : objhit, nobj, nex, near_count);
+    CK(cudaGetLastError());
+    // B's statistics: its one object's device header (a mesh), else a copy
+    double* Bstats = B.n_obj == 1 ? B.d_obj_stats : nullptr;
+    double* Bstats_copy = nullptr;
+    if (!Bstats) {
+        CK(cudaMallocAsync(&Bstats_copy, kObjStats * sizeof(double), st));
+        CK(cudaMemcpyAsync(Bstats_copy, B.stats, kObjStats * sizeof(double), cudaMemcpyHostToDevice, st));
+        Bstats = Bstats_copy;
     }
-    CK(cudaMallocAsync(&nex, sizeof(unsigned long long), st));
-    CK(cudaMallocAsync(&Bstats, kObjStats * sizeof(double), st));
-    CK(cudaMemsetAsync(nex, 0, sizeof(unsigned long long), st));
-    CK(cudaMemcpyAsync(Bstats, B.stats, kObjStats * sizeof(double), cudaMemcpyHostToDevice, st));
     EventPair& evs = thread_events();
     cudaEvent_t e0 = evs.e[0], e1 = evs.e[1], e2 = evs.e[2];
-    NearDev near;
-    near.alloc(st);
     double* caabb = nullptr;
     if (cx.mode == TDB_MODE_CULL) {
         CK(cudaMallocAsync(&caabb, n_chunks * 6 * sizeof(double), st));
@@ -389,20 +409,21 @@ void run_intersects_batch(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t
                                                                   sel.row_lo, sel.row_hi, B.planes, B.n_pad, B.n,
                                                                   n_chunks, chunk, sel.obj0, A.d_obj_stats, Bstats,
                                                                   objhit, nex, caabb ? A.d_tile_aabb : nullptr,
-                                                                  caabb, near.log, B.fplanes, B.origin[0],
+                                                                  caabb, nlog, B.fplanes, B.origin[0],
                                                                   B.origin[1], B.origin[2], rb});
     CK(cudaGetLastError());
     CK(cudaEventRecord(e1, st));
-    std::vector<unsigned long long> hp(nobj);
-    unsigned long long hn = 0;
-    CK(cudaMemcpyAsync(hp.data(), objhit, nobj * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&hn, nex, sizeof hn, cudaMemcpyDeviceToHost, st));
+    thread_local std::vector<unsigned long long> hres;
+    hres.resize(result_bytes / 8);
+    CK(cudaMemcpyAsync(hres.data(), base, result_bytes, cudaMemcpyDeviceToHost, st));
+    unsigned long long shared_best = kNone;
+    if (shared) CK(cudaMemcpyAsync(&shared_best, objhit, sizeof shared_best, cudaMemcpyDeviceToHost, st));
     CK(cudaEventRecord(e2, st));
-    if (!shared) CK(cudaFreeAsync(objhit, st));
-    CK(cudaFreeAsync(nex, st));
-    CK(cudaFreeAsync(Bstats, st));
+    CK(cudaFreeAsync(base, st));
+    if (Bstats_copy) CK(cudaFreeAsync(Bstats_copy, st));
     if (caabb) CK(cudaFreeAsync(caabb, st));
     CK(cudaStreamSynchronize(st));
+    const unsigned long long* hp = shared ? &shared_best : hres.data() + o_hit / 8;
     for (uint64_t o = 0; o < nobj; ++o) {
         pair[o] = hp[o];
         if (hit) hit[o] = hp[o] != kNone;
@@ -420,12 +441,14 @@ void run_intersects_batch(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t
     }
     S.pairs = pairs;
     S.items = n_items;
-    S.exact_pairs = hn;
+    S.exact_pairs = hres[o_nex / 8];
     S.pairs_evaluated = pairs;  // covered (early exit and culls are not subtracted)
-    S.kernels = 1;
+    S.kernels = 2;
     S.rounds = 1;
-    near.fetch(st, cx.near);
-    S.near_degenerate = cx.near->count;
+    const unsigned long long nc = hres[o_nc / 8];
+    cx.near->count = nc;
+    cx.near->entries.assign(hres.data() + o_ne / 8, hres.data() + o_ne / 8 + 2 * std::min<uint64_t>(nc, kNearLogCap));
+    S.near_degenerate = nc;
 }
 
 }  // namespace
