@@ -398,18 +398,22 @@ def run_reference(args, wl, rank, world):
     rows = args.ref_rows or max(threads, (wl.cpu_default_rows(threads) // 2) // threads * threads)
     for _ in range(args.warmup):
         wl.cpu_rate(rows, threads)
-    total_pairs, total_t, kind, sample = 0.0, 0.0, "reference", ""
+    total_pairs, total_t, kind, sample, rates = 0.0, 0.0, "reference", "", []
     for _ in range(args.steps):
         rate, dt, kind, sample = wl.cpu_rate(rows, threads)
         total_pairs += rate * dt
         total_t += dt
+        rates.append(rate)
     value = total_pairs / total_t
     out = base_line(args, wl, world, value, 1e3 * total_t)
     out.update({
         "impl": "reference",
         "config": {"workload": wl.desc, "op": wl.op, "parallelism": f"cpu{threads}"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": sample + " per step"},
+                         "sample": sample + " per step", "cpu_model": cpu_model(),
+                         # the reference's own timing rule (bench.cpp:54-59,82): mean and sample stddev over repeats
+                         "step_rate_mean": statistics.mean(rates),
+                         "step_rate_stddev": statistics.stdev(rates) if len(rates) > 1 else 0.0},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     })
     print(json.dumps(out), flush=True)
