@@ -420,15 +420,10 @@ __global__ void q_flag_kernel(QArgs a, uint64_t n_items, const double* band2, un
 }
 
 // exact rescan of flagged items, TMA-staged like the filter
-__global__ void __launch_bounds__(kTile, 4) q_verify_kernel(QArgs a, const unsigned long long* list, int pass,
-                                                            const double* band2, unsigned long long* qD,
-                                                            unsigned long long* qP, unsigned long long* ncand,
-                                                            NearLog near) {
-    __shared__ alignas(128) double sm[2][kFilterPlanes * kSB];
-    __shared__ alignas(8) uint64_t bar[2];
-    Stream<kFilterPlanes> S{sm, bar, kDistPlaneIds};
-    S.init();
-    const uint64_t item = list[blockIdx.x];
+template <class SS>
+__device__ __forceinline__ void q_verify_item(const QArgs& a, SS& S, uint64_t item, int pass, const double* band2,
+                                              unsigned long long* qD, unsigned long long* qP,
+                                              unsigned long long* ncand, const NearLog& near) {
     const uint64_t tl = item / a.n_chunks, ch = item - tl * a.n_chunks;
     const uint64_t q = min(tl * kTile + threadIdx.x, a.Qn - 1);
     const bool active = tl * kTile + threadIdx.x < a.Qn;
@@ -456,6 +451,21 @@ __global__ void __launch_bounds__(kTile, 4) q_verify_kernel(QArgs a, const unsig
         }
     });
     if (cand) atomicAdd(ncand, cand);
+}
+
+// Grid-stride over the flagged items (the count stays on the device: no
+// host round trip between the flag and verify passes).
+__global__ void __launch_bounds__(kTile, 4) q_verify_kernel(QArgs a, const unsigned long long* list,
+                                                            const unsigned long long* count, int pass,
+                                                            const double* band2, unsigned long long* qD,
+                                                            unsigned long long* qP, unsigned long long* ncand,
+                                                            NearLog near) {
+    __shared__ alignas(128) double sm[2][kFilterPlanes * kSB];
+    __shared__ alignas(8) uint64_t bar[2];
+    Stream<kFilterPlanes> S{sm, bar, kDistPlaneIds};
+    S.init();
+    const uint64_t nflag = *count;
+    for (uint64_t w = blockIdx.x; w < nflag; w += gridDim.x) q_verify_item(a, S, list[w], pass, band2, qD, qP, ncand, near);
 }
 
 __global__ void q_check_kernel(QArgs a, const double* Bs, double* band2, double* band, unsigned long long* qD,
@@ -683,21 +693,17 @@ void run_queries(const Ctx& cx, int op, const QuerySet& qs, const Geom& B, doubl
             CK(cudaMemsetAsync(ctr + 2, 0, 2 * sizeof(unsigned long long), st));  // flagged, retry
             q_flag_kernel<<<(unsigned)((n_items + 255) / 256), 256, 0, st>>>(a, n_items, band2, list, ctr + 2);
             CK(cudaGetLastError());
-            unsigned long long nflag = 0;
-            CK(cudaMemcpyAsync(&nflag, ctr + 2, sizeof nflag, cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            flagged += nflag;
-            if (nflag) {
-                for (int pass = 1; pass <= 2; ++pass) {
-                    q_verify_kernel<<<(unsigned)nflag, kTile, 0, st>>>(a, list, pass, band2, rD, rP, ctr, near.log);
-                    CK(cudaGetLastError());
-                }
+            const unsigned vgrid = (unsigned)std::min<uint64_t>(n_items, (uint64_t)cx.sms * 4);
+            for (int pass = 1; pass <= 2; ++pass) {
+                q_verify_kernel<<<vgrid, kTile, 0, st>>>(a, list, ctr + 2, pass, band2, rD, rP, ctr, near.log);
+                CK(cudaGetLastError());
             }
             q_check_kernel<<<qb, 256, 0, st>>>(a, Bs, band2, band, rD, rP, ctr + 3);
             CK(cudaGetLastError());
             launches += 4;
             CK(cudaMemcpyAsync(hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
+            flagged += hc[2];
             if (hc[3] == 0 || rounds >= 8) break;
         }
         CK(cudaEventRecord(ev[2], st));
