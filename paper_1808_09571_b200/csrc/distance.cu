@@ -385,7 +385,7 @@ struct DistScratch {
     unsigned long long* objD;  // result block begins here
     unsigned long long* objP;
     double* wit;
-    unsigned long long* ctr;   // flagged, candidates, retry, pairs evaluated
+    unsigned long long* ctr;   // [1] candidates, [3] pairs evaluated; round r: [4+2r] flagged, [5+2r] retry
     unsigned long long* near_count;
     unsigned long long* near_entries;
     size_t result_bytes;       // objD .. near_entries end
@@ -397,11 +397,14 @@ struct DistScratch {
     void* base;
 };
 
+constexpr int kMaxRounds = 8;                  // band widenings (2 in practice)
+constexpr int kCtrSlots = 4 + 2 * kMaxRounds;  // per-round counters: no memsets between rounds
+
 __global__ void dist_init_kernel(unsigned long long* objmin, uint64_t nobj, unsigned long long* ctr, double* wit,
                                  unsigned long long* near_count) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < nobj) objmin[i] = kNone;
-    if (i < 4) ctr[i] = 0;
+    if (i < kCtrSlots) ctr[i] = 0;
     if (i < 6) wit[i] = 0.0;
     if (i == 0) *near_count = 0;
 }
@@ -483,7 +486,7 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
         off = (off + std::max<size_t>(bytes, 8) + 255) & ~size_t(255);
         return o;
     };
-    const size_t o_D = piece(nobj * 8), o_P = piece(nobj * 8), o_w = piece(6 * 8), o_c = piece(4 * 8),
+    const size_t o_D = piece(nobj * 8), o_P = piece(nobj * 8), o_w = piece(6 * 8), o_c = piece(kCtrSlots * 8),
                  o_nc = piece(8), o_ne = piece(2 * kNearLogCap * 8);
     const size_t result_end = off;
     const size_t o_im = piece(n_items * 8), o_om = piece(nobj * 8), o_b2 = piece(nobj * 8), o_b = piece(nobj * 8),
@@ -563,18 +566,18 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
     unsigned long long flagged_total = 0;
     for (;;) {
         ++rounds;
-        CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));          // flagged count
-        CK(cudaMemsetAsync(ctr + 2, 0, sizeof(unsigned long long), st));      // retry count
+        unsigned long long* const flagged = ctr + 4 + 2 * (rounds - 1);  // zeroed by dist_init_kernel
+        unsigned long long* const retry = flagged + 1;
         flag_kernel<<<(unsigned)((n_items + 255) / 256), 256, 0, st>>>(
-            FlagArgs{A.d_tiles, sel.tile0, n_chunks, n_items, sel.obj0, sc.itemmin, sc.band2, sc.list, ctr});
+            FlagArgs{A.d_tiles, sel.tile0, n_chunks, n_items, sel.obj0, sc.itemmin, sc.band2, sc.list, flagged});
         CK(cudaGetLastError());
         for (int pass = 1; pass <= 2; ++pass) {
             verify_kernel<<<vgrid, kTile, 0, st>>>(
-                VerifyArgs{da, sc.list, ctr, nsplit, pass, sc.band2, sc.objD, sc.objP, ctr + 1, nlog});
+                VerifyArgs{da, sc.list, flagged, nsplit, pass, sc.band2, sc.objD, sc.objP, ctr + 1, nlog});
             CK(cudaGetLastError());
         }
         check_kernel<<<ob, 256, 0, st>>>(CheckArgs{nobj, sel.obj0, A.d_obj_stats, Bstats, sc.band2, sc.band,
-                                                   sc.objD, sc.objP, ctr + 2});
+                                                   sc.objD, sc.objP, retry});
         CK(cudaGetLastError());
         launches += 4;
         if (want_witness) {  // for this round's winner; recomputed if the band widens
@@ -584,13 +587,12 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
             CK(cudaGetLastError());
             ++launches;
         }
+        CK(cudaEventRecord(ev.e[2], st));  // end of the device work (the last round's record stands)
         CK(cudaMemcpyAsync(hres.data(), base, sc.result_bytes, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        flagged_total += h_ctr[0];
-        if (h_ctr[2] == 0 || rounds >= 8) break;
+        flagged_total += h_ctr[4 + 2 * (rounds - 1)];
+        if (h_ctr[5 + 2 * (rounds - 1)] == 0 || rounds >= kMaxRounds) break;
     }
-    CK(cudaEventRecord(ev.e[2], st));
-    CK(cudaEventRecord(ev.e[3], st));
     CK(cudaFreeAsync(base, st));
     for (void* p : {(void*)Bstats_copy, (void*)perm, (void*)lb2, cull_mem[0], cull_mem[1], cull_mem[2], cull_mem[3]})
         if (p) CK(cudaFreeAsync(p, st));
@@ -605,13 +607,13 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
         }
     }
     if (want_witness) std::memcpy(witness6, hres.data() + o_w / 8, 6 * sizeof(double));
-    CK(cudaEventSynchronize(ev.e[3]));
+    CK(cudaEventSynchronize(ev.e[2]));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, ev.e[0], ev.e[1]));
     S.ms_filter = ms;
     CK(cudaEventElapsedTime(&ms, ev.e[1], ev.e[2]));
     S.ms_verify = ms;
-    CK(cudaEventElapsedTime(&ms, ev.e[0], ev.e[3]));
+    CK(cudaEventElapsedTime(&ms, ev.e[0], ev.e[2]));
     S.ms_total = ms;
     uint64_t pairs = 0;
     for (uint64_t t = sel.tile0; t < sel.tile1; ++t) {
