@@ -65,7 +65,7 @@ struct HitArgs {
     const double* tile_aabb;
     const double* chunk_aabb;
     NearLog near;
-    // FP32 pre-cull: B's vertices relative to its origin (9 float planes),
+    // FP32 pre-cull: B's vertices relative to its origin (3 float4 planes),
     // the origin, and a bound on |v - origin| over B
     const float* Bf;
     double ox, oy, oz, RB;
@@ -133,7 +133,7 @@ __global__ void hit_init_kernel(unsigned long long* objhit, uint64_t nobj, unsig
 #endif
 __global__ void __launch_bounds__(32 * kWarps, TDB_HIT_MINB) hit_kernel(HitArgs a) {
     __shared__ alignas(128) double sm[2][kHitPlanes * kSBH];
-    __shared__ alignas(128) float smf[2][9 * kSBH];
+    __shared__ alignas(128) float4 smf[2][3 * kSBH];
     __shared__ alignas(8) uint64_t bar[2];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -219,13 +219,15 @@ __global__ void __launch_bounds__(32 * kWarps, TDB_HIT_MINB) hit_kernel(HitArgs 
         const uint64_t f0 = b0 + (uint64_t)s * kSBH;
         const int cnt = (int)min((uint64_t)kSBH, b1 - f0);
         const uint32_t bytes = (uint32_t)(((cnt + 1) & ~1) * sizeof(double));
-        const uint32_t fbytes = (uint32_t)(((cnt + 3) & ~3) * sizeof(float));
-        mbar_expect_tx(&bar[st], bytes * kHitPlanes + fbytes * 9);
+        const uint32_t fbytes = (uint32_t)(cnt * sizeof(float4));
+        mbar_expect_tx(&bar[st], bytes * kHitPlanes + fbytes * 3);
 #pragma unroll 1
         for (int f = 0; f < kHitPlanes; ++f)
             bulk_g2s(&sm[st][f * kSBH], a.Bp + (uint64_t)kHitPlaneOf[f] * a.Bn_pad + f0, bytes, &bar[st]);
 #pragma unroll 1
-        for (int f = 0; f < 9; ++f) bulk_g2s(&smf[st][f * kSBH], a.Bf + (uint64_t)f * a.Bn_pad + f0, fbytes, &bar[st]);
+        for (int f = 0; f < 3; ++f)
+            bulk_g2s(&smf[st][f * kSBH], reinterpret_cast<const float4*>(a.Bf) + (uint64_t)f * a.Bn_pad + f0, fbytes,
+                     &bar[st]);
     };
     if (threadIdx.x == 0) {
         issue(0);
@@ -248,15 +250,14 @@ __global__ void __launch_bounds__(32 * kWarps, TDB_HIT_MINB) hit_kernel(HitArgs 
             }
         }
         if (__any_sync(0xffffffffu, live != 0)) {
-            const float* fb = smf[st];
+            const float4* fb = smf[st];
             const int* degw = reinterpret_cast<const int*>(sb + HS_DEG * kSBH) + 1;  // high words
 #pragma unroll 1
             for (int j = 0; j < cnt; ++j) {
                 if (degw[2 * j] != 0) continue;  // uniform
-                const float* fv = fb + j;
-                const float X0 = fv[0], Y0 = fv[kSBH], Z0 = fv[2 * kSBH];
-                const float X1 = fv[3 * kSBH], Y1 = fv[4 * kSBH], Z1 = fv[5 * kSBH];
-                const float X2 = fv[6 * kSBH], Y2 = fv[7 * kSBH], Z2 = fv[8 * kSBH];
+                const float4 V0 = fb[j], V1 = fb[kSBH + j], V2 = fb[2 * kSBH + j];  // 3 x LDS.128
+                const float X0 = V0.x, Y0 = V0.y, Z0 = V0.z, X1 = V1.x, Y1 = V1.y, Z1 = V1.z;
+                const float X2 = V2.x, Y2 = V2.y, Z2 = V2.z;
                 bool sep[kRows];
 #pragma unroll
                 for (int r = 0; r < kRows; ++r) {  // FP32 pre-cull

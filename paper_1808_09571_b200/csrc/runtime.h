@@ -54,7 +54,8 @@ struct Geom {
     std::vector<uint64_t> obj_tile0;   // first tile of each object (n_obj + 1)
     double stats[kObjStats] = {};      // aggregate: aabb lo/hi, max edge, max |coord|
     // FP32 copies of the vertices relative to `origin` (the first vertex of
-    // face 0): 9 planes of n_pad floats, for the intersects FP32 pre-cull
+    // face 0): 3 planes (one per vertex) of n_pad float4 (x, y, z, 0), for
+    // the intersects FP32 pre-cull
     double origin[3] = {0.0, 0.0, 0.0};
     float* fplanes = nullptr;
 };

@@ -99,7 +99,10 @@ __global__ void prep_kernel(const double* __restrict__ aos, uint64_t n, uint64_t
         }
         const double o3[3] = {ox, oy, oz};
 #pragma unroll
-        for (int k = 0; k < 9; ++k) fplanes[(uint64_t)k * n_pad + f] = __double2float_rn(v[k] - o3[k % 3]);
+        for (int k = 0; k < 3; ++k)  // vertex k as one float4 (x, y, z, 0) in plane k
+            reinterpret_cast<float4*>(fplanes)[(uint64_t)k * n_pad + f] =
+                make_float4(__double2float_rn(v[3 * k] - o3[0]), __double2float_rn(v[3 * k + 1] - o3[1]),
+                            __double2float_rn(v[3 * k + 2] - o3[2]), 0.0f);
     }
 
     // ---- per-object statistics, warp-aggregated when the warp is one object
@@ -236,8 +239,8 @@ void geom_build(Geom* g, const double* host_tri9, uint64_t n, const uint64_t* ho
     CK(cudaMallocAsync(&ndeg, 2 * sizeof(unsigned long long), st));  // degenerate, non-finite
     CK(cudaMemsetAsync(ndeg, 0, 2 * sizeof(unsigned long long), st));
     CK(cudaMemsetAsync(g->planes, 0, (size_t)NF * g->n_pad * sizeof(double), st));
-    CK(cudaMallocAsync(&g->fplanes, (size_t)9 * g->n_pad * sizeof(float), st));
-    CK(cudaMemsetAsync(g->fplanes, 0, (size_t)9 * g->n_pad * sizeof(float), st));
+    CK(cudaMallocAsync(&g->fplanes, (size_t)3 * g->n_pad * sizeof(float4), st));
+    CK(cudaMemsetAsync(g->fplanes, 0, (size_t)3 * g->n_pad * sizeof(float4), st));
 
     if (n && !tri9_on_device)
         h2d(staging, host_tri9, 9 * n * sizeof(double), st);
