@@ -87,6 +87,21 @@ constexpr double kCull32 = 1e-6;
 // all three h on one side, beyond tau: min > tau or max < -tau. (A NaN h
 // needs an infinite input; the caller sets tau = +inf whenever FP32 could
 // overflow, and then nothing is separated here.)
+// Packed FP32 pairs (two rows at once): ptxas folds a {x, x} pack into an
+// FFMA2 scalar-broadcast operand, so one FFMA2 does the FMA of two rows.
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+    unsigned long long d;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(a), "f"(b));
+    return d;
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ float lo2(unsigned long long x) { return __uint_as_float((unsigned)x); }
+__device__ __forceinline__ float hi2(unsigned long long x) { return __uint_as_float((unsigned)(x >> 32)); }
+
 __device__ __forceinline__ bool separated32(float h0, float h1, float h2, float tau) {
     return fminf(fminf(h0, h1), h2) > tau || fmaxf(fmaxf(h0, h1), h2) < -tau;
 }
@@ -194,6 +209,14 @@ __global__ void __launch_bounds__(32 * kWarps, TDB_HIT_MINB) hit_kernel(HitArgs 
         const double t32 = kCull32 * (a.RB + fabs(cB)) + tau;
         tau32[r] = a.RB + fabs(cB) < 1e30 ? __double2float_ru(t32) : __int_as_float(0x7f800000);  // +inf: no FP32 cull
     }
+    static_assert(kRows % 2 == 0, "rows are packed in pairs");
+    unsigned long long nq[kRows / 2][3], cq[kRows / 2];  // {row 2q, row 2q+1}
+#pragma unroll
+    for (int q = 0; q < kRows / 2; ++q) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) nq[q][k] = pk2(an32[2 * q][k], an32[2 * q + 1][k]);
+        cq[q] = pk2(-ac32[2 * q], -ac32[2 * q + 1]);
+    }
     const uint64_t Bn = a.Bn;
     auto row_pmin = [&](int r, uint64_t f0) { return (rowv[r] - T.obj_row0) * Bn + f0; };
     {  // a lower pair of this object already hit: nothing here can lower it
@@ -260,11 +283,15 @@ __global__ void __launch_bounds__(32 * kWarps, TDB_HIT_MINB) hit_kernel(HitArgs 
                 const float X2 = V2.x, Y2 = V2.y, Z2 = V2.z;
                 bool sep[kRows];
 #pragma unroll
-                for (int r = 0; r < kRows; ++r) {  // FP32 pre-cull
-                    const float h0 = fmaf(an32[r][0], X0, fmaf(an32[r][1], Y0, fmaf(an32[r][2], Z0, -ac32[r])));
-                    const float h1 = fmaf(an32[r][0], X1, fmaf(an32[r][1], Y1, fmaf(an32[r][2], Z1, -ac32[r])));
-                    const float h2 = fmaf(an32[r][0], X2, fmaf(an32[r][1], Y2, fmaf(an32[r][2], Z2, -ac32[r])));
-                    sep[r] = separated32(h0, h1, h2, tau32[r]);
+                for (int q = 0; q < kRows / 2; ++q) {  // FP32 pre-cull, rows 2q and 2q+1 packed
+                    const unsigned long long h0 =
+                        ffma2(nq[q][0], pk2(X0, X0), ffma2(nq[q][1], pk2(Y0, Y0), ffma2(nq[q][2], pk2(Z0, Z0), cq[q])));
+                    const unsigned long long h1 =
+                        ffma2(nq[q][0], pk2(X1, X1), ffma2(nq[q][1], pk2(Y1, Y1), ffma2(nq[q][2], pk2(Z1, Z1), cq[q])));
+                    const unsigned long long h2 =
+                        ffma2(nq[q][0], pk2(X2, X2), ffma2(nq[q][1], pk2(Y2, Y2), ffma2(nq[q][2], pk2(Z2, Z2), cq[q])));
+                    sep[2 * q] = separated32(lo2(h0), lo2(h1), lo2(h2), tau32[2 * q]);
+                    sep[2 * q + 1] = separated32(hi2(h0), hi2(h1), hi2(h2), tau32[2 * q + 1]);
                 }
                 if (sep[0] & sep[1] & sep[2] & sep[3]) continue;  // the common case: all four culled
                 unsigned need = 0;
