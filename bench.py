@@ -53,6 +53,7 @@ W_I = 282.0            # algorithmic FP64 flops per pair, intersects no-hit (SUR
 FILTER_DP_INSTR = 304  # FP64-pipe instructions per pair in filter_kernel (cuobjdump -sass count)
 FILTER_FLOPS = 478     # executed FP64 flops per pair (174 DFMA x 2 + 79 DMUL + 51 DADD)
 U64_MAX = (1 << 64) - 1
+C3S_AXIS, C3S_ANGLE = (1.0, 2.0, 3.0), 0.37  # C3 stress variant rotation
 
 
 def env_int(k, d):
@@ -63,9 +64,71 @@ def env_int(k, d):
 
 
 # --------------------------------------------------------------------------
+# mesh sources. The GPU arm builds its inputs with the product's generators;
+# the reference arm (--impl reference) with the reference's own
+# (oracle/_ref: dataset.cpp, rng.hpp) and never imports the product package.
+# Both are pinned bit-for-bit to each other (tests/test_cpu_host.py).
+# --------------------------------------------------------------------------
+class ProductGen:
+    def __init__(self):
+        import paper_1808_09571_b200 as T
+        self.unit_sphere, self.ore_body, self.terrain = T.unit_sphere, T.ore_body, T.terrain
+        self.drills = lambda n, seed: T.drills(n, seed)
+
+
+class ReferenceGen:
+    def __init__(self):
+        import oracle as O
+        if O.REF is None:
+            raise RuntimeError("oracle/_ref (the reference build) is missing")
+        self.unit_sphere, self.ore_body, self.terrain = O.ref_unit_sphere, O.ref_ore_body, O.ref_terrain
+        self.drills = lambda n, seed: O.ref_make_drills(seed, n, 0)
+
+
+def translate(tris, dx=0.0, dy=0.0, dz=0.0):
+    """Per-vertex translation (fixtures.cpp:37-46 translated)."""
+    t = np.array(tris, dtype=np.float64, copy=True)
+    t[:, 0::3] += dx
+    t[:, 1::3] += dy
+    t[:, 2::3] += dz
+    return t
+
+
+def rotate_scale(tris, axis, angle, scale):
+    """scale * R(axis, angle) applied to every vertex (Rodrigues; C3's stress
+    variant: '0.999 A rotated')."""
+    k = np.asarray(axis, np.float64)
+    k = k / np.linalg.norm(k)
+    K = np.array([[0, -k[2], k[1]], [k[2], 0, -k[0]], [-k[1], k[0], 0]])
+    R = np.eye(3) + np.sin(angle) * K + (1.0 - np.cos(angle)) * (K @ K)
+    v = np.asarray(tris, np.float64).reshape(-1, 3) @ (scale * R).T
+    return np.ascontiguousarray(v.reshape(-1, 9))
+
+
+# --------------------------------------------------------------------------
 # workloads (SURVEY.md 8(d))
 # --------------------------------------------------------------------------
-class MeshWorkload:
+class Workload:
+    """Common step -> unit-range mapping. Units are A rows (mesh / query
+    workloads) or records (table). A step is one batch of `batch_units`
+    units. Weak scaling: rank r of W takes whole batch s*W + r. Strong
+    scaling: every rank takes its slice of batch s (tile-aligned contiguous
+    shards, shard.row_shards), so the job per step is fixed as W grows."""
+
+    align = 128
+
+    def span(self, s, rank=0, world=1, strong=False):
+        if not strong:
+            b = (s * world + rank) % self.n_batches
+            return b * self.batch_units, min(self.n_units, (b + 1) * self.batch_units)
+        b = s % self.n_batches
+        lo, hi = b * self.batch_units, min(self.n_units, (b + 1) * self.batch_units)
+        tiles = (hi - lo + self.align - 1) // self.align
+        t0, t1 = (tiles * rank) // world, (tiles * (rank + 1)) // world
+        return min(hi, lo + t0 * self.align), min(hi, lo + t1 * self.align)
+
+
+class MeshWorkload(Workload):
     """A x B mesh workload; a step is a batch of A rows against all of B."""
 
     table = False
@@ -73,33 +136,27 @@ class MeshWorkload:
     def __init__(self, name, op, desc, make, batch_rows):
         self.name, self.op, self.desc, self._make, self.batch_rows = name, op, desc, make, batch_rows
 
-    def build(self, T, ref=False):
-        self.A, self.B = self._make(T, ref)
+    def build(self, gen):
+        self.A, self.B = self._make(gen)
         self.NA, self.M = len(self.A), len(self.B)
         self.BR = min(self.batch_rows, self.NA)
         self.n_batches = (self.NA + self.BR - 1) // self.BR
+        self.n_units, self.batch_units = self.NA, self.BR
 
-    def batch(self, b):
-        b %= self.n_batches
-        return b * self.BR, min(self.NA, (b + 1) * self.BR)
-
-    def pairs(self, b):
-        r0, r1 = self.batch(b)
+    def pairs(self, r0, r1):
         return (r1 - r0) * self.M
 
     def upload(self, T):
         self.dA, self.dB = T.Mesh(self.A), T.Mesh(self.B)
 
-    def run(self, T, b):
-        r0, r1 = self.batch(b)
+    def run(self, T, r0, r1):
         if self.op == "distance":
             r = T.mesh_mesh_distance(self.dA, self.dB, rows=(r0, r1))
             return (r.distance, r.pair_index if r.pair_index is not None else U64_MAX)
         h = T.mesh_mesh_intersects(self.dA, self.dB, rows=(r0, r1))
         return (0.0 if h.hit else float("inf"), h.pair_index if h.hit else U64_MAX)
 
-    def run_host(self, T, pinA, pinB, b):
-        r0, r1 = self.batch(b)
+    def run_host(self, T, pinA, pinB, r0, r1):
         if self.op == "distance":
             r = T.distance_host(pinA[r0:r1], pinB)
             res = (r.distance, r.pair_index)
@@ -128,11 +185,12 @@ class MeshWorkload:
         return max(threads, int(20.0 * threads / max(per_row, 1e-6)))
 
 
-class TableWorkload:
+class TableWorkload(Workload):
     """C4: a table of small objects (records) x one query mesh; a step is a
     batch of records, each record getting its own distance (run_batch)."""
 
     table = True
+    align = 1
 
     def __init__(self, n_objects, batch_objects, op):
         self.name, self.op = "c4", op
@@ -140,10 +198,9 @@ class TableWorkload:
         self.desc = (f"C4: query orebody 81,920 tris vs table of {n_objects:,} objects x 1,280 tris "
                      f"(unit_sphere(1000) x U[2,10] + U(box)), per-record ST_3D{'Distance' if op == 'distance' else 'Intersects'}")
 
-    def build(self, T, ref=False):
-        import oracle as O
-        self.Q = O.ref_ore_body(100_000) if (ref and O.REF is not None) else T.ore_body(100_000)
-        base = T.unit_sphere(1000)
+    def build(self, gen):
+        self.Q = gen.ore_body(100_000)
+        base = gen.unit_sphere(1000)
         rng = np.random.default_rng(42)
         scale = rng.uniform(2.0, 10.0, self.n_objects)
         ctr = np.stack([rng.uniform(0, 1000, self.n_objects), rng.uniform(0, 1000, self.n_objects),
@@ -156,26 +213,21 @@ class TableWorkload:
         self.M = len(self.Q)
         self.n_batches = (self.n_objects + self.batch_objects - 1) // self.batch_objects
         self.NA = len(self.tab)
+        self.n_units, self.batch_units = self.n_objects, self.batch_objects
 
-    def objs(self, b):
-        b %= self.n_batches
-        return b * self.batch_objects, min(self.n_objects, (b + 1) * self.batch_objects)
-
-    def pairs(self, b):
-        o0, o1 = self.objs(b)
+    def pairs(self, o0, o1):
         return (o1 - o0) * self.nf * self.M
 
     def upload(self, T):
         off = np.arange(self.n_objects + 1, dtype=np.uint64) * self.nf
         self.dT, self.dQ = T.Table(self.tab, off), T.Mesh(self.Q)
 
-    def run(self, T, b):
+    def run(self, T, o0, o1):
         op = T.OP_DISTANCE if self.op == "distance" else T.OP_INTERSECTS
-        v, p = T.table_eval(op, self.dT, self.dQ, objects=self.objs(b))
+        v, p = T.table_eval(op, self.dT, self.dQ, objects=(o0, o1))
         return (float(np.min(v)) if self.op == "distance" else float(np.any(v)), int(p.min()) if len(p) else U64_MAX)
 
-    def run_host(self, T, pinT, pinQ, b):
-        o0, o1 = self.objs(b)
+    def run_host(self, T, pinT, pinQ, o0, o1):
         off = np.arange(o1 - o0 + 1, dtype=np.uint64) * self.nf
         t = T.Table(pinT[o0 * self.nf:o1 * self.nf], off)
         q = T.Mesh(pinQ)
@@ -188,7 +240,10 @@ class TableWorkload:
     def cpu_rate(self, rows, threads):
         import oracle as O
         kind = "reference" if O.REF is not None else "port"
-        f = O.ref_mesh_mesh_distance if O.REF is not None else O.mesh_mesh_distance
+        if self.op == "distance":
+            f = O.ref_mesh_mesh_distance if O.REF is not None else O.mesh_mesh_distance
+        else:
+            f = O.ref_mesh_mesh_intersects if O.REF is not None else O.mesh_mesh_intersects
         objs = max(1, rows)
         t0 = time.perf_counter()
         for o in range(objs):
@@ -200,10 +255,12 @@ class TableWorkload:
         return max(1, int(10.0 * threads * 1e6 / (self.nf * self.M)))
 
 
-class QueryWorkload:
+class QueryWorkload(Workload):
     """The paper's own workload: drill segments
     (make_drills, seed 42) x the ore body, per-segment distance_to_mesh /
     intersects_mesh. A step is one batch of drills against the whole ore."""
+
+    align = 1
 
     table = False
 
@@ -213,28 +270,25 @@ class QueryWorkload:
                      f"per-segment ST_3D{'Distance' if op == 'distance' else 'Intersects'} "
                      "(PAPER.md:352-361: 5M x 500 faces, 0.685 s on V100)")
 
-    def build(self, T, ref=False):
-        import oracle as O
-        self.A = O.ref_make_drills(42, self.n_drills, 0) if (ref and O.REF is not None) else T.drills(self.n_drills, 42)
-        self.B = O.ref_ore_body(self.face_target) if (ref and O.REF is not None) else T.ore_body(self.face_target)
+    def build(self, gen):
+        self.A = gen.drills(self.n_drills, 42)
+        self.B = gen.ore_body(self.face_target)
         self.NA, self.M = len(self.A), len(self.B)
         self.BR = min(self.batch_rows, self.NA)
         self.n_batches = (self.NA + self.BR - 1) // self.BR
+        self.n_units, self.batch_units = self.NA, self.BR
 
-    def batch(self, b):
-        b %= self.n_batches
-        return b * self.BR, min(self.NA, (b + 1) * self.BR)
-
-    def pairs(self, b):
-        r0, r1 = self.batch(b)
+    def pairs(self, r0, r1):
         return (r1 - r0) * self.M
 
     def upload(self, T):
         self.dB = T.Mesh(self.B)
-        self.dQ = [T.Queries(self.A[slice(*self.batch(b))]) for b in range(self.n_batches)]
+        self.dQ = {}
 
-    def run(self, T, b):
-        q = self.dQ[b % self.n_batches]
+    def run(self, T, r0, r1):
+        q = self.dQ.get((r0, r1))
+        if q is None:  # query columns are resident like the meshes (uploaded on first use, untimed in warmup)
+            q = self.dQ[(r0, r1)] = T.Queries(self.A[r0:r1])
         if self.op == "distance":
             d, f = T.queries_mesh_distance(q, self.dB)
             k = int(np.argmin(d))
@@ -243,8 +297,7 @@ class QueryWorkload:
         lowest = int(f.min())  # UINT64_MAX for the queries without a hit
         return (0.0, lowest) if lowest != U64_MAX else (float("inf"), U64_MAX)
 
-    def run_host(self, T, pinA, pinB, b):
-        r0, r1 = self.batch(b)
+    def run_host(self, T, pinA, pinB, r0, r1):
         m = T.Mesh(pinB)
         if self.op == "distance":
             res = T.segments_mesh_distance(pinA[r0:r1], m)
@@ -273,25 +326,24 @@ class QueryWorkload:
 def workload(name, op_override, objects):
     if name == "paper":
         return QueryWorkload(5_000_000, 500, op_override or "distance", 5_000_000)
-    def c1(T, ref):
-        import oracle as O
-        a = O.ref_unit_sphere(10000) if (ref and O.REF is not None) else T.unit_sphere(10000)
-        return a, T.translate(a, 2.5 if op_override != "intersects" else 0.5, 0, 0)
+    def c1(gen):
+        a = gen.unit_sphere(10000)
+        return a, translate(a, 2.5 if op_override != "intersects" else 0.5, 0, 0)
 
-    def c2(T, ref):
-        import oracle as O
-        ore = O.ref_ore_body(1_000_000) if (ref and O.REF is not None) else T.ore_body(1_000_000)
-        return T.terrain(1024, 512, 20.0, 42), ore
+    def c2(gen):
+        return gen.terrain(1024, 512, 20.0, 42), gen.ore_body(1_000_000)
 
-    def c3(T, ref):
-        import oracle as O
-        a = O.ref_unit_sphere(1_000_000) if (ref and O.REF is not None) else T.unit_sphere(1_000_000)
+    def c3(gen):
+        a = gen.unit_sphere(1_000_000)
         return a, a * 0.9
 
-    def c5(T, ref):
-        import oracle as O
-        a = O.ref_unit_sphere(10_000_000) if (ref and O.REF is not None) else T.unit_sphere(10_000_000)
-        return a, T.translate(a, 2.5, 0, 0)
+    def c3s(gen):
+        a = gen.unit_sphere(1_000_000)
+        return a, rotate_scale(a, C3S_AXIS, C3S_ANGLE, 0.999)
+
+    def c5(gen):
+        a = gen.unit_sphere(10_000_000)
+        return a, translate(a, 2.5, 0, 0)
 
     if name == "c1":
         op = op_override or "distance"
@@ -306,6 +358,11 @@ def workload(name, op_override, objects):
         return MeshWorkload("c3", op, "C3: 1,310,720-tri sphere vs 0.9x copy (overlapping AABBs, no hit: "
                             f"worst case), ST_3D{'Intersects' if op == 'intersects' else 'Distance'}", c3,
                             131072 if op == "intersects" else 65536)
+    if name == "c3s":
+        op = op_override or "intersects"
+        return MeshWorkload("c3s", op, "C3 stress: 1,310,720-tri sphere vs 0.999x copy rotated 0.37 rad about (1,2,3) "
+                            f"(surfaces 1e-3 apart, no hit), ST_3D{'Intersects' if op == 'intersects' else 'Distance'}",
+                            c3s, 131072 if op == "intersects" else 65536)
     if name == "c4":
         return TableWorkload(objects, 1000, op_override or "distance")
     if name == "c5":
@@ -383,16 +440,31 @@ def base_line(args, wl, world, value, ms):
     return {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
     }
 
 
+def config_of(args, wl, world):
+    """The workload's config dict; both arms print exactly this."""
+    return {"workload": wl.desc, "op": wl.op, "mode": args.mode,
+            "pairs_per_step": wl.pairs(*wl.span(0)) * (1 if args.scaling == "strong" else world),
+            "steps_per_job": wl.n_batches if args.scaling == "strong" else -(-wl.n_batches // world),
+            "parallelism": f"rows{world}",
+            "l2": "inputs larger than L2 (B / table stores of 288 B per face in HBM)"}
+
+
 def run_reference(args, wl, rank, world):
-    """--impl reference: the reference CPU path on the host cores (rank 0)."""
+    """--impl reference: the reference CPU path on the host cores (rank 0).
+    Inputs come from the reference's own generators (oracle/_ref); this arm
+    never imports paper_1808_09571_b200."""
     if rank != 0:
         return
-    import paper_1808_09571_b200 as T
-    wl.build(T, ref=True)
+    try:
+        gen = ReferenceGen()
+    except RuntimeError as e:
+        print(json.dumps({"impl": "reference", "unavailable": str(e)}), flush=True)
+        return
+    wl.build(gen)
     threads = os.cpu_count() or 1
     # a whole number of rows per host thread (no idle threads in a step), ~3-4 s of CPU work per step
     rows = args.ref_rows or max(threads, (wl.cpu_default_rows(threads) // 2) // threads * threads)
@@ -408,7 +480,7 @@ def run_reference(args, wl, rank, world):
     out = base_line(args, wl, world, value, 1e3 * total_t)
     out.update({
         "impl": "reference",
-        "config": {"workload": wl.desc, "op": wl.op, "parallelism": f"cpu{threads}"},
+        "config": config_of(args, wl, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
                          "sample": sample + " per step", "cpu_model": cpu_model(),
                          # the reference's own timing rule (bench.cpp:54-59,82): mean and sample stddev over repeats
@@ -419,13 +491,54 @@ def run_reference(args, wl, rank, world):
     print(json.dumps(out), flush=True)
 
 
+def spawn_ranks(n):
+    """--gpus N without a launcher: one process per GPU under
+    torch.distributed.run (the same launch the driver uses), rendezvous on
+    127.0.0.1; returns the launcher's exit code."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def plan_only(args, wl, rank, world):
+    """Host-only check of the rank plan (tests/test_bench_contract.py): every
+    rank reports the unit ranges it would evaluate in the timed steps; rank 0
+    prints them with n_gpus. Builds the workload's inputs (the shapes fix the
+    ranges) but touches no device."""
+    import torch.distributed as dist
+    from paper_1808_09571_b200 import shard
+    if world > 1:
+        dist.init_process_group(os.environ.get("TDB_BENCH_BACKEND", "gloo"))
+    wl.build(ProductGen())
+    strong = args.scaling == "strong"
+    mine = [wl.span(args.warmup + s, rank, world, strong) for s in range(args.steps)]
+    spans = [mine]
+    if world > 1:
+        spans = [None] * world
+        dist.all_gather_object(spans, mine)
+        # the answer every rank would hold after the step's reduction: here
+        # the lexicographic min over ranks of each rank's (first unit, rank)
+        d, p = shard.combine_min(float(mine[0][0]), rank)
+    else:
+        d, p = float(mine[0][0]), 0
+    if rank == 0:
+        print(json.dumps({"n_gpus": world, "scaling": args.scaling, "n_units": wl.n_units,
+                          "batch_units": wl.batch_units, "spans": spans, "combined": [d, p]}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=16)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "paper"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c3s", "c4", "c5", "paper"])
     ap.add_argument("--op", default=None, choices=[None, "distance", "intersects"])
     ap.add_argument("--batch-rows", type=int, default=0, help="A rows per step (0 = config default)")
     ap.add_argument("--objects", type=int, default=100_000, help="c4 table records")
@@ -434,15 +547,30 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--mode", default="full", choices=["full", "cull"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: each rank takes whole batches; strong: every step's batch is split over the ranks")
+    ap.add_argument("--plan-only", action="store_true",
+                    help="print the per-rank unit ranges of the timed steps and exit (no device work)")
     args = ap.parse_args()
-    assert args.warmup >= 0 and args.steps >= 1
+    assert args.warmup >= 0 and args.steps >= 1 and args.gpus >= 1
+
+    if "WORLD_SIZE" not in os.environ:
+        if args.gpus > 1 and args.impl == "ours":
+            return spawn_ranks(args.gpus)
+        world_env = args.gpus  # reference arm: rank 0 only, reporting the job's GPU count
+    else:
+        world_env = env_int("WORLD_SIZE", 1)
+        if world_env != args.gpus:
+            raise SystemExit(f"bench.py: WORLD_SIZE={world_env} but --gpus {args.gpus}")
 
     wl = workload(args.config, args.op, args.objects)
     if args.batch_rows and not wl.table:
         wl.batch_rows = args.batch_rows
-    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    rank, world, local = env_int("RANK", 0), world_env, env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
         return run_reference(args, wl, rank, world)
+    if args.plan_only:
+        return plan_only(args, wl, rank, world)
 
     import torch
     import torch.distributed as dist
@@ -456,6 +584,8 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         backend = os.environ.get("TDB_BENCH_BACKEND", "nccl")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines (nranks) stay in the log
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -470,23 +600,31 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    def max_over_ranks(x):
+    def over_ranks(x, op):
         if world == 1:
             return x
         t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=op)
         return float(t.item())
 
+    def max_over_ranks(x):
+        return over_ranks(x, dist.ReduceOp.MAX if world > 1 else None)
+
+    def sum_over_ranks(x):
+        return over_ranks(x, dist.ReduceOp.SUM if world > 1 else None)
+
     fp64_tf, _ = T.fp64_peak()
-    wl.build(T)
+    wl.build(ProductGen())
     wl.upload(T)
 
     results, k_ms, k_pairs, kernels = [], [], [], 0
 
+    strong = args.scaling == "strong"
+
     def step(s, record=True):
         nonlocal kernels
-        b = s * world + rank
-        d, p = wl.run(T, b)
+        lo, hi = wl.span(s, rank, world, strong)
+        d, p = wl.run(T, lo, hi)
         st = T.last_stats()
         d, p = shard.combine_min(d, p, device="cuda")  # NCCL MIN all-reduce (distance, then pair)
         if record:
@@ -494,7 +632,7 @@ def main():
             k_ms.append(st["ms_filter"])
             k_pairs.append(st["pairs"])
             kernels += st["kernels"]
-        return wl.pairs(b)
+        return wl.pairs(lo, hi)
 
     for s in range(args.warmup):
         step(s, record=False)
@@ -510,7 +648,7 @@ def main():
     barrier()
     clk = clocks.stop()
     ms = max_over_ranks(e0.elapsed_time(e1))
-    pairs_total = max_over_ranks(float(pairs_rank)) * world
+    pairs_total = sum_over_ranks(float(pairs_rank))  # units all ranks processed
     value = pairs_total / (ms * 1e-3)
 
     # ---- e2e: one-shot C-ABI calls from pinned host buffers -----------------
@@ -528,17 +666,17 @@ def main():
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
     for s in range(e2e_steps):
-        b = (args.warmup + s) * world + rank
-        _, hb, db = wl.run_host(T, pinA, pinB, b)
+        lo, hi = wl.span(args.warmup + s, rank, world, strong)
+        _, hb, db = wl.run_host(T, pinA, pinB, lo, hi)
         h2d += hb
         d2h += db
-        e2e_pairs += wl.pairs(b)
+        e2e_pairs += wl.pairs(lo, hi)
     e3.record(stream)
     barrier()
     wall_e2e = time.perf_counter() - t0
     clk_e2e = clocks_e2e.stop()
     ms_e2e = max_over_ranks(max(e2.elapsed_time(e3), wall_e2e * 1e3))
-    e2e_value = max_over_ranks(float(e2e_pairs)) * world / (ms_e2e * 1e-3)
+    e2e_value = sum_over_ranks(float(e2e_pairs)) / (ms_e2e * 1e-3)
 
     # ---- roofline of the roofline kernel -------------------------------------
     f_ms = sum(k_ms) / len(k_ms)
@@ -592,10 +730,7 @@ def main():
         best = min(results) if results else (None, None)
         out = base_line(args, wl, world, value, ms)
         out.update({
-            "config": {"workload": wl.desc, "op": wl.op, "mode": args.mode,
-                       "pairs_per_step": wl.pairs(0) * world, "steps_per_job": wl.n_batches,
-                       "parallelism": f"rows{world}",
-                       "l2": "inputs larger than L2 (B / table stores of 288 B per face in HBM)"},
+            "config": config_of(args, wl, world),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d // max(1, e2e_steps),
                     "d2h_bytes_per_step": d2h // max(1, e2e_steps), "steps": e2e_steps},
             "roofline": roofline, "cpu_baseline": cpu, "clocks": clk, "clocks_e2e": clk_e2e,

@@ -99,6 +99,8 @@ def _load_ref():
     L.ref_unit_sphere.restype = ct.c_uint64
     L.ref_ore_body.argtypes = [ct.c_uint64, _D]
     L.ref_ore_body.restype = ct.c_uint64
+    L.ref_terrain.argtypes = [ct.c_uint32, ct.c_uint32, ct.c_double, ct.c_uint64, _D]
+    L.ref_terrain.restype = ct.c_uint64
     L.ref_random_triangles.argtypes = [ct.c_uint64, ct.c_uint64, ct.c_double, ct.c_double, _D]
     for fn in ("ref_segments_mesh_distance", "ref_points_mesh_distance"):
         getattr(L, fn).argtypes = [_D, ct.c_uint64, _D, ct.c_uint64, ct.c_int, _D, _U64]
@@ -297,6 +299,14 @@ def ref_ore_body(face_target):
     n = REF.ref_ore_body(face_target, None)
     out = np.empty((n, 9), np.float64)
     REF.ref_ore_body(face_target, _dp(out))
+    return out
+
+
+def ref_terrain(nx=1024, ny=512, amp=20.0, seed=42):
+    """C2's terrain over the reference's Rng (ref_composition.cpp ref_terrain)."""
+    n = REF.ref_terrain(nx, ny, ct.c_double(amp), seed, None)
+    out = np.empty((n, 9), np.float64)
+    REF.ref_terrain(nx, ny, ct.c_double(amp), seed, _dp(out))
     return out
 
 

@@ -30,6 +30,7 @@
 #include <tindb/executor.hpp>
 #include <tindb/geometry.hpp>
 #include <tindb/kernels.hpp>
+#include <tindb/rng.hpp>
 #include <tindb/wkt.hpp>
 
 #include "support/fixtures.hpp"
@@ -250,6 +251,36 @@ void ref_random_triangles(std::uint64_t seed, std::uint64_t n, double lo, double
         Triangle t = tindb::fixtures::random_triangle(rng, lo, hi);
         std::memcpy(out + 9 * k, &t, sizeof(Triangle));
     }
+}
+
+// C2's terrain: the reference has no terrain generator, so
+// this is the NEW heightfield restated over the reference's own Rng
+// (rng.hpp:12-30, uniform(lo, hi) at :21): an nx x ny lattice over x, y in
+// [0, 1000], per-vertex z = rng.uniform(-amp, amp) in row-major order, two
+// CCW-up triangles per cell (v00 v10 v11, v00 v11 v01). The bench's reference
+// arm builds C2 from this, never from the product library; tests pin it
+// bit-for-bit to tdb_gen_terrain.
+std::uint64_t ref_terrain(std::uint32_t nx, std::uint32_t ny, double amp, std::uint64_t seed, double* out) {
+    const std::uint64_t faces = 2ull * nx * ny;
+    if (!out || nx == 0 || ny == 0) return faces;
+    tindb::Rng rng(seed);
+    const std::uint64_t W = nx + 1ull;
+    std::vector<Point3> v(W * (ny + 1ull));
+    for (std::uint32_t iy = 0; iy <= ny; ++iy)
+        for (std::uint32_t ix = 0; ix <= nx; ++ix)
+            v[iy * W + ix] = Point3{1000.0 * ix / nx, 1000.0 * iy / ny, rng.uniform(-amp, amp)};
+    std::uint64_t k = 0;
+    auto put = [&](const Point3& a, const Point3& b, const Point3& c) {
+        const Triangle t{a, b, c};
+        std::memcpy(out + 9 * k++, &t, sizeof(Triangle));
+    };
+    for (std::uint32_t iy = 0; iy < ny; ++iy)
+        for (std::uint32_t ix = 0; ix < nx; ++ix) {
+            const std::uint64_t r0 = iy * W, r1 = (iy + 1ull) * W;
+            put(v[r0 + ix], v[r0 + ix + 1], v[r1 + ix + 1]);
+            put(v[r0 + ix], v[r1 + ix + 1], v[r1 + ix]);
+        }
+    return faces;
 }
 
 std::uint64_t ref_unit_cube(double* out) { return copy_mesh(tindb::fixtures::unit_cube(), out); }

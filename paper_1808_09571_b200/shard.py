@@ -79,12 +79,13 @@ def combine_min(dist: float, pair: Optional[int], group=None, device=None) -> Tu
     """All ranks get the lexicographic (distance, pair) min over ranks."""
     import torch.distributed as dist_
 
-    p = U64_MAX if pair is None else int(pair)
+    none = pair is None or int(pair) == U64_MAX  # both spell "no pair" (callers pass either)
+    p = U64_MAX if none else int(pair)
     if not dist_.is_initialized() or dist_.get_world_size(group) == 1:
         return float(dist), p
     dbits = int(np.float64(dist).view(np.int64))  # >= 0 (or +inf): orders as the double
     gbits = _allreduce_min(dbits, group, device)
-    mine = p if (dbits == gbits and pair is not None) else I64_MAX
+    mine = p if (dbits == gbits and not none) else I64_MAX
     gp = _allreduce_min(mine, group, device)
     return float(np.int64(gbits).view(np.float64)), (U64_MAX if gp == I64_MAX else gp)
 
@@ -95,7 +96,8 @@ def combine_hit(pair: Optional[int], group=None, device=None) -> Optional[int]:
 
     if not dist_.is_initialized() or dist_.get_world_size(group) == 1:
         return pair
-    gp = _allreduce_min(I64_MAX if pair is None else int(pair), group, device)
+    none = pair is None or int(pair) == U64_MAX
+    gp = _allreduce_min(I64_MAX if none else int(pair), group, device)
     return None if gp == I64_MAX else gp
 
 

@@ -12,6 +12,7 @@ import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+import bench
 import oracle as O
 from paper_1808_09571_b200 import shard
 
@@ -55,8 +56,25 @@ def worker(rank, world, port, q):
         counts = [e - s for s, e in shard.object_shards(off, world)]
         allp = shard.gather_slices(pp, counts)
         alld = shard.gather_slices(dd, counts)
+        # no rank holds a pair: bench.py passes U64_MAX, the shard API None
+        nohit = (shard.combine_min(float("inf"), shard.U64_MAX), shard.combine_min(float("inf"), None),
+                 shard.combine_hit(shard.U64_MAX), shard.combine_hit(None))
+        # bench.py's own step -> rank plan, weak and strong, each step reduced
+        steps = {}
+        for strong in (False, True):
+            wl = bench.MeshWorkload("t", "distance", "t", lambda gen: (a, b), 128)
+            wl.build(None)
+            n_steps = wl.n_batches if strong else -(-wl.n_batches // world)
+            res = []
+            for s_ in range(n_steps):
+                lo, hi = wl.span(s_, rank, world, strong)
+                if not strong and s_ * world + rank >= wl.n_batches:
+                    lo, hi = 0, 0  # past the end of the job: this rank idles
+                d_, p_, f_, _, _ = O.mesh_mesh_distance(a, b, threads=1, rows=(lo, hi, 1))
+                res.append(shard.combine_min(d_, p_ if f_ else shard.U64_MAX))
+            steps[strong] = shard.lexmin(res)
         if rank == 0:
-            q.put((best, lowest, alld, allp))
+            q.put((best, lowest, alld, allp, nohit, steps))
     finally:
         dist.destroy_process_group()
 
@@ -88,7 +106,7 @@ def test_two_rank_gloo_reduction_matches_single_process():
     procs = [ctx.Process(target=worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    best, lowest, alld, allp = q.get(timeout=170)
+    best, lowest, alld, allp, nohit, steps = q.get(timeout=170)
     for p in procs:
         p.join(60)
         assert p.exitcode == 0
@@ -100,3 +118,8 @@ def test_two_rank_gloo_reduction_matches_single_process():
     t, off, qm = table()
     dd, pp = O.table_eval("distance", t, off, qm, threads=2)
     assert np.array_equal(alld.view(np.uint64), dd.view(np.uint64)) and np.array_equal(allp, pp)
+    inf = float("inf")
+    assert nohit == ((inf, shard.U64_MAX), (inf, shard.U64_MAX), None, None)
+    for strong in (False, True):
+        assert np.float64(steps[strong][0]).view(np.uint64) == np.float64(d).view(np.uint64), strong
+        assert steps[strong][1] == p, strong
