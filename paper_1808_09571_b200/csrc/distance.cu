@@ -149,8 +149,10 @@ struct BandArgs {
     unsigned long long* objP;
 };
 
-__device__ __forceinline__ double band_eta(const double* As, const double* Bs) {
-    return kBandEdge * fmax(As[6], Bs[6]) + kBandAbs * fmax(As[7], Bs[7]);
+// eta(m) (tdb_internal.h) for objects A and B. It grows with m, so a check
+// against eta(band) >= eta(D) is the safe side.
+__device__ __forceinline__ double band_eta(const double* As, const double* Bs, double m) {
+    return band_eta_of(fmax(As[6], Bs[6]), fmax(As[8], Bs[8]), fmax(As[7], Bs[7]), m);
 }
 
 __global__ void band_kernel(BandArgs a) {
@@ -164,8 +166,8 @@ __global__ void band_kernel(BandArgs a) {
         a.band[o] = -1.0;
         return;
     }
-    const double eta = band_eta(a.Astats + (a.obj0 + o) * kObjStats, a.Bstats);
-    const double b = sqrt(__longlong_as_double((long long)e)) * (1.0 + kBandRel) + 2.0 * eta;
+    const double m = sqrt(__longlong_as_double((long long)e));
+    const double b = m * (1.0 + kBandRel) + 2.0 * band_eta(a.Astats + (a.obj0 + o) * kObjStats, a.Bstats, m);
     a.band[o] = b;
     a.band2[o] = b * b * (1.0 + 4e-16);
 }
@@ -303,9 +305,10 @@ __global__ void check_kernel(CheckArgs a) {
     // d == kNone: no pair fell in the band although the band contains the
     // filter minimum -> cannot happen unless every in-band pair evaluated to
     // NaN/inf; treat as done.
-    const double eta = band_eta(a.Astats + (a.obj0 + o) * kObjStats, a.Bstats);
-    if (d != kNone && __longlong_as_double((long long)d) > b - eta) {
-        const double nb = __longlong_as_double((long long)d) * (1.0 + kBandRel) + 2.0 * eta;
+    const double* As = a.Astats + (a.obj0 + o) * kObjStats;
+    if (d != kNone && __longlong_as_double((long long)d) > b - band_eta(As, a.Bstats, b)) {
+        const double m = __longlong_as_double((long long)d);
+        const double nb = m * (1.0 + kBandRel) + 2.0 * band_eta(As, a.Bstats, m);
         a.band[o] = nb;
         a.band2[o] = nb * nb * (1.0 + 4e-16);
         a.objD[o] = kNone;

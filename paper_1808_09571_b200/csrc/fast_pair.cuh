@@ -8,9 +8,9 @@
 // Intersecting pairs are caught by a plane-straddle test followed by a
 // division-free piercing test (rare branch, out of line). Everything is
 // squared distances with FMA; the only reciprocal is rcp.approx
-// (MUFU.RCP64H) for the first s, which only perturbs the evaluated point pair
-// to second order (the value is always a distance between two real points of
-// the triangles). Per pair: 27 DADD (vertex differences) + 6 x 12
+// (MUFU.RCP64H) + one Newton step for the first s (the value is always a
+// distance between two real points of the triangles; its excess over the
+// true distance is bounded in DESIGN.md 4.2). Per pair: 27 DADD (vertex differences) + 6 x 12
 // (vertex/face) + 9 x 27 (edge/edge) = 342 FP64 pipe instructions, no
 // DDIV/DSQRT.
 //
@@ -48,6 +48,21 @@ __device__ __forceinline__ double rcp_approx(double x) {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
     return r;
+}
+
+// eta(m) of tdb_internal.h: L = max edge, kmax = max F_K, ext = max |coord|
+__device__ __forceinline__ double band_eta_of(double L, double kmax, double ext, double m) {
+    const double w = m + 4.0 * L;
+    return kBandEdge * sqrt(L * w) + kmax * w + kBandAbs * ext;
+}
+
+// 1/x to ~2^-40 relative: rcp.approx (MUFU.RCP64H, ~2^-20) plus one Newton
+// step (2 DFMA). Drops the first-parameter error of the edge/edge solve from
+// first order in 2^-20 to the cancellation floor of its num / den
+// (DESIGN.md 4.2).
+__device__ __forceinline__ double rcp_nr(double x) {
+    const double r = rcp_approx(x);
+    return fma(r, fma(-x, r, 1.0), r);
 }
 
 __device__ __forceinline__ bool all_nonneg(double a, double b, double c) {
@@ -142,14 +157,6 @@ static __device__ __noinline__ bool pierce_slow(const double* ap, uint64_t as, c
     return edges_pierce(hb, ub, vb) || edges_pierce(ha, ua, va);
 }
 
-// clamp to [0,1] on the high word only. Used for the first parameter
-// estimate, whose precision is already bounded by rcp.approx.
-__device__ __forceinline__ double clamp01_hi(double x) {
-    // the low word is kept as is (no register move to zero it): x >= 1 lands
-    // in [1 - 2^-20, 1), x < 0 on a subnormal
-    return __hiloint2double(min(max(__double2hiint(x), 0), 0x3fefffff), __double2loint(x));
-}
-
 constexpr int kInfHi = 0x7ff00000;  // high word of +inf
 
 
@@ -220,7 +227,7 @@ __device__ __forceinline__ double pair_d2(const AFace& A, const P& bt, const dou
             const double bbI = bb * ILb;
             const double den = fma(-bbI, bb, A.L[j]);
             const double num = fma(-bbI, fw, cw);
-            double s = clamp01_hi(num * rcp_approx(den));
+            double s = clamp01(num * rcp_nr(den));
             const double t = clamp01(fma(bb, s, -fw) * ILb);
             s = clamp01(fma(bb, t, cw) * A.IL[j]);
             const double dx = fma(s, ea[0], fma(-t, ebx, -w[j][0]));

@@ -7,27 +7,29 @@
 // no hit). The object result is the lowest hit pair p = i*|B| + j
 // (kernels.cpp:407-432).
 //
-// Per pair the kernel first runs a conservative separating-plane test in
-// FP64: if all three vertices of one triangle lie strictly on one side of
-// the other's plane by more than tau (tdb_internal.h: 1e-10 x diag of the
-// pair's bounding box + 1e-13 x max |coord|), no directed edge can pass the
-// reference predicate. Why: with heights h_P, h_Q of an edge's endpoints
-// above the other plane (same sign, |h| > tau), the reference's
-// t = h_P / (h_P - h_Q) lies outside [-1e-12, 1+1e-12] unless
-// min|h| <= (c*u + 2e-12)*|w| with |w| <= diag (kernels.cpp:243-244,
-// kernels.hpp:53-54), which tau exceeds >= 30x; an edge of the other
-// triangle lies in its own plane, at distance >= tau from this triangle.
-// Survivors run the bit-exact predicate (exact.cuh), so booleans and indices
-// are the reference's (tests/test_gpu_parity.py).
+// Culls (DESIGN.md 4.3 states and proves them; tdb_internal.h has the
+// constants). They bound what the reference's OWN arithmetic can report,
+// not only the exact geometry: its Cramer solve is noisy when a face is a
+// sliver (noise ~ K = |e0||e1|/|N|) or an edge is nearly parallel to the
+// other plane (noise up to 7.2e-3 D at its 1e-12 validity edge).
+//   one-way : the other triangle's vertices beyond (kCullOne + kappa) D on
+//             one side of this triangle's plane;
+//   two-way : each triangle's vertices beyond (kCullTwo + kappa) D of the
+//             other's plane (a t-rejection of all six edges);
+//   apart   : object / tile / chunk boxes separated by kApart D.
+// Everything else runs the bit-exact predicate (exact.cuh), so booleans and
+// indices are the reference's (tests/test_gpu_parity.py, test_gpu_bounds.py).
 //
 // Layout: one warp per A-tile, each lane holds four rows (register blocking:
 // one staged B face feeds four pair tests); B sub-tiles of kSBH faces are
-// TMA bulk copies (14 SoA planes) double-buffered on mbarriers.
+// TMA bulk copies (15 SoA planes + 3 FP32 vertex planes) double-buffered on
+// mbarriers. The hot test is the one-way cull of B's vertices against the
+// row's plane, in FP32 first.
 //
 // Early exit: a warp skips its tile when the object's current lowest hit is
 // below the tile's smallest pair index (kernels.cpp:413-415); a row stops at
-// its first hit; an object whose AABB header is separated from B's by more
-// than tau is skipped whole.
+// its first hit; an object whose AABB header is apart from B's is skipped
+// whole.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -42,9 +44,10 @@ namespace tdb {
 namespace {
 
 constexpr unsigned long long kNone = ~0ull;
-constexpr int kHitPlanes = 14;  // V (9), N (3), C, DEG
-__device__ __constant__ int kHitPlaneOf[kHitPlanes] = {0, 1, 2, 3, 4, 5, 6, 7, 8, F_N, F_N + 1, F_N + 2, F_C, F_DEG};
-enum { HS_V = 0, HS_N = 9, HS_C = 12, HS_DEG = 13 };
+constexpr int kHitPlanes = 15;  // V (9), N (3), C, DEG, K
+__device__ __constant__ int kHitPlaneOf[kHitPlanes] = {0,   1,   2,       3,       4,   5,     6,  7,
+                                                       8,   F_N, F_N + 1, F_N + 2, F_C, F_DEG, F_K};
+enum { HS_V = 0, HS_N = 9, HS_C = 12, HS_DEG = 13, HS_K = 14 };
 constexpr int kSBH = 128;          // B faces per staged sub-tile
 constexpr int kRows = 4;           // A rows per lane
 constexpr int kWarps = 4;          // tiles per CTA (one per warp)
@@ -78,10 +81,10 @@ __device__ __forceinline__ exact::tri load_tri(const double* P, uint64_t pad, ui
     return exact::tri{{v[0], v[1], v[2]}, {v[3], v[4], v[5]}, {v[6], v[7], v[8]}};
 }
 
-// FP32 pre-cull: the same separation test on h32 = n32 . (v - O) - c32 with
+// FP32 pre-cull: the same one-way test on h32 = n32 . (v - O) - c32 with
 // |h32 - h| <= 6 * 2^-24 * (|v - O| + |c|) (roundings of n, v - O, c and
-// three FMAs), so tau32 = kCull32 * (RB + |c|) + tau implies the FP64 test
-// separates too: the pre-cull never drops a pair the FP64 test keeps.
+// three FMAs), so tau32 = kCull32 * (RB + |c|) + tau_one implies the FP64
+// test separates too: the pre-cull never drops a pair the FP64 test keeps.
 constexpr double kCull32 = 1e-6;
 
 // all three h on one side, beyond tau: min > tau or max < -tau. (A NaN h
@@ -106,28 +109,29 @@ __device__ __forceinline__ bool separated32(float h0, float h1, float h2, float 
     return fminf(fminf(h0, h1), h2) > tau || fmaxf(fmaxf(h0, h1), h2) < -tau;
 }
 
-// all three |h| > tau with one common sign
+// all three h beyond tau on one common side (false for any NaN, or tau NaN)
 __device__ __forceinline__ bool separated(double h0, double h1, double h2, double tau) {
-    const double q0 = fabs(h0) - tau, q1 = fabs(h1) - tau, q2 = fabs(h2) - tau;
-    const int s0 = __double2hiint(h0), s1 = __double2hiint(h1), s2 = __double2hiint(h2);
-    const int same = (s0 ^ s1) | (s0 ^ s2);
-    return (same | __double2hiint(q0) | __double2hiint(q1) | __double2hiint(q2)) >= 0 &&
-           q0 != 0.0 && q1 != 0.0 && q2 != 0.0;
+    return (h0 > tau && h1 > tau && h2 > tau) || (h0 < -tau && h1 < -tau && h2 < -tau);
 }
 
-// Second plane test + exact reference predicate (rare path, out of line).
+// The rest of the cull (the other one-way direction, then the two-way
+// t-rejection) and the exact reference predicate: the rare path, out of line.
+// h0..h2 are B's vertex heights above A's plane, kA / kB the faces' kappa.
 static __device__ __noinline__ bool slow_pair(const double* Ap, uint64_t An_pad, uint64_t row, const double* sb,
-                                              int j, double tau, const NearLog& near, unsigned long long obj,
+                                              int j, double h0, double h1, double h2, double kA, double D,
+                                              double abs_tol, const NearLog& near, unsigned long long obj,
                                               unsigned long long pair) {
     double av[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) av[k] = __ldg(Ap + (uint64_t)(F_V + k) * An_pad + row);
     const double bn0 = sb[(HS_N + 0) * kSBH + j], bn1 = sb[(HS_N + 1) * kSBH + j], bn2 = sb[(HS_N + 2) * kSBH + j],
-                 bc = sb[HS_C * kSBH + j];
+                 bc = sb[HS_C * kSBH + j], kB = sb[HS_K * kSBH + j];
     const double g0 = fma(bn0, av[0], fma(bn1, av[1], fma(bn2, av[2], -bc)));
     const double g1 = fma(bn0, av[3], fma(bn1, av[4], fma(bn2, av[5], -bc)));
     const double g2 = fma(bn0, av[6], fma(bn1, av[7], fma(bn2, av[8], -bc)));
-    if (separated(g0, g1, g2, tau)) return false;
+    if (separated(g0, g1, g2, (kCullOne + kB) * D + abs_tol)) return false;
+    if (separated(g0, g1, g2, (kCullTwo + kB) * D + abs_tol) && separated(h0, h1, h2, (kCullTwo + kA) * D + abs_tol))
+        return false;
     const double* bv = sb + HS_V * kSBH + j;
     const exact::tri ta{{av[0], av[1], av[2]}, {av[3], av[4], av[5]}, {av[6], av[7], av[8]}};
     const exact::tri tb{{bv[0], bv[kSBH], bv[2 * kSBH]}, {bv[3 * kSBH], bv[4 * kSBH], bv[5 * kSBH]},
@@ -172,14 +176,15 @@ __global__ void __launch_bounds__(32 * kWarps, TDB_HIT_MINB) hit_kernel(HitArgs 
         const double lo = fmin(As[k], Bs[k]), hi = fmax(As[3 + k], Bs[3 + k]);
         diag2 += (hi - lo) * (hi - lo);
     }
-    const double tau = kCullDiag * sqrt(diag2) + kCullAbs * fmax(As[7], Bs[7]);
+    const double D = sqrt(diag2), abs_tol = kCullAbs * fmax(As[7], Bs[7]);
+    const double gap = kApart * D + abs_tol;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) apart |= (As[k] > Bs[3 + k] + tau) || (Bs[k] > As[3 + k] + tau);
+    for (int k = 0; k < 3; ++k) apart |= (As[k] > Bs[3 + k] + gap) || (Bs[k] > As[3 + k] + gap);
     if (a.chunk_aabb) {  // CULL: the warp's tile box vs this item's B-chunk box
         const double* ta = a.tile_aabb + (a.tile0 + (has_tile ? tl : a.ntiles - 1)) * 6;
         const double* cb = a.chunk_aabb + ch * 6;
 #pragma unroll
-        for (int k = 0; k < 3; ++k) apart |= (ta[k] > cb[3 + k] + tau) || (cb[k] > ta[3 + k] + tau);
+        for (int k = 0; k < 3; ++k) apart |= (ta[k] > cb[3 + k] + gap) || (cb[k] > ta[3 + k] + gap);
     }
 
     // this lane's rows: lane, lane+32, lane+64, lane+96 of the warp's tile
@@ -206,7 +211,8 @@ __global__ void __launch_bounds__(32 * kWarps, TDB_HIT_MINB) hit_kernel(HitArgs 
 #pragma unroll
         for (int k = 0; k < 3; ++k) an32[r][k] = __double2float_rn(an[r][k]);
         ac32[r] = __double2float_rn(cB);
-        const double t32 = kCull32 * (a.RB + fabs(cB)) + tau;
+        const double kA = __ldg(a.Ap + (uint64_t)F_K * a.An_pad + rowv[r]);
+        const double t32 = kCull32 * (a.RB + fabs(cB)) + (kCullOne + kA) * D + abs_tol;
         tau32[r] = a.RB + fabs(cB) < 1e30 ? __double2float_ru(t32) : __int_as_float(0x7f800000);  // +inf: no FP32 cull
     }
     static_assert(kRows % 2 == 0, "rows are packed in pairs");
@@ -307,9 +313,11 @@ __global__ void __launch_bounds__(32 * kWarps, TDB_HIT_MINB) hit_kernel(HitArgs 
                         fma(an[r][0], bv[3 * kSBH], fma(an[r][1], bv[4 * kSBH], fma(an[r][2], bv[5 * kSBH], -ac[r])));
                     const double h2 =
                         fma(an[r][0], bv[6 * kSBH], fma(an[r][1], bv[7 * kSBH], fma(an[r][2], bv[8 * kSBH], -ac[r])));
-                    if (separated(h0, h1, h2, tau)) continue;
+                    const double kA = __ldg(a.Ap + (uint64_t)F_K * a.An_pad + rowv[r]);
+                    if (separated(h0, h1, h2, (kCullOne + kA) * D + abs_tol)) continue;
                     ++nex;
-                    if (slow_pair(a.Ap, a.An_pad, rowv[r], sb, j, tau, a.near, a.obj0 + o, row_pmin(r, f0 + j))) {
+                    if (slow_pair(a.Ap, a.An_pad, rowv[r], sb, j, h0, h1, h2, kA, D, abs_tol, a.near, a.obj0 + o,
+                                  row_pmin(r, f0 + j))) {
                         atomicMin(a.objhit + o, row_pmin(r, f0 + j));
                         live &= ~(1u << r);  // later j of this row only give larger p
                     }

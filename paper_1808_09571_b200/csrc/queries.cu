@@ -104,11 +104,38 @@ struct Stream {
 __device__ __constant__ int kDistPlaneIds[kFilterPlanes] = {0,  1,  2,  3,  4,  5,  6,  7,  8,  9,  10, 11,
                                                              12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22, 23,
                                                              24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34};
-constexpr int kHitPlanes = 20;  // V (9), N (3), C, DEG, face AABB lo/hi (6)
-__device__ __constant__ int kHitPlaneIds[kHitPlanes] = {0,   1,   2,       3,       4,       5,       6,
-                                                         7,   8,   F_N,     F_N + 1, F_N + 2, F_C,     F_DEG,
-                                                         F_LO, F_LO + 1, F_LO + 2, F_HI, F_HI + 1, F_HI + 2};
-enum { HP_N = 9, HP_C = 12, HP_DEG = 13, HP_LO = 14, HP_HI = 17 };
+constexpr int kHitPlanes = 21;  // V (9), N (3), C, DEG, face AABB lo/hi (6), K
+__device__ __constant__ int kHitPlaneIds[kHitPlanes] = {0,    1,        2,        3,    4,        5,        6,
+                                                         7,    8,        F_N,      F_N + 1, F_N + 2, F_C,   F_DEG,
+                                                         F_LO, F_LO + 1, F_LO + 2, F_HI, F_HI + 1, F_HI + 2, F_K};
+enum { HP_N = 9, HP_C = 12, HP_DEG = 13, HP_LO = 14, HP_HI = 17, HP_K = 20 };
+
+// Segment x face intersects cull: the pair's box diagonal D
+// (segment box u face box) bounds every length in the reference's solve; the
+// reference cannot hit when (1) the boxes are apart by kApart D, or (2) both
+// endpoints lie beyond (kCullTwo + kappa) D on one side of the face plane
+// (its t-test fails despite its own rounding). slo/shi: the segment's box.
+__device__ __forceinline__ bool seg_face_culled(const double* p0, const double* p1, const double* slo,
+                                                const double* shi, const double flo[3], const double fhi[3],
+                                                double n0, double n1, double n2, double c, double kappa,
+                                                double abs_tol) {
+    double d2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double e = fmax(shi[k], fhi[k]) - fmin(slo[k], flo[k]);
+        d2 = fma(e, e, d2);
+    }
+    const double D = sqrt(d2) * (1.0 + 1e-15);
+    const double gap = kApart * D + abs_tol;
+    bool apart = false;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) apart |= (flo[k] > shi[k] + gap) | (fhi[k] < slo[k] - gap);
+    if (apart) return true;
+    const double tau = (kCullTwo + kappa) * D + abs_tol;
+    const double h0 = fma(n0, p0[0], fma(n1, p0[1], fma(n2, p0[2], -c)));
+    const double h1 = fma(n0, p1[0], fma(n1, p1[1], fma(n2, p1[2], -c)));
+    return (h0 > tau && h1 > tau) || (h0 < -tau && h1 < -tau);
+}
 
 // ---- filter values -----------------------------------------------------------
 // point P vs face B: vertex/face projection + the three clamped point/edge
@@ -179,7 +206,7 @@ __device__ __forceinline__ int seg_d2(const double p0[3], const double d[3], dou
         const double bbI = bb * ILb;
         const double den = fma(-bbI, bb, Ld);
         const double num = fma(-bbI, fw, cw);
-        double s = clamp01_hi(num * rcp_approx(den));
+        double s = clamp01(num * rcp_nr(den));
         const double t = clamp01(fma(bb, s, -fw) * ILb);
         s = clamp01(fma(bb, t, cw) * ILd);
         const double dx = fma(s, d[0], fma(-t, ebx, -w[k][0]));
@@ -233,12 +260,13 @@ __device__ __forceinline__ unsigned long long exact_bits(const QueryRegs& Q, con
     return (unsigned long long)__double_as_longlong(d);
 }
 
-// eta of one query: max edge over B and the segment, max |coord| over both
-__device__ __forceinline__ double q_eta(const QueryRegs& Q, const double* Bs) {
+// eta(m) of one query (tdb_internal.h): max edge over B and the segment,
+// B's max kappa, max |coord| over both. Grows with m: checks use eta(band).
+__device__ __forceinline__ double q_eta(const QueryRegs& Q, const double* Bs, double m) {
     double ext = 0.0;
 #pragma unroll
     for (int k = 0; k < 3; ++k) ext = fmax(ext, fmax(fabs(Q.p0[k]), fabs(Q.p1[k])));
-    return kBandEdge * fmax(Bs[6], sqrt(Q.Ld)) + kBandAbs * fmax(Bs[7], ext);
+    return band_eta_of(fmax(Bs[6], sqrt(Q.Ld)), Bs[8], fmax(Bs[7], ext), m);
 }
 
 // ---- fused path: the whole mesh is one chunk --------------------------------
@@ -261,8 +289,11 @@ __global__ void __launch_bounds__(kTile, TDB_QF_MINB) q_fused_kernel(QArgs a, co
     const bool active = qi < a.Qn;
     const uint64_t q = min(qi, a.Qn - 1);
     const QueryRegs Q = load_query(a, q);
-    const double eta = q_eta(Q, Bs);
-    auto band_of = [&](double m2) { return sqrt(m2) * (1.0 + kBandRel) + 2.0 * eta; };
+    auto band_of = [&](double m2) {
+        const double m = sqrt(m2);
+        return m * (1.0 + kBandRel) + 2.0 * q_eta(Q, Bs, m);
+    };
+    auto widen = [&](double D) { return D * (1.0 + kBandRel) + 2.0 * q_eta(Q, Bs, D); };
     double best = pos_inf(), cut2 = pos_inf(), evicted = pos_inf();
     int nc = 0;
     S.run(a.Bp, a.Bn_pad, 0, a.Bn, [&](const double* sb, int cnt, uint64_t f0) {
@@ -319,9 +350,10 @@ __global__ void __launch_bounds__(kTile, TDB_QF_MINB) q_fused_kernel(QArgs a, co
             if (Q.point ? exact::near_area(t) : exact::near_degenerate_seg(p0, p1, t)) near_log(near, q, j);
         }
         // complete only if nothing in the band was dropped and the band holds
+        const double eta = q_eta(Q, Bs, band);
         again = evicted <= b2 || D == kNone || __longlong_as_double((long long)D) > band - eta;
         if (again && D != kNone && __longlong_as_double((long long)D) > band - eta)
-            band = __longlong_as_double((long long)D) * (1.0 + kBandRel) + 2.0 * eta;
+            band = widen(__longlong_as_double((long long)D));
     }
     int rounds = 1;
     while (__syncthreads_or(again)) {  // fallback exact rescan (list overflow or a widened band)
@@ -340,8 +372,8 @@ __global__ void __launch_bounds__(kTile, TDB_QF_MINB) q_fused_kernel(QArgs a, co
             }
         });
         if (again) {
-            if (D != kNone && __longlong_as_double((long long)D) > band - eta) {
-                band = __longlong_as_double((long long)D) * (1.0 + kBandRel) + 2.0 * eta;
+            if (D != kNone && __longlong_as_double((long long)D) > band - q_eta(Q, Bs, band)) {
+                band = widen(__longlong_as_double((long long)D));
             } else {
                 again = false;
             }
@@ -403,7 +435,8 @@ __global__ void q_band_kernel(QArgs a, const double* Bs, double* band2, double* 
         band2[q] = band[q] = -1.0;
         return;
     }
-    const double b = sqrt(__longlong_as_double((long long)e)) * (1.0 + kBandRel) + 2.0 * q_eta(load_query(a, q), Bs);
+    const double m = sqrt(__longlong_as_double((long long)e));
+    const double b = m * (1.0 + kBandRel) + 2.0 * q_eta(load_query(a, q), Bs, m);
     band[q] = b;
     band2[q] = b * b * (1.0 + 4e-16);
 }
@@ -477,10 +510,11 @@ __global__ void q_check_kernel(QArgs a, const double* Bs, double* band2, double*
         band2[q] = -1.0;
         return;
     }
-    const double eta = q_eta(load_query(a, q), Bs);
+    const QueryRegs Q = load_query(a, q);
     const unsigned long long d = qD[q];
-    if (d != kNone && __longlong_as_double((long long)d) > b - eta) {
-        const double nb = __longlong_as_double((long long)d) * (1.0 + kBandRel) + 2.0 * eta;
+    if (d != kNone && __longlong_as_double((long long)d) > b - q_eta(Q, Bs, b)) {
+        const double m = __longlong_as_double((long long)d);
+        const double nb = m * (1.0 + kBandRel) + 2.0 * q_eta(Q, Bs, m);
         band[q] = nb;
         band2[q] = nb * nb * (1.0 + 4e-16);
         qD[q] = kNone;
@@ -519,13 +553,11 @@ __global__ void __launch_bounds__(kTile, 4) q_hit_kernel(QArgs a, const double* 
         const double l = fmin(Bs[k], fmin(p0[k], p1[k])), h = fmax(Bs[3 + k], fmax(p0[k], p1[k]));
         diag2 += (h - l) * (h - l);
         ext = fmax(ext, fmax(fabs(p0[k]), fabs(p1[k])));
+        lo[k] = fmin(p0[k], p1[k]);
+        hi[k] = fmax(p0[k], p1[k]);
     }
-    const double tau = kCullDiag * sqrt(diag2) + kCullAbs * ext;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        lo[k] = fmin(p0[k], p1[k]) - tau;
-        hi[k] = fmax(p0[k], p1[k]) + tau;
-    }
+    // coarse box test against the whole mesh's diagonal (>= every pair's D)
+    const double abs_tol = kCullAbs * ext, gap_mesh = kApart * sqrt(diag2) * (1.0 + 1e-15) + abs_tol;
     bool live = tl * kTile + threadIdx.x < a.Qn && *(volatile unsigned long long*)(qhit + q) >= b0;
     if (!__syncthreads_or(live)) return;
     unsigned long long nex = 0;
@@ -536,17 +568,15 @@ __global__ void __launch_bounds__(kTile, 4) q_hit_kernel(QArgs a, const double* 
         for (int j = 0; j < cnt; ++j) {
             if (!live) continue;
             bool apart = false;
+            double flo[3], fhi[3];
 #pragma unroll
-            for (int k = 0; k < 3; ++k)
-                apart |= (sb[(HP_LO + k) * kSB + j] > hi[k]) | (sb[(HP_HI + k) * kSB + j] < lo[k]);
+            for (int k = 0; k < 3; ++k) {
+                flo[k] = sb[(HP_LO + k) * kSB + j], fhi[k] = sb[(HP_HI + k) * kSB + j];
+                apart |= (flo[k] > hi[k] + gap_mesh) | (fhi[k] < lo[k] - gap_mesh);
+            }
             if (apart) continue;
-            const double n0 = sb[HP_N * kSB + j], n1 = sb[(HP_N + 1) * kSB + j], n2 = sb[(HP_N + 2) * kSB + j],
-                         c = sb[HP_C * kSB + j];
-            const double h0 = fma(n0, p0[0], fma(n1, p0[1], fma(n2, p0[2], -c)));
-            const double h1 = fma(n0, p1[0], fma(n1, p1[1], fma(n2, p1[2], -c)));
-            const double q0 = fabs(h0) - tau, q1 = fabs(h1) - tau;
-            if (((__double2hiint(h0) ^ __double2hiint(h1)) | __double2hiint(q0) | __double2hiint(q1)) >= 0 &&
-                q0 != 0.0 && q1 != 0.0)
+            if (seg_face_culled(p0, p1, lo, hi, flo, fhi, sb[HP_N * kSB + j], sb[(HP_N + 1) * kSB + j],
+                                sb[(HP_N + 2) * kSB + j], sb[HP_C * kSB + j], sb[HP_K * kSB + j], abs_tol))
                 continue;
             ++nex;
             const double* bv = sb + j;
@@ -794,8 +824,8 @@ __global__ void lt_band_kernel(QArgs a, uint64_t n_obj, const double* obj_stats,
         band2[o] = band[o] = -1.0;
         return;
     }
-    const double b = sqrt(__longlong_as_double((long long)objmin[o])) * (1.0 + kBandRel) +
-                     2.0 * q_eta(load_query(a, 0), obj_stats + o * kObjStats);
+    const double m = sqrt(__longlong_as_double((long long)objmin[o]));
+    const double b = m * (1.0 + kBandRel) + 2.0 * q_eta(load_query(a, 0), obj_stats + o * kObjStats, m);
     band[o] = b;
     band2[o] = b * b * (1.0 + 4e-16);
 }
@@ -834,10 +864,12 @@ __global__ void lt_check_kernel(QArgs a, uint64_t n_obj, const double* obj_stats
         band2[o] = -1.0;
         return;
     }
-    const double eta = q_eta(load_query(a, 0), obj_stats + o * kObjStats);
+    const QueryRegs Q = load_query(a, 0);
+    const double* Bs = obj_stats + o * kObjStats;
     const unsigned long long d = D[o];
-    if (d != kNone && __longlong_as_double((long long)d) > b - eta) {
-        const double nb = __longlong_as_double((long long)d) * (1.0 + kBandRel) + 2.0 * eta;
+    if (d != kNone && __longlong_as_double((long long)d) > b - q_eta(Q, Bs, b)) {
+        const double m = __longlong_as_double((long long)d);
+        const double nb = m * (1.0 + kBandRel) + 2.0 * q_eta(Q, Bs, m);
         band[o] = nb;
         band2[o] = nb * nb * (1.0 + 4e-16);
         D[o] = Pf[o] = kNone;
@@ -864,28 +896,16 @@ __global__ void __launch_bounds__(kTile) lt_hit_kernel(QArgs a, const Tile* tile
         p1[k] = __ldg(a.Q + (uint64_t)(3 + k) * a.Qpad);
     }
     const double* Bs = obj_stats + (uint64_t)T.obj * kObjStats;
-    double diag2 = 0.0, ext = Bs[7];
+    double ext = Bs[7], slo[3], shi[3], flo[3], fhi[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        const double l = fmin(Bs[k], fmin(p0[k], p1[k])), h = fmax(Bs[3 + k], fmax(p0[k], p1[k]));
-        diag2 += (h - l) * (h - l);
         ext = fmax(ext, fmax(fabs(p0[k]), fabs(p1[k])));
+        slo[k] = fmin(p0[k], p1[k]), shi[k] = fmax(p0[k], p1[k]);
+        flo[k] = __ldg(P + (uint64_t)(F_LO + k) * pad + f), fhi[k] = __ldg(P + (uint64_t)(F_HI + k) * pad + f);
     }
-    const double tau = kCullDiag * sqrt(diag2) + kCullAbs * ext;
-    bool apart = false;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const double lo = fmin(p0[k], p1[k]) - tau, hi = fmax(p0[k], p1[k]) + tau;
-        apart |= (__ldg(P + (uint64_t)(F_LO + k) * pad + f) > hi) | (__ldg(P + (uint64_t)(F_HI + k) * pad + f) < lo);
-    }
-    if (apart) return;
-    const double n0 = __ldg(P + (uint64_t)F_N * pad + f), n1 = __ldg(P + (uint64_t)(F_N + 1) * pad + f),
-                 n2 = __ldg(P + (uint64_t)(F_N + 2) * pad + f), c = __ldg(P + (uint64_t)F_C * pad + f);
-    const double h0 = fma(n0, p0[0], fma(n1, p0[1], fma(n2, p0[2], -c)));
-    const double h1 = fma(n0, p1[0], fma(n1, p1[1], fma(n2, p1[2], -c)));
-    const double q0 = fabs(h0) - tau, q1 = fabs(h1) - tau;
-    if (((__double2hiint(h0) ^ __double2hiint(h1)) | __double2hiint(q0) | __double2hiint(q1)) >= 0 && q0 != 0.0 &&
-        q1 != 0.0)
+    if (seg_face_culled(p0, p1, slo, shi, flo, fhi, __ldg(P + (uint64_t)F_N * pad + f),
+                        __ldg(P + (uint64_t)(F_N + 1) * pad + f), __ldg(P + (uint64_t)(F_N + 2) * pad + f),
+                        __ldg(P + (uint64_t)F_C * pad + f), __ldg(P + (uint64_t)F_K * pad + f), kCullAbs * ext))
         return;
     atomicAdd(nexact, 1ull);
     const exact::tri t = face_tri(P, pad, f);

@@ -68,6 +68,10 @@ __global__ void prep_kernel(const double* __restrict__ aos, uint64_t n, uint64_t
     const double Nx = a1 * b2 - a2 * b1, Ny = a2 * b0 - a0 * b2, Nz = a0 * b1 - a1 * b0;
     const double N2 = Nx * Nx + Ny * Ny + Nz * Nz;
     double n3[3] = {0, 0, 0}, U[3] = {0, 0, 0}, W[3] = {0, 0, 0}, c = 0.0;
+    // conditioning of the reference's solve against this face: its t / (u, v)
+    // noise scales with K = |e0||e1|/|N|; +inf when N = 0
+    const double kappa = N2 > 0.0 ? 8.0000001e-15 * sqrt((a0 * a0 + a1 * a1 + a2 * a2) * L[2] / N2)
+                                  : __longlong_as_double(0x7ff0000000000000ll);
     if (!deg && N2 > 0.0) {
         const double inv = 1.0 / sqrt(N2), inv2 = 1.0 / N2;
         n3[0] = Nx * inv, n3[1] = Ny * inv, n3[2] = Nz * inv;
@@ -92,6 +96,7 @@ __global__ void prep_kernel(const double* __restrict__ aos, uint64_t n, uint64_t
         }
         p[F_C * n_pad] = c;
         p[F_DEG * n_pad] = deg ? 1.0 : 0.0;
+        p[F_K * n_pad] = kappa;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             p[(F_LO + k) * n_pad] = fmin(v[k], fmin(v[3 + k], v[6 + k]));
@@ -116,6 +121,7 @@ __global__ void prep_kernel(const double* __restrict__ aos, uint64_t n, uint64_t
     s[5] = fmax(v[2], fmax(v[5], v[8]));
     s[6] = sqrt(fmax(L[0], fmax(L[1], L[2])));
     s[7] = fmax(fmax(fmax(-s[0], s[3]), fmax(-s[1], s[4])), fmax(-s[2], s[5]));
+    s[8] = deg ? 0.0 : kappa;
     unsigned long long* st = stats + (uint64_t)obj * kObjStats;
     const unsigned mask = __activemask();
     const uint32_t obj0 = __shfl_sync(mask, obj, 0);
@@ -293,7 +299,7 @@ void geom_build(Geom* g, const double* host_tri9, uint64_t n, const uint64_t* ho
         throw std::invalid_argument(std::to_string(nd2[1]) +
                                     " face(s) with non-finite coordinates (geometry.hpp:16-18 requires finite)");
     g->n_degenerate = nd2[0];
-    double agg[kObjStats] = {pos_inf_h(), pos_inf_h(), pos_inf_h(), -pos_inf_h(), -pos_inf_h(), -pos_inf_h(), 0.0, 0.0};
+    double agg[kObjStats] = {pos_inf_h(), pos_inf_h(), pos_inf_h(), -pos_inf_h(), -pos_inf_h(), -pos_inf_h(), 0.0, 0.0, 0.0};
     for (uint64_t o = 0; o < n_obj; ++o) {
         if (g->h_off[o + 1] == g->h_off[o]) continue;
         const double* s = &os[o * kObjStats];

@@ -23,7 +23,8 @@ enum Field : int {
     F_DEG = 34,  // 1.0 when degenerate (geometry.hpp:75, evaluated exactly)
     F_LO = 35,   // face AABB lo xyz
     F_HI = 38,   // face AABB hi xyz
-    NF = 41
+    F_K = 41,    // intersects noise coefficient kappa_T = 8e-15 * |e0||e1|/|N| (+inf when N = 0)
+    NF = 42
 };
 constexpr int kFilterPlanes = F_DEG + 1;  // planes the distance filters stage (V .. DEG)
 
@@ -43,27 +44,40 @@ constexpr uint64_t kChunk = 8192;   // B faces per work item
 constexpr int kSB = TDB_KSB;        // B faces per TMA-staged sub-tile
 constexpr int kPlanePad = 64;
 
-// per-object statistics (doubles): aabb lo xyz, hi xyz, max edge, max |coord|
-constexpr int kObjStats = 8;
+// per-object statistics (doubles): aabb lo xyz, hi xyz, max edge, max |coord|,
+// max kappa (F_K) over its non-degenerate faces
+constexpr int kObjStats = 9;
 
-// Pair-filter tolerances:
-//   eta   = kBandEdge * max edge + kBandAbs * max |coord|   (>= filter error
-//           |d~ - d_true| plus the rounding of the reference's witnesses)
-//   band  = sqrt(min d~^2) * (1 + kBandRel) + 2 eta          (candidates: d~ <= band)
-//   done when the exact minimum D <= band - eta, else band = D (1 + kBandRel) + 2 eta
+// Pair-filter tolerance (DESIGN.md 4.2 states and proves the bound):
+//   eta(m) = kBandEdge * sqrt(L (m + 4L)) + kappa_max (m + 4L) + kBandAbs * max |coord|
+// with L the max edge of the two objects, kappa_max their max F_K, m the band's
+// base distance. For every pair, d~ <= d_true + eta(m) whenever d_true <= the
+// band: the first term is the edge/edge solve's cancellation floor after the
+// Newton-refined first parameter (<= 5.2e-8 sqrt(L (|w| + L))), the second the
+// misclassification of a vertex projection / piercing on a face of
+// conditioning K (<= 6.7e-16 K |w|), the third the rounding of the values.
+//   band  = m (1 + kBandRel) + 2 eta(m), m = sqrt(min d~^2)   (candidates: d~ <= band)
+//   done when the exact minimum D <= band - eta(m), else m = D and repeat
 // kBandRel covers the 2^-20 high-word truncation of d~^2 (fast_pair.cuh).
-// intersects plane cull margin:
-//   tau   = kCullDiag * diag(AABB(A obj u B)) + kCullAbs * max |coord|
 constexpr double kBandRel = 4e-6;
-// kBandEdge: the filter's first parameter s0 comes from rcp.approx (about
-// 2^-20 relative). Ericson's refinement (t for s0, then s for t) damps that by
-// cos^2(theta), but when two edges pass within d << |E| of each other the
-// distance error is first order: <= 0.38 * 1.2e-6 * |E| ~ 4.6e-7 |E| (4.0e-7
-// |E| seen in tests/test_gpu_bounds.py over 2M adversarial pairs). 4e-6 keeps
-// a ~9x margin; the band only widens by a few 1e-6 of an edge.
-constexpr double kBandEdge = 4e-6;
+constexpr double kBandEdge = 2e-7;  // 4x the proven 5.2e-8
 constexpr double kBandAbs = 1e-12;
-constexpr double kCullDiag = 1e-10;
+
+// Intersects culls ("when can the reference report a hit").
+// D = diag of a box holding both triangles (or segment and triangle),
+// kappa_T = F_K of triangle T (8e-15 K_T, K_T = |e0||e1|/|N| its conditioning),
+// abs = kCullAbs * max |coord|:
+//   one-way : all vertices of T2 beyond (kCullOne + kappa_T1) D + abs on one
+//             side of T1's plane  => no directed edge of either triangle hits
+//   two-way : T2 beyond (kCullTwo + kappa_T1) D + abs of T1's plane AND
+//             T1 beyond (kCullTwo + kappa_T2) D + abs of T2's plane
+//   apart   : the boxes of the two triangles (segment) separated by
+//             kApart D + abs along an axis
+// The margins cover the reference's own rounding noise (its Cramer solve at
+// its 1e-12 validity edge moves the solution by <= 7.2e-3 D), not only ours.
+constexpr double kCullOne = 2.5e-2;
+constexpr double kCullTwo = 1.01e-12;
+constexpr double kApart = 5e-2;
 constexpr double kCullAbs = 1e-13;
 
 }  // namespace tdb
