@@ -17,7 +17,9 @@
  *    (kernels.cpp:359,368-376); intersects reports the lowest hit p
  *    (kernels.cpp:407-432).
  *  - Degenerate triangles (norm2((v1-v0)x(v2-v0)) <= 1e-30, geometry.hpp:75)
- *    contribute +inf to distance minima and never intersect.
+ *    make a mesh x mesh pair contribute +inf to distance minima and never
+ *    intersect. Point / segment queries follow the store's
+ *    has_degenerate_faces flags (tdb_geom_set_has_degenerate_faces).
  *  - Every call returns 0 on success and a negative TDB_E* code otherwise;
  *    tdb_last_error() (thread-local) holds the message. No C++ exception
  *    crosses this boundary. There is no CPU fallback: without a usable
@@ -130,6 +132,18 @@ int tdb_geom_download(tdb_mesh g, double* tri9_out);
 int tdb_geom_offsets(tdb_mesh g, uint64_t* off_out);
 int tdb_geom_info(tdb_mesh g, uint64_t* n_tris, uint64_t* n_objects, uint64_t* n_degenerate,
                   double* aabb6);
+/* The reference's TriangleMesh::has_degenerate_faces per object
+ * (geometry.hpp:84-97): point / segment distance queries against an object
+ * (distance_to_mesh, run_batch with a Point / Segment literal over a mesh
+ * column) skip its degenerate faces only when its flag is set
+ * (reduce_min_over_faces, kernels.cpp:350,357); otherwise they evaluate them
+ * through the reference's degenerate fallbacks (kernels.cpp:127-134,151-156).
+ * flags: n_objects bytes (NULL = all set). A new store has every flag set,
+ * what refresh_degeneracy_flag() gives for meshes that have degenerate faces
+ * (parse_wkt and the generators call it, wkt.cpp:170, dataset.cpp:110).
+ * Mesh x mesh (A17) always skips degenerate faces; intersects never does
+ * (intersects_mesh has no skip, kernels.cpp:407-432). */
+int tdb_geom_set_has_degenerate_faces(tdb_mesh g, const uint8_t* flags, uint64_t n_objects);
 void tdb_mesh_free(tdb_mesh m);
 void tdb_table_free(tdb_table t);
 

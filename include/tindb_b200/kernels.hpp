@@ -67,9 +67,16 @@ inline const double* faces_of(const TriangleMesh& m) {
 // immutable once Ready, store_types.hpp:21-32, so copies may be cached).
 class DeviceMesh {
   public:
+    // carries m.has_degenerate_faces: point / segment queries skip the
+    // degenerate faces only when it is set (kernels.cpp:350,357)
     explicit DeviceMesh(const TriangleMesh& m) {
         check(tdb_mesh_upload(faces_of(m), m.triangles.size(), &h_));
         faces_ = m.triangles.size();
+        const std::uint8_t flag = m.has_degenerate_faces ? 1 : 0;
+        if (const int rc = tdb_geom_set_has_degenerate_faces(h_, &flag, 1); rc != TDB_OK) {
+            tdb_mesh_free(h_);
+            check(rc);
+        }
     }
     ~DeviceMesh() { tdb_mesh_free(h_); }
     DeviceMesh(const DeviceMesh&) = delete;
@@ -355,6 +362,10 @@ struct DeviceColumns {
                     std::copy(faces_of(m), faces_of(m) + 9 * m.triangles.size(), faces.begin() + 9 * off[k]);
                 }
                 check(tdb_table_upload(faces.data(), off.data(), mesh_rows.size(), &meshes));
+                std::vector<std::uint8_t> flags(mesh_rows.size());
+                for (std::size_t k = 0; k < mesh_rows.size(); ++k)
+                    flags[k] = std::get<TriangleMesh>(records[mesh_rows[k]].geometry).has_degenerate_faces ? 1 : 0;
+                check(tdb_geom_set_has_degenerate_faces(meshes, flags.data(), flags.size()));
             }
             if (!seg_rows.empty()) {
                 std::vector<double> q(6 * seg_rows.size());

@@ -99,6 +99,8 @@ def _load_ref():
     L.ref_unit_sphere.restype = ct.c_uint64
     L.ref_ore_body.argtypes = [ct.c_uint64, _D]
     L.ref_ore_body.restype = ct.c_uint64
+    L.ref_queries_mesh_distance_flag.argtypes = [ct.c_int, _D, ct.c_uint64, _D, ct.c_uint64, ct.c_int, ct.c_int, _D,
+                                                 _U64]
     L.ref_terrain.argtypes = [ct.c_uint32, ct.c_uint32, ct.c_double, ct.c_uint64, _D]
     L.ref_terrain.restype = ct.c_uint64
     L.ref_random_triangles.argtypes = [ct.c_uint64, ct.c_uint64, ct.c_double, ct.c_double, _D]
@@ -228,6 +230,18 @@ def ref_points_mesh_distance(pts, mesh, threads=None):
 
 def ref_segments_mesh_intersects(segs, mesh, threads=None):
     return _queries(REF, "ref_", "intersects", segs, mesh, threads)
+
+
+def ref_queries_mesh_distance_flag(q, mesh, has_degenerate_faces, points=False, threads=None):
+    """distance_to_mesh per query with the mesh's has_degenerate_faces set to
+    the given value (not refreshed): kernels.cpp:350,357."""
+    q = _f64(q).reshape(-1, 3 if points else 6)
+    m = _f64(mesh).reshape(-1, 9)
+    d, f = np.empty(len(q)), np.empty(len(q), np.uint64)
+    REF.ref_queries_mesh_distance_flag(1 if points else 0, _dp(q), len(q), _dp(m), len(m),
+                                       threads or os.cpu_count() or 1, 1 if has_degenerate_faces else 0,
+                                       _dp(d), f.ctypes.data_as(_U64))
+    return d, f
 
 
 def ref_make_drills(seed, count, style=0):

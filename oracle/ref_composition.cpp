@@ -322,6 +322,28 @@ void ref_points_mesh_distance(const double* p3, std::uint64_t n, const double* t
     });
 }
 
+// distance_to_mesh with the mesh's has_degenerate_faces set explicitly
+// (flag 0/1) instead of refreshed: the reference then evaluates (0) or skips
+// (1) degenerate faces (kernels.cpp:350,357). kind 0 = segments, 1 = points.
+void ref_queries_mesh_distance_flag(int kind, const double* q, std::uint64_t n, const double* t9, std::uint64_t m,
+                                    int threads, int flag, double* dist, std::uint64_t* face) {
+    TriangleMesh mesh;
+    mesh.triangles = load_mesh(t9, m);
+    mesh.has_degenerate_faces = flag != 0;
+    const auto inner = K::ExecutorConfig::sequential();
+    K::for_each_chunk(row_cfg(threads), n, [&](std::size_t, std::size_t lo, std::size_t hi) {
+        for (std::size_t k = lo; k < hi; ++k) {
+            const K::DistanceResult r =
+                kind == 0 ? K::distance_to_mesh(LineSegment{{q[6 * k], q[6 * k + 1], q[6 * k + 2]},
+                                                            {q[6 * k + 3], q[6 * k + 4], q[6 * k + 5]}},
+                                                mesh, inner)
+                          : K::distance_to_mesh(Point3{q[3 * k], q[3 * k + 1], q[3 * k + 2]}, mesh, inner);
+            dist[k] = r.distance;
+            face[k] = r.face_index ? *r.face_index : ~std::uint64_t(0);
+        }
+    });
+}
+
 void ref_segments_mesh_intersects(const double* s6, std::uint64_t n, const double* t9, std::uint64_t m, int threads,
                                   std::uint8_t* hit, std::uint64_t* face) {
     const TriangleMesh mesh = mesh_of(t9, m);

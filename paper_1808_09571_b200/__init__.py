@@ -112,6 +112,7 @@ _SIGS = [
     ("tdb_table_from_wkt", ct.c_int, [ct.c_char_p, _U64, ct.c_uint64, ct.POINTER(ct.c_void_p), _U64, _U64]),
     ("tdb_geom_download", ct.c_int, [ct.c_void_p, _D]),
     ("tdb_geom_offsets", ct.c_int, [ct.c_void_p, _U64]),
+    ("tdb_geom_set_has_degenerate_faces", ct.c_int, [ct.c_void_p, _U8, ct.c_uint64]),
     ("tdb_mesh_free", None, [ct.c_void_p]),
     ("tdb_table_free", None, [ct.c_void_p]),
     ("tdb_mesh_mesh_distance", ct.c_int, [ct.c_void_p, ct.c_void_p, ct.POINTER(DistOut)]),
@@ -261,6 +262,16 @@ class _Geom:
         out = np.empty((n, 9), np.float64)
         _check(lib().tdb_geom_download(self._h, _dp(out)))
         return out
+
+    def set_has_degenerate_faces(self, flags) -> "_Geom":
+        """TriangleMesh::has_degenerate_faces per object (geometry.hpp:84):
+        point / segment distance queries skip an object's degenerate faces
+        only when its flag is set (kernels.cpp:350,357). A bool applies to
+        every object."""
+        n = self.info()["objects"]
+        f = np.broadcast_to(np.asarray(flags, dtype=np.uint8), (n,)).copy()
+        _check(lib().tdb_geom_set_has_degenerate_faces(self._h, f.ctypes.data_as(_U8), n))
+        return self
 
     def free(self):
         if self._h is not None and self._h.value:

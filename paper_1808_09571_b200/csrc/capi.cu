@@ -303,6 +303,20 @@ int tdb_geom_info(tdb_mesh g, uint64_t* n, uint64_t* n_obj, uint64_t* n_deg, dou
     });
 }
 
+int tdb_geom_set_has_degenerate_faces(tdb_mesh g, const uint8_t* flags, uint64_t n_objects) {
+    return guarded([&] {
+        need(g != nullptr, "null handle");
+        need(n_objects == g->g.n_obj, "n_objects must equal the store's object count");
+        for (uint64_t o = 0; o < n_objects; ++o) g->g.h_keep_deg[o] = flags && !flags[o] ? 1 : 0;
+        cudaSetDevice(g->g.device);
+        const cudaStream_t st = lib_stream(g->g.device);
+        if (n_objects) {
+            CK(cudaMemcpyAsync(g->g.d_keep_deg, g->g.h_keep_deg.data(), n_objects, cudaMemcpyHostToDevice, st));
+            CK(cudaStreamSynchronize(st));
+        }
+    });
+}
+
 void tdb_mesh_free(tdb_mesh m) {
     if (!m) return;
     cudaSetDevice(m->g.device);

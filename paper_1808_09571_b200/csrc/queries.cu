@@ -49,7 +49,16 @@ struct QArgs {
     uint64_t Bn_pad, Bn, n_chunks, chunk;
     double* itemmin;
     unsigned long long* qmin;
+    // per B object: 1 = evaluate its degenerate faces (the reference's
+    // TriangleMesh::has_degenerate_faces is false, kernels.cpp:350,357),
+    // 0 = skip them
+    const uint8_t* keep_deg;
 };
+
+// face j of the staged sub-tile is skipped: degenerate and its object skips them
+__device__ __forceinline__ bool skip_face(const QArgs& a, const double* sb, int j, uint32_t obj = 0) {
+    return reinterpret_cast<const int*>(sb + F_DEG * kSB + j)[1] != 0 && !a.keep_deg[obj];
+}
 
 // ---- TMA-staged streaming of B faces [b0, b1) through 2 SMEM stages ------
 // `g` counts sub-tiles across calls so the mbarrier phases stay consistent
@@ -323,10 +332,9 @@ __global__ void __launch_bounds__(kTile, TDB_QF_MINB) q_fused_kernel(QArgs a, co
                 }
             }
         };
-        auto deg = [&](int j) { return reinterpret_cast<const int*>(sb + F_DEG * kSB + j)[1] != 0; };  // uniform
 #pragma unroll 1
         for (int j = 0; j < cnt; ++j)
-            if (!deg(j)) take(query_d2(Q, FaceRef{sb + j, (uint64_t)kSB}), j);
+            if (!skip_face(a, sb, j)) take(query_d2(Q, FaceRef{sb + j, (uint64_t)kSB}), j);  // uniform
     });
     double band = active && best < pos_inf() ? band_of(best) : -1.0;
     unsigned long long D = kNone, P = kNone, cand = 0;
@@ -363,7 +371,7 @@ __global__ void __launch_bounds__(kTile, TDB_QF_MINB) q_fused_kernel(QArgs a, co
         S.run(a.Bp, a.Bn_pad, 0, a.Bn, [&](const double* sb, int cnt, uint64_t f0) {
 #pragma unroll 1
             for (int j = 0; j < cnt; ++j) {
-                if (reinterpret_cast<const int*>(sb + F_DEG * kSB + j)[1] != 0) continue;
+                if (skip_face(a, sb, j)) continue;
                 if (b2 < 0.0) continue;
                 if (query_d2(Q, FaceRef{sb + j, (uint64_t)kSB}) > b2) continue;
                 ++cand;
@@ -405,7 +413,7 @@ __global__ void __launch_bounds__(kTile, 4) q_filter_kernel(QArgs a) {
     S.run(a.Bp, a.Bn_pad, b0, b1, [&](const double* sb, int cnt, uint64_t) {
 #pragma unroll 1
         for (int j = 0; j < cnt; ++j) {
-            if (reinterpret_cast<const int*>(sb + F_DEG * kSB + j)[1] != 0) continue;
+            if (skip_face(a, sb, j)) continue;
             best = min_nn(best, query_d2(Q, FaceRef{sb + j, (uint64_t)kSB}));
         }
     });
@@ -467,7 +475,7 @@ __device__ __forceinline__ void q_verify_item(const QArgs& a, SS& S, uint64_t it
     S.run(a.Bp, a.Bn_pad, b0, b1, [&](const double* sb, int cnt, uint64_t f0) {
 #pragma unroll 1
         for (int j = 0; j < cnt; ++j) {
-            if (reinterpret_cast<const int*>(sb + F_DEG * kSB + j)[1] != 0) continue;
+            if (skip_face(a, sb, j)) continue;
             if (b2 < 0.0 || query_d2(Q, FaceRef{sb + j, (uint64_t)kSB}) > b2) continue;
             const unsigned long long e = exact_bits(Q, sb, j);
             if (pass == 1) {
@@ -686,7 +694,7 @@ void run_queries(const Ctx& cx, int op, const QuerySet& qs, const Geom& B, doubl
     near.alloc(st);
     cudaEvent_t* ev = thread_events().e;
     CK(cudaEventRecord(ev[0], st));
-    QArgs a{qs.planes, n, qs.pad, qs.kind, B.planes, B.n_pad, B.n, n_chunks, chunk, nullptr, nullptr};
+    QArgs a{qs.planes, n, qs.pad, qs.kind, B.planes, B.n_pad, B.n, n_chunks, chunk, nullptr, nullptr, B.d_keep_deg};
     uint64_t launches = 0, flagged = 0;
     int rounds = 0;
     unsigned long long hc[4] = {0, 0, 0, 0};
@@ -781,8 +789,9 @@ void run_queries(const Ctx& cx, int op, const QuerySet& qs, const Geom& B, doubl
 // own AABB / scale header.
 namespace {
 
-__device__ __forceinline__ bool face_degenerate(const double* P, uint64_t pad, uint64_t f) {
-    return reinterpret_cast<const int*>(P + (uint64_t)F_DEG * pad + f)[1] != 0;
+// face f of object obj is skipped: degenerate and the object skips them
+__device__ __forceinline__ bool face_skipped(const QArgs& a, const double* P, uint64_t pad, uint64_t f, uint32_t obj) {
+    return reinterpret_cast<const int*>(P + (uint64_t)F_DEG * pad + f)[1] != 0 && !a.keep_deg[obj];
 }
 
 __device__ __forceinline__ exact::tri face_tri(const double* P, uint64_t pad, uint64_t f) {
@@ -800,7 +809,7 @@ __global__ void __launch_bounds__(kTile) lt_filter_kernel(QArgs a, const Tile* t
     double d2 = pos_inf();
     if (threadIdx.x < T.count) {
         const uint64_t f = T.row0 + threadIdx.x;
-        if (!face_degenerate(P, pad, f)) d2 = query_d2(Q, FaceRefLdg{P + f, pad});
+        if (!face_skipped(a, P, pad, f, T.obj)) d2 = query_d2(Q, FaceRefLdg{P + f, pad});
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) d2 = min_nn(d2, __shfl_xor_sync(0xffffffffu, d2, o));
@@ -838,7 +847,7 @@ __global__ void __launch_bounds__(kTile) lt_verify_kernel(QArgs a, const Tile* t
     const double b2 = band2[T.obj];
     if (b2 < 0.0 || threadIdx.x >= T.count) return;
     const uint64_t f = T.row0 + threadIdx.x;
-    if (face_degenerate(P, pad, f)) return;
+    if (face_skipped(a, P, pad, f, T.obj)) return;
     const QueryRegs Q = load_query(a, 0);
     if (query_d2(Q, FaceRefLdg{P + f, pad}) > b2) return;
     const exact::tri t = face_tri(P, pad, f);
@@ -947,7 +956,7 @@ void run_literal_table(const Ctx& cx, int op, const QuerySet& q1, const Geom& B,
     unsigned long long* Pf = (unsigned long long*)alloc(n_obj * sizeof(unsigned long long));
     NearDev near;
     near.alloc(st);
-    QArgs a{q1.planes, 1, q1.pad, q1.kind, B.planes, B.n_pad, B.n, 1, B.n, nullptr, nullptr};
+    QArgs a{q1.planes, 1, q1.pad, q1.kind, B.planes, B.n_pad, B.n, 1, B.n, nullptr, nullptr, B.d_keep_deg};
     cudaEvent_t* ev = thread_events().e;
     CK(cudaEventRecord(ev[0], st));
     uint64_t launches = 0;

@@ -58,6 +58,11 @@ struct Geom {
     // the intersects FP32 pre-cull
     double origin[3] = {0.0, 0.0, 0.0};
     float* fplanes = nullptr;
+    // per object: 1 = point / segment queries evaluate its degenerate faces
+    // (TriangleMesh::has_degenerate_faces == false, kernels.cpp:350,357);
+    // 0 (default) = skip them. tdb_geom_set_has_degenerate_faces.
+    uint8_t* d_keep_deg = nullptr;
+    std::vector<uint8_t> h_keep_deg;
 };
 
 // tri9: 9 doubles per face (AoS), on the host unless tri9_on_device

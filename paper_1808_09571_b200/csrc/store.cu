@@ -79,6 +79,13 @@ __global__ void prep_kernel(const double* __restrict__ aos, uint64_t n, uint64_t
         // U = (e1 x N)/|N|^2, W = (N x e0)/|N|^2
         U[0] = (b1 * Nz - b2 * Ny) * inv2, U[1] = (b2 * Nx - b0 * Nz) * inv2, U[2] = (b0 * Ny - b1 * Nx) * inv2;
         W[0] = (Ny * a2 - Nz * a1) * inv2, W[1] = (Nz * a0 - Nx * a2) * inv2, W[2] = (Nx * a1 - Ny * a0) * inv2;
+    } else {
+        // degenerate: no vertex projects "inside" (NaN barycentrics fail every
+        // inside test), so a face the queries evaluate anyway (its mesh's
+        // has_degenerate_faces is false) gets only edge candidates, the
+        // reference's fallback (kernels.cpp:127-134, 151-156, 262-316)
+        const double nan = __longlong_as_double(0x7ff8000000000000ll);
+        U[0] = U[1] = U[2] = W[0] = W[1] = W[2] = nan;
     }
     if (live) {
         double* p = planes + f;
@@ -239,6 +246,9 @@ void geom_build(Geom* g, const double* host_tri9, uint64_t n, const uint64_t* ho
     CK(cudaMallocAsync(&g->d_tiles, std::max<size_t>(1, g->h_tiles.size()) * sizeof(Tile), st));
     CK(cudaMallocAsync(&g->d_obj_stats, std::max<uint64_t>(1, n_obj) * kObjStats * sizeof(double), st));
     CK(cudaMallocAsync(&g->d_tile_aabb, std::max<size_t>(1, g->h_tiles.size()) * 6 * sizeof(double), st));
+    g->h_keep_deg.assign(std::max<uint64_t>(1, n_obj), 0);  // default: skip degenerate faces
+    CK(cudaMallocAsync(&g->d_keep_deg, g->h_keep_deg.size(), st));
+    CK(cudaMemsetAsync(g->d_keep_deg, 0, g->h_keep_deg.size(), st));
     unsigned long long* ustats = nullptr;
     unsigned long long* ndeg = nullptr;
     CK(cudaMallocAsync(&ustats, std::max<uint64_t>(1, n_obj) * kObjStats * sizeof(unsigned long long), st));
@@ -328,8 +338,10 @@ void geom_release(Geom* g, cudaStream_t st) {
     cudaFreeAsync(g->d_obj_stats, st);
     cudaFreeAsync(g->d_tile_aabb, st);
     cudaFreeAsync(g->fplanes, st);
+    cudaFreeAsync(g->d_keep_deg, st);
     g->planes = nullptr;
     g->fplanes = nullptr;
+    g->d_keep_deg = nullptr;
 }
 
 }  // namespace tdb

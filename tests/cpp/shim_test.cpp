@@ -191,6 +191,31 @@ int main() {
         EXPECT(threw);
     }
 
+    // has_degenerate_faces is honoured as the reference reads it
+    // (kernels.cpp:350,357): test_distance.cpp:278-290's mesh, without and with
+    // refresh_degeneracy_flag()
+    {
+        TriangleMesh m;
+        m.triangles.push_back(Triangle{{0, 0, 1}, {1, 0, 1}, {2, 0, 1}});  // degenerate, closer
+        m.triangles.push_back(Triangle{{0, 0, 0}, {1, 0, 0}, {0, 1, 0}});
+        for (int refresh = 0; refresh < 2; ++refresh) {
+            if (refresh) m.refresh_degeneracy_flag();
+            const Point3 p{0.2, 0.1, 2.0};
+            const LineSegment seg{{0.2, 0.1, 2.0}, {0.3, 0.2, 1.5}};
+            const K::DistanceResult a = K::b200::distance_to_mesh(p, m, cfg), b = K::distance_to_mesh(p, m, cfg);
+            EXPECT(same_bits(a.distance, b.distance) && a.face_index == b.face_index);
+            EXPECT(a.face_index && *a.face_index == (refresh ? 1u : 0u));
+            const K::DistanceResult c = K::b200::distance_to_mesh(seg, m, cfg), d = K::distance_to_mesh(seg, m, cfg);
+            EXPECT(same_bits(c.distance, d.distance) && c.face_index == d.face_index);
+            // run_batch: a Point literal over a Mesh column (batch.cpp:44-48)
+            std::vector<store::GeometryRecord> recs{{7, Geometry{m}}, {8, Geometry{shifted(m, 0, 0, 0.5)}}};
+            const auto rb = K::b200::run_batch_b200(K::BatchOp::Distance, recs, Geometry{p}, cfg);
+            const auto rr = K::run_batch(K::BatchOp::Distance, recs, Geometry{p}, cfg);
+            for (int k = 0; k < 2; ++k)
+                EXPECT(same_bits(std::get<double>(rb[k].value), std::get<double>(rr[k].value)));
+        }
+    }
+
     if (fails == 0) std::printf("SHIM OK\n");
     return fails ? 1 : 0;
 }
