@@ -149,8 +149,10 @@ struct BandArgs {
     unsigned long long* objP;
 };
 
-// eta(m) (tdb_internal.h) for objects A and B. It grows with m, so a check
-// against eta(band) >= eta(D) is the safe side.
+// eta(m) (tdb_internal.h) for objects A and B. The round is complete when the
+// exact minimum D satisfies D + eta(D) <= band: every pair the reference can
+// rank at or below D has d~ <= d_true + eta(d_true) <= D + eta(D) (eta grows
+// with m), so it was flagged.
 __device__ __forceinline__ double band_eta(const double* As, const double* Bs, double m) {
     return band_eta_of(fmax(As[6], Bs[6]), fmax(As[8], Bs[8]), fmax(As[7], Bs[7]), m);
 }
@@ -306,8 +308,8 @@ __global__ void check_kernel(CheckArgs a) {
     // filter minimum -> cannot happen unless every in-band pair evaluated to
     // NaN/inf; treat as done.
     const double* As = a.Astats + (a.obj0 + o) * kObjStats;
-    if (d != kNone && __longlong_as_double((long long)d) > b - band_eta(As, a.Bstats, b)) {
-        const double m = __longlong_as_double((long long)d);
+    const double m = d != kNone ? __longlong_as_double((long long)d) : 0.0;
+    if (d != kNone && m + band_eta(As, a.Bstats, m) > b) {
         const double nb = m * (1.0 + kBandRel) + 2.0 * band_eta(As, a.Bstats, m);
         a.band[o] = nb;
         a.band2[o] = nb * nb * (1.0 + 4e-16);

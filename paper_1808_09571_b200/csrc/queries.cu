@@ -270,7 +270,8 @@ __device__ __forceinline__ unsigned long long exact_bits(const QueryRegs& Q, con
 }
 
 // eta(m) of one query (tdb_internal.h): max edge over B and the segment,
-// B's max kappa, max |coord| over both. Grows with m: checks use eta(band).
+// B's max kappa, max |coord| over both. A band is complete when the exact
+// minimum D has D + eta(D) <= band (distance.cu check_kernel).
 __device__ __forceinline__ double q_eta(const QueryRegs& Q, const double* Bs, double m) {
     double ext = 0.0;
 #pragma unroll
@@ -358,10 +359,10 @@ __global__ void __launch_bounds__(kTile, TDB_QF_MINB) q_fused_kernel(QArgs a, co
             if (Q.point ? exact::near_area(t) : exact::near_degenerate_seg(p0, p1, t)) near_log(near, q, j);
         }
         // complete only if nothing in the band was dropped and the band holds
-        const double eta = q_eta(Q, Bs, band);
-        again = evicted <= b2 || D == kNone || __longlong_as_double((long long)D) > band - eta;
-        if (again && D != kNone && __longlong_as_double((long long)D) > band - eta)
-            band = widen(__longlong_as_double((long long)D));
+        const double Dd = D != kNone ? __longlong_as_double((long long)D) : 0.0;
+        const bool out = D != kNone && Dd + q_eta(Q, Bs, Dd) > band;
+        again = evicted <= b2 || D == kNone || out;
+        if (out) band = widen(Dd);
     }
     int rounds = 1;
     while (__syncthreads_or(again)) {  // fallback exact rescan (list overflow or a widened band)
@@ -380,8 +381,9 @@ __global__ void __launch_bounds__(kTile, TDB_QF_MINB) q_fused_kernel(QArgs a, co
             }
         });
         if (again) {
-            if (D != kNone && __longlong_as_double((long long)D) > band - q_eta(Q, Bs, band)) {
-                band = widen(__longlong_as_double((long long)D));
+            const double Dd = D != kNone ? __longlong_as_double((long long)D) : 0.0;
+            if (D != kNone && Dd + q_eta(Q, Bs, Dd) > band) {
+                band = widen(Dd);
             } else {
                 again = false;
             }
@@ -520,8 +522,8 @@ __global__ void q_check_kernel(QArgs a, const double* Bs, double* band2, double*
     }
     const QueryRegs Q = load_query(a, q);
     const unsigned long long d = qD[q];
-    if (d != kNone && __longlong_as_double((long long)d) > b - q_eta(Q, Bs, b)) {
-        const double m = __longlong_as_double((long long)d);
+    const double m = d != kNone ? __longlong_as_double((long long)d) : 0.0;
+    if (d != kNone && m + q_eta(Q, Bs, m) > b) {
         const double nb = m * (1.0 + kBandRel) + 2.0 * q_eta(Q, Bs, m);
         band[q] = nb;
         band2[q] = nb * nb * (1.0 + 4e-16);
@@ -876,8 +878,8 @@ __global__ void lt_check_kernel(QArgs a, uint64_t n_obj, const double* obj_stats
     const QueryRegs Q = load_query(a, 0);
     const double* Bs = obj_stats + o * kObjStats;
     const unsigned long long d = D[o];
-    if (d != kNone && __longlong_as_double((long long)d) > b - q_eta(Q, Bs, b)) {
-        const double m = __longlong_as_double((long long)d);
+    const double m = d != kNone ? __longlong_as_double((long long)d) : 0.0;
+    if (d != kNone && m + q_eta(Q, Bs, m) > b) {
         const double nb = m * (1.0 + kBandRel) + 2.0 * q_eta(Q, Bs, m);
         band[o] = nb;
         band2[o] = nb * nb * (1.0 + 4e-16);
