@@ -35,6 +35,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstring>
 #include <limits>
 #include <map>
 #include <memory>
@@ -42,6 +43,7 @@
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <utility>
 #include <variant>
 #include <vector>
@@ -89,6 +91,84 @@ class DeviceMesh {
     std::size_t faces_ = 0;
 };
 
+// Device copies of host meshes, reused across calls ("device
+// copies may be cached"; the per-record calls run_batch makes, batch.cpp:
+// 98-103, and the per-query distance_to_mesh / intersects_mesh calls would
+// otherwise upload the same mesh again each time). Keyed by content: a 64-bit
+// hash of the faces, confirmed by a byte compare against a host copy, plus
+// the has_degenerate_faces flag. Least recently used entries go first once
+// the cached faces exceed max_faces. Thread-safe.
+class MeshCache {
+  public:
+    explicit MeshCache(std::size_t max_faces = std::size_t(1) << 23) : max_faces_(max_faces) {}
+
+    std::shared_ptr<const DeviceMesh> get(const TriangleMesh& m) {
+        const std::size_t n = m.triangles.size();
+        const std::uint64_t h = hash(m);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            for (auto [it, end] = map_.equal_range(h); it != end; ++it) {
+                Entry& e = it->second;
+                if (e.flag == m.has_degenerate_faces && e.faces.size() == n &&
+                    std::memcmp(e.faces.data(), m.triangles.data(), n * sizeof(Triangle)) == 0) {
+                    e.tick = ++tick_;
+                    return e.dev;
+                }
+            }
+        }
+        auto dev = std::make_shared<const DeviceMesh>(m);  // upload outside the lock
+        std::lock_guard<std::mutex> lk(mu_);
+        map_.emplace(h, Entry{m.triangles, m.has_degenerate_faces, dev, ++tick_});
+        faces_ += n;
+        while (faces_ > max_faces_ && map_.size() > 1) {  // evict the least recently used
+            auto victim = map_.begin();
+            for (auto it = map_.begin(); it != map_.end(); ++it)
+                if (it->second.tick < victim->second.tick) victim = it;
+            faces_ -= victim->second.faces.size();
+            map_.erase(victim);
+        }
+        return dev;
+    }
+    void clear() {
+        std::lock_guard<std::mutex> lk(mu_);
+        map_.clear();
+        faces_ = 0;
+    }
+    std::size_t size() const {
+        std::lock_guard<std::mutex> lk(mu_);
+        return map_.size();
+    }
+
+  private:
+    struct Entry {
+        std::vector<Triangle> faces;
+        bool flag;
+        std::shared_ptr<const DeviceMesh> dev;
+        std::uint64_t tick;
+    };
+    static std::uint64_t hash(const TriangleMesh& m) {
+        const std::size_t words = m.triangles.size() * sizeof(Triangle) / 8;
+        const auto* p = reinterpret_cast<const unsigned char*>(m.triangles.data());
+        std::uint64_t h = 0x9E3779B97F4A7C15ull ^ words;
+        for (std::size_t i = 0; i < words; ++i) {
+            std::uint64_t w;
+            std::memcpy(&w, p + 8 * i, 8);
+            h = (h ^ w) * 0xFF51AFD7ED558CCDull;
+            h ^= h >> 32;
+        }
+        return h ^ (m.has_degenerate_faces ? 0x5851F42D4C957F2Dull : 0);
+    }
+    mutable std::mutex mu_;
+    std::unordered_multimap<std::uint64_t, Entry> map_;
+    std::size_t faces_ = 0, max_faces_;
+    std::uint64_t tick_ = 0;
+};
+
+inline MeshCache& default_mesh_cache() {
+    static MeshCache cache;
+    return cache;
+}
+
 struct MeshPairInfo {
     std::optional<std::uint64_t> pair_index;  // i * |b| + j, lowest on ties
     std::optional<std::size_t> face_a, face_b;
@@ -118,8 +198,8 @@ inline DistanceResult mesh_mesh_distance(const DeviceMesh& a, const DeviceMesh& 
 inline DistanceResult mesh_mesh_distance(const TriangleMesh& a, const TriangleMesh& b,
                                          const ExecutorConfig& /*cfg*/ = ExecutorConfig::sequential(),
                                          MeshPairInfo* info = nullptr) {
-    DeviceMesh da(a), db(b);
-    return mesh_mesh_distance(da, db, info);
+    const auto da = default_mesh_cache().get(a), db = default_mesh_cache().get(b);
+    return mesh_mesh_distance(*da, *db, info);
 }
 
 inline IntersectionResult mesh_mesh_intersects(const DeviceMesh& a, const DeviceMesh& b,
@@ -139,8 +219,8 @@ inline IntersectionResult mesh_mesh_intersects(const DeviceMesh& a, const Device
 inline IntersectionResult mesh_mesh_intersects(const TriangleMesh& a, const TriangleMesh& b,
                                                const ExecutorConfig& /*cfg*/ = ExecutorConfig::sequential(),
                                                MeshPairInfo* info = nullptr) {
-    DeviceMesh da(a), db(b);
-    return mesh_mesh_intersects(da, db, info);
+    const auto da = default_mesh_cache().get(a), db = default_mesh_cache().get(b);
+    return mesh_mesh_intersects(*da, *db, info);
 }
 
 // Several devices from this process (tdb_group_*): geometry replicated on
@@ -226,9 +306,9 @@ inline double mesh_volume(const TriangleMesh& mesh, const ExecutorConfig& cfg, b
                                 " boundary edge(s), " + std::to_string(report.inconsistent_edge_count) +
                                 " inconsistent directed edge use(s)");
     }
-    DeviceMesh d(mesh);
+    const auto d = default_mesh_cache().get(mesh);
     double v = 0.0;
-    check(tdb_mesh_volume(d.handle(), cfg.chunk_size, &v));
+    check(tdb_mesh_volume(d->handle(), cfg.chunk_size, &v));
     return v;
 }
 
@@ -258,20 +338,20 @@ inline DistanceResult distance_result_for(const TriangleMesh& mesh, int kind, co
 inline DistanceResult distance_to_mesh(const Point3& query, const TriangleMesh& mesh,
                                        const ExecutorConfig& /*cfg*/) {
     const double q[3] = {query.x, query.y, query.z};
-    DeviceMesh dm(mesh);
+    const auto dm = default_mesh_cache().get(mesh);
     double d = 0.0;
     std::uint64_t face = 0;
-    check(tdb_points_mesh_distance(q, 1, dm.handle(), &d, &face));
+    check(tdb_points_mesh_distance(q, 1, dm->handle(), &d, &face));
     return distance_result_for(mesh, TDB_QUERY_POINTS, q, d, face);
 }
 
 inline DistanceResult distance_to_mesh(const LineSegment& query, const TriangleMesh& mesh,
                                        const ExecutorConfig& /*cfg*/) {
     const double q[6] = {query.p0.x, query.p0.y, query.p0.z, query.p1.x, query.p1.y, query.p1.z};
-    DeviceMesh dm(mesh);
+    const auto dm = default_mesh_cache().get(mesh);
     double d = 0.0;
     std::uint64_t face = 0;
-    check(tdb_segments_mesh_distance(q, 1, dm.handle(), &d, &face));  // zero length: a point query
+    check(tdb_segments_mesh_distance(q, 1, dm->handle(), &d, &face));  // zero length: a point query
     return distance_result_for(mesh, TDB_QUERY_SEGMENTS, q, d, face);
 }
 
@@ -289,10 +369,10 @@ inline DistanceResult distance_to_mesh(const Geometry& query, const TriangleMesh
 inline IntersectionResult intersects_mesh(const LineSegment& query, const TriangleMesh& mesh,
                                           const ExecutorConfig& /*cfg*/) {
     const double q[6] = {query.p0.x, query.p0.y, query.p0.z, query.p1.x, query.p1.y, query.p1.z};
-    DeviceMesh dm(mesh);
+    const auto dm = default_mesh_cache().get(mesh);
     std::uint8_t hit = 0;
     std::uint64_t face = 0;
-    check(tdb_segments_mesh_intersects(q, 1, dm.handle(), &hit, &face));
+    check(tdb_segments_mesh_intersects(q, 1, dm->handle(), &hit, &face));
     IntersectionResult r;
     if (!hit) return r;
     tdb_face_result f{};
@@ -468,7 +548,8 @@ inline std::vector<KernelResult> run_batch_columns(BatchOp op, const std::vector
     }
     const bool need_lit = cols.meshes || cols.segments || (cols.points && op == BatchOp::Distance);
     if (!need_lit) return out;
-    DeviceMesh lit(std::get<TriangleMesh>(literal));
+    const auto litp = default_mesh_cache().get(std::get<TriangleMesh>(literal));
+    const DeviceMesh& lit = *litp;
     auto put = [&](const std::vector<std::size_t>& rows, const std::vector<double>& dist,
                    const std::vector<std::uint8_t>& hit) {
         for (std::size_t k = 0; k < rows.size(); ++k) {

@@ -38,16 +38,68 @@ thread_local uint64_t t_wkt_literal = 0, t_wkt_pos = 0;
 thread_local unsigned long long* t_shared_hit = nullptr;
 
 std::mutex g_mu;
-std::vector<cudaStream_t> g_streams;  // library stream per device
+std::vector<cudaStream_t> g_streams;  // library stream per device (stream-ordered frees)
 std::vector<int> g_sms;
+// Per-device pool of call streams (SURVEY.md 8(b) threading): every C-ABI
+// call runs on a stream of its own, taken from the pool when the call starts
+// and returned (idle) when it ends, so calls from concurrent threads — the
+// reference server runs plan_and_execute on one thread per connection,
+// pg_server.cpp:231,496 — overlap on the device instead of queueing on one
+// stream. A thread that set its own stream (tdb_set_stream) uses that.
+std::vector<std::vector<cudaStream_t>> g_pool;
+thread_local int t_depth = 0;  // nesting of guarded() on this thread
+
+struct HeldStream {
+    cudaStream_t s = nullptr;
+    int dev = -1;
+    bool scoped = false;  // taken inside a C-ABI call: returned when it ends
+    void give_back() {
+        if (!s) return;
+        cudaSetDevice(dev);
+        cudaStreamSynchronize(s);  // idle before anyone else gets it (error paths included)
+        std::lock_guard<std::mutex> lk(g_mu);
+        g_pool[dev].push_back(s);
+        s = nullptr;
+    }
+    ~HeldStream() { give_back(); }
+};
+thread_local HeldStream t_held;
+
+cudaStream_t pooled_stream(int dev) {
+    if (t_held.s && t_held.dev == dev) return t_held.s;
+    t_held.give_back();
+    cudaStream_t s = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (!g_pool[dev].empty()) {
+            s = g_pool[dev].back();
+            g_pool[dev].pop_back();
+        }
+    }
+    if (!s) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    t_held.s = s;
+    t_held.dev = dev;
+    t_held.scoped = t_depth > 0;
+    return s;
+}
 
 int fail(int code, const std::string& msg) {
     t_err = msg;
     return code;
 }
 
+// a call-scoped pooled stream goes back to the pool when the outermost
+// C-ABI call of this thread returns (every call has synchronized by then)
+struct CallScope {
+    CallScope() { ++t_depth; }
+    ~CallScope() {
+        if (--t_depth == 0 && t_held.scoped) t_held.give_back();
+    }
+};
+
 template <class F>
 int guarded(F&& f) {
+    CallScope scope;
     try {
         f();
         t_err.clear();
@@ -86,6 +138,7 @@ void ensure_device() {
     if ((int)g_streams.size() < n) {
         g_streams.resize(n, nullptr);
         g_sms.resize(n, 0);
+        g_pool.resize(n);
     }
     if (!g_streams[dev]) {
         CK(cudaStreamCreateWithFlags(&g_streams[dev], cudaStreamNonBlocking));
@@ -110,7 +163,7 @@ cudaStream_t lib_stream(int dev) {
 tdb::Ctx ctx() {
     ensure_device();
     tdb::Ctx c;
-    c.stream = t_stream_set ? t_stream : g_streams[t_device];
+    c.stream = t_stream_set ? t_stream : pooled_stream(t_device);
     c.mode = t_mode;
     c.sms = g_sms[t_device];
     c.stats = &t_stats;
@@ -504,6 +557,17 @@ int tdb_queries_mesh_intersects(tdb_queries q, tdb_mesh mesh, uint8_t* hit_out, 
 
 static int one_shot_queries(const double* q, uint64_t n, int kind, int op, tdb_mesh mesh, double* dist,
                             uint8_t* hit, uint64_t* face) {
+    if (mesh && n > 0 && n <= (uint64_t)tdb::kDirectQueries && n * mesh->g.n <= tdb::direct_query_pairs())
+        return guarded([&] {  // small call: one launch, no query upload (direct.cu)
+            need(q != nullptr && face != nullptr && (op == TDB_OP_DISTANCE ? dist != nullptr : hit != nullptr),
+                 "null argument");
+            need(kind == TDB_QUERY_SEGMENTS || kind == TDB_QUERY_POINTS, "unknown query kind");
+            need(op == TDB_OP_DISTANCE || kind == TDB_QUERY_SEGMENTS,
+                 "intersects takes segment queries (intersects_mesh, kernels.hpp:80)");
+            need(mesh->g.n_obj == 1, "the argument must be a mesh (one object)");
+            tdb::run_queries_direct(ctx(), op, q, n, kind == TDB_QUERY_POINTS ? tdb::kQueryPoints : tdb::kQuerySegments,
+                                    mesh->g, dist, hit, face);
+        });
     tdb_queries qs = nullptr;
     int rc = tdb_queries_upload(q, n, kind, &qs);
     if (rc == TDB_OK)

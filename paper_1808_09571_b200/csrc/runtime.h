@@ -218,6 +218,30 @@ inline std::vector<ASel> tile_batches(const ASel& sel, uint64_t max_tiles) {
 void run_distance(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, uint64_t* pair,
                   double* witness6);
 void run_intersects(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit, uint64_t* pair);
+// Small calls in one launch each (direct.cu): the exact composition on every
+// pair, no filter / band. Used for one-object selections of at most
+// direct_pairs() pairs, and for at most kDirectQueries one-shot queries of at
+// most direct_query_pairs() (query, face) pairs. TDB_DIRECT_PAIRS overrides
+// both limits (0 = never; tests run both paths on the same inputs).
+constexpr int kDirectQueries = 16;
+inline uint64_t direct_limit(uint64_t dflt) {
+    const char* e = getenv("TDB_DIRECT_PAIRS");
+    return e ? (uint64_t)strtoull(e, nullptr, 10) : dflt;
+}
+inline uint64_t direct_pairs() {
+    static const uint64_t v = direct_limit(1ull << 15);
+    return v;
+}
+inline uint64_t direct_query_pairs() {
+    static const uint64_t v = direct_limit(1ull << 16);
+    return v;
+}
+bool direct_eligible(const ASel& sel, const Geom& B);
+void run_distance_direct(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, uint64_t* pair,
+                         double* witness6);
+void run_intersects_direct(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit, uint64_t* pair);
+void run_queries_direct(const Ctx& cx, int op, const double* q, uint64_t n, int kind, const Geom& B, double* dist,
+                        uint8_t* hit, uint64_t* face);
 
 // Exact composition over aligned pair arrays (parity entry points).
 void run_pairs(const Ctx& cx, const double* a9, const double* b9, uint64_t n, double* dist,

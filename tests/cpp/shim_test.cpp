@@ -5,6 +5,7 @@
 #include <tindb/batch.hpp>
 #include <tindb/dataset.hpp>
 
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <cstdint>
@@ -214,6 +215,23 @@ int main() {
             for (int k = 0; k < 2; ++k)
                 EXPECT(same_bits(std::get<double>(rb[k].value), std::get<double>(rr[k].value)));
         }
+    }
+
+    // the device mesh cache: same content -> one upload, any change -> a new entry
+    {
+        auto& cache = K::b200::default_mesh_cache();
+        cache.clear();
+        const TriangleMesh m = bench::unit_sphere(1000);
+        const Point3 p{0.3, -0.2, 1.7};
+        const auto r1 = K::b200::distance_to_mesh(p, m, cfg);
+        const auto r2 = K::b200::distance_to_mesh(p, TriangleMesh(m), cfg);  // equal copy: a hit
+        EXPECT(cache.size() == 1 && same_bits(r1.distance, r2.distance) && r1.face_index == r2.face_index);
+        TriangleMesh moved = m;
+        moved.triangles[5].v1.x = std::nextafter(moved.triangles[5].v1.x, 2.0);
+        const auto r3 = K::b200::distance_to_mesh(p, moved, cfg);
+        EXPECT(cache.size() == 2);
+        const auto r4 = K::distance_to_mesh(p, moved, cfg);
+        EXPECT(same_bits(r3.distance, r4.distance) && r3.face_index == r4.face_index);
     }
 
     if (fails == 0) std::printf("SHIM OK\n");
