@@ -50,8 +50,14 @@ METRIC = "triangle-pair tests/sec (3DDistance, 3DIntersects) at 1/2/4/8 B200 vs 
 UNIT = "pairs/s"
 W_D = 975.0            # algorithmic FP64 flops per pair, distance
 W_I = 282.0            # algorithmic FP64 flops per pair, intersects no-hit
-FILTER_DP_INSTR = 304  # FP64-pipe instructions per pair in filter_kernel (cuobjdump -sass count)
-FILTER_FLOPS = 478     # executed FP64 flops per pair (174 DFMA x 2 + 79 DMUL + 51 DADD)
+# filter_kernel's three candidate loops (scripts/sass_loops.py build/distance.o
+# filter_kernel): (FP64-pipe instructions, executed FP64 flops) per iteration
+# of the B-face, B-vertex and B-edge loops. Per pair (one A row x one B face)
+# the kernel runs the face loop once and the vertex / edge loops
+# (distinct vertices / edges per 64-face block) / (faces) times.
+FILTER_LOOP_FACE = (55, 79)
+FILTER_LOOP_VERTEX = (13, 19)
+FILTER_LOOP_EDGE = (89, 145)
 U64_MAX = (1 << 64) - 1
 C3S_AXIS, C3S_ANGLE = (1.0, 2.0, 3.0), 0.37  # C3 stress variant rotation
 
@@ -706,8 +712,14 @@ def main():
         "kernel_share_of_step": sum(k_ms) / ms if world == 1 else None,
     }
     if wl.op == "distance" and wl.name != "paper":
-        roofline["fp64_pipe_frac"] = FILTER_DP_INSTR * f_pairs / (f_ms * 1e-3) / (fp64_tf * 1e12 / 2)
-        roofline["executed_fp64_tflops"] = FILTER_FLOPS * f_pairs / (f_ms * 1e-3) / 1e12
+        fc = (wl.dQ if wl.table else wl.dB).feature_counts()
+        per_face_v, per_face_e = fc["vertices"] / fc["faces"], fc["edges"] / fc["faces"]
+        instr = FILTER_LOOP_FACE[0] + per_face_v * FILTER_LOOP_VERTEX[0] + per_face_e * FILTER_LOOP_EDGE[0]
+        flops = FILTER_LOOP_FACE[1] + per_face_v * FILTER_LOOP_VERTEX[1] + per_face_e * FILTER_LOOP_EDGE[1]
+        roofline["b_features_per_face"] = {"vertices": per_face_v, "edges": per_face_e}
+        roofline["fp64_instr_per_pair"] = instr
+        roofline["fp64_pipe_frac"] = instr * f_pairs / (f_ms * 1e-3) / (fp64_tf * 1e12 / 2)
+        roofline["executed_fp64_tflops"] = flops * f_pairs / (f_ms * 1e-3) / 1e12
     elif wl.op == "intersects":
         roofline["note"] = ("culled pairs skip the W_i work (conservative FP32/FP64 separating-plane test, "
                             "DESIGN.md 4.3): frac > 1 is algorithmic, not hardware")

@@ -370,6 +370,25 @@ int tdb_geom_set_has_degenerate_faces(tdb_mesh g, const uint8_t* flags, uint64_t
     });
 }
 
+int tdb_geom_feature_counts(tdb_mesh g, uint64_t* faces, uint64_t* vertices, uint64_t* edges) {
+    return guarded([&] {
+        need(g != nullptr, "null handle");
+        cudaSetDevice(g->g.device);
+        const cudaStream_t st = lib_stream(g->g.device);
+        tdb::geom_feature_blocks(g->g, st);
+        std::vector<uint4> h(g->g.n_fblocks);
+        if (!h.empty()) {
+            CK(cudaMemcpyAsync(h.data(), g->g.d_fhdr, h.size() * sizeof(uint4), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        }
+        uint64_t t[3] = {0, 0, 0};
+        for (const uint4& b : h) t[0] += b.x, t[1] += b.y, t[2] += b.z;
+        if (faces) *faces = t[0];
+        if (vertices) *vertices = t[1];
+        if (edges) *edges = t[2];
+    });
+}
+
 void tdb_mesh_free(tdb_mesh m) {
     if (!m) return;
     cudaSetDevice(m->g.device);

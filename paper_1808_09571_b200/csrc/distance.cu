@@ -51,6 +51,10 @@ struct DistArgs {
     const unsigned long long* perm;
     const unsigned long long* lb2;
     unsigned long long* evaluated;  // pairs actually run through the filter
+    // B's feature blocks (tdb_internal.h kFB) and the staged block capacity
+    const double* Bfb;
+    const uint4* Bfhdr;
+    uint32_t stage;  // doubles per SMEM stage (>= every block's used doubles, even)
 };
 
 __device__ __forceinline__ double warp_min_nn(double x) {
@@ -63,7 +67,7 @@ __device__ __forceinline__ double warp_min_nn(double x) {
 #define TDB_FILTER_MINB 3
 #endif
 __global__ void __launch_bounds__(kTile, TDB_FILTER_MINB) filter_kernel(DistArgs a) {
-    __shared__ alignas(128) double sm[2][kFilterPlanes * kSB];
+    extern __shared__ __align__(128) double dsm[];  // 2 stages of a.stage doubles: one feature block each
     __shared__ alignas(8) uint64_t bar[2];
     __shared__ double red[kTile / 32];
 
@@ -87,8 +91,10 @@ __global__ void __launch_bounds__(kTile, TDB_FILTER_MINB) filter_kernel(DistArgs
     load_aface(A, FaceRefLdg{a.Ap + row, a.An_pad});
     active = active && __ldg(a.Ap + (uint64_t)F_DEG * a.An_pad + row) == 0.0;
 
+    // the item's B faces [b0, b1) are whole feature blocks (chunk % kFB == 0)
     const uint64_t b0 = ch * a.chunk, b1 = min(a.Bn, b0 + a.chunk);
-    const int nsub = (int)((b1 - b0 + kSB - 1) / kSB);
+    const uint64_t blk0 = b0 / kFB;
+    const int nblk = (int)((b1 - b0 + kFB - 1) / kFB);
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -97,44 +103,72 @@ __global__ void __launch_bounds__(kTile, TDB_FILTER_MINB) filter_kernel(DistArgs
     __syncthreads();
     auto issue = [&](int s) {
         const int st = s & 1;
-        const uint64_t f0 = b0 + (uint64_t)s * kSB;
-        const int cnt = (int)min((uint64_t)kSB, b1 - f0);
-        const uint32_t bytes = (uint32_t)(((cnt + 1) & ~1) * sizeof(double));
-        mbar_expect_tx(&bar[st], bytes * kFilterPlanes);
-#pragma unroll 1
-        for (int f = 0; f < kFilterPlanes; ++f) bulk_g2s(&sm[st][f * kSB], a.Bp + (uint64_t)f * a.Bn_pad + f0, bytes, &bar[st]);
+        const uint32_t bytes = __ldg(&a.Bfhdr[blk0 + s].w) * (uint32_t)sizeof(double);
+        mbar_expect_tx(&bar[st], bytes);
+        if (bytes) bulk_g2s(dsm + (size_t)st * a.stage, a.Bfb + (blk0 + s) * (uint64_t)kFBCap, bytes, &bar[st]);
     };
     if (threadIdx.x == 0) {
         issue(0);
-        if (nsub > 1) issue(1);
+        if (nblk > 1) issue(1);
     }
-    double best = pos_inf();
+    int best = kInfHi, hmin = kInfHi;
+    bool pierce = false;
 #pragma unroll 1
-    for (int s = 0; s < nsub; ++s) {
+    for (int s = 0; s < nblk; ++s) {
         const int st = s & 1;
+        const uint4 h = __ldg(&a.Bfhdr[blk0 + s]);
         mbar_wait(&bar[st], (uint32_t)((s >> 1) & 1));
-        const int cnt = (int)min((uint64_t)kSB, b1 - (b0 + (uint64_t)s * kSB));
-        const double* sb = sm[st];
-        int j = 0;
+        const double* fr = dsm + (size_t)st * a.stage;
+        const double* vr = fr + kFR * h.x;
+        const double* er = vr + kVR * h.y;
+        // faces: A's vertices against B's face, straddle -> piercing test
 #pragma unroll 1
-        for (; j < cnt; ++j) {
-            if (reinterpret_cast<const int*>(sb + F_DEG * kSB + j)[1] != 0) continue;  // uniform across the CTA
-            best = min_nn(best, pair_d2(A, FaceRef{sb + j, (uint64_t)kSB}, a.Ap + row, a.An_pad));
+        for (int j = 0; j < (int)h.x; ++j) {
+            const double2* q = reinterpret_cast<const double2*>(fr + kFR * j);
+            double b[9], nb[3], ub[3], vb[3];
+            {
+                const double2 q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3], q4 = q[4], q5 = q[5], q6 = q[6],
+                              q7 = q[7], q8 = q[8];
+                b[0] = q0.x, b[1] = q0.y, b[2] = q1.x, b[3] = q1.y, b[4] = q2.x, b[5] = q2.y, b[6] = q3.x;
+                b[7] = q3.y, b[8] = q4.x;
+                nb[0] = q4.y, nb[1] = q5.x, nb[2] = q5.y;
+                ub[0] = q6.x, ub[1] = q6.y, ub[2] = q7.x;
+                vb[0] = q7.y, vb[1] = q8.x, vb[2] = q8.y;
+            }
+            if (face_cand(A, b, nb, ub, vb, hmin)) {
+                const uint64_t fi = (uint64_t)__double_as_longlong(fr[kFR * j + FR_IDX]);
+                pierce |= pierce_slow(a.Ap + row, a.An_pad, a.Bp + fi, a.Bn_pad);
+            }
+        }
+        // B's distinct vertices against A's face
+#pragma unroll 1
+        for (int j = 0; j < (int)h.y; ++j) {
+            const double2 p0 = reinterpret_cast<const double2*>(vr + kVR * j)[0];
+            const double pz = vr[kVR * j + 2];
+            hmin = min(hmin, vertex_cand(A, p0.x, p0.y, pz));
+        }
+        // B's distinct edges against A's edges
+#pragma unroll 1
+        for (int j = 0; j < (int)h.z; ++j) {
+            const double2* q = reinterpret_cast<const double2*>(er + kER * j);
+            const double2 q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3];
+            best = min(best, edge_cand(A, q0.x, q0.y, q1.x, q1.y, q2.x, q2.y, q3.x, q3.y));
         }
         __syncthreads();
-        if (threadIdx.x == 0 && s + 2 < nsub) issue(s + 2);
+        if (threadIdx.x == 0 && s + 2 < nblk) issue(s + 2);
     }
-    if (!active) best = pos_inf();
-    best = warp_min_nn(best);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+    double m = __hiloint2double(pierce ? 0 : min(best, hmin_sq(hmin)), 0);
+    if (!active || b1 <= b0) m = pos_inf();
+    m = warp_min_nn(m);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
     const int rows_live = __syncthreads_count(active);
     if (threadIdx.x == 0) {
-        double m = red[0];
+        double mm = red[0];
 #pragma unroll
-        for (int w = 1; w < kTile / 32; ++w) m = min_nn(m, red[w]);
-        a.itemmin[item] = m;
+        for (int w = 1; w < kTile / 32; ++w) mm = min_nn(mm, red[w]);
+        a.itemmin[item] = mm;
         atomicAdd(a.evaluated, (unsigned long long)rows_live * (b1 - b0));
-        if (m < pos_inf()) atomicMin(a.objmin + (T.obj - a.obj0), (unsigned long long)__double_as_longlong(m));
+        if (mm < pos_inf()) atomicMin(a.objmin + (T.obj - a.obj0), (unsigned long long)__double_as_longlong(mm));
     }
 }
 
@@ -425,7 +459,7 @@ void run_distance(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, u
                   double* witness6) {
     if (direct_eligible(sel, B)) return run_distance_direct(cx, sel, B, dist, pair, witness6);
     const uint64_t ntiles = sel.tile1 - sel.tile0;
-    const uint64_t chunk = pick_chunk(ntiles, B.n, cx.sms, 12);
+    const uint64_t chunk = pick_chunk(ntiles, B.n, cx.sms, 12, kFB);
     const uint64_t n_chunks = (B.n + chunk - 1) / chunk;
     if (ntiles * n_chunks <= max_items() || ntiles <= 1) return run_distance_batch(cx, sel, B, dist, pair, witness6);
     // too many items for one launch: tile batches, merged per object
@@ -470,7 +504,7 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
     const cudaStream_t st = cx.stream;
     const uint64_t nobj = sel.obj1 - sel.obj0;
     const uint64_t ntiles = sel.tile1 - sel.tile0;
-    const uint64_t chunk = pick_chunk(ntiles, B.n, cx.sms, 12);
+    const uint64_t chunk = pick_chunk(ntiles, B.n, cx.sms, 12, kFB);
     const uint64_t n_chunks = (B.n + chunk - 1) / chunk;
     const uint64_t n_items = ntiles * n_chunks;
     for (uint64_t o = 0; o < nobj; ++o) {
@@ -548,9 +582,15 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
         cull_mem[0] = caabb, cull_mem[1] = keys, cull_mem[2] = vals, cull_mem[3] = tmp;
         launches += 3;
     }
+    geom_feature_blocks(B, st);
+    const uint32_t stage = (std::max<uint32_t>(B.fblock_max, 2) + 15) & ~15u;  // 128-byte aligned stages
+    const size_t smem = 2 * (size_t)stage * sizeof(double);
+    // per device (a device group calls from one thread per device); cheap
+    CK(cudaFuncSetAttribute(filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            2 * kFBCap * (int)sizeof(double)));
     DistArgs da{A.planes, A.n_pad, A.d_tiles, sel.tile0, sel.row_lo, sel.row_hi, B.planes, B.n_pad, B.n,
-                n_chunks, chunk, sel.obj0, sc.itemmin, sc.objmin, perm, lb2, ctr + 3};
-    filter_kernel<<<(unsigned)n_items, kTile, 0, st>>>(da);
+                n_chunks, chunk, sel.obj0, sc.itemmin, sc.objmin, perm, lb2, ctr + 3, B.fblocks, B.d_fhdr, stage};
+    filter_kernel<<<(unsigned)n_items, kTile, smem, st>>>(da);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ev.e[1], st));
     ++launches;

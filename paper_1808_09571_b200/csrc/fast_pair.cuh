@@ -10,9 +10,9 @@
 // squared distances with FMA; the only reciprocal is rcp.approx
 // (MUFU.RCP64H) + one Newton step for the first s (the value is always a
 // distance between two real points of the triangles; its excess over the
-// true distance is bounded in DESIGN.md 4.2). Per pair: 27 DADD (vertex differences) + 6 x 12
-// (vertex/face) + 9 x 27 (edge/edge) = 342 FP64 pipe instructions, no
-// DDIV/DSQRT.
+// true distance is bounded in DESIGN.md 4.2). No DDIV/DSQRT. Cost per
+// candidate (FP64 pipe): vertex/face 12, a face's three A vertices + the
+// straddle signs 51, an edge of B against A's three edges 90.
 //
 // The value d~^2 approximates the A17 composition's distance
 // closely enough to bound it: the exact pass (distance.cu) re-evaluates with
@@ -168,86 +168,111 @@ __device__ __forceinline__ bool inside(double u, double v) {
     return ((__double2hiint(u) | __double2hiint(v)) >= 0) & (__double2hiint(u + v) < 0x3ff00000);
 }
 
-// d~^2 for face A (registers) against face B, truncated to its high word
-// (a lower bound within a relative 2^-20 of the value; the minima are kept
-// as 32-bit integers — one VIMNMX per candidate). `ap`/`as` locate A's
-// fields again for the out-of-line piercing test.
-//
-// Edge/edge dot products run incrementally across the 3x3 grid:
-//   cw_{j,k+1} = cw_{j,k} + bb_{j,k}   (w_{j,k+1} = w_{j,k} + Eb_k)
-//   fw_{j+1,k} = fw_{j,k} - bb_{j,k}   (w_{j+1,k} = w_{j,k} - Ea_j)
+// ---- the candidate families -------------------------------
+// Minima are kept as the high 32 bits of non-negative doubles (a lower bound
+// within a relative 2^-20 of the value: one VIMNMX per candidate).
+
+// Vertex P of B against face A: |h| when P projects inside A (w = P - A_0).
+__device__ __forceinline__ int vertex_cand(const AFace& A, double px, double py, double pz) {
+    const double wx = px - A.v[0], wy = py - A.v[1], wz = pz - A.v[2];
+    const double h = dot3(A.n, wx, wy, wz);
+    const double u = dot3(A.U, wx, wy, wz);
+    const double v = dot3(A.W, wx, wy, wz);
+    return inside(u, v) ? (__double2hiint(h) & 0x7fffffff) : kInfHi;
+}
+
+// Face B (vertices b[9], unit normal nb, dual basis ub / vb) against face A:
+// the vertices of A against B (|h| when inside, min into hmin); returns true
+// when each triangle straddles the other's plane (an edge may pierce a face).
+__device__ __forceinline__ bool face_cand(const AFace& A, const double b[9], const double nb[3], const double ub[3],
+                                          const double vb[3], int& hmin) {
+    int ha_or = 0, ha_and = -1;
+    double w0[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {  // A_j - B_0
+        const double wx = A.v[3 * j] - b[0], wy = A.v[3 * j + 1] - b[1], wz = A.v[3 * j + 2] - b[2];
+        if (j == 0) w0[0] = wx, w0[1] = wy, w0[2] = wz;
+        const double h = dot3(nb, wx, wy, wz);
+        const double u = dot3(ub, wx, wy, wz);
+        const double v = dot3(vb, wx, wy, wz);
+        ha_or |= __double2hiint(h);
+        ha_and &= __double2hiint(h);
+        hmin = min(hmin, inside(u, v) ? (__double2hiint(h) & 0x7fffffff) : kInfHi);
+    }
+    // B's vertices against A's plane (B_0 - A_0 = -(A_0 - B_0) exactly)
+    const double h0 = -dot3(A.n, w0[0], w0[1], w0[2]);
+    const double h1 = dot3(A.n, b[3] - A.v[0], b[4] - A.v[1], b[5] - A.v[2]);
+    const double h2 = dot3(A.n, b[6] - A.v[0], b[7] - A.v[1], b[8] - A.v[2]);
+    const int hb_or = __double2hiint(h0) | __double2hiint(h1) | __double2hiint(h2);
+    const int hb_and = __double2hiint(h0) & __double2hiint(h1) & __double2hiint(h2);
+    return !(hb_or >= 0 || hb_and < 0) && !(ha_or >= 0 || ha_and < 0);
+}
+
+// Edge P -> P + E of B (|E|^2 = Lb, 1/|E|^2 = ILb) against A's three edges:
+// Ericson's clamped segment distance (s from the unconstrained solve with a
+// Newton-refined reciprocal, t optimal for s, s optimal for the clamped t).
+// fw runs incrementally: w_j+1 = w_j - Ea_j => E.w_j+1 = E.w_j - E.Ea_j.
+__device__ __forceinline__ int edge_cand(const AFace& A, double px, double py, double pz, double ebx, double eby,
+                                         double ebz, double Lb, double ILb) {
+    double w[3][3];  // w_j = P - A_j
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        w[j][0] = px - A.v[3 * j];
+        w[j][1] = py - A.v[3 * j + 1];
+        w[j][2] = pz - A.v[3 * j + 2];
+    }
+    double fw = fma(ebx, w[0][0], fma(eby, w[0][1], ebz * w[0][2]));
+    int cand[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {  // edge A_j -> A_j+1
+        const double* ea = A.e + 3 * j;
+        const double bb = dot3(ea, ebx, eby, ebz);
+        const double cw = dot3(ea, w[j][0], w[j][1], w[j][2]);
+        // s0 = (cw Lb - bb fw) / (La Lb - bb^2), both terms divided by Lb
+        const double bbI = bb * ILb;
+        const double den = fma(-bbI, bb, A.L[j]);
+        const double num = fma(-bbI, fw, cw);
+        double s = clamp01(num * rcp_nr(den));
+        const double t = clamp01(fma(bb, s, -fw) * ILb);
+        s = clamp01(fma(bb, t, cw) * A.IL[j]);
+        const double dx = fma(s, ea[0], fma(-t, ebx, -w[j][0]));
+        const double dy = fma(s, ea[1], fma(-t, eby, -w[j][1]));
+        const double dz = fma(s, ea[2], fma(-t, ebz, -w[j][2]));
+        cand[j] = __double2hiint(fma(dx, dx, fma(dy, dy, dz * dz)));
+        fw = fw - bb;
+    }
+    return min(min(cand[0], cand[1]), cand[2]);
+}
+
+// The smallest |h| high word (hmin) as the high word of h^2.
+__device__ __forceinline__ int hmin_sq(int hmin) {
+    const double hv = __hiloint2double(hmin, 0);  // truncated |h|
+    return __double2hiint(hv * hv);
+}
+
+// d~^2 of the pair (face A in registers, face B through `bt`, plane layout),
+// truncated to its high word: the minimum of the pair's 15 candidates
+// (vertex_cand x 3, face_cand's 3, edge_cand x 3), 0 when an edge pierces a
+// face. The filter kernel evaluates the same candidates, each shared vertex
+// and edge once per feature block (distance.cu). `ap`/`as` locate A's fields
+// for the out-of-line piercing test.
 template <class P>
 __device__ __forceinline__ double pair_d2(const AFace& A, const P& bt, const double* ap, uint64_t as) {
-    int best = kInfHi;
-    int hmin = kInfHi;  // min |h| (high word) over vertices projecting inside the other face
-    int hb_or = 0, hb_and = -1, ha_or = 0, ha_and = -1;  // sign words of the plane heights
-    double cw_prev[3], bb_prev[3];
+    double b[9], nb[3], ub[3], vb[3];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) b[k] = bt(F_V + k);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) nb[k] = bt(F_N + k), ub[k] = bt(F_U + k), vb[k] = bt(F_W + k);
+    int hmin = kInfHi, best = kInfHi;
+    const bool straddle = face_cand(A, b, nb, ub, vb, hmin);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        const double bx = bt(F_V + 3 * k), by = bt(F_V + 3 * k + 1), bz = bt(F_V + 3 * k + 2);
-        double w[3][3];  // w_j = B_k - A_j
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-            w[j][0] = bx - A.v[3 * j];
-            w[j][1] = by - A.v[3 * j + 1];
-            w[j][2] = bz - A.v[3 * j + 2];
-        }
-        {  // vertex B_k against face A
-            const double h = dot3(A.n, w[0][0], w[0][1], w[0][2]);
-            const double u = dot3(A.U, w[0][0], w[0][1], w[0][2]);
-            const double v = dot3(A.W, w[0][0], w[0][1], w[0][2]);
-            hb_or |= __double2hiint(h);
-            hb_and &= __double2hiint(h);
-            hmin = min(hmin, inside(u, v) ? (__double2hiint(h) & 0x7fffffff) : kInfHi);
-        }
-        if (k == 0) {  // vertices A_j against face B: A_j - B_0 = -w_j
-            const double nb[3] = {bt(F_N), bt(F_N + 1), bt(F_N + 2)};
-            const double ub[3] = {bt(F_U), bt(F_U + 1), bt(F_U + 2)};
-            const double vb[3] = {bt(F_W), bt(F_W + 1), bt(F_W + 2)};
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                const double h = dot3(nb, w[j][0], w[j][1], w[j][2]);
-                const double u = -dot3(ub, w[j][0], w[j][1], w[j][2]);
-                const double v = -dot3(vb, w[j][0], w[j][1], w[j][2]);
-                ha_or |= __double2hiint(h);
-                ha_and &= __double2hiint(h);
-                hmin = min(hmin, inside(u, v) ? (__double2hiint(h) & 0x7fffffff) : kInfHi);
-            }
-        }
-        const double ebx = bt(F_E + 3 * k), eby = bt(F_E + 3 * k + 1), ebz = bt(F_E + 3 * k + 2);
-        const double Lb = bt(F_L + k), ILb = bt(F_IL + k);
-        double fw = fma(ebx, w[0][0], fma(eby, w[0][1], ebz * w[0][2]));
-        int cand[3];
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {  // edge A_j->A_j+1 against edge B_k->B_k+1
-            const double* ea = A.e + 3 * j;
-            const double bb = dot3(ea, ebx, eby, ebz);
-            const double cw = k == 0 ? dot3(ea, w[j][0], w[j][1], w[j][2]) : cw_prev[j] + bb_prev[j];
-            // s0 = (cw Lb - bb fw) / (La Lb - bb^2), both terms divided by Lb
-            const double bbI = bb * ILb;
-            const double den = fma(-bbI, bb, A.L[j]);
-            const double num = fma(-bbI, fw, cw);
-            double s = clamp01(num * rcp_nr(den));
-            const double t = clamp01(fma(bb, s, -fw) * ILb);
-            s = clamp01(fma(bb, t, cw) * A.IL[j]);
-            const double dx = fma(s, ea[0], fma(-t, ebx, -w[j][0]));
-            const double dy = fma(s, ea[1], fma(-t, eby, -w[j][1]));
-            const double dz = fma(s, ea[2], fma(-t, ebz, -w[j][2]));
-            cand[j] = __double2hiint(fma(dx, dx, fma(dy, dy, dz * dz)));
-            cw_prev[j] = cw;
-            bb_prev[j] = bb;
-            fw = fw - bb;
-        }
-        best = min(min(best, cand[0]), min(cand[1], cand[2]));  // VIMNMX3 pairs
+        hmin = min(hmin, vertex_cand(A, b[3 * k], b[3 * k + 1], b[3 * k + 2]));
+        best = min(best, edge_cand(A, b[3 * k], b[3 * k + 1], b[3 * k + 2], bt(F_E + 3 * k), bt(F_E + 3 * k + 1),
+                                   bt(F_E + 3 * k + 2), bt(F_L + k), bt(F_IL + k)));
     }
-    // Both triangles straddle the other's plane: an edge may pierce a face.
-    const bool sb = !(hb_or >= 0 || hb_and < 0);
-    const bool sa = !(ha_or >= 0 || ha_and < 0);
-    {
-        const double hv = __hiloint2double(hmin, 0);  // truncated |h|: one square per pair
-        best = min(best, __double2hiint(hv * hv));
-    }
-    if (sa && sb && pierce_slow(ap, as, bt.p, bt.stride)) best = 0;
+    best = min(best, hmin_sq(hmin));
+    if (straddle && pierce_slow(ap, as, bt.p, bt.stride)) best = 0;
     return __hiloint2double(best, 0);
 }
 

@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -63,7 +64,18 @@ struct Geom {
     // 0 (default) = skip them. tdb_geom_set_has_degenerate_faces.
     uint8_t* d_keep_deg = nullptr;
     std::vector<uint8_t> h_keep_deg;
+    // feature blocks (tdb_internal.h kFB): built on first use as the B side
+    // of a distance filter (geom_feature_blocks), kept until release
+    mutable double* fblocks = nullptr;  // n_fblocks x kFBCap doubles
+    mutable uint4* d_fhdr = nullptr;    // per block: faces, vertices, edges, doubles used
+    mutable uint64_t n_fblocks = 0;
+    mutable uint32_t fblock_max = 0;    // max doubles used by one block
+    std::shared_ptr<std::mutex> fmu = std::make_shared<std::mutex>();
 };
+
+// Builds g's feature blocks once (thread-safe; the build is complete on the
+// device when this returns).
+void geom_feature_blocks(const Geom& g, cudaStream_t st);
 
 // tri9: 9 doubles per face (AoS), on the host unless tri9_on_device
 void geom_build(Geom* g, const double* tri9, uint64_t n, const uint64_t* host_off, uint64_t n_obj,

@@ -330,8 +330,155 @@ void chunk_aabbs(const Geom& g, uint64_t len, double* out, cudaStream_t st) {
 // from it with cudaMallocAsync): a plain cudaFree hands the pages back to the
 // driver, and the next large upload then waits for them to be mapped again.
 // Every call that used the store has synchronized before it returns.
+namespace {
+
+// One CTA (kFB threads, one per face) per feature block: bitwise-distinct
+// vertices and unordered-vertex-pair edges of the block's non-degenerate
+// faces, packed as [faces | vertices | edges] (tdb_internal.h). A vertex or
+// edge is represented by its first occurrence in face order.
+__global__ void __launch_bounds__(kFB) fblock_kernel(const double* __restrict__ planes, uint64_t n, uint64_t n_pad,
+                                                     double* __restrict__ out, uint4* __restrict__ hdr,
+                                                     unsigned* __restrict__ max_used) {
+    constexpr int R = 3 * kFB;  // vertex / edge references of the block
+    __shared__ unsigned long long vx[R], vy[R], vz[R];
+    __shared__ int rep[R];
+    __shared__ unsigned ekey[R];
+    __shared__ int live_s[kFB];
+    __shared__ int scan[3][kFB + 1];
+    const int t = threadIdx.x;
+    const uint64_t blk = blockIdx.x, f = blk * kFB + t;
+    const bool live = f < n && planes[(uint64_t)F_DEG * n_pad + f] == 0.0;
+    live_s[t] = live;
+    double v[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) v[k] = f < n ? planes[(uint64_t)(F_V + k) * n_pad + f] : 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        vx[3 * t + k] = (unsigned long long)__double_as_longlong(v[3 * k]);
+        vy[3 * t + k] = (unsigned long long)__double_as_longlong(v[3 * k + 1]);
+        vz[3 * t + k] = (unsigned long long)__double_as_longlong(v[3 * k + 2]);
+    }
+    __syncthreads();
+    int uv[3], ue[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int r = 3 * t + k;
+        int rr = r;
+        if (live)
+            for (int q = 0; q < r; ++q)
+                if (live_s[q / 3] && vx[q] == vx[r] && vy[q] == vy[r] && vz[q] == vz[r]) {
+                    rr = q;
+                    break;
+                }
+        rep[r] = rr;
+        uv[k] = live && rr == r;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const unsigned a = (unsigned)rep[3 * t + k], b = (unsigned)rep[3 * t + (k == 2 ? 0 : k + 1)];
+        ekey[3 * t + k] = min(a, b) << 16 | max(a, b);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int r = 3 * t + k;
+        bool first = live;
+        if (live)
+            for (int q = 0; q < r; ++q)
+                if (live_s[q / 3] && ekey[q] == ekey[r]) {
+                    first = false;
+                    break;
+                }
+        ue[k] = first;
+    }
+    // exclusive scans of (faces, vertices, edges) over the block's threads
+    if (t == 0) scan[0][0] = scan[1][0] = scan[2][0] = 0;
+    __syncthreads();
+    if (t == 0) {
+        for (int q = 0; q < kFB; ++q) scan[0][q + 1] = scan[0][q] + live_s[q];
+    }
+    scan[1][t + 1] = uv[0] + uv[1] + uv[2];
+    scan[2][t + 1] = ue[0] + ue[1] + ue[2];
+    __syncthreads();
+    if (t == 0) {
+        for (int q = 0; q < kFB; ++q) {
+            scan[1][q + 1] += scan[1][q];
+            scan[2][q + 1] += scan[2][q];
+        }
+    }
+    __syncthreads();
+    const int NF = scan[0][kFB], NV = scan[1][kFB], NE = scan[2][kFB];
+    double* base = out + blk * (uint64_t)kFBCap;
+    if (live) {
+        double* fr = base + (uint64_t)kFR * scan[0][t];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) fr[FR_V + k] = v[k];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            fr[FR_N + k] = planes[(uint64_t)(F_N + k) * n_pad + f];
+            fr[FR_U + k] = planes[(uint64_t)(F_U + k) * n_pad + f];
+            fr[FR_W + k] = planes[(uint64_t)(F_W + k) * n_pad + f];
+        }
+        fr[FR_IDX] = __longlong_as_double((long long)f);
+        fr[FR_IDX + 1] = 0.0;
+        int vs = scan[1][t], es = scan[2][t];
+        double* vr = base + (uint64_t)kFR * NF;
+        double* er = vr + (uint64_t)kVR * NV;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if (uv[k]) {
+                double* p = vr + (uint64_t)kVR * vs++;
+                p[0] = v[3 * k], p[1] = v[3 * k + 1], p[2] = v[3 * k + 2], p[3] = 0.0;
+            }
+            if (ue[k]) {
+                double* p = er + (uint64_t)kER * es++;
+                p[ER_P] = v[3 * k], p[ER_P + 1] = v[3 * k + 1], p[ER_P + 2] = v[3 * k + 2];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) p[ER_E + c] = planes[(uint64_t)(F_E + 3 * k + c) * n_pad + f];
+                p[ER_L] = planes[(uint64_t)(F_L + k) * n_pad + f];
+                p[ER_IL] = planes[(uint64_t)(F_IL + k) * n_pad + f];
+            }
+        }
+    }
+    if (t == 0) {
+        const unsigned used = (unsigned)(kFR * NF + kVR * NV + kER * NE);
+        hdr[blk] = make_uint4((unsigned)NF, (unsigned)NV, (unsigned)NE, used);
+        atomicMax(max_used, used);
+    }
+}
+
+}  // namespace
+
+void geom_feature_blocks(const Geom& g, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(*g.fmu);
+    if (g.fblocks || g.n == 0) return;
+    const uint64_t nb = (g.n + kFB - 1) / kFB;
+    double* blocks = nullptr;
+    uint4* hdr = nullptr;
+    unsigned* mx = nullptr;
+    CK(cudaMallocAsync(&blocks, nb * (uint64_t)kFBCap * sizeof(double), st));
+    CK(cudaMallocAsync(&hdr, nb * sizeof(uint4), st));
+    CK(cudaMallocAsync(&mx, sizeof(unsigned), st));
+    CK(cudaMemsetAsync(mx, 0, sizeof(unsigned), st));
+    fblock_kernel<<<(unsigned)nb, kFB, 0, st>>>(g.planes, g.n, g.n_pad, blocks, hdr, mx);
+    CK(cudaGetLastError());
+    unsigned used = 0;
+    CK(cudaMemcpyAsync(&used, mx, sizeof used, cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(mx, st));
+    CK(cudaStreamSynchronize(st));
+    g.fblocks = blocks;
+    g.d_fhdr = hdr;
+    g.n_fblocks = nb;
+    g.fblock_max = used;
+}
+
 void geom_release(Geom* g, cudaStream_t st) {
     if (!g) return;
+    cudaFreeAsync(g->fblocks, st);
+    cudaFreeAsync(g->d_fhdr, st);
+    g->fblocks = nullptr;
+    g->d_fhdr = nullptr;
     cudaFreeAsync(g->planes, st);
     cudaFreeAsync(g->d_off, st);
     cudaFreeAsync(g->d_tiles, st);

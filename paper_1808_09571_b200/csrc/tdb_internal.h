@@ -44,6 +44,23 @@ constexpr uint64_t kChunk = 8192;   // B faces per work item
 constexpr int kSB = TDB_KSB;        // B faces per TMA-staged sub-tile
 constexpr int kPlanePad = 64;
 
+// ---- B feature blocks (the distance filter's B side) -------
+// B's faces in blocks of kFB consecutive faces. Per block, three AoS lists,
+// packed back to back from the block's base (fixed capacity kFBCap doubles):
+//   faces    (non-degenerate only): kFR doubles = V (9), N, U, W, face index
+//   vertices (distinct within the block, bitwise): kVR doubles = x y z 0
+//   edges    (distinct within the block, unordered vertex pair): kER doubles
+//            = start P (3), E = V_k+1 - V_k (3), |E|^2, 1/|E|^2 of the first
+//            face that has it
+// A pair's filter value is the minimum over its 6 vertex/face and 9 edge/edge
+// candidates; a shared vertex or edge is the same candidate for every face
+// of the block that has it, so the filter evaluates it once per block.
+constexpr int kFB = 64;
+enum : int { FR_V = 0, FR_N = 9, FR_U = 12, FR_W = 15, FR_IDX = 18, kFR = 20 };
+enum : int { ER_P = 0, ER_E = 3, ER_L = 6, ER_IL = 7, kER = 8 };
+constexpr int kVR = 4;
+constexpr int kFBCap = kFB * (kFR + 3 * kVR + 3 * kER);  // doubles per block (28,672 B)
+
 // per-object statistics (doubles): aabb lo xyz, hi xyz, max edge, max |coord|,
 // max kappa (F_K) over its non-degenerate faces
 constexpr int kObjStats = 9;
