@@ -144,11 +144,13 @@ int tdb_geom_info(tdb_mesh g, uint64_t* n_tris, uint64_t* n_objects, uint64_t* n
  * Mesh x mesh (A17) always skips degenerate faces; intersects never does
  * (intersects_mesh has no skip, kernels.cpp:407-432). */
 int tdb_geom_set_has_degenerate_faces(tdb_mesh g, const uint8_t* flags, uint64_t n_objects);
-/* The distance filter's B-side feature blocks (built on first
- * use, or here): totals over the store of the non-degenerate faces, distinct
- * vertices and distinct edges per block of 64 faces. No reference
+/* The distance filter's shared candidates (built on first use,
+ * or here): as the B side, totals over the store's 64-face feature blocks of
+ * non-degenerate faces, distinct vertices and distinct edges; as the A side,
+ * the total of the distinct edges of its 128-face tiles. No reference
  * counterpart (instrumentation for the roofline accounting). */
-int tdb_geom_feature_counts(tdb_mesh g, uint64_t* faces, uint64_t* vertices, uint64_t* edges);
+int tdb_geom_feature_counts(tdb_mesh g, uint64_t* faces, uint64_t* vertices, uint64_t* edges,
+                            uint64_t* tile_edges);
 void tdb_mesh_free(tdb_mesh m);
 void tdb_table_free(tdb_table t);
 

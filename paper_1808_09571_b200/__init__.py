@@ -108,7 +108,7 @@ _SIGS = [
     ("tdb_mesh_upload", ct.c_int, [_D, ct.c_uint64, ct.POINTER(ct.c_void_p)]),
     ("tdb_table_upload", ct.c_int, [_D, _U64, ct.c_uint64, ct.POINTER(ct.c_void_p)]),
     ("tdb_geom_info", ct.c_int, [ct.c_void_p, _U64, _U64, _U64, _D]),
-    ("tdb_geom_feature_counts", ct.c_int, [ct.c_void_p, _U64, _U64, _U64]),
+    ("tdb_geom_feature_counts", ct.c_int, [ct.c_void_p, _U64, _U64, _U64, _U64]),
     ("tdb_mesh_from_wkt", ct.c_int, [ct.c_char_p, ct.c_uint64, ct.POINTER(ct.c_void_p), _U64]),
     ("tdb_table_from_wkt", ct.c_int, [ct.c_char_p, _U64, ct.c_uint64, ct.POINTER(ct.c_void_p), _U64, _U64]),
     ("tdb_geom_download", ct.c_int, [ct.c_void_p, _D]),
@@ -258,12 +258,13 @@ class _Geom:
         return {"faces": n.value, "objects": no.value, "degenerate": nd.value, "aabb": list(box)}
 
     def feature_counts(self):
-        """The distance filter's B-side feature blocks: total
-        non-degenerate faces, distinct vertices and distinct edges over the
-        store's 64-face blocks."""
-        f, v, e = ct.c_uint64(), ct.c_uint64(), ct.c_uint64()
-        _check(lib().tdb_geom_feature_counts(self._h, ct.byref(f), ct.byref(v), ct.byref(e)))
-        return {"faces": f.value, "vertices": v.value, "edges": e.value}
+        """The distance filter's shared candidates: as the B
+        side, total non-degenerate faces, distinct vertices and distinct edges
+        over the store's 64-face blocks; as the A side, the distinct edges of
+        its 128-face tiles (tile_edges)."""
+        f, v, e, te = ct.c_uint64(), ct.c_uint64(), ct.c_uint64(), ct.c_uint64()
+        _check(lib().tdb_geom_feature_counts(self._h, ct.byref(f), ct.byref(v), ct.byref(e), ct.byref(te)))
+        return {"faces": f.value, "vertices": v.value, "edges": e.value, "tile_edges": te.value}
 
     def download(self) -> np.ndarray:
         """The stored faces as (n, 9) float64, face order (the AoS the store was built from)."""

@@ -370,7 +370,8 @@ int tdb_geom_set_has_degenerate_faces(tdb_mesh g, const uint8_t* flags, uint64_t
     });
 }
 
-int tdb_geom_feature_counts(tdb_mesh g, uint64_t* faces, uint64_t* vertices, uint64_t* edges) {
+int tdb_geom_feature_counts(tdb_mesh g, uint64_t* faces, uint64_t* vertices, uint64_t* edges,
+                            uint64_t* tile_edges) {
     return guarded([&] {
         need(g != nullptr, "null handle");
         cudaSetDevice(g->g.device);
@@ -386,6 +387,10 @@ int tdb_geom_feature_counts(tdb_mesh g, uint64_t* faces, uint64_t* vertices, uin
         if (faces) *faces = t[0];
         if (vertices) *vertices = t[1];
         if (edges) *edges = t[2];
+        if (tile_edges) {
+            tdb::geom_edge_tiles(g->g, st);
+            *tile_edges = g->g.h_aeoff.empty() ? 0 : g->g.h_aeoff.back();
+        }
     });
 }
 

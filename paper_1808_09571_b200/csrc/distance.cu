@@ -66,10 +66,26 @@ __device__ __forceinline__ double warp_min_nn(double x) {
 #ifndef TDB_FILTER_MINB
 #define TDB_FILTER_MINB 3
 #endif
+// unroll factors of the vertex / face / edge candidate loops
+#ifndef TDB_UV
+#define TDB_UV 4
+#endif
+#ifndef TDB_UF
+#define TDB_UF 2
+#endif
+#ifndef TDB_UE
+#define TDB_UE 2
+#endif
+constexpr int kUV = TDB_UV, kUF = TDB_UF, kUE = TDB_UE;
+// kEdges: also B's edges against each row's three edges (CULL mode, one
+// kernel per item); FULL mode runs those in edge_kernel over A's distinct
+// edges instead.
+template <bool kEdges>
 __global__ void __launch_bounds__(kTile, TDB_FILTER_MINB) filter_kernel(DistArgs a) {
     extern __shared__ __align__(128) double dsm[];  // 2 stages of a.stage doubles: one feature block each
     __shared__ alignas(8) uint64_t bar[2];
     __shared__ double red[kTile / 32];
+    __shared__ unsigned sgn[3 * kFB / 32][kTile];  // per thread: sign bits of the block's vertex heights
 
     const uint64_t item = a.perm ? a.perm[blockIdx.x] : blockIdx.x;
     const uint64_t tl = item / a.n_chunks, ch = item - tl * a.n_chunks;
@@ -103,7 +119,8 @@ __global__ void __launch_bounds__(kTile, TDB_FILTER_MINB) filter_kernel(DistArgs
     __syncthreads();
     auto issue = [&](int s) {
         const int st = s & 1;
-        const uint32_t bytes = __ldg(&a.Bfhdr[blk0 + s].w) * (uint32_t)sizeof(double);
+        const uint4 hb = __ldg(&a.Bfhdr[blk0 + s]);
+        const uint32_t bytes = (kEdges ? hb.w : kFR * hb.x + kVR * hb.y) * (uint32_t)sizeof(double);
         mbar_expect_tx(&bar[st], bytes);
         if (bytes) bulk_g2s(dsm + (size_t)st * a.stage, a.Bfb + (blk0 + s) * (uint64_t)kFBCap, bytes, &bar[st]);
     };
@@ -121,35 +138,46 @@ __global__ void __launch_bounds__(kTile, TDB_FILTER_MINB) filter_kernel(DistArgs
         const double* fr = dsm + (size_t)st * a.stage;
         const double* vr = fr + kFR * h.x;
         const double* er = vr + kVR * h.y;
-        // faces: A's vertices against B's face, straddle -> piercing test
+        // B's distinct vertices against A's face; the sign bits of their
+        // heights above A's plane go to this thread's words of sgn
 #pragma unroll 1
+        for (int j0 = 0; j0 < (int)h.y; j0 += 32) {
+            unsigned bits = 0;
+            const int j1 = min((int)h.y, j0 + 32);
+#pragma unroll kUV
+            for (int j = j0; j < j1; ++j) {
+                const double2 p0 = reinterpret_cast<const double2*>(vr + kVR * j)[0];
+                const double pz = vr[kVR * j + 2];
+                int hs;
+                hmin = min(hmin, vertex_cand(A, p0.x, p0.y, pz, hs));
+                bits |= (unsigned)hs >> 31 << (j - j0);
+            }
+            sgn[j0 >> 5][threadIdx.x] = bits;
+        }
+        // faces: A's vertices against B's face; both straddle -> piercing test
+#pragma unroll kUF
         for (int j = 0; j < (int)h.x; ++j) {
             const double2* q = reinterpret_cast<const double2*>(fr + kFR * j);
-            double b[9], nb[3], ub[3], vb[3];
-            {
-                const double2 q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3], q4 = q[4], q5 = q[5], q6 = q[6],
-                              q7 = q[7], q8 = q[8];
-                b[0] = q0.x, b[1] = q0.y, b[2] = q1.x, b[3] = q1.y, b[4] = q2.x, b[5] = q2.y, b[6] = q3.x;
-                b[7] = q3.y, b[8] = q4.x;
-                nb[0] = q4.y, nb[1] = q5.x, nb[2] = q5.y;
-                ub[0] = q6.x, ub[1] = q6.y, ub[2] = q7.x;
-                vb[0] = q7.y, vb[1] = q8.x, vb[2] = q8.y;
+            const double2 q0 = q[0], q1 = q[1], q6 = q[6], q7 = q[7], q8 = q[8], q9 = q[9];
+            const double2 q4 = q[4], q5 = q[5];
+            const double nb[3] = {q4.y, q5.x, q5.y}, ub[3] = {q6.x, q6.y, q7.x}, vb[3] = {q7.y, q8.x, q8.y};
+            double w0[3];
+            if (a_vertex_cand(A, q0.x, q0.y, q1.x, nb, ub, vb, hmin, w0)) {
+                const unsigned long long sl = (unsigned long long)__double_as_longlong(q9.y);
+                const unsigned s0 = (unsigned)sl & 1023u, s1 = (unsigned)(sl >> 10) & 1023u,
+                               s2 = (unsigned)(sl >> 20) & 1023u;
+                const unsigned g0 = sgn[s0 >> 5][threadIdx.x] >> (s0 & 31) & 1u;
+                const unsigned g1 = sgn[s1 >> 5][threadIdx.x] >> (s1 & 31) & 1u;
+                const unsigned g2 = sgn[s2 >> 5][threadIdx.x] >> (s2 & 31) & 1u;
+                if ((g0 | g1 | g2) && !(g0 & g1 & g2)) {
+                    const uint64_t fi = (uint64_t)__double_as_longlong(q9.x);
+                    pierce |= pierce_slow(a.Ap + row, a.An_pad, a.Bp + fi, a.Bn_pad);
+                }
             }
-            if (face_cand(A, b, nb, ub, vb, hmin)) {
-                const uint64_t fi = (uint64_t)__double_as_longlong(fr[kFR * j + FR_IDX]);
-                pierce |= pierce_slow(a.Ap + row, a.An_pad, a.Bp + fi, a.Bn_pad);
-            }
-        }
-        // B's distinct vertices against A's face
-#pragma unroll 1
-        for (int j = 0; j < (int)h.y; ++j) {
-            const double2 p0 = reinterpret_cast<const double2*>(vr + kVR * j)[0];
-            const double pz = vr[kVR * j + 2];
-            hmin = min(hmin, vertex_cand(A, p0.x, p0.y, pz));
         }
         // B's distinct edges against A's edges
-#pragma unroll 1
-        for (int j = 0; j < (int)h.z; ++j) {
+#pragma unroll kUE
+        for (int j = 0; j < (kEdges ? (int)h.z : 0); ++j) {
             const double2* q = reinterpret_cast<const double2*>(er + kER * j);
             const double2 q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3];
             best = min(best, edge_cand(A, q0.x, q0.y, q1.x, q1.y, q2.x, q2.y, q3.x, q3.y));
@@ -169,6 +197,92 @@ __global__ void __launch_bounds__(kTile, TDB_FILTER_MINB) filter_kernel(DistArgs
         a.itemmin[item] = mm;
         atomicAdd(a.evaluated, (unsigned long long)rows_live * (b1 - b0));
         if (mm < pos_inf()) atomicMin(a.objmin + (T.obj - a.obj0), (unsigned long long)__double_as_longlong(mm));
+    }
+}
+
+#ifndef TDB_EDGE_MINB
+#define TDB_EDGE_MINB 4
+#endif
+#ifndef TDB_UEE
+#define TDB_UEE 4
+#endif
+constexpr int kUEE = TDB_UEE;
+
+struct EdgeArgs {
+    const double* Ae;        // A edge entries (tdb_internal.h kAER)
+    uint64_t e_lo, e_hi;     // the selection's entries
+    uint64_t tile0;          // the selection's first tile
+    const Tile* tiles;
+    const double* Bfb;
+    const uint4* Bfhdr;
+    uint32_t stage;
+    uint64_t Bn, n_chunks, chunk, obj0;
+    unsigned long long* itemmin;  // the filter's item minima (non-negative doubles as u64)
+    unsigned long long* objmin;
+};
+
+// Edge/edge candidates of FULL mode: one A distinct edge per thread (kTile
+// consecutive entries of A's edge tiles per CTA) against every distinct edge
+// of the item's B chunk (staged per feature block by one TMA bulk copy).
+// Each thread's minimum goes into the (tile, chunk) item of its edge's tile
+// and its object: a pair's nine edge/edge candidates are among these, so the
+// item minimum is the minimum over its pairs of pair_d2 (up to the edge
+// direction of a shared edge). A tile partly outside
+// [row_lo, row_hi) contributes all its edges: a lower item minimum only
+// widens the band (check_kernel), never drops a pair.
+__global__ void __launch_bounds__(kTile, TDB_EDGE_MINB) edge_kernel(EdgeArgs a) {
+    extern __shared__ __align__(128) double dsm[];
+    __shared__ alignas(8) uint64_t bar[2];
+    const uint64_t et = blockIdx.x / a.n_chunks, ch = blockIdx.x - et * a.n_chunks;
+    const uint64_t e = a.e_lo + et * kTile + threadIdx.x;
+    const bool active = e < a.e_hi;
+    const double* q = a.Ae + min(e, a.e_hi - 1) * kAER;
+    const double2 q0 = __ldg(reinterpret_cast<const double2*>(q)), q1 = __ldg(reinterpret_cast<const double2*>(q) + 1),
+                  q2 = __ldg(reinterpret_cast<const double2*>(q) + 2), q3 = __ldg(reinterpret_cast<const double2*>(q) + 3);
+    const uint64_t tile = (uint64_t)__double_as_longlong(__ldg(q + AR_TILE));
+    const double Qx = q0.x, Qy = q0.y, Qz = q1.x, Ex = q1.y, Ey = q2.x, Ez = q2.y, La = q3.x, ILa = q3.y;
+
+    const uint64_t b0 = ch * a.chunk, b1 = min(a.Bn, b0 + a.chunk);
+    const uint64_t blk0 = b0 / kFB;
+    const int nblk = (int)((b1 - b0 + kFB - 1) / kFB);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    auto issue = [&](int s) {
+        const int st = s & 1;
+        const uint4 hb = __ldg(&a.Bfhdr[blk0 + s]);
+        const uint32_t bytes = kER * hb.z * (uint32_t)sizeof(double);
+        mbar_expect_tx(&bar[st], bytes);
+        if (bytes)
+            bulk_g2s(dsm + (size_t)st * a.stage, a.Bfb + (blk0 + s) * (uint64_t)kFBCap + kFR * hb.x + kVR * hb.y, bytes,
+                     &bar[st]);
+    };
+    if (threadIdx.x == 0) {
+        issue(0);
+        if (nblk > 1) issue(1);
+    }
+    int best = kInfHi;
+#pragma unroll 1
+    for (int s = 0; s < nblk; ++s) {
+        const int st = s & 1;
+        const int ne = (int)__ldg(&a.Bfhdr[blk0 + s].z);
+        mbar_wait(&bar[st], (uint32_t)((s >> 1) & 1));
+        const double2* er = reinterpret_cast<const double2*>(dsm + (size_t)st * a.stage);
+#pragma unroll kUEE
+        for (int j = 0; j < ne; ++j) {
+            const double2 p0 = er[4 * j], p1 = er[4 * j + 1], p2 = er[4 * j + 2], p3 = er[4 * j + 3];
+            best = min(best, edge_pair(Qx, Qy, Qz, Ex, Ey, Ez, La, ILa, p0.x, p0.y, p1.x, p1.y, p2.x, p2.y, p3.x, p3.y));
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && s + 2 < nblk) issue(s + 2);
+    }
+    if (active && best < kInfHi) {
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(__hiloint2double(best, 0));
+        atomicMin(a.itemmin + (tile - a.tile0) * a.n_chunks + ch, bits);
+        atomicMin(a.objmin + (a.tiles[tile].obj - a.obj0), bits);
     }
 }
 
@@ -518,6 +632,8 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
     if (n_items == 0) return;
 
     const Geom& A = *sel.A;
+    geom_feature_blocks(B, st);  // B's feature blocks, once per store
+    if (cx.mode != TDB_MODE_CULL) geom_edge_tiles(A, st);  // A's edge tiles, once per store
     // ---- scratch layout (256-byte aligned pieces), one cudaMallocAsync
     DistScratch sc{};
     size_t off = 0;
@@ -582,16 +698,33 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
         cull_mem[0] = caabb, cull_mem[1] = keys, cull_mem[2] = vals, cull_mem[3] = tmp;
         launches += 3;
     }
-    geom_feature_blocks(B, st);
     const uint32_t stage = (std::max<uint32_t>(B.fblock_max, 2) + 15) & ~15u;  // 128-byte aligned stages
     const size_t smem = 2 * (size_t)stage * sizeof(double);
     // per device (a device group calls from one thread per device); cheap
-    CK(cudaFuncSetAttribute(filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(filter_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            2 * kFBCap * (int)sizeof(double)));
+    CK(cudaFuncSetAttribute(filter_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            2 * kFBCap * (int)sizeof(double)));
+    CK(cudaFuncSetAttribute(edge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             2 * kFBCap * (int)sizeof(double)));
     DistArgs da{A.planes, A.n_pad, A.d_tiles, sel.tile0, sel.row_lo, sel.row_hi, B.planes, B.n_pad, B.n,
                 n_chunks, chunk, sel.obj0, sc.itemmin, sc.objmin, perm, lb2, ctr + 3, B.fblocks, B.d_fhdr, stage};
-    filter_kernel<<<(unsigned)n_items, kTile, smem, st>>>(da);
-    CK(cudaGetLastError());
+    if (cx.mode == TDB_MODE_CULL) {
+        filter_kernel<true><<<(unsigned)n_items, kTile, smem, st>>>(da);
+        CK(cudaGetLastError());
+    } else {
+        filter_kernel<false><<<(unsigned)n_items, kTile, smem, st>>>(da);
+        CK(cudaGetLastError());
+        const uint64_t e_lo = A.h_aeoff[sel.tile0], e_hi = A.h_aeoff[sel.tile1];
+        const uint64_t n_et = (e_hi - e_lo + kTile - 1) / kTile;
+        if (n_et) {
+            edge_kernel<<<(unsigned)(n_et * n_chunks), kTile, smem, st>>>(
+                EdgeArgs{A.aedges, e_lo, e_hi, sel.tile0, A.d_tiles, B.fblocks, B.d_fhdr, stage, B.n, n_chunks, chunk,
+                         sel.obj0, (unsigned long long*)sc.itemmin, sc.objmin});
+            CK(cudaGetLastError());
+            ++launches;
+        }
+    }
     CK(cudaEventRecord(ev.e[1], st));
     ++launches;
 

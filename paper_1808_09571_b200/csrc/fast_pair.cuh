@@ -172,25 +172,26 @@ __device__ __forceinline__ bool inside(double u, double v) {
 // Minima are kept as the high 32 bits of non-negative doubles (a lower bound
 // within a relative 2^-20 of the value: one VIMNMX per candidate).
 
-// Vertex P of B against face A: |h| when P projects inside A (w = P - A_0).
-__device__ __forceinline__ int vertex_cand(const AFace& A, double px, double py, double pz) {
+// Vertex P of B against face A: |h| when P projects inside A (w = P - A_0);
+// hs = the high word of h (its sign says which side of A's plane P is on).
+__device__ __forceinline__ int vertex_cand(const AFace& A, double px, double py, double pz, int& hs) {
     const double wx = px - A.v[0], wy = py - A.v[1], wz = pz - A.v[2];
     const double h = dot3(A.n, wx, wy, wz);
     const double u = dot3(A.U, wx, wy, wz);
     const double v = dot3(A.W, wx, wy, wz);
-    return inside(u, v) ? (__double2hiint(h) & 0x7fffffff) : kInfHi;
+    hs = __double2hiint(h);
+    return inside(u, v) ? (hs & 0x7fffffff) : kInfHi;
 }
 
-// Face B (vertices b[9], unit normal nb, dual basis ub / vb) against face A:
-// the vertices of A against B (|h| when inside, min into hmin); returns true
-// when each triangle straddles the other's plane (an edge may pierce a face).
-__device__ __forceinline__ bool face_cand(const AFace& A, const double b[9], const double nb[3], const double ub[3],
-                                          const double vb[3], int& hmin) {
+// The vertices of A against face B (vertex B_0, unit normal nb, dual basis
+// ub / vb): |h| when inside, min into hmin. Returns true when A straddles B's
+// plane; w0 = A_0 - B_0.
+__device__ __forceinline__ bool a_vertex_cand(const AFace& A, double b0x, double b0y, double b0z, const double nb[3],
+                                              const double ub[3], const double vb[3], int& hmin, double w0[3]) {
     int ha_or = 0, ha_and = -1;
-    double w0[3];
 #pragma unroll
     for (int j = 0; j < 3; ++j) {  // A_j - B_0
-        const double wx = A.v[3 * j] - b[0], wy = A.v[3 * j + 1] - b[1], wz = A.v[3 * j + 2] - b[2];
+        const double wx = A.v[3 * j] - b0x, wy = A.v[3 * j + 1] - b0y, wz = A.v[3 * j + 2] - b0z;
         if (j == 0) w0[0] = wx, w0[1] = wy, w0[2] = wz;
         const double h = dot3(nb, wx, wy, wz);
         const double u = dot3(ub, wx, wy, wz);
@@ -199,49 +200,54 @@ __device__ __forceinline__ bool face_cand(const AFace& A, const double b[9], con
         ha_and &= __double2hiint(h);
         hmin = min(hmin, inside(u, v) ? (__double2hiint(h) & 0x7fffffff) : kInfHi);
     }
-    // B's vertices against A's plane (B_0 - A_0 = -(A_0 - B_0) exactly)
+    return !(ha_or >= 0 || ha_and < 0);
+}
+
+// B's vertices b[9] straddle A's plane (sign words of their heights; B_0's
+// from w0 = A_0 - B_0: B_0 - A_0 = -w0 exactly).
+__device__ __forceinline__ bool b_straddles(const AFace& A, const double b[9], const double w0[3]) {
     const double h0 = -dot3(A.n, w0[0], w0[1], w0[2]);
     const double h1 = dot3(A.n, b[3] - A.v[0], b[4] - A.v[1], b[5] - A.v[2]);
     const double h2 = dot3(A.n, b[6] - A.v[0], b[7] - A.v[1], b[8] - A.v[2]);
     const int hb_or = __double2hiint(h0) | __double2hiint(h1) | __double2hiint(h2);
     const int hb_and = __double2hiint(h0) & __double2hiint(h1) & __double2hiint(h2);
-    return !(hb_or >= 0 || hb_and < 0) && !(ha_or >= 0 || ha_and < 0);
+    return !(hb_or >= 0 || hb_and < 0);
 }
 
-// Edge P -> P + E of B (|E|^2 = Lb, 1/|E|^2 = ILb) against A's three edges:
-// Ericson's clamped segment distance (s from the unconstrained solve with a
-// Newton-refined reciprocal, t optimal for s, s optimal for the clamped t).
-// fw runs incrementally: w_j+1 = w_j - Ea_j => E.w_j+1 = E.w_j - E.Ea_j.
+// Edge Q -> Q + Ea of A (|Ea|^2 = La, 1/|Ea|^2 = ILa) against edge P -> P + Eb
+// of B: Ericson's clamped segment distance, squared, high word (s from the
+// unconstrained solve with a Newton-refined reciprocal, t optimal for s, s
+// optimal for the clamped t; every value is the distance between two real
+// points of the segments).
+__device__ __forceinline__ int edge_pair(double qx, double qy, double qz, double eax, double eay, double eaz,
+                                         double La, double ILa, double px, double py, double pz, double ebx,
+                                         double eby, double ebz, double Lb, double ILb) {
+    const double wx = px - qx, wy = py - qy, wz = pz - qz;  // w = P - Q
+    const double fw = fma(ebx, wx, fma(eby, wy, ebz * wz));
+    const double bb = fma(eax, ebx, fma(eay, eby, eaz * ebz));
+    const double cw = fma(eax, wx, fma(eay, wy, eaz * wz));
+    // s0 = (cw Lb - bb fw) / (La Lb - bb^2), both terms divided by Lb
+    const double bbI = bb * ILb;
+    const double den = fma(-bbI, bb, La);
+    const double num = fma(-bbI, fw, cw);
+    double s = clamp01(num * rcp_nr(den));
+    const double t = clamp01(fma(bb, s, -fw) * ILb);
+    s = clamp01(fma(bb, t, cw) * ILa);
+    const double dx = fma(s, eax, fma(-t, ebx, -wx));
+    const double dy = fma(s, eay, fma(-t, eby, -wy));
+    const double dz = fma(s, eaz, fma(-t, ebz, -wz));
+    return __double2hiint(fma(dx, dx, fma(dy, dy, dz * dz)));
+}
+
+// Edge P -> P + Eb of B (|Eb|^2 = Lb, 1/|Eb|^2 = ILb) against A's three edges.
 __device__ __forceinline__ int edge_cand(const AFace& A, double px, double py, double pz, double ebx, double eby,
                                          double ebz, double Lb, double ILb) {
-    double w[3][3];  // w_j = P - A_j
+    int c[3];
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
-        w[j][0] = px - A.v[3 * j];
-        w[j][1] = py - A.v[3 * j + 1];
-        w[j][2] = pz - A.v[3 * j + 2];
-    }
-    double fw = fma(ebx, w[0][0], fma(eby, w[0][1], ebz * w[0][2]));
-    int cand[3];
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {  // edge A_j -> A_j+1
-        const double* ea = A.e + 3 * j;
-        const double bb = dot3(ea, ebx, eby, ebz);
-        const double cw = dot3(ea, w[j][0], w[j][1], w[j][2]);
-        // s0 = (cw Lb - bb fw) / (La Lb - bb^2), both terms divided by Lb
-        const double bbI = bb * ILb;
-        const double den = fma(-bbI, bb, A.L[j]);
-        const double num = fma(-bbI, fw, cw);
-        double s = clamp01(num * rcp_nr(den));
-        const double t = clamp01(fma(bb, s, -fw) * ILb);
-        s = clamp01(fma(bb, t, cw) * A.IL[j]);
-        const double dx = fma(s, ea[0], fma(-t, ebx, -w[j][0]));
-        const double dy = fma(s, ea[1], fma(-t, eby, -w[j][1]));
-        const double dz = fma(s, ea[2], fma(-t, ebz, -w[j][2]));
-        cand[j] = __double2hiint(fma(dx, dx, fma(dy, dy, dz * dz)));
-        fw = fw - bb;
-    }
-    return min(min(cand[0], cand[1]), cand[2]);
+    for (int j = 0; j < 3; ++j)
+        c[j] = edge_pair(A.v[3 * j], A.v[3 * j + 1], A.v[3 * j + 2], A.e[3 * j], A.e[3 * j + 1], A.e[3 * j + 2],
+                         A.L[j], A.IL[j], px, py, pz, ebx, eby, ebz, Lb, ILb);
+    return min(min(c[0], c[1]), c[2]);
 }
 
 // The smallest |h| high word (hmin) as the high word of h^2.
@@ -252,7 +258,7 @@ __device__ __forceinline__ int hmin_sq(int hmin) {
 
 // d~^2 of the pair (face A in registers, face B through `bt`, plane layout),
 // truncated to its high word: the minimum of the pair's 15 candidates
-// (vertex_cand x 3, face_cand's 3, edge_cand x 3), 0 when an edge pierces a
+// (vertex_cand x 3, a_vertex_cand's 3, edge_cand x 3), 0 when an edge pierces a
 // face. The filter kernel evaluates the same candidates, each shared vertex
 // and edge once per feature block (distance.cu). `ap`/`as` locate A's fields
 // for the out-of-line piercing test.
@@ -263,11 +269,13 @@ __device__ __forceinline__ double pair_d2(const AFace& A, const P& bt, const dou
     for (int k = 0; k < 9; ++k) b[k] = bt(F_V + k);
 #pragma unroll
     for (int k = 0; k < 3; ++k) nb[k] = bt(F_N + k), ub[k] = bt(F_U + k), vb[k] = bt(F_W + k);
-    int hmin = kInfHi, best = kInfHi;
-    const bool straddle = face_cand(A, b, nb, ub, vb, hmin);
+    int hmin = kInfHi, best = kInfHi, hs;
+    double w0[3];
+    bool straddle = a_vertex_cand(A, b[0], b[1], b[2], nb, ub, vb, hmin, w0);
+    straddle = straddle && b_straddles(A, b, w0);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        hmin = min(hmin, vertex_cand(A, b[3 * k], b[3 * k + 1], b[3 * k + 2]));
+        hmin = min(hmin, vertex_cand(A, b[3 * k], b[3 * k + 1], b[3 * k + 2], hs));
         best = min(best, edge_cand(A, b[3 * k], b[3 * k + 1], b[3 * k + 2], bt(F_E + 3 * k), bt(F_E + 3 * k + 1),
                                    bt(F_E + 3 * k + 2), bt(F_L + k), bt(F_IL + k)));
     }

@@ -70,12 +70,17 @@ struct Geom {
     mutable uint4* d_fhdr = nullptr;    // per block: faces, vertices, edges, doubles used
     mutable uint64_t n_fblocks = 0;
     mutable uint32_t fblock_max = 0;    // max doubles used by one block
+    // A edge tiles (tdb_internal.h kAER): built on first use as the A side of
+    // a distance filter (geom_edge_tiles); aeoff[t] = first entry of tile t
+    mutable double* aedges = nullptr;
+    mutable std::vector<uint64_t> h_aeoff;  // n_tiles + 1
     std::shared_ptr<std::mutex> fmu = std::make_shared<std::mutex>();
 };
 
-// Builds g's feature blocks once (thread-safe; the build is complete on the
-// device when this returns).
+// Builds g's feature blocks / edge tiles once (thread-safe; complete on the
+// device when these return).
 void geom_feature_blocks(const Geom& g, cudaStream_t st);
+void geom_edge_tiles(const Geom& g, cudaStream_t st);
 
 // tri9: 9 doubles per face (AoS), on the host unless tri9_on_device
 void geom_build(Geom* g, const double* tri9, uint64_t n, const uint64_t* host_off, uint64_t n_obj,

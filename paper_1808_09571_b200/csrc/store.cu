@@ -345,6 +345,7 @@ __global__ void __launch_bounds__(kFB) fblock_kernel(const double* __restrict__ 
     __shared__ unsigned ekey[R];
     __shared__ int live_s[kFB];
     __shared__ int scan[3][kFB + 1];
+    __shared__ int vslot[R];
     const int t = threadIdx.x;
     const uint64_t blk = blockIdx.x, f = blk * kFB + t;
     const bool live = f < n && planes[(uint64_t)F_DEG * n_pad + f] == 0.0;
@@ -409,6 +410,13 @@ __global__ void __launch_bounds__(kFB) fblock_kernel(const double* __restrict__ 
     }
     __syncthreads();
     const int NF = scan[0][kFB], NV = scan[1][kFB], NE = scan[2][kFB];
+    {
+        int vs = scan[1][t];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            if (uv[k]) vslot[3 * t + k] = vs++;
+    }
+    __syncthreads();
     double* base = out + blk * (uint64_t)kFBCap;
     if (live) {
         double* fr = base + (uint64_t)kFR * scan[0][t];
@@ -421,7 +429,10 @@ __global__ void __launch_bounds__(kFB) fblock_kernel(const double* __restrict__ 
             fr[FR_W + k] = planes[(uint64_t)(F_W + k) * n_pad + f];
         }
         fr[FR_IDX] = __longlong_as_double((long long)f);
-        fr[FR_IDX + 1] = 0.0;
+        const unsigned long long slots = (unsigned long long)vslot[rep[3 * t]] |
+                                         (unsigned long long)vslot[rep[3 * t + 1]] << 10 |
+                                         (unsigned long long)vslot[rep[3 * t + 2]] << 20;
+        fr[FR_SLOT] = __longlong_as_double((long long)slots);
         int vs = scan[1][t], es = scan[2][t];
         double* vr = base + (uint64_t)kFR * NF;
         double* er = vr + (uint64_t)kVR * NV;
@@ -448,7 +459,124 @@ __global__ void __launch_bounds__(kFB) fblock_kernel(const double* __restrict__ 
     }
 }
 
+// One CTA (kTile threads, one per face) per A tile: its distinct edges
+// (first occurrence in face order represents an edge). Pass 0 counts them
+// (cnt[t]); pass 1 writes them from off[t] (tdb_internal.h kAER).
+__global__ void __launch_bounds__(kTile) aedge_kernel(const double* __restrict__ planes, uint64_t n_pad,
+                                                      const Tile* __restrict__ tiles, int pass,
+                                                      unsigned* __restrict__ cnt, const uint64_t* __restrict__ off,
+                                                      double* __restrict__ out) {
+    constexpr int R = 3 * kTile;
+    __shared__ unsigned long long vx[R], vy[R], vz[R];
+    __shared__ int rep[R];
+    __shared__ unsigned ekey[R];
+    __shared__ int live_s[kTile];
+    __shared__ int scan[kTile + 1];
+    const int t = threadIdx.x;
+    const Tile T = tiles[blockIdx.x];
+    const uint64_t f = T.row0 + min((uint32_t)t, T.count - 1);
+    const bool live = (uint32_t)t < T.count && planes[(uint64_t)F_DEG * n_pad + f] == 0.0;
+    live_s[t] = live;
+    double v[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) v[k] = planes[(uint64_t)(F_V + k) * n_pad + f];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        vx[3 * t + k] = (unsigned long long)__double_as_longlong(v[3 * k]);
+        vy[3 * t + k] = (unsigned long long)__double_as_longlong(v[3 * k + 1]);
+        vz[3 * t + k] = (unsigned long long)__double_as_longlong(v[3 * k + 2]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int r = 3 * t + k;
+        int rr = r;
+        if (live)
+            for (int q = 0; q < r; ++q)
+                if (live_s[q / 3] && vx[q] == vx[r] && vy[q] == vy[r] && vz[q] == vz[r]) {
+                    rr = q;
+                    break;
+                }
+        rep[r] = rr;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const unsigned a = (unsigned)rep[3 * t + k], b = (unsigned)rep[3 * t + (k == 2 ? 0 : k + 1)];
+        ekey[3 * t + k] = min(a, b) << 16 | max(a, b);
+    }
+    __syncthreads();
+    int ue[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int r = 3 * t + k;
+        bool first = live;
+        if (live)
+            for (int q = 0; q < r; ++q)
+                if (live_s[q / 3] && ekey[q] == ekey[r]) {
+                    first = false;
+                    break;
+                }
+        ue[k] = first;
+    }
+    scan[t + 1] = ue[0] + ue[1] + ue[2];
+    if (t == 0) scan[0] = 0;
+    __syncthreads();
+    if (t == 0)
+        for (int q = 0; q < kTile; ++q) scan[q + 1] += scan[q];
+    __syncthreads();
+    if (pass == 0) {
+        if (t == 0) cnt[blockIdx.x] = (unsigned)scan[kTile];
+        return;
+    }
+    double* base = out + (off[blockIdx.x] + scan[t]) * (uint64_t)kAER;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        if (!ue[k]) continue;
+        double* p = base;
+        base += kAER;
+        p[AR_Q] = v[3 * k], p[AR_Q + 1] = v[3 * k + 1], p[AR_Q + 2] = v[3 * k + 2];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) p[AR_E + c] = planes[(uint64_t)(F_E + 3 * k + c) * n_pad + f];
+        p[AR_L] = planes[(uint64_t)(F_L + k) * n_pad + f];
+        p[AR_IL] = planes[(uint64_t)(F_IL + k) * n_pad + f];
+        p[AR_TILE] = __longlong_as_double((long long)blockIdx.x);
+        p[AR_TILE + 1] = 0.0;
+    }
+}
+
 }  // namespace
+
+void geom_edge_tiles(const Geom& g, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(*g.fmu);
+    if (!g.h_aeoff.empty()) return;
+    const uint64_t nt = g.h_tiles.size();
+    std::vector<uint64_t> off(nt + 1, 0);
+    if (nt == 0) {
+        g.h_aeoff = off;
+        return;
+    }
+    unsigned* cnt = nullptr;
+    uint64_t* d_off = nullptr;
+    CK(cudaMallocAsync(&cnt, nt * sizeof(unsigned), st));
+    aedge_kernel<<<(unsigned)nt, kTile, 0, st>>>(g.planes, g.n_pad, g.d_tiles, 0, cnt, nullptr, nullptr);
+    CK(cudaGetLastError());
+    std::vector<unsigned> h(nt);
+    CK(cudaMemcpyAsync(h.data(), cnt, nt * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (uint64_t t = 0; t < nt; ++t) off[t + 1] = off[t] + h[t];
+    double* out = nullptr;
+    CK(cudaMallocAsync(&out, std::max<uint64_t>(off[nt], 1) * kAER * sizeof(double), st));
+    CK(cudaMallocAsync(&d_off, nt * sizeof(uint64_t), st));
+    CK(cudaMemcpyAsync(d_off, off.data(), nt * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+    aedge_kernel<<<(unsigned)nt, kTile, 0, st>>>(g.planes, g.n_pad, g.d_tiles, 1, cnt, d_off, out);
+    CK(cudaGetLastError());
+    CK(cudaFreeAsync(cnt, st));
+    CK(cudaFreeAsync(d_off, st));
+    CK(cudaStreamSynchronize(st));
+    g.aedges = out;
+    g.h_aeoff = off;
+}
 
 void geom_feature_blocks(const Geom& g, cudaStream_t st) {
     std::lock_guard<std::mutex> lk(*g.fmu);
@@ -477,6 +605,9 @@ void geom_release(Geom* g, cudaStream_t st) {
     if (!g) return;
     cudaFreeAsync(g->fblocks, st);
     cudaFreeAsync(g->d_fhdr, st);
+    cudaFreeAsync(g->aedges, st);
+    g->aedges = nullptr;
+    g->h_aeoff.clear();
     g->fblocks = nullptr;
     g->d_fhdr = nullptr;
     cudaFreeAsync(g->planes, st);

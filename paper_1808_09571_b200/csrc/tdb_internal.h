@@ -47,7 +47,8 @@ constexpr int kPlanePad = 64;
 // ---- B feature blocks (the distance filter's B side) -------
 // B's faces in blocks of kFB consecutive faces. Per block, three AoS lists,
 // packed back to back from the block's base (fixed capacity kFBCap doubles):
-//   faces    (non-degenerate only): kFR doubles = V (9), N, U, W, face index
+//   faces    (non-degenerate only): kFR doubles = V (9), N, U, W, face index,
+//            vertex slots
 //   vertices (distinct within the block, bitwise): kVR doubles = x y z 0
 //   edges    (distinct within the block, unordered vertex pair): kER doubles
 //            = start P (3), E = V_k+1 - V_k (3), |E|^2, 1/|E|^2 of the first
@@ -55,11 +56,23 @@ constexpr int kPlanePad = 64;
 // A pair's filter value is the minimum over its 6 vertex/face and 9 edge/edge
 // candidates; a shared vertex or edge is the same candidate for every face
 // of the block that has it, so the filter evaluates it once per block.
-constexpr int kFB = 64;
-enum : int { FR_V = 0, FR_N = 9, FR_U = 12, FR_W = 15, FR_IDX = 18, kFR = 20 };
+#ifndef TDB_KFB
+#define TDB_KFB 64
+#endif
+constexpr int kFB = TDB_KFB;
+// face record: ... FR_IDX = face index (u64 bits), FR_SLOT = the block's
+// vertex slots of V0, V1, V2 (10 bits each, u64 bits)
+enum : int { FR_V = 0, FR_N = 9, FR_U = 12, FR_W = 15, FR_IDX = 18, FR_SLOT = 19, kFR = 20 };
 enum : int { ER_P = 0, ER_E = 3, ER_L = 6, ER_IL = 7, kER = 8 };
 constexpr int kVR = 4;
 constexpr int kFBCap = kFB * (kFR + 3 * kVR + 3 * kER);  // doubles per block (28,672 B)
+
+// ---- A edge tiles (the distance filter's A side of the edge/edge candidates)
+// Per A tile (kTile faces), its distinct edges (unordered bitwise vertex pair,
+// non-degenerate faces only), concatenated in tile order; entry e of the list
+// is kAER doubles = start Q (3), E (3), |E|^2, 1/|E|^2, the tile's index (u64
+// bits), 0. The edge kernel runs kTile consecutive entries per CTA.
+enum : int { AR_Q = 0, AR_E = 3, AR_L = 6, AR_IL = 7, AR_TILE = 8, kAER = 10 };
 
 // per-object statistics (doubles): aabb lo xyz, hi xyz, max edge, max |coord|,
 // max kappa (F_K) over its non-degenerate faces

@@ -1,16 +1,17 @@
 """Per-loop instruction mix of a kernel (innermost loops with FP64 work):
 instructions, DFMA / DMUL / DADD, executed FP64 flops, and the register-read
-cost model of scripts/sass_cost.py. For filter_kernel the three loops are the
-face, vertex and edge candidate loops (in that order); bench.py's
-FILTER_LOOP_* constants come from here.
-usage: python scripts/sass_loops.py build/distance.o filter_kernel"""
+cost model of scripts/sass_cost.py. For filter_kernel<false> (FULL mode) the
+loops are the vertex and face candidate loops; for edge_kernel the edge/edge
+loop (unrolled: divide by its unroll factor). bench.py's FILTER_LOOP_*
+constants come from here.
+usage: python scripts/sass_loops.py build/distance.o filter_kernelILb0   (name: regex)"""
 import re, subprocess, sys
 from collections import Counter
 
 obj, name = sys.argv[1], sys.argv[2]
 sass = subprocess.run(["cuobjdump", "-sass", obj], capture_output=True, text=True).stdout
 funcs = re.split(r"\n\s+Function : ", sass)
-body = next(f for f in funcs if name in f.split("\n", 1)[0])
+body = next(f for f in funcs if re.search(name, f.split("\n", 1)[0]))
 ins = [(int(m.group(1), 16), m.group(2).strip()) for m in re.finditer(r"\s+/\*([0-9a-f]{4,})\*/\s+(.*?);", body)]
 loops = []
 for addr, txt in ins:
