@@ -80,8 +80,11 @@ constexpr int kUV = TDB_UV, kUF = TDB_UF, kUE = TDB_UE;
 // kEdges: also B's edges against each row's three edges (CULL mode, one
 // kernel per item); FULL mode runs those in edge_kernel over A's distinct
 // edges instead.
+#ifndef TDB_FACE_MINB
+#define TDB_FACE_MINB 4
+#endif
 template <bool kEdges>
-__global__ void __launch_bounds__(kTile, TDB_FILTER_MINB) filter_kernel(DistArgs a) {
+__global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MINB) filter_kernel(DistArgs a) {
     extern __shared__ __align__(128) double dsm[];  // 2 stages of a.stage doubles: one feature block each
     __shared__ alignas(8) uint64_t bar[2];
     __shared__ double red[kTile / 32];
@@ -154,26 +157,31 @@ __global__ void __launch_bounds__(kTile, TDB_FILTER_MINB) filter_kernel(DistArgs
             }
             sgn[j0 >> 5][threadIdx.x] = bits;
         }
-        // faces: A's vertices against B's face; both straddle -> piercing test
+        // faces: A's vertices against B's face (CULL; FULL runs them in
+        // vertex_kernel over A's distinct vertices); both triangles straddle
+        // the other's plane -> piercing test
 #pragma unroll kUF
         for (int j = 0; j < (int)h.x; ++j) {
             const double2* q = reinterpret_cast<const double2*>(fr + kFR * j);
-            const double2 q0 = q[0], q1 = q[1], q6 = q[6], q7 = q[7], q8 = q[8], q9 = q[9];
-            const double2 q4 = q[4], q5 = q[5];
-            const double nb[3] = {q4.y, q5.x, q5.y}, ub[3] = {q6.x, q6.y, q7.x}, vb[3] = {q7.y, q8.x, q8.y};
-            double w0[3];
-            if (a_vertex_cand(A, q0.x, q0.y, q1.x, nb, ub, vb, hmin, w0)) {
-                const unsigned long long sl = (unsigned long long)__double_as_longlong(q9.y);
-                const unsigned s0 = (unsigned)sl & 1023u, s1 = (unsigned)(sl >> 10) & 1023u,
-                               s2 = (unsigned)(sl >> 20) & 1023u;
-                const unsigned g0 = sgn[s0 >> 5][threadIdx.x] >> (s0 & 31) & 1u;
-                const unsigned g1 = sgn[s1 >> 5][threadIdx.x] >> (s1 & 31) & 1u;
-                const unsigned g2 = sgn[s2 >> 5][threadIdx.x] >> (s2 & 31) & 1u;
-                if ((g0 | g1 | g2) && !(g0 & g1 & g2)) {
-                    const uint64_t fi = (uint64_t)__double_as_longlong(q9.x);
-                    pierce |= pierce_slow(a.Ap + row, a.An_pad, a.Bp + fi, a.Bn_pad);
-                }
+            const double2 q9 = q[9];
+            const unsigned long long sl = (unsigned long long)__double_as_longlong(q9.y);
+            const unsigned s0 = (unsigned)sl & 1023u, s1 = (unsigned)(sl >> 10) & 1023u, s2 = (unsigned)(sl >> 20) & 1023u;
+            const unsigned g0 = sgn[s0 >> 5][threadIdx.x] >> (s0 & 31) & 1u;
+            const unsigned g1 = sgn[s1 >> 5][threadIdx.x] >> (s1 & 31) & 1u;
+            const unsigned g2 = sgn[s2 >> 5][threadIdx.x] >> (s2 & 31) & 1u;
+            const bool sb = (g0 | g1 | g2) && !(g0 & g1 & g2);  // B straddles A's plane
+            bool sa;
+            if (kEdges || sb) {
+                const double2 q0 = q[0], q1 = q[1], q6 = q[6], q7 = q[7], q8 = q[8], q4 = q[4], q5 = q[5];
+                const double nb[3] = {q4.y, q5.x, q5.y}, ub[3] = {q6.x, q6.y, q7.x}, vb[3] = {q7.y, q8.x, q8.y};
+                double w0[3];
+                int hm = hmin;
+                sa = a_vertex_cand(A, q0.x, q0.y, q1.x, nb, ub, vb, hm, w0);
+                if (kEdges) hmin = hm;
+            } else {
+                sa = false;
             }
+            if (sa && sb) pierce |= pierce_slow(a.Ap + row, a.An_pad, a.Bp + (uint64_t)__double_as_longlong(q9.x), a.Bn_pad);
         }
         // B's distinct edges against A's edges
 #pragma unroll kUE
@@ -281,6 +289,89 @@ __global__ void __launch_bounds__(kTile, TDB_EDGE_MINB) edge_kernel(EdgeArgs a) 
     }
     if (active && best < kInfHi) {
         const unsigned long long bits = (unsigned long long)__double_as_longlong(__hiloint2double(best, 0));
+        atomicMin(a.itemmin + (tile - a.tile0) * a.n_chunks + ch, bits);
+        atomicMin(a.objmin + (a.tiles[tile].obj - a.obj0), bits);
+    }
+}
+
+struct VertArgs {
+    const double* Av;        // A vertex entries (tdb_internal.h kAVR)
+    uint64_t v_lo, v_hi;     // the selection's entries
+    uint64_t tile0;
+    const Tile* tiles;
+    const double* Bfb;
+    const uint4* Bfhdr;
+    uint32_t stage;
+    uint64_t Bn, n_chunks, chunk, obj0;
+    unsigned long long* itemmin;
+    unsigned long long* objmin;
+};
+
+#ifndef TDB_VERT_MINB
+#define TDB_VERT_MINB 4
+#endif
+#ifndef TDB_UVF
+#define TDB_UVF 4
+#endif
+constexpr int kUVF = TDB_UVF;
+
+// Vertex/face candidates of FULL mode with A's vertices shared: one distinct
+// vertex of an A tile per thread against every face of the item's B chunk
+// (|h| when it projects inside; a_vertex_cand's arithmetic for that vertex).
+// Minima into the (tile, chunk) items and objects as edge_kernel.
+__global__ void __launch_bounds__(kTile, TDB_VERT_MINB) vertex_kernel(VertArgs a) {
+    extern __shared__ __align__(128) double dsm[];
+    __shared__ alignas(8) uint64_t bar[2];
+    const uint64_t vt = blockIdx.x / a.n_chunks, ch = blockIdx.x - vt * a.n_chunks;
+    const uint64_t e = a.v_lo + vt * kTile + threadIdx.x;
+    const bool active = e < a.v_hi;
+    const double* q = a.Av + min(e, a.v_hi - 1) * kAVR;
+    const double2 q0 = __ldg(reinterpret_cast<const double2*>(q)), q1 = __ldg(reinterpret_cast<const double2*>(q) + 1);
+    const double ax = q0.x, ay = q0.y, az = q1.x;
+    const uint64_t tile = (uint64_t)__double_as_longlong(q1.y);
+
+    const uint64_t b0 = ch * a.chunk, b1 = min(a.Bn, b0 + a.chunk);
+    const uint64_t blk0 = b0 / kFB;
+    const int nblk = (int)((b1 - b0 + kFB - 1) / kFB);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    auto issue = [&](int s) {
+        const int st = s & 1;
+        const uint32_t bytes = kFR * __ldg(&a.Bfhdr[blk0 + s].x) * (uint32_t)sizeof(double);
+        mbar_expect_tx(&bar[st], bytes);
+        if (bytes) bulk_g2s(dsm + (size_t)st * a.stage, a.Bfb + (blk0 + s) * (uint64_t)kFBCap, bytes, &bar[st]);
+    };
+    if (threadIdx.x == 0) {
+        issue(0);
+        if (nblk > 1) issue(1);
+    }
+    int hmin = kInfHi;
+#pragma unroll 1
+    for (int s = 0; s < nblk; ++s) {
+        const int st = s & 1;
+        const int nf = (int)__ldg(&a.Bfhdr[blk0 + s].x);
+        mbar_wait(&bar[st], (uint32_t)((s >> 1) & 1));
+        const double2* fr = reinterpret_cast<const double2*>(dsm + (size_t)st * a.stage);
+#pragma unroll kUVF
+        for (int j = 0; j < nf; ++j) {
+            const double2* r = fr + (kFR / 2) * j;
+            const double2 r0 = r[0], r1 = r[1], r4 = r[4], r5 = r[5], r6 = r[6], r7 = r[7], r8 = r[8];
+            const double wx = ax - r0.x, wy = ay - r0.y, wz = az - r1.x;  // A_v - B_0
+            const double nb[3] = {r4.y, r5.x, r5.y}, ub[3] = {r6.x, r6.y, r7.x}, vb[3] = {r7.y, r8.x, r8.y};
+            const double h = dot3(nb, wx, wy, wz);
+            const double u = dot3(ub, wx, wy, wz);
+            const double v = dot3(vb, wx, wy, wz);
+            hmin = min(hmin, inside(u, v) ? (__double2hiint(h) & 0x7fffffff) : kInfHi);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && s + 2 < nblk) issue(s + 2);
+    }
+    if (active && hmin < kInfHi) {
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(__hiloint2double(hmin_sq(hmin), 0));
         atomicMin(a.itemmin + (tile - a.tile0) * a.n_chunks + ch, bits);
         atomicMin(a.objmin + (a.tiles[tile].obj - a.obj0), bits);
     }
@@ -633,8 +724,7 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
 
     const Geom& A = *sel.A;
     geom_feature_blocks(B, st);  // B's feature blocks, once per store
-    if (cx.mode != TDB_MODE_CULL) geom_edge_tiles(A, st);  // A's edge tiles, once per store
-    // ---- scratch layout (256-byte aligned pieces), one cudaMallocAsync
+    if (cx.mode != TDB_MODE_CULL) geom_edge_tiles(A, st);  // A's edge / vertex tiles, once per store    // ---- scratch layout (256-byte aligned pieces), one cudaMallocAsync
     DistScratch sc{};
     size_t off = 0;
     auto piece = [&](size_t bytes) {
@@ -698,14 +788,21 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
         cull_mem[0] = caabb, cull_mem[1] = keys, cull_mem[2] = vals, cull_mem[3] = tmp;
         launches += 3;
     }
-    const uint32_t stage = (std::max<uint32_t>(B.fblock_max, 2) + 15) & ~15u;  // 128-byte aligned stages
-    const size_t smem = 2 * (size_t)stage * sizeof(double);
+    // SMEM stages (128-byte aligned): a whole block (CULL), or only the part
+    // each FULL kernel stages
+    auto stage_of = [](uint32_t doubles) { return (std::max<uint32_t>(doubles, 2) + 15) & ~15u; };
+    const uint32_t stage = stage_of(cx.mode == TDB_MODE_CULL ? B.fblock_max : B.fblock_max_fv);
+    const uint32_t stage_e = stage_of(B.fblock_max_e), stage_f = stage_of(B.fblock_max_f);
+    const size_t smem = 2 * (size_t)stage * sizeof(double), smem_e = 2 * (size_t)stage_e * sizeof(double),
+                 smem_f = 2 * (size_t)stage_f * sizeof(double);
     // per device (a device group calls from one thread per device); cheap
     CK(cudaFuncSetAttribute(filter_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             2 * kFBCap * (int)sizeof(double)));
     CK(cudaFuncSetAttribute(filter_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             2 * kFBCap * (int)sizeof(double)));
     CK(cudaFuncSetAttribute(edge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            2 * kFBCap * (int)sizeof(double)));
+    CK(cudaFuncSetAttribute(vertex_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             2 * kFBCap * (int)sizeof(double)));
     DistArgs da{A.planes, A.n_pad, A.d_tiles, sel.tile0, sel.row_lo, sel.row_hi, B.planes, B.n_pad, B.n,
                 n_chunks, chunk, sel.obj0, sc.itemmin, sc.objmin, perm, lb2, ctr + 3, B.fblocks, B.d_fhdr, stage};
@@ -715,11 +812,20 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
     } else {
         filter_kernel<false><<<(unsigned)n_items, kTile, smem, st>>>(da);
         CK(cudaGetLastError());
+        const uint64_t v_lo = A.h_avoff[sel.tile0], v_hi = A.h_avoff[sel.tile1];
+        const uint64_t n_vt = (v_hi - v_lo + kTile - 1) / kTile;
+        if (n_vt) {
+            vertex_kernel<<<(unsigned)(n_vt * n_chunks), kTile, smem_f, st>>>(
+                VertArgs{A.averts, v_lo, v_hi, sel.tile0, A.d_tiles, B.fblocks, B.d_fhdr, stage_f, B.n, n_chunks, chunk,
+                         sel.obj0, (unsigned long long*)sc.itemmin, sc.objmin});
+            CK(cudaGetLastError());
+            ++launches;
+        }
         const uint64_t e_lo = A.h_aeoff[sel.tile0], e_hi = A.h_aeoff[sel.tile1];
         const uint64_t n_et = (e_hi - e_lo + kTile - 1) / kTile;
         if (n_et) {
-            edge_kernel<<<(unsigned)(n_et * n_chunks), kTile, smem, st>>>(
-                EdgeArgs{A.aedges, e_lo, e_hi, sel.tile0, A.d_tiles, B.fblocks, B.d_fhdr, stage, B.n, n_chunks, chunk,
+            edge_kernel<<<(unsigned)(n_et * n_chunks), kTile, smem_e, st>>>(
+                EdgeArgs{A.aedges, e_lo, e_hi, sel.tile0, A.d_tiles, B.fblocks, B.d_fhdr, stage_e, B.n, n_chunks, chunk,
                          sel.obj0, (unsigned long long*)sc.itemmin, sc.objmin});
             CK(cudaGetLastError());
             ++launches;

@@ -70,10 +70,15 @@ struct Geom {
     mutable uint4* d_fhdr = nullptr;    // per block: faces, vertices, edges, doubles used
     mutable uint64_t n_fblocks = 0;
     mutable uint32_t fblock_max = 0;    // max doubles used by one block
+    mutable uint32_t fblock_max_fv = 0; //   ... by its faces + vertices
+    mutable uint32_t fblock_max_e = 0;  //   ... by its edges
+    mutable uint32_t fblock_max_f = 0;  //   ... by its faces
     // A edge tiles (tdb_internal.h kAER): built on first use as the A side of
     // a distance filter (geom_edge_tiles); aeoff[t] = first entry of tile t
     mutable double* aedges = nullptr;
     mutable std::vector<uint64_t> h_aeoff;  // n_tiles + 1
+    mutable double* averts = nullptr;       // the tiles' distinct vertices (kAVR)
+    mutable std::vector<uint64_t> h_avoff;  // n_tiles + 1
     std::shared_ptr<std::mutex> fmu = std::make_shared<std::mutex>();
 };
 

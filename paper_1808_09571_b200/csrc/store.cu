@@ -456,22 +456,27 @@ __global__ void __launch_bounds__(kFB) fblock_kernel(const double* __restrict__ 
         const unsigned used = (unsigned)(kFR * NF + kVR * NV + kER * NE);
         hdr[blk] = make_uint4((unsigned)NF, (unsigned)NV, (unsigned)NE, used);
         atomicMax(max_used, used);
+        atomicMax(max_used + 1, (unsigned)(kFR * NF + kVR * NV));
+        atomicMax(max_used + 2, (unsigned)(kER * NE));
+        atomicMax(max_used + 3, (unsigned)(kFR * NF));
     }
 }
 
-// One CTA (kTile threads, one per face) per A tile: its distinct edges
-// (first occurrence in face order represents an edge). Pass 0 counts them
-// (cnt[t]); pass 1 writes them from off[t] (tdb_internal.h kAER).
+// One CTA (kTile threads, one per face) per A tile: its distinct edges and
+// vertices (first occurrence in face order represents one). Pass 0 counts
+// them (cnt[2t], cnt[2t + 1]); pass 1 writes them from eoff[t] / voff[t]
+// (tdb_internal.h kAER, kAVR).
 __global__ void __launch_bounds__(kTile) aedge_kernel(const double* __restrict__ planes, uint64_t n_pad,
                                                       const Tile* __restrict__ tiles, int pass,
-                                                      unsigned* __restrict__ cnt, const uint64_t* __restrict__ off,
-                                                      double* __restrict__ out) {
+                                                      unsigned* __restrict__ cnt, const uint64_t* __restrict__ eoff,
+                                                      double* __restrict__ out, const uint64_t* __restrict__ voff,
+                                                      double* __restrict__ vout) {
     constexpr int R = 3 * kTile;
     __shared__ unsigned long long vx[R], vy[R], vz[R];
     __shared__ int rep[R];
     __shared__ unsigned ekey[R];
     __shared__ int live_s[kTile];
-    __shared__ int scan[kTile + 1];
+    __shared__ int scan[kTile + 1], vscan[kTile + 1];
     const int t = threadIdx.x;
     const Tile T = tiles[blockIdx.x];
     const uint64_t f = T.row0 + min((uint32_t)t, T.count - 1);
@@ -500,10 +505,12 @@ __global__ void __launch_bounds__(kTile) aedge_kernel(const double* __restrict__
         rep[r] = rr;
     }
     __syncthreads();
+    int uv[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         const unsigned a = (unsigned)rep[3 * t + k], b = (unsigned)rep[3 * t + (k == 2 ? 0 : k + 1)];
         ekey[3 * t + k] = min(a, b) << 16 | max(a, b);
+        uv[k] = live && a == (unsigned)(3 * t + k);
     }
     __syncthreads();
     int ue[3];
@@ -520,16 +527,25 @@ __global__ void __launch_bounds__(kTile) aedge_kernel(const double* __restrict__
         ue[k] = first;
     }
     scan[t + 1] = ue[0] + ue[1] + ue[2];
-    if (t == 0) scan[0] = 0;
+    vscan[t + 1] = uv[0] + uv[1] + uv[2];
+    if (t == 0) scan[0] = vscan[0] = 0;
     __syncthreads();
     if (t == 0)
-        for (int q = 0; q < kTile; ++q) scan[q + 1] += scan[q];
+        for (int q = 0; q < kTile; ++q) scan[q + 1] += scan[q], vscan[q + 1] += vscan[q];
     __syncthreads();
     if (pass == 0) {
-        if (t == 0) cnt[blockIdx.x] = (unsigned)scan[kTile];
+        if (t == 0) cnt[2 * blockIdx.x] = (unsigned)scan[kTile], cnt[2 * blockIdx.x + 1] = (unsigned)vscan[kTile];
         return;
     }
-    double* base = out + (off[blockIdx.x] + scan[t]) * (uint64_t)kAER;
+    double* vb = vout + (voff[blockIdx.x] + vscan[t]) * (uint64_t)kAVR;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        if (!uv[k]) continue;
+        vb[0] = v[3 * k], vb[1] = v[3 * k + 1], vb[2] = v[3 * k + 2];
+        vb[3] = __longlong_as_double((long long)blockIdx.x);
+        vb += kAVR;
+    }
+    double* base = out + (eoff[blockIdx.x] + scan[t]) * (uint64_t)kAER;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         if (!ue[k]) continue;
@@ -551,31 +567,37 @@ void geom_edge_tiles(const Geom& g, cudaStream_t st) {
     std::lock_guard<std::mutex> lk(*g.fmu);
     if (!g.h_aeoff.empty()) return;
     const uint64_t nt = g.h_tiles.size();
-    std::vector<uint64_t> off(nt + 1, 0);
+    std::vector<uint64_t> eoff(nt + 1, 0), voff(nt + 1, 0);
     if (nt == 0) {
-        g.h_aeoff = off;
+        g.h_avoff = voff;
+        g.h_aeoff = eoff;
         return;
     }
     unsigned* cnt = nullptr;
     uint64_t* d_off = nullptr;
-    CK(cudaMallocAsync(&cnt, nt * sizeof(unsigned), st));
-    aedge_kernel<<<(unsigned)nt, kTile, 0, st>>>(g.planes, g.n_pad, g.d_tiles, 0, cnt, nullptr, nullptr);
+    CK(cudaMallocAsync(&cnt, 2 * nt * sizeof(unsigned), st));
+    aedge_kernel<<<(unsigned)nt, kTile, 0, st>>>(g.planes, g.n_pad, g.d_tiles, 0, cnt, nullptr, nullptr, nullptr,
+                                                  nullptr);
     CK(cudaGetLastError());
-    std::vector<unsigned> h(nt);
-    CK(cudaMemcpyAsync(h.data(), cnt, nt * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    std::vector<unsigned> h(2 * nt);
+    CK(cudaMemcpyAsync(h.data(), cnt, 2 * nt * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    for (uint64_t t = 0; t < nt; ++t) off[t + 1] = off[t] + h[t];
-    double* out = nullptr;
-    CK(cudaMallocAsync(&out, std::max<uint64_t>(off[nt], 1) * kAER * sizeof(double), st));
-    CK(cudaMallocAsync(&d_off, nt * sizeof(uint64_t), st));
-    CK(cudaMemcpyAsync(d_off, off.data(), nt * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
-    aedge_kernel<<<(unsigned)nt, kTile, 0, st>>>(g.planes, g.n_pad, g.d_tiles, 1, cnt, d_off, out);
+    for (uint64_t t = 0; t < nt; ++t) eoff[t + 1] = eoff[t] + h[2 * t], voff[t + 1] = voff[t] + h[2 * t + 1];
+    double *eout = nullptr, *vout = nullptr;
+    CK(cudaMallocAsync(&eout, std::max<uint64_t>(eoff[nt], 1) * kAER * sizeof(double), st));
+    CK(cudaMallocAsync(&vout, std::max<uint64_t>(voff[nt], 1) * kAVR * sizeof(double), st));
+    CK(cudaMallocAsync(&d_off, 2 * nt * sizeof(uint64_t), st));
+    CK(cudaMemcpyAsync(d_off, eoff.data(), nt * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_off + nt, voff.data(), nt * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+    aedge_kernel<<<(unsigned)nt, kTile, 0, st>>>(g.planes, g.n_pad, g.d_tiles, 1, cnt, d_off, eout, d_off + nt, vout);
     CK(cudaGetLastError());
     CK(cudaFreeAsync(cnt, st));
     CK(cudaFreeAsync(d_off, st));
     CK(cudaStreamSynchronize(st));
-    g.aedges = out;
-    g.h_aeoff = off;
+    g.aedges = eout;
+    g.averts = vout;
+    g.h_avoff = voff;
+    g.h_aeoff = eoff;
 }
 
 void geom_feature_blocks(const Geom& g, cudaStream_t st) {
@@ -587,18 +609,21 @@ void geom_feature_blocks(const Geom& g, cudaStream_t st) {
     unsigned* mx = nullptr;
     CK(cudaMallocAsync(&blocks, nb * (uint64_t)kFBCap * sizeof(double), st));
     CK(cudaMallocAsync(&hdr, nb * sizeof(uint4), st));
-    CK(cudaMallocAsync(&mx, sizeof(unsigned), st));
-    CK(cudaMemsetAsync(mx, 0, sizeof(unsigned), st));
+    CK(cudaMallocAsync(&mx, 4 * sizeof(unsigned), st));
+    CK(cudaMemsetAsync(mx, 0, 4 * sizeof(unsigned), st));
     fblock_kernel<<<(unsigned)nb, kFB, 0, st>>>(g.planes, g.n, g.n_pad, blocks, hdr, mx);
     CK(cudaGetLastError());
-    unsigned used = 0;
-    CK(cudaMemcpyAsync(&used, mx, sizeof used, cudaMemcpyDeviceToHost, st));
+    unsigned used[4] = {0, 0, 0, 0};
+    CK(cudaMemcpyAsync(used, mx, sizeof used, cudaMemcpyDeviceToHost, st));
     CK(cudaFreeAsync(mx, st));
     CK(cudaStreamSynchronize(st));
     g.fblocks = blocks;
     g.d_fhdr = hdr;
     g.n_fblocks = nb;
-    g.fblock_max = used;
+    g.fblock_max = used[0];
+    g.fblock_max_fv = used[1];
+    g.fblock_max_e = used[2];
+    g.fblock_max_f = used[3];
 }
 
 void geom_release(Geom* g, cudaStream_t st) {
@@ -606,8 +631,10 @@ void geom_release(Geom* g, cudaStream_t st) {
     cudaFreeAsync(g->fblocks, st);
     cudaFreeAsync(g->d_fhdr, st);
     cudaFreeAsync(g->aedges, st);
-    g->aedges = nullptr;
+    cudaFreeAsync(g->averts, st);
+    g->aedges = g->averts = nullptr;
     g->h_aeoff.clear();
+    g->h_avoff.clear();
     g->fblocks = nullptr;
     g->d_fhdr = nullptr;
     cudaFreeAsync(g->planes, st);

@@ -73,6 +73,9 @@ constexpr int kFBCap = kFB * (kFR + 3 * kVR + 3 * kER);  // doubles per block (2
 // is kAER doubles = start Q (3), E (3), |E|^2, 1/|E|^2, the tile's index (u64
 // bits), 0. The edge kernel runs kTile consecutive entries per CTA.
 enum : int { AR_Q = 0, AR_E = 3, AR_L = 6, AR_IL = 7, AR_TILE = 8, kAER = 10 };
+// ... and its distinct vertices (bitwise, non-degenerate faces), likewise:
+// kAVR doubles = x y z, the tile's index (u64 bits).
+constexpr int kAVR = 4;
 
 // per-object statistics (doubles): aabb lo xyz, hi xyz, max edge, max |coord|,
 // max kappa (F_K) over its non-degenerate faces
