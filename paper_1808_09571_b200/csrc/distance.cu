@@ -724,7 +724,8 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
 
     const Geom& A = *sel.A;
     geom_feature_blocks(B, st);  // B's feature blocks, once per store
-    if (cx.mode != TDB_MODE_CULL) geom_edge_tiles(A, st);  // A's edge / vertex tiles, once per store    // ---- scratch layout (256-byte aligned pieces), one cudaMallocAsync
+    if (cx.mode != TDB_MODE_CULL) geom_edge_tiles(A, st);  // A's edge / vertex tiles, once per store
+    // ---- scratch layout (256-byte aligned pieces), one cudaMallocAsync
     DistScratch sc{};
     size_t off = 0;
     auto piece = [&](size_t bytes) {
