@@ -51,15 +51,15 @@ UNIT = "pairs/s"
 W_D = 975.0            # algorithmic FP64 flops per pair, distance
 W_I = 282.0            # algorithmic FP64 flops per pair, intersects no-hit
 # FULL-mode distance filter (scripts/sass_loops.py build/distance.o
-# filter_kernelILb0 / edge_kernel): (FP64-pipe instructions, executed FP64
-# flops) per iteration of the B-face loop and the B-vertex loop of
-# filter_kernel<false>, and per edge pair of edge_kernel. Per pair (one A face
-# x one B face) the kernels run the face loop once, the vertex loop
-# (B distinct vertices / B face) times and the edge pair (A tile edges / A
-# face) x (B block edges / B face) times.
-FILTER_LOOP_FACE = (39, 57)
-FILTER_LOOP_VERTEX = (13, 19)
-FILTER_EDGE_PAIR = (31, 51)
+# filter_kernelILb0 | vertex_kernel | edge_kernel): (FP64-pipe instructions,
+# executed FP64 flops) per iteration. Per pair (one A face x one B face) the
+# kernels run the face loop once, the vertex loop (B distinct vertices / B
+# face) times, the vertex pair (A tile vertices / A face) times and the edge
+# pair (A tile edges / A face) x (B block edges / B face) times.
+FILTER_LOOP_FACE = (9, 18)     # filter_kernel<false> face loop: B's vertex heights (the straddle test)
+FILTER_LOOP_VERTEX = (13, 19)  # filter_kernel<false> vertex loop: a B vertex against the A face
+FILTER_VERT_PAIR = (13, 19)    # vertex_kernel: an A tile vertex against a B face
+FILTER_EDGE_PAIR = (31, 51)    # edge_kernel: an A tile edge against a B block edge
 U64_MAX = (1 << 64) - 1
 C3S_AXIS, C3S_ANGLE = (1.0, 2.0, 3.0), 0.37  # C3 stress variant rotation
 
@@ -717,11 +717,14 @@ def main():
         fb = (wl.dQ if wl.table else wl.dB).feature_counts()
         fa = (wl.dT if wl.table else wl.dA).feature_counts()
         per_face_v, per_face_e = fb["vertices"] / fb["faces"], fb["edges"] / fb["faces"]
-        a_edges = fa["tile_edges"] / fa["faces"]
+        a_edges, a_verts = fa["tile_edges"] / fa["faces"], fa["tile_vertices"] / fa["faces"]
         ep = a_edges * per_face_e  # edge pairs per face pair
-        instr = FILTER_LOOP_FACE[0] + per_face_v * FILTER_LOOP_VERTEX[0] + ep * FILTER_EDGE_PAIR[0]
-        flops = FILTER_LOOP_FACE[1] + per_face_v * FILTER_LOOP_VERTEX[1] + ep * FILTER_EDGE_PAIR[1]
-        roofline["features_per_face"] = {"b_vertices": per_face_v, "b_edges": per_face_e, "a_tile_edges": a_edges}
+        instr = (FILTER_LOOP_FACE[0] + per_face_v * FILTER_LOOP_VERTEX[0] + a_verts * FILTER_VERT_PAIR[0]
+                 + ep * FILTER_EDGE_PAIR[0])
+        flops = (FILTER_LOOP_FACE[1] + per_face_v * FILTER_LOOP_VERTEX[1] + a_verts * FILTER_VERT_PAIR[1]
+                 + ep * FILTER_EDGE_PAIR[1])
+        roofline["features_per_face"] = {"b_vertices": per_face_v, "b_edges": per_face_e, "a_tile_edges": a_edges,
+                                         "a_tile_vertices": a_verts}
         roofline["fp64_instr_per_pair"] = instr
         roofline["note"] = ("achieved/frac count W_d = 975 flops per pair (the per-pair algorithm, SURVEY.md 8(d)); "
                             "the kernels evaluate each distinct vertex / edge of a B block and each distinct edge of "

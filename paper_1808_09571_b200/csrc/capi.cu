@@ -371,7 +371,7 @@ int tdb_geom_set_has_degenerate_faces(tdb_mesh g, const uint8_t* flags, uint64_t
 }
 
 int tdb_geom_feature_counts(tdb_mesh g, uint64_t* faces, uint64_t* vertices, uint64_t* edges,
-                            uint64_t* tile_edges) {
+                            uint64_t* tile_edges, uint64_t* tile_vertices) {
     return guarded([&] {
         need(g != nullptr, "null handle");
         cudaSetDevice(g->g.device);
@@ -387,9 +387,10 @@ int tdb_geom_feature_counts(tdb_mesh g, uint64_t* faces, uint64_t* vertices, uin
         if (faces) *faces = t[0];
         if (vertices) *vertices = t[1];
         if (edges) *edges = t[2];
-        if (tile_edges) {
+        if (tile_edges || tile_vertices) {
             tdb::geom_edge_tiles(g->g, st);
-            *tile_edges = g->g.h_aeoff.empty() ? 0 : g->g.h_aeoff.back();
+            if (tile_edges) *tile_edges = g->g.h_aeoff.empty() ? 0 : g->g.h_aeoff.back();
+            if (tile_vertices) *tile_vertices = g->g.h_avoff.empty() ? 0 : g->g.h_avoff.back();
         }
     });
 }

@@ -88,7 +88,6 @@ __global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MIN
     extern __shared__ __align__(128) double dsm[];  // 2 stages of a.stage doubles: one feature block each
     __shared__ alignas(8) uint64_t bar[2];
     __shared__ double red[kTile / 32];
-    __shared__ unsigned sgn[3 * kFB / 32][kTile];  // per thread: sign bits of the block's vertex heights
 
     const uint64_t item = a.perm ? a.perm[blockIdx.x] : blockIdx.x;
     const uint64_t tl = item / a.n_chunks, ch = item - tl * a.n_chunks;
@@ -123,9 +122,11 @@ __global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MIN
     auto issue = [&](int s) {
         const int st = s & 1;
         const uint4 hb = __ldg(&a.Bfhdr[blk0 + s]);
-        const uint32_t bytes = (kEdges ? hb.w : kFR * hb.x + kVR * hb.y) * (uint32_t)sizeof(double);
+        // CULL: the whole block; FULL: [vertices of faces | distinct vertices]
+        const uint32_t off = kEdges ? 0u : kFP * hb.x;
+        const uint32_t bytes = (kEdges ? hb.w : kFV * hb.x + kVR * hb.y) * (uint32_t)sizeof(double);
         mbar_expect_tx(&bar[st], bytes);
-        if (bytes) bulk_g2s(dsm + (size_t)st * a.stage, a.Bfb + (blk0 + s) * (uint64_t)kFBCap, bytes, &bar[st]);
+        if (bytes) bulk_g2s(dsm + (size_t)st * a.stage, a.Bfb + (blk0 + s) * (uint64_t)kFBCap + off, bytes, &bar[st]);
     };
     if (threadIdx.x == 0) {
         issue(0);
@@ -133,57 +134,56 @@ __global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MIN
     }
     int best = kInfHi, hmin = kInfHi;
     bool pierce = false;
+    // A's plane n.x = c, for the signs of B's vertex heights (the straddle
+    // test; a sign is wrong only within rounding of the plane, where the
+    // vertex / edge candidates already bound the pair)
+    const double cA = dot3(A.n, A.v[0], A.v[1], A.v[2]);
 #pragma unroll 1
     for (int s = 0; s < nblk; ++s) {
         const int st = s & 1;
         const uint4 h = __ldg(&a.Bfhdr[blk0 + s]);
         mbar_wait(&bar[st], (uint32_t)((s >> 1) & 1));
-        const double* fr = dsm + (size_t)st * a.stage;
-        const double* vr = fr + kFR * h.x;
-        const double* er = vr + kVR * h.y;
-        // B's distinct vertices against A's face; the sign bits of their
-        // heights above A's plane go to this thread's words of sgn
-#pragma unroll 1
-        for (int j0 = 0; j0 < (int)h.y; j0 += 32) {
-            unsigned bits = 0;
-            const int j1 = min((int)h.y, j0 + 32);
+        const double* base = dsm + (size_t)st * a.stage;
+        const double* fp = base;                                // face planes (CULL only)
+        const double* fv = kEdges ? base + kFP * h.x : base;    // vertices of faces
+        const double* vr = fv + kFV * h.x;                      // distinct vertices
+        const double* er = vr + kVR * h.y;                      // distinct edges (CULL only)
+        // B's distinct vertices against A's face
 #pragma unroll kUV
-            for (int j = j0; j < j1; ++j) {
-                const double2 p0 = reinterpret_cast<const double2*>(vr + kVR * j)[0];
-                const double pz = vr[kVR * j + 2];
-                int hs;
-                hmin = min(hmin, vertex_cand(A, p0.x, p0.y, pz, hs));
-                bits |= (unsigned)hs >> 31 << (j - j0);
-            }
-            sgn[j0 >> 5][threadIdx.x] = bits;
+        for (int j = 0; j < (int)h.y; ++j) {
+            const double2 p0 = reinterpret_cast<const double2*>(vr + kVR * j)[0];
+            const double pz = vr[kVR * j + 2];
+            int hs;
+            hmin = min(hmin, vertex_cand(A, p0.x, p0.y, pz, hs));
         }
-        // faces: A's vertices against B's face (CULL; FULL runs them in
-        // vertex_kernel over A's distinct vertices); both triangles straddle
-        // the other's plane -> piercing test
+        // B's faces: does B straddle A's plane? Then A's vertices against B
+        // (CULL runs them on every face; FULL runs them in vertex_kernel over
+        // A's distinct vertices and here only to decide the piercing test)
 #pragma unroll kUF
         for (int j = 0; j < (int)h.x; ++j) {
-            const double2* q = reinterpret_cast<const double2*>(fr + kFR * j);
-            const double2 q9 = q[9];
-            const unsigned long long sl = (unsigned long long)__double_as_longlong(q9.y);
-            const unsigned s0 = (unsigned)sl & 1023u, s1 = (unsigned)(sl >> 10) & 1023u, s2 = (unsigned)(sl >> 20) & 1023u;
-            const unsigned g0 = sgn[s0 >> 5][threadIdx.x] >> (s0 & 31) & 1u;
-            const unsigned g1 = sgn[s1 >> 5][threadIdx.x] >> (s1 & 31) & 1u;
-            const unsigned g2 = sgn[s2 >> 5][threadIdx.x] >> (s2 & 31) & 1u;
-            const bool sb = (g0 | g1 | g2) && !(g0 & g1 & g2);  // B straddles A's plane
-            bool sa;
+            const double2* q = reinterpret_cast<const double2*>(fv + kFV * j);
+            const double2 q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3], q4 = q[4];
+            const double g0 = fma(A.n[0], q0.x, fma(A.n[1], q0.y, fma(A.n[2], q1.x, -cA)));
+            const double g1 = fma(A.n[0], q1.y, fma(A.n[1], q2.x, fma(A.n[2], q2.y, -cA)));
+            const double g2 = fma(A.n[0], q3.x, fma(A.n[1], q3.y, fma(A.n[2], q4.x, -cA)));
+            const int sor = __double2hiint(g0) | __double2hiint(g1) | __double2hiint(g2);
+            const int sand = __double2hiint(g0) & __double2hiint(g1) & __double2hiint(g2);
+            const bool sb = !(sor >= 0 || sand < 0);  // B straddles A's plane
             if (kEdges || sb) {
-                const double2 q0 = q[0], q1 = q[1], q6 = q[6], q7 = q[7], q8 = q[8], q4 = q[4], q5 = q[5];
-                const double nb[3] = {q4.y, q5.x, q5.y}, ub[3] = {q6.x, q6.y, q7.x}, vb[3] = {q7.y, q8.x, q8.y};
+                const double* pl = kEdges ? fp + kFP * j
+                                          : a.Bfb + (blk0 + s) * (uint64_t)kFBCap + kFP * j;  // rare: from HBM / L2
+                const double nb[3] = {pl[FP_N], pl[FP_N + 1], pl[FP_N + 2]};
+                const double ub[3] = {pl[FP_U], pl[FP_U + 1], pl[FP_U + 2]};
+                const double vb[3] = {pl[FP_W], pl[FP_W + 1], pl[FP_W + 2]};
                 double w0[3];
                 int hm = hmin;
-                sa = a_vertex_cand(A, q0.x, q0.y, q1.x, nb, ub, vb, hm, w0);
+                const bool sa = a_vertex_cand(A, q0.x, q0.y, q1.x, nb, ub, vb, hm, w0);
                 if (kEdges) hmin = hm;
-            } else {
-                sa = false;
+                if (sa && sb)
+                    pierce |= pierce_slow(a.Ap + row, a.An_pad, a.Bp + (uint64_t)__double_as_longlong(q4.y), a.Bn_pad);
             }
-            if (sa && sb) pierce |= pierce_slow(a.Ap + row, a.An_pad, a.Bp + (uint64_t)__double_as_longlong(q9.x), a.Bn_pad);
         }
-        // B's distinct edges against A's edges
+        // B's distinct edges against A's edges (CULL; FULL: edge_kernel)
 #pragma unroll kUE
         for (int j = 0; j < (kEdges ? (int)h.z : 0); ++j) {
             const double2* q = reinterpret_cast<const double2*>(er + kER * j);
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(kTile, TDB_EDGE_MINB) edge_kernel(EdgeArgs a) 
         const uint32_t bytes = kER * hb.z * (uint32_t)sizeof(double);
         mbar_expect_tx(&bar[st], bytes);
         if (bytes)
-            bulk_g2s(dsm + (size_t)st * a.stage, a.Bfb + (blk0 + s) * (uint64_t)kFBCap + kFR * hb.x + kVR * hb.y, bytes,
+            bulk_g2s(dsm + (size_t)st * a.stage, a.Bfb + (blk0 + s) * (uint64_t)kFBCap + (kFP + kFV) * hb.x + kVR * hb.y, bytes,
                      &bar[st]);
     };
     if (threadIdx.x == 0) {
@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(kTile, TDB_VERT_MINB) vertex_kernel(VertArgs a
     __syncthreads();
     auto issue = [&](int s) {
         const int st = s & 1;
-        const uint32_t bytes = kFR * __ldg(&a.Bfhdr[blk0 + s].x) * (uint32_t)sizeof(double);
+        const uint32_t bytes = (kFP + kFV) * __ldg(&a.Bfhdr[blk0 + s].x) * (uint32_t)sizeof(double);
         mbar_expect_tx(&bar[st], bytes);
         if (bytes) bulk_g2s(dsm + (size_t)st * a.stage, a.Bfb + (blk0 + s) * (uint64_t)kFBCap, bytes, &bar[st]);
     };
@@ -355,13 +355,15 @@ __global__ void __launch_bounds__(kTile, TDB_VERT_MINB) vertex_kernel(VertArgs a
         const int st = s & 1;
         const int nf = (int)__ldg(&a.Bfhdr[blk0 + s].x);
         mbar_wait(&bar[st], (uint32_t)((s >> 1) & 1));
-        const double2* fr = reinterpret_cast<const double2*>(dsm + (size_t)st * a.stage);
+        const double2* fp = reinterpret_cast<const double2*>(dsm + (size_t)st * a.stage);  // face planes
+        const double2* fv = fp + (kFP / 2) * nf;                                           // vertices of faces
 #pragma unroll kUVF
         for (int j = 0; j < nf; ++j) {
-            const double2* r = fr + (kFR / 2) * j;
-            const double2 r0 = r[0], r1 = r[1], r4 = r[4], r5 = r[5], r6 = r[6], r7 = r[7], r8 = r[8];
-            const double wx = ax - r0.x, wy = ay - r0.y, wz = az - r1.x;  // A_v - B_0
-            const double nb[3] = {r4.y, r5.x, r5.y}, ub[3] = {r6.x, r6.y, r7.x}, vb[3] = {r7.y, r8.x, r8.y};
+            const double2* r = fp + (kFP / 2) * j;
+            const double2 r0 = r[0], r1 = r[1], r2 = r[2], r3 = r[3], r4 = r[4];
+            const double2 v0 = fv[(kFV / 2) * j], v1 = fv[(kFV / 2) * j + 1];
+            const double wx = ax - v0.x, wy = ay - v0.y, wz = az - v1.x;  // A_v - B_0
+            const double nb[3] = {r0.x, r0.y, r1.x}, ub[3] = {r1.y, r2.x, r2.y}, vb[3] = {r3.x, r3.y, r4.x};
             const double h = dot3(nb, wx, wy, wz);
             const double u = dot3(ub, wx, wy, wz);
             const double v = dot3(vb, wx, wy, wz);

@@ -345,7 +345,6 @@ __global__ void __launch_bounds__(kFB) fblock_kernel(const double* __restrict__ 
     __shared__ unsigned ekey[R];
     __shared__ int live_s[kFB];
     __shared__ int scan[3][kFB + 1];
-    __shared__ int vslot[R];
     const int t = threadIdx.x;
     const uint64_t blk = blockIdx.x, f = blk * kFB + t;
     const bool live = f < n && planes[(uint64_t)F_DEG * n_pad + f] == 0.0;
@@ -410,31 +409,23 @@ __global__ void __launch_bounds__(kFB) fblock_kernel(const double* __restrict__ 
     }
     __syncthreads();
     const int NF = scan[0][kFB], NV = scan[1][kFB], NE = scan[2][kFB];
-    {
-        int vs = scan[1][t];
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-            if (uv[k]) vslot[3 * t + k] = vs++;
-    }
-    __syncthreads();
+
     double* base = out + blk * (uint64_t)kFBCap;
     if (live) {
-        double* fr = base + (uint64_t)kFR * scan[0][t];
+        double* fp = base + (uint64_t)kFP * scan[0][t];
+        double* fv = base + (uint64_t)kFP * NF + (uint64_t)kFV * scan[0][t];
 #pragma unroll
-        for (int k = 0; k < 9; ++k) fr[FR_V + k] = v[k];
+        for (int k = 0; k < 9; ++k) fv[FV_V + k] = v[k];
+        fv[FV_IDX] = __longlong_as_double((long long)f);
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            fr[FR_N + k] = planes[(uint64_t)(F_N + k) * n_pad + f];
-            fr[FR_U + k] = planes[(uint64_t)(F_U + k) * n_pad + f];
-            fr[FR_W + k] = planes[(uint64_t)(F_W + k) * n_pad + f];
+            fp[FP_N + k] = planes[(uint64_t)(F_N + k) * n_pad + f];
+            fp[FP_U + k] = planes[(uint64_t)(F_U + k) * n_pad + f];
+            fp[FP_W + k] = planes[(uint64_t)(F_W + k) * n_pad + f];
         }
-        fr[FR_IDX] = __longlong_as_double((long long)f);
-        const unsigned long long slots = (unsigned long long)vslot[rep[3 * t]] |
-                                         (unsigned long long)vslot[rep[3 * t + 1]] << 10 |
-                                         (unsigned long long)vslot[rep[3 * t + 2]] << 20;
-        fr[FR_SLOT] = __longlong_as_double((long long)slots);
+        fp[9] = 0.0;
         int vs = scan[1][t], es = scan[2][t];
-        double* vr = base + (uint64_t)kFR * NF;
+        double* vr = base + (uint64_t)(kFP + kFV) * NF;
         double* er = vr + (uint64_t)kVR * NV;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
@@ -453,12 +444,12 @@ __global__ void __launch_bounds__(kFB) fblock_kernel(const double* __restrict__ 
         }
     }
     if (t == 0) {
-        const unsigned used = (unsigned)(kFR * NF + kVR * NV + kER * NE);
+        const unsigned used = (unsigned)((kFP + kFV) * NF + kVR * NV + kER * NE);
         hdr[blk] = make_uint4((unsigned)NF, (unsigned)NV, (unsigned)NE, used);
         atomicMax(max_used, used);
-        atomicMax(max_used + 1, (unsigned)(kFR * NF + kVR * NV));
-        atomicMax(max_used + 2, (unsigned)(kER * NE));
-        atomicMax(max_used + 3, (unsigned)(kFR * NF));
+        atomicMax(max_used + 1, (unsigned)(kFV * NF + kVR * NV));  // filter_kernel (FULL)
+        atomicMax(max_used + 2, (unsigned)(kER * NE));             // edge_kernel
+        atomicMax(max_used + 3, (unsigned)((kFP + kFV) * NF));     // vertex_kernel
     }
 }
 

@@ -45,27 +45,29 @@ constexpr int kSB = TDB_KSB;        // B faces per TMA-staged sub-tile
 constexpr int kPlanePad = 64;
 
 // ---- B feature blocks (the distance filter's B side) -------
-// B's faces in blocks of kFB consecutive faces. Per block, three AoS lists,
-// packed back to back from the block's base (fixed capacity kFBCap doubles):
-//   faces    (non-degenerate only): kFR doubles = V (9), N, U, W, face index,
-//            vertex slots
+// B's faces in blocks of kFB consecutive faces. Per block (fixed capacity
+// kFBCap doubles), four AoS lists packed back to back from the block's base:
+//   face planes   (non-degenerate faces): kFP doubles = N, U, W, 0
+//   face vertices (the same faces):       kFV doubles = V (9), face index (u64 bits)
 //   vertices (distinct within the block, bitwise): kVR doubles = x y z 0
 //   edges    (distinct within the block, unordered vertex pair): kER doubles
 //            = start P (3), E = V_k+1 - V_k (3), |E|^2, 1/|E|^2 of the first
 //            face that has it
-// A pair's filter value is the minimum over its 6 vertex/face and 9 edge/edge
-// candidates; a shared vertex or edge is the same candidate for every face
-// of the block that has it, so the filter evaluates it once per block.
+// so each kernel stages one contiguous range: [planes | vertices of faces]
+// (vertex_kernel), [vertices of faces | distinct vertices] (filter_kernel),
+// [edges] (edge_kernel). A pair's filter value is the minimum over its 6
+// vertex/face and 9 edge/edge candidates; a shared vertex or edge is the
+// same candidate for every face of the block that has it, so the filter
+// evaluates it once per block.
 #ifndef TDB_KFB
 #define TDB_KFB 64
 #endif
 constexpr int kFB = TDB_KFB;
-// face record: ... FR_IDX = face index (u64 bits), FR_SLOT = the block's
-// vertex slots of V0, V1, V2 (10 bits each, u64 bits)
-enum : int { FR_V = 0, FR_N = 9, FR_U = 12, FR_W = 15, FR_IDX = 18, FR_SLOT = 19, kFR = 20 };
+enum : int { FP_N = 0, FP_U = 3, FP_W = 6, kFP = 10 };
+enum : int { FV_V = 0, FV_IDX = 9, kFV = 10 };
 enum : int { ER_P = 0, ER_E = 3, ER_L = 6, ER_IL = 7, kER = 8 };
 constexpr int kVR = 4;
-constexpr int kFBCap = kFB * (kFR + 3 * kVR + 3 * kER);  // doubles per block (28,672 B)
+constexpr int kFBCap = kFB * (kFP + kFV + 3 * kVR + 3 * kER);  // doubles per block (28,672 B)
 
 // ---- A edge tiles (the distance filter's A side of the edge/edge candidates)
 // Per A tile (kTile faces), its distinct edges (unordered bitwise vertex pair,
