@@ -83,6 +83,7 @@ constexpr int kUV = TDB_UV, kUF = TDB_UF, kUE = TDB_UE;
 #ifndef TDB_FACE_MINB
 #define TDB_FACE_MINB 4
 #endif
+static_assert(kFB <= 64, "the face loop's straddle mask is 64 bits");
 template <bool kEdges>
 __global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MINB) filter_kernel(DistArgs a) {
     extern __shared__ __align__(128) double dsm[];  // 2 stages of a.stage doubles: one feature block each
@@ -156,9 +157,26 @@ __global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MIN
             int hs;
             hmin = min(hmin, vertex_cand(A, p0.x, p0.y, pz, hs));
         }
-        // B's faces: does B straddle A's plane? Then A's vertices against B
-        // (CULL runs them on every face; FULL runs them in vertex_kernel over
-        // A's distinct vertices and here only to decide the piercing test)
+        // B's faces: does B straddle A's plane? CULL runs A's vertices
+        // against every face here; FULL runs them in vertex_kernel over A's
+        // distinct vertices, and here only on the (rare) straddling faces, to
+        // decide the piercing test: the face loop collects them in a mask
+        // and stays branch-free.
+        const double* fpl = kEdges ? fp : a.Bfb + (blk0 + s) * (uint64_t)kFBCap;  // FULL: planes from L2
+        auto straddling = [&](int j) {  // A's vertices against face j (+ hmin in CULL), piercing test
+            const double2* q = reinterpret_cast<const double2*>(fv + kFV * j);
+            const double2 q0 = q[0], q1 = q[1], q4 = q[4];
+            const double* pl = fpl + kFP * j;
+            const double nb[3] = {pl[FP_N], pl[FP_N + 1], pl[FP_N + 2]};
+            const double ub[3] = {pl[FP_U], pl[FP_U + 1], pl[FP_U + 2]};
+            const double vb[3] = {pl[FP_W], pl[FP_W + 1], pl[FP_W + 2]};
+            double w0[3];
+            int hm = hmin;
+            const bool sa = a_vertex_cand(A, q0.x, q0.y, q1.x, nb, ub, vb, hm, w0);
+            if (kEdges) hmin = hm;
+            return sa;
+        };
+        unsigned long long smask = 0;
 #pragma unroll kUF
         for (int j = 0; j < (int)h.x; ++j) {
             const double2* q = reinterpret_cast<const double2*>(fv + kFV * j);
@@ -169,18 +187,19 @@ __global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MIN
             const int sor = __double2hiint(g0) | __double2hiint(g1) | __double2hiint(g2);
             const int sand = __double2hiint(g0) & __double2hiint(g1) & __double2hiint(g2);
             const bool sb = !(sor >= 0 || sand < 0);  // B straddles A's plane
-            if (kEdges || sb) {
-                const double* pl = kEdges ? fp + kFP * j
-                                          : a.Bfb + (blk0 + s) * (uint64_t)kFBCap + kFP * j;  // rare: from HBM / L2
-                const double nb[3] = {pl[FP_N], pl[FP_N + 1], pl[FP_N + 2]};
-                const double ub[3] = {pl[FP_U], pl[FP_U + 1], pl[FP_U + 2]};
-                const double vb[3] = {pl[FP_W], pl[FP_W + 1], pl[FP_W + 2]};
-                double w0[3];
-                int hm = hmin;
-                const bool sa = a_vertex_cand(A, q0.x, q0.y, q1.x, nb, ub, vb, hm, w0);
-                if (kEdges) hmin = hm;
-                if (sa && sb)
+            if (kEdges) {
+                if (straddling(j) && sb)
                     pierce |= pierce_slow(a.Ap + row, a.An_pad, a.Bp + (uint64_t)__double_as_longlong(q4.y), a.Bn_pad);
+            } else {
+                smask |= (unsigned long long)sb << j;
+            }
+        }
+        while (smask) {  // FULL, rare
+            const int j = __ffsll((long long)smask) - 1;
+            smask &= smask - 1;
+            if (straddling(j)) {
+                const double idx = fv[kFV * j + FV_IDX];
+                pierce |= pierce_slow(a.Ap + row, a.An_pad, a.Bp + (uint64_t)__double_as_longlong(idx), a.Bn_pad);
             }
         }
         // B's distinct edges against A's edges (CULL; FULL: edge_kernel)
@@ -238,17 +257,32 @@ struct EdgeArgs {
 // direction of a shared edge). A tile partly outside
 // [row_lo, row_hi) contributes all its edges: a lower item minimum only
 // widens the band (check_kernel), never drops a pair.
+#ifndef TDB_EDGE_APT
+#define TDB_EDGE_APT 2
+#endif
+constexpr int kEdgeAPT = TDB_EDGE_APT;  // A edges per thread (a B edge loaded once feeds kEdgeAPT pairs)
+
 __global__ void __launch_bounds__(kTile, TDB_EDGE_MINB) edge_kernel(EdgeArgs a) {
     extern __shared__ __align__(128) double dsm[];
     __shared__ alignas(8) uint64_t bar[2];
     const uint64_t et = blockIdx.x / a.n_chunks, ch = blockIdx.x - et * a.n_chunks;
-    const uint64_t e = a.e_lo + et * kTile + threadIdx.x;
-    const bool active = e < a.e_hi;
-    const double* q = a.Ae + min(e, a.e_hi - 1) * kAER;
-    const double2 q0 = __ldg(reinterpret_cast<const double2*>(q)), q1 = __ldg(reinterpret_cast<const double2*>(q) + 1),
-                  q2 = __ldg(reinterpret_cast<const double2*>(q) + 2), q3 = __ldg(reinterpret_cast<const double2*>(q) + 3);
-    const uint64_t tile = (uint64_t)__double_as_longlong(__ldg(q + AR_TILE));
-    const double Qx = q0.x, Qy = q0.y, Qz = q1.x, Ex = q1.y, Ey = q2.x, Ez = q2.y, La = q3.x, ILa = q3.y;
+    double Q[kEdgeAPT][8];
+    uint64_t tile[kEdgeAPT];
+    bool active[kEdgeAPT];
+    int best[kEdgeAPT];
+#pragma unroll
+    for (int i = 0; i < kEdgeAPT; ++i) {
+        const uint64_t e = a.e_lo + (et * kEdgeAPT + i) * kTile + threadIdx.x;
+        active[i] = e < a.e_hi;
+        const double2* q = reinterpret_cast<const double2*>(a.Ae + min(e, a.e_hi - 1) * kAER);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double2 v = __ldg(q + k);
+            Q[i][2 * k] = v.x, Q[i][2 * k + 1] = v.y;
+        }
+        tile[i] = (uint64_t)__double_as_longlong(__ldg(reinterpret_cast<const double*>(q) + AR_TILE));
+        best[i] = kInfHi;
+    }
 
     const uint64_t b0 = ch * a.chunk, b1 = min(a.Bn, b0 + a.chunk);
     const uint64_t blk0 = b0 / kFB;
@@ -272,7 +306,6 @@ __global__ void __launch_bounds__(kTile, TDB_EDGE_MINB) edge_kernel(EdgeArgs a) 
         issue(0);
         if (nblk > 1) issue(1);
     }
-    int best = kInfHi;
 #pragma unroll 1
     for (int s = 0; s < nblk; ++s) {
         const int st = s & 1;
@@ -282,16 +315,21 @@ __global__ void __launch_bounds__(kTile, TDB_EDGE_MINB) edge_kernel(EdgeArgs a) 
 #pragma unroll kUEE
         for (int j = 0; j < ne; ++j) {
             const double2 p0 = er[4 * j], p1 = er[4 * j + 1], p2 = er[4 * j + 2], p3 = er[4 * j + 3];
-            best = min(best, edge_pair(Qx, Qy, Qz, Ex, Ey, Ez, La, ILa, p0.x, p0.y, p1.x, p1.y, p2.x, p2.y, p3.x, p3.y));
+#pragma unroll
+            for (int i = 0; i < kEdgeAPT; ++i)
+                best[i] = min(best[i], edge_pair(Q[i][0], Q[i][1], Q[i][2], Q[i][3], Q[i][4], Q[i][5], Q[i][6], Q[i][7],
+                                                 p0.x, p0.y, p1.x, p1.y, p2.x, p2.y, p3.x, p3.y));
         }
         __syncthreads();
         if (threadIdx.x == 0 && s + 2 < nblk) issue(s + 2);
     }
-    if (active && best < kInfHi) {
-        const unsigned long long bits = (unsigned long long)__double_as_longlong(__hiloint2double(best, 0));
-        atomicMin(a.itemmin + (tile - a.tile0) * a.n_chunks + ch, bits);
-        atomicMin(a.objmin + (a.tiles[tile].obj - a.obj0), bits);
-    }
+#pragma unroll
+    for (int i = 0; i < kEdgeAPT; ++i)
+        if (active[i] && best[i] < kInfHi) {
+            const unsigned long long bits = (unsigned long long)__double_as_longlong(__hiloint2double(best[i], 0));
+            atomicMin(a.itemmin + (tile[i] - a.tile0) * a.n_chunks + ch, bits);
+            atomicMin(a.objmin + (a.tiles[tile[i]].obj - a.obj0), bits);
+        }
 }
 
 struct VertArgs {
@@ -319,16 +357,29 @@ constexpr int kUVF = TDB_UVF;
 // vertex of an A tile per thread against every face of the item's B chunk
 // (|h| when it projects inside; a_vertex_cand's arithmetic for that vertex).
 // Minima into the (tile, chunk) items and objects as edge_kernel.
+#ifndef TDB_VERT_APT
+#define TDB_VERT_APT 2
+#endif
+constexpr int kVertAPT = TDB_VERT_APT;  // A vertices per thread (a B face loaded once feeds kVertAPT pairs)
+
 __global__ void __launch_bounds__(kTile, TDB_VERT_MINB) vertex_kernel(VertArgs a) {
     extern __shared__ __align__(128) double dsm[];
     __shared__ alignas(8) uint64_t bar[2];
     const uint64_t vt = blockIdx.x / a.n_chunks, ch = blockIdx.x - vt * a.n_chunks;
-    const uint64_t e = a.v_lo + vt * kTile + threadIdx.x;
-    const bool active = e < a.v_hi;
-    const double* q = a.Av + min(e, a.v_hi - 1) * kAVR;
-    const double2 q0 = __ldg(reinterpret_cast<const double2*>(q)), q1 = __ldg(reinterpret_cast<const double2*>(q) + 1);
-    const double ax = q0.x, ay = q0.y, az = q1.x;
-    const uint64_t tile = (uint64_t)__double_as_longlong(q1.y);
+    double ax[kVertAPT], ay[kVertAPT], az[kVertAPT];
+    uint64_t tile[kVertAPT];
+    bool active[kVertAPT];
+    int hmin[kVertAPT];
+#pragma unroll
+    for (int i = 0; i < kVertAPT; ++i) {
+        const uint64_t e = a.v_lo + (vt * kVertAPT + i) * kTile + threadIdx.x;
+        active[i] = e < a.v_hi;
+        const double2* q = reinterpret_cast<const double2*>(a.Av + min(e, a.v_hi - 1) * kAVR);
+        const double2 q0 = __ldg(q), q1 = __ldg(q + 1);
+        ax[i] = q0.x, ay[i] = q0.y, az[i] = q1.x;
+        tile[i] = (uint64_t)__double_as_longlong(q1.y);
+        hmin[i] = kInfHi;
+    }
 
     const uint64_t b0 = ch * a.chunk, b1 = min(a.Bn, b0 + a.chunk);
     const uint64_t blk0 = b0 / kFB;
@@ -349,7 +400,6 @@ __global__ void __launch_bounds__(kTile, TDB_VERT_MINB) vertex_kernel(VertArgs a
         issue(0);
         if (nblk > 1) issue(1);
     }
-    int hmin = kInfHi;
 #pragma unroll 1
     for (int s = 0; s < nblk; ++s) {
         const int st = s & 1;
@@ -362,21 +412,27 @@ __global__ void __launch_bounds__(kTile, TDB_VERT_MINB) vertex_kernel(VertArgs a
             const double2* r = fp + (kFP / 2) * j;
             const double2 r0 = r[0], r1 = r[1], r2 = r[2], r3 = r[3], r4 = r[4];
             const double2 v0 = fv[(kFV / 2) * j], v1 = fv[(kFV / 2) * j + 1];
-            const double wx = ax - v0.x, wy = ay - v0.y, wz = az - v1.x;  // A_v - B_0
             const double nb[3] = {r0.x, r0.y, r1.x}, ub[3] = {r1.y, r2.x, r2.y}, vb[3] = {r3.x, r3.y, r4.x};
-            const double h = dot3(nb, wx, wy, wz);
-            const double u = dot3(ub, wx, wy, wz);
-            const double v = dot3(vb, wx, wy, wz);
-            hmin = min(hmin, inside(u, v) ? (__double2hiint(h) & 0x7fffffff) : kInfHi);
+#pragma unroll
+            for (int i = 0; i < kVertAPT; ++i) {
+                const double wx = ax[i] - v0.x, wy = ay[i] - v0.y, wz = az[i] - v1.x;  // A_v - B_0
+                const double h = dot3(nb, wx, wy, wz);
+                const double u = dot3(ub, wx, wy, wz);
+                const double v = dot3(vb, wx, wy, wz);
+                hmin[i] = min(hmin[i], inside(u, v) ? (__double2hiint(h) & 0x7fffffff) : kInfHi);
+            }
         }
         __syncthreads();
         if (threadIdx.x == 0 && s + 2 < nblk) issue(s + 2);
     }
-    if (active && hmin < kInfHi) {
-        const unsigned long long bits = (unsigned long long)__double_as_longlong(__hiloint2double(hmin_sq(hmin), 0));
-        atomicMin(a.itemmin + (tile - a.tile0) * a.n_chunks + ch, bits);
-        atomicMin(a.objmin + (a.tiles[tile].obj - a.obj0), bits);
-    }
+#pragma unroll
+    for (int i = 0; i < kVertAPT; ++i)
+        if (active[i] && hmin[i] < kInfHi) {
+            const unsigned long long bits =
+                (unsigned long long)__double_as_longlong(__hiloint2double(hmin_sq(hmin[i]), 0));
+            atomicMin(a.itemmin + (tile[i] - a.tile0) * a.n_chunks + ch, bits);
+            atomicMin(a.objmin + (a.tiles[tile[i]].obj - a.obj0), bits);
+        }
 }
 
 struct BandArgs {
@@ -816,7 +872,7 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
         filter_kernel<false><<<(unsigned)n_items, kTile, smem, st>>>(da);
         CK(cudaGetLastError());
         const uint64_t v_lo = A.h_avoff[sel.tile0], v_hi = A.h_avoff[sel.tile1];
-        const uint64_t n_vt = (v_hi - v_lo + kTile - 1) / kTile;
+        const uint64_t n_vt = (v_hi - v_lo + kTile * kVertAPT - 1) / (kTile * kVertAPT);
         if (n_vt) {
             vertex_kernel<<<(unsigned)(n_vt * n_chunks), kTile, smem_f, st>>>(
                 VertArgs{A.averts, v_lo, v_hi, sel.tile0, A.d_tiles, B.fblocks, B.d_fhdr, stage_f, B.n, n_chunks, chunk,
@@ -825,7 +881,7 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
             ++launches;
         }
         const uint64_t e_lo = A.h_aeoff[sel.tile0], e_hi = A.h_aeoff[sel.tile1];
-        const uint64_t n_et = (e_hi - e_lo + kTile - 1) / kTile;
+        const uint64_t n_et = (e_hi - e_lo + kTile * kEdgeAPT - 1) / (kTile * kEdgeAPT);
         if (n_et) {
             edge_kernel<<<(unsigned)(n_et * n_chunks), kTile, smem_e, st>>>(
                 EdgeArgs{A.aedges, e_lo, e_hi, sel.tile0, A.d_tiles, B.fblocks, B.d_fhdr, stage_e, B.n, n_chunks, chunk,
