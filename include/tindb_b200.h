@@ -69,7 +69,7 @@ typedef struct {
 
 /* Per-call device statistics of the last compute call on this thread. */
 typedef struct {
-    double ms_total;        /* whole call on the device (events) */
+    double ms_total;        /* whole call on the device (events); one-launch small calls: host time from launch to results */
     double ms_filter;       /* the roofline kernel (fast FP64 filter / cull) */
     double ms_verify;       /* exact re-evaluation of candidate pairs */
     uint64_t pairs;         /* triangle pairs covered by the call */

@@ -720,7 +720,7 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
 
 void run_distance(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, uint64_t* pair,
                   double* witness6) {
-    if (direct_eligible(sel, B)) return run_distance_direct(cx, sel, B, dist, pair, witness6);
+    if (direct_eligible(sel, B, TDB_OP_DISTANCE)) return run_distance_direct(cx, sel, B, dist, pair, witness6);
     const uint64_t ntiles = sel.tile1 - sel.tile0;
     const uint64_t chunk = pick_chunk(ntiles, B.n, cx.sms, 12, kFB);
     const uint64_t n_chunks = (B.n + chunk - 1) / chunk;

@@ -328,11 +328,12 @@ constexpr uint32_t kNearLogCap = 1024;
 struct NearLog {
     unsigned long long* count;
     unsigned long long* entries;  // 2 per entry: object, pair
+    unsigned long long base = 0;  // the count's value when the call began (a counter that is never reset)
 };
 
 __device__ __forceinline__ void near_log(const NearLog& L, unsigned long long obj, unsigned long long pair) {
     if (!L.count) return;
-    const unsigned long long k = atomicAdd(L.count, 1ull);
+    const unsigned long long k = atomicAdd(L.count, 1ull) - L.base;
     if (k < kNearLogCap) {
         L.entries[2 * k] = obj;
         L.entries[2 * k + 1] = pair;

@@ -337,7 +337,7 @@ void run_intersects_batch(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t
 }  // namespace
 
 void run_intersects(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit, uint64_t* pair) {
-    if (direct_eligible(sel, B) && !cx.shared_hit) return run_intersects_direct(cx, sel, B, hit, pair);
+    if (direct_eligible(sel, B, TDB_OP_INTERSECTS) && !cx.shared_hit) return run_intersects_direct(cx, sel, B, hit, pair);
     const uint64_t ntiles = sel.tile1 - sel.tile0;
     const uint64_t groups = (ntiles + kWarps - 1) / kWarps;
     const uint64_t chunk = pick_chunk(groups, B.n, cx.sms, 12, 256);

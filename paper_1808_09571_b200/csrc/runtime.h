@@ -242,23 +242,26 @@ void run_distance(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, u
 void run_intersects(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit, uint64_t* pair);
 // Small calls in one launch each (direct.cu): the exact composition on every
 // pair, no filter / band. Used for one-object selections of at most
-// direct_pairs() pairs, and for at most kDirectQueries one-shot queries of at
-// most direct_query_pairs() (query, face) pairs. TDB_DIRECT_PAIRS overrides
-// both limits (0 = never; tests run both paths on the same inputs).
+// direct_pairs(op) pairs, and for at most kDirectQueries one-shot queries of
+// at most direct_query_pairs() (query, face) pairs. The limits are the
+// measured crossovers against the pipeline on one B200
+// (scripts/direct_crossover.py: distance ~1e5 pairs, intersects ~4e5).
+// TDB_DIRECT_PAIRS overrides every limit (0 = never; tests run both paths on
+// the same inputs).
 constexpr int kDirectQueries = 16;
 inline uint64_t direct_limit(uint64_t dflt) {
     const char* e = getenv("TDB_DIRECT_PAIRS");
     return e ? (uint64_t)strtoull(e, nullptr, 10) : dflt;
 }
-inline uint64_t direct_pairs() {
-    static const uint64_t v = direct_limit(1ull << 15);
-    return v;
+inline uint64_t direct_pairs(int op) {
+    static const uint64_t d = direct_limit(98304), h = direct_limit(262144);
+    return op == TDB_OP_DISTANCE ? d : h;
 }
 inline uint64_t direct_query_pairs() {
     static const uint64_t v = direct_limit(1ull << 16);
     return v;
 }
-bool direct_eligible(const ASel& sel, const Geom& B);
+bool direct_eligible(const ASel& sel, const Geom& B, int op);
 void run_distance_direct(const Ctx& cx, const ASel& sel, const Geom& B, double* dist, uint64_t* pair,
                          double* witness6);
 void run_intersects_direct(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t* hit, uint64_t* pair);
