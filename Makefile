@@ -10,7 +10,7 @@ PKG      := paper_1808_09571_b200
 SRC      := $(PKG)/csrc
 BUILD    := build
 LIB      := $(PKG)/libtindb_b200.so
-CU_SRCS  := $(SRC)/store.cu $(SRC)/distance.cu $(SRC)/intersects.cu $(SRC)/pairs.cu $(SRC)/volume.cu $(SRC)/queries.cu $(SRC)/wkt.cu $(SRC)/host_copy.cu $(SRC)/group.cu $(SRC)/direct.cu $(SRC)/capi.cu
+CU_SRCS  := $(SRC)/store.cu $(SRC)/distance.cu $(SRC)/intersects.cu $(SRC)/pairs.cu $(SRC)/volume.cu $(SRC)/queries.cu $(SRC)/wkt.cu $(SRC)/host_copy.cu $(SRC)/group.cu $(SRC)/direct.cu $(SRC)/atiles.cu $(SRC)/capi.cu
 CU_OBJS  := $(patsubst $(SRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
 CPP_OBJS := $(BUILD)/generators.o
 HDRS     := $(wildcard $(SRC)/*.h $(SRC)/*.cuh) include/tindb_b200.h

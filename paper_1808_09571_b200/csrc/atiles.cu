@@ -1,0 +1,337 @@
+// A side of the shared candidates: the distinct edges and
+// vertices of each "super-tile" — kSuperTile consecutive 128-face tiles of
+// one object — each listed with (at most) two of the tiles whose faces have
+// it (a vertex in more tiles gets one entry per two tiles).
+//
+// Deduplicating within a super-tile instead of within a tile shares the
+// edges between tiles too: a 1024-wide terrain's 128-face tiles are strips
+// of one grid row, 2.0 distinct edges per face each, while a super-tile of
+// 128 tiles (8 rows) has 1.56. The edge kernel attributes an entry's
+// candidate to both of its tiles' items.
+//
+// Build (once per store, on the device): corner keys (super-tile, x, y, z
+// bits) are radix-sorted (four stable passes), equal runs give vertex ids;
+// edge keys (min id, max id) are sorted, and each run of faces sharing an
+// edge becomes ceil(len / 2) entries (two tiles each; a manifold edge has one
+// run of two). Ids are ordered by super-tile, so the entries of a super-tile
+// are contiguous: per-super-tile offsets select a call's tiles.
+#include <algorithm>
+#include <vector>
+
+#include <cub/cub.cuh>
+
+#include "runtime.h"
+
+namespace tdb {
+
+namespace {
+
+constexpr unsigned kNoSt = 0xffffffffu;
+
+__global__ void face_tile_kernel(const Tile* __restrict__ tiles, uint64_t n_tiles, uint32_t* __restrict__ face_tile) {
+    const uint64_t t = blockIdx.x;
+    if (t >= n_tiles) return;
+    const Tile T = tiles[t];
+    for (uint32_t i = threadIdx.x; i < T.count; i += blockDim.x) face_tile[T.row0 + i] = (uint32_t)t;
+}
+
+// corners c = 3f + k: coordinate keys, super-tile key (kNoSt for degenerate
+// faces: sorted last, no edges)
+__global__ void corner_kernel(const double* __restrict__ planes, uint64_t n, uint64_t n_pad,
+                              const uint32_t* __restrict__ face_tile, const uint32_t* __restrict__ tile_st,
+                              unsigned long long* __restrict__ kx, unsigned long long* __restrict__ ky,
+                              unsigned long long* __restrict__ kz, uint32_t* __restrict__ kst,
+                              uint32_t* __restrict__ idx) {
+    const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= 3 * n) return;
+    const uint64_t f = c / 3, k = c - 3 * f;
+    const bool live = planes[(uint64_t)F_DEG * n_pad + f] == 0.0;
+    kx[c] = (unsigned long long)__double_as_longlong(planes[(uint64_t)(F_V + 3 * k) * n_pad + f]);
+    ky[c] = (unsigned long long)__double_as_longlong(planes[(uint64_t)(F_V + 3 * k + 1) * n_pad + f]);
+    kz[c] = (unsigned long long)__double_as_longlong(planes[(uint64_t)(F_V + 3 * k + 2) * n_pad + f]);
+    kst[c] = live ? tile_st[face_tile[f]] : kNoSt;
+    idx[c] = (uint32_t)c;
+}
+
+template <class K>
+__global__ void gather_kernel(const K* __restrict__ src, const uint32_t* __restrict__ idx, uint64_t m,
+                              K* __restrict__ dst) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) dst[i] = src[idx[i]];
+}
+
+// sorted corner i starts a new vertex when its (st, x, y, z) differs from i-1
+__global__ void vflag_kernel(const uint32_t* __restrict__ idx, uint64_t m, const unsigned long long* __restrict__ kx,
+                             const unsigned long long* __restrict__ ky, const unsigned long long* __restrict__ kz,
+                             const uint32_t* __restrict__ kst, uint32_t* __restrict__ flag) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const uint32_t a = idx[i];
+    if (i == 0) {
+        flag[i] = 1;
+        return;
+    }
+    const uint32_t b = idx[i - 1];
+    flag[i] = kst[a] != kst[b] || kx[a] != kx[b] || ky[a] != ky[b] || kz[a] != kz[b];
+}
+
+__global__ void vid_scatter_kernel(const uint32_t* __restrict__ idx, const uint32_t* __restrict__ vid_sorted,
+                                   uint64_t m, uint32_t* __restrict__ vid) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) vid[idx[i]] = vid_sorted[i] - 1;  // inclusive scan of flags: ids from 1
+}
+
+// edge (f, k): V_k -> V_k+1, keyed by the unordered vertex id pair
+__global__ void ekey_kernel(const uint32_t* __restrict__ vid, const uint32_t* __restrict__ kst, uint64_t n,
+                            unsigned long long* __restrict__ key, uint32_t* __restrict__ val) {
+    const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= 3 * n) return;
+    const uint64_t f = c / 3, k = c - 3 * f;
+    const uint32_t a = vid[c], b = vid[3 * f + (k == 2 ? 0 : k + 1)];
+    key[c] = kst[c] == kNoSt ? ~0ull : (unsigned long long)min(a, b) << 32 | max(a, b);
+    val[c] = (uint32_t)c;
+}
+
+// run starts (as their index, else 0; a max-scan gives each element its run
+// start) and entry flags (even offset within the run)
+__global__ void run_kernel(const unsigned long long* __restrict__ key, uint64_t m, uint32_t* __restrict__ start) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) start[i] = (i == 0 || key[i] != key[i - 1]) ? (uint32_t)i : 0u;
+}
+
+__global__ void eflag_kernel(const unsigned long long* __restrict__ key, const uint32_t* __restrict__ start,
+                             uint64_t m, uint32_t* __restrict__ flag) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) flag[i] = key[i] != ~0ull && ((i - start[i]) & 1) == 0;
+}
+
+// entry at sorted position i (an even offset in its run): the run's first
+// edge (its face's direction) for the geometry, tiles of elements i and i+1
+__global__ void entry_kernel(const double* __restrict__ planes, uint64_t n_pad,
+                             const unsigned long long* __restrict__ key, const uint32_t* __restrict__ val,
+                             const uint32_t* __restrict__ start, const uint32_t* __restrict__ flag,
+                             const uint32_t* __restrict__ pos, uint64_t m, const uint32_t* __restrict__ face_tile,
+                             const uint32_t* __restrict__ tile_st, double* __restrict__ out,
+                             unsigned long long* __restrict__ st_count) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m || !flag[i]) return;
+    const uint32_t rc = val[start[i]];
+    const uint64_t f = rc / 3, k = rc - 3 * f;
+    const uint32_t ta = face_tile[val[i] / 3];
+    const uint32_t tb = (i + 1 < m && key[i + 1] == key[i]) ? face_tile[val[i + 1] / 3] : ta;
+    double* p = out + (uint64_t)pos[i] * kAER;
+    p[AR_Q] = planes[(uint64_t)(F_V + 3 * k) * n_pad + f];
+    p[AR_Q + 1] = planes[(uint64_t)(F_V + 3 * k + 1) * n_pad + f];
+    p[AR_Q + 2] = planes[(uint64_t)(F_V + 3 * k + 2) * n_pad + f];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) p[AR_E + c] = planes[(uint64_t)(F_E + 3 * k + c) * n_pad + f];
+    p[AR_L] = planes[(uint64_t)(F_L + k) * n_pad + f];
+    p[AR_IL] = planes[(uint64_t)(F_IL + k) * n_pad + f];
+    p[AR_TILE] = __longlong_as_double((long long)((unsigned long long)tb << 32 | ta));
+    p[AR_TILE + 1] = 0.0;
+    atomicAdd(st_count + tile_st[ta], 1ull);
+}
+
+// vertex entries. Sorted corner i: its vertex run starts at vstart[i]
+// (max-scan); a corner is "tile-new" when its tile differs from the previous
+// corner's in the run (corners of a run are in face order, so tiles ascend).
+// Tile-new corners at an even rank in their run become entries carrying
+// their tile and the next tile-new corner's (one entry per two tiles).
+__global__ void vstart_kernel(const uint32_t* __restrict__ vflag, uint64_t m, uint32_t* __restrict__ vs) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) vs[i] = vflag[i] ? (uint32_t)i : 0u;
+}
+
+__global__ void tnew_kernel(const uint32_t* __restrict__ cur, const uint32_t* __restrict__ vstart, uint64_t m,
+                            const uint32_t* __restrict__ face_tile, const uint32_t* __restrict__ kst,
+                            uint32_t* __restrict__ tnew) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const uint32_t c = cur[i];
+    tnew[i] = kst[c] != kNoSt && (vstart[i] == i || face_tile[c / 3] != face_tile[cur[i - 1] / 3]);
+}
+
+__global__ void vflag2_kernel(const uint32_t* __restrict__ tnew, const uint32_t* __restrict__ rank,
+                              const uint32_t* __restrict__ vstart, uint64_t m, uint32_t* __restrict__ vent) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) vent[i] = tnew[i] && ((rank[i] - rank[vstart[i]]) & 1) == 0;
+}
+
+__global__ void ventry_kernel(const double* __restrict__ planes, uint64_t n_pad, const uint32_t* __restrict__ cur,
+                              const uint32_t* __restrict__ vstart, const uint32_t* __restrict__ tnew,
+                              const uint32_t* __restrict__ vent, const uint32_t* __restrict__ pos, uint64_t m,
+                              const uint32_t* __restrict__ face_tile, const uint32_t* __restrict__ tile_st,
+                              double* __restrict__ out, unsigned long long* __restrict__ st_count) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m || !vent[i]) return;
+    const uint32_t c = cur[i];
+    const uint64_t f = c / 3, k = c - 3 * f;
+    const uint32_t ta = face_tile[f];
+    uint32_t tb = ta;
+    for (uint64_t j = i + 1; j < m && vstart[j] == vstart[i]; ++j)  // the next tile-new corner of the run
+        if (tnew[j]) {
+            tb = face_tile[cur[j] / 3];
+            break;
+        }
+    double* p = out + (uint64_t)pos[i] * kAVR;
+    p[0] = planes[(uint64_t)(F_V + 3 * k) * n_pad + f];
+    p[1] = planes[(uint64_t)(F_V + 3 * k + 1) * n_pad + f];
+    p[2] = planes[(uint64_t)(F_V + 3 * k + 2) * n_pad + f];
+    p[3] = __longlong_as_double((long long)((unsigned long long)tb << 32 | ta));
+    atomicAdd(st_count + tile_st[ta], 1ull);
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    cudaStream_t st;
+    DevBuf(uint64_t n, cudaStream_t s) : st(s) { CK(cudaMallocAsync(&p, std::max<uint64_t>(n, 1) * sizeof(T), s)); }
+    ~DevBuf() { cudaFreeAsync(p, st); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+};
+
+struct MaxOp {
+    __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
+};
+
+}  // namespace
+
+void geom_super_tiles(const Geom& g, cudaStream_t st) {
+    // caller holds g.fmu
+    const uint64_t nt = g.h_tiles.size(), n = g.n, m = 3 * n;
+    // super-tiles: kSuperTile consecutive tiles of one object
+    std::vector<uint32_t> tile_st(nt);
+    uint32_t n_st = 0;
+    for (uint64_t o = 0; o + 1 < g.obj_tile0.size(); ++o) {
+        const uint64_t t0 = g.obj_tile0[o], t1 = g.obj_tile0[o + 1];
+        for (uint64_t t = t0; t < t1; ++t) tile_st[t] = n_st + (uint32_t)((t - t0) / kSuperTile);
+        n_st += (uint32_t)((t1 - t0 + kSuperTile - 1) / kSuperTile);
+    }
+    g.h_tile_st = tile_st;
+    g.h_steoff.assign(n_st + 1, 0);
+    g.h_stvoff.assign(n_st + 1, 0);
+    if (nt == 0 || m == 0) return;
+    if (m >= 0xffffffffull) throw std::invalid_argument("edge super-tiles: more than 2^32 face corners");
+    DevBuf<uint32_t> d_tile_st(nt, st), face_tile(n, st);
+    CK(cudaMemcpyAsync(d_tile_st.p, tile_st.data(), nt * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    face_tile_kernel<<<(unsigned)nt, 128, 0, st>>>(g.d_tiles, nt, face_tile.p);
+    CK(cudaGetLastError());
+    DevBuf<unsigned long long> kx(m, st), ky(m, st), kz(m, st), ks(m, st);
+    DevBuf<uint32_t> kst(m, st), idx(m, st), idx2(m, st), tmp32(m, st), vid(m, st);
+    const unsigned grid = (unsigned)((m + 255) / 256);
+    corner_kernel<<<grid, 256, 0, st>>>(g.planes, n, g.n_pad, face_tile.p, d_tile_st.p, kx.p, ky.p, kz.p, kst.p,
+                                        idx.p);
+    CK(cudaGetLastError());
+    // LSD: z, y, x (64-bit), then the super-tile (32-bit); stable passes
+    size_t tb = 0, tb2 = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, ks.p, ks.p, idx.p, idx2.p, (int)m, 0, 64, st));
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb2, tmp32.p, tmp32.p, idx.p, idx2.p, (int)m, 0, 32, st));
+    size_t tbs = 0;
+    CK(cub::DeviceScan::InclusiveSum(nullptr, tbs, tmp32.p, tmp32.p, (int)m, st));
+    size_t tbm = 0;
+    CK(cub::DeviceScan::InclusiveScan(nullptr, tbm, tmp32.p, tmp32.p, MaxOp{}, (int)m, st));
+    DevBuf<unsigned char> temp(std::max(std::max(tb, tb2), std::max(tbs, tbm)), st);
+    const size_t tcap = std::max(std::max(tb, tb2), std::max(tbs, tbm));
+    DevBuf<unsigned long long> ksorted(m, st);
+    uint32_t* cur = idx.p;
+    uint32_t* nxt = idx2.p;
+    for (const unsigned long long* key : {kz.p, ky.p, kx.p}) {
+        gather_kernel<<<grid, 256, 0, st>>>(key, cur, m, ks.p);
+        CK(cudaGetLastError());
+        size_t t = tcap;
+        CK(cub::DeviceRadixSort::SortPairs(temp.p, t, ks.p, ksorted.p, cur, nxt, (int)m, 0, 64, st));
+        std::swap(cur, nxt);
+    }
+    {
+        gather_kernel<<<grid, 256, 0, st>>>(kst.p, cur, m, tmp32.p);
+        CK(cudaGetLastError());
+        DevBuf<uint32_t> stsorted(m, st);
+        size_t t = tcap;
+        CK(cub::DeviceRadixSort::SortPairs(temp.p, t, tmp32.p, stsorted.p, cur, nxt, (int)m, 0, 32, st));
+        std::swap(cur, nxt);
+    }
+    // vertex ids (ordered by super-tile)
+    vflag_kernel<<<grid, 256, 0, st>>>(cur, m, kx.p, ky.p, kz.p, kst.p, tmp32.p);
+    CK(cudaGetLastError());
+    {
+        size_t t = tcap;
+        CK(cub::DeviceScan::InclusiveSum(temp.p, t, tmp32.p, nxt, (int)m, st));
+    }
+    vid_scatter_kernel<<<grid, 256, 0, st>>>(cur, nxt, m, vid.p);
+    CK(cudaGetLastError());
+    {  // vertex entries (tmp32 still holds the vertex-start flags)
+        DevBuf<uint32_t> vs0(m, st), vstart(m, st), tnew(m, st), rank(m, st), vent(m, st), vpos(m, st);
+        vstart_kernel<<<grid, 256, 0, st>>>(tmp32.p, m, vs0.p);
+        CK(cudaGetLastError());
+        size_t t = tcap;
+        CK(cub::DeviceScan::InclusiveScan(temp.p, t, vs0.p, vstart.p, MaxOp{}, (int)m, st));
+        tnew_kernel<<<grid, 256, 0, st>>>(cur, vstart.p, m, face_tile.p, kst.p, tnew.p);
+        CK(cudaGetLastError());
+        t = tcap;
+        CK(cub::DeviceScan::ExclusiveSum(temp.p, t, tnew.p, rank.p, (int)m, st));
+        vflag2_kernel<<<grid, 256, 0, st>>>(tnew.p, rank.p, vstart.p, m, vent.p);
+        CK(cudaGetLastError());
+        t = tcap;
+        CK(cub::DeviceScan::ExclusiveSum(temp.p, t, vent.p, vpos.p, (int)m, st));
+        uint32_t lp = 0, lf = 0;
+        CK(cudaMemcpyAsync(&lp, vpos.p + m - 1, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&lf, vent.p + m - 1, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const uint64_t nv = (uint64_t)lp + lf;
+        double* vout = nullptr;
+        CK(cudaMallocAsync(&vout, std::max<uint64_t>(nv, 1) * kAVR * sizeof(double), st));
+        DevBuf<unsigned long long> vcount(n_st, st);
+        CK(cudaMemsetAsync(vcount.p, 0, std::max<uint32_t>(n_st, 1) * sizeof(unsigned long long), st));
+        ventry_kernel<<<grid, 256, 0, st>>>(g.planes, g.n_pad, cur, vstart.p, tnew.p, vent.p, vpos.p, m, face_tile.p,
+                                            d_tile_st.p, vout, vcount.p);
+        CK(cudaGetLastError());
+        std::vector<unsigned long long> cnt(n_st);
+        CK(cudaMemcpyAsync(cnt.data(), vcount.p, n_st * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        g.h_stvoff.assign(n_st + 1, 0);
+        for (uint32_t q = 0; q < n_st; ++q) g.h_stvoff[q + 1] = g.h_stvoff[q] + cnt[q];
+        g.averts = vout;
+    }
+    // edges
+    DevBuf<unsigned long long> ekey(m, st);
+    ekey_kernel<<<grid, 256, 0, st>>>(vid.p, kst.p, n, ks.p, idx.p);
+    CK(cudaGetLastError());
+    {
+        size_t t = tcap;
+        CK(cub::DeviceRadixSort::SortPairs(temp.p, t, ks.p, ekey.p, idx.p, idx2.p, (int)m, 0, 64, st));
+    }
+    const uint32_t* val = idx2.p;
+    run_kernel<<<grid, 256, 0, st>>>(ekey.p, m, tmp32.p);
+    CK(cudaGetLastError());
+    DevBuf<uint32_t> start(m, st), flag(m, st), pos(m, st);
+    {
+        size_t t = tcap;
+        CK(cub::DeviceScan::InclusiveScan(temp.p, t, tmp32.p, start.p, MaxOp{}, (int)m, st));
+    }
+    eflag_kernel<<<grid, 256, 0, st>>>(ekey.p, start.p, m, flag.p);
+    CK(cudaGetLastError());
+    {
+        size_t t = tcap;
+        CK(cub::DeviceScan::ExclusiveSum(temp.p, t, flag.p, pos.p, (int)m, st));
+    }
+    uint32_t last_pos = 0, last_flag = 0;
+    CK(cudaMemcpyAsync(&last_pos, pos.p + m - 1, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&last_flag, flag.p + m - 1, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const uint64_t n_entries = (uint64_t)last_pos + last_flag;
+    double* out = nullptr;
+    CK(cudaMallocAsync(&out, std::max<uint64_t>(n_entries, 1) * kAER * sizeof(double), st));
+    DevBuf<unsigned long long> st_count(n_st, st);
+    CK(cudaMemsetAsync(st_count.p, 0, std::max<uint32_t>(n_st, 1) * sizeof(unsigned long long), st));
+    entry_kernel<<<grid, 256, 0, st>>>(g.planes, g.n_pad, ekey.p, val, start.p, flag.p, pos.p, m, face_tile.p,
+                                       d_tile_st.p, out, st_count.p);
+    CK(cudaGetLastError());
+    std::vector<unsigned long long> cnt(n_st);
+    CK(cudaMemcpyAsync(cnt.data(), st_count.p, n_st * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (uint32_t s = 0; s < n_st; ++s) g.h_steoff[s + 1] = g.h_steoff[s] + cnt[s];
+    g.aedges = out;
+}
+
+}  // namespace tdb

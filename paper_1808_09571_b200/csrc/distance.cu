@@ -238,7 +238,7 @@ constexpr int kUEE = TDB_UEE;
 struct EdgeArgs {
     const double* Ae;        // A edge entries (tdb_internal.h kAER)
     uint64_t e_lo, e_hi;     // the selection's entries
-    uint64_t tile0;          // the selection's first tile
+    uint64_t tile0, tile1;   // the selection's tiles
     const Tile* tiles;
     const double* Bfb;
     const uint4* Bfhdr;
@@ -327,15 +327,21 @@ __global__ void __launch_bounds__(kTile, TDB_EDGE_MINB) edge_kernel(EdgeArgs a) 
     for (int i = 0; i < kEdgeAPT; ++i)
         if (active[i] && best[i] < kInfHi) {
             const unsigned long long bits = (unsigned long long)__double_as_longlong(__hiloint2double(best[i], 0));
-            atomicMin(a.itemmin + (tile[i] - a.tile0) * a.n_chunks + ch, bits);
-            atomicMin(a.objmin + (a.tiles[tile[i]].obj - a.obj0), bits);
+            const uint64_t t2[2] = {tile[i] & 0xffffffffull, tile[i] >> 32};  // the edge's tiles
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const uint64_t t = t2[q];
+                if ((q == 1 && t == t2[0]) || t < a.tile0 || t >= a.tile1) continue;  // outside the selection
+                atomicMin(a.itemmin + (t - a.tile0) * a.n_chunks + ch, bits);
+                atomicMin(a.objmin + (a.tiles[t].obj - a.obj0), bits);
+            }
         }
 }
 
 struct VertArgs {
     const double* Av;        // A vertex entries (tdb_internal.h kAVR)
     uint64_t v_lo, v_hi;     // the selection's entries
-    uint64_t tile0;
+    uint64_t tile0, tile1;
     const Tile* tiles;
     const double* Bfb;
     const uint4* Bfhdr;
@@ -430,8 +436,14 @@ __global__ void __launch_bounds__(kTile, TDB_VERT_MINB) vertex_kernel(VertArgs a
         if (active[i] && hmin[i] < kInfHi) {
             const unsigned long long bits =
                 (unsigned long long)__double_as_longlong(__hiloint2double(hmin_sq(hmin[i]), 0));
-            atomicMin(a.itemmin + (tile[i] - a.tile0) * a.n_chunks + ch, bits);
-            atomicMin(a.objmin + (a.tiles[tile[i]].obj - a.obj0), bits);
+            const uint64_t t2[2] = {tile[i] & 0xffffffffull, tile[i] >> 32};  // the vertex's tiles
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const uint64_t t = t2[q];
+                if ((q == 1 && t == t2[0]) || t < a.tile0 || t >= a.tile1) continue;  // outside the selection
+                atomicMin(a.itemmin + (t - a.tile0) * a.n_chunks + ch, bits);
+                atomicMin(a.objmin + (a.tiles[t].obj - a.obj0), bits);
+            }
         }
 }
 
@@ -782,7 +794,7 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
 
     const Geom& A = *sel.A;
     geom_feature_blocks(B, st);  // B's feature blocks, once per store
-    if (cx.mode != TDB_MODE_CULL) geom_edge_tiles(A, st);  // A's edge / vertex tiles, once per store
+    if (cx.mode != TDB_MODE_CULL) geom_edge_tiles(A, st);  // A's super-tile lists, once per store
     // ---- scratch layout (256-byte aligned pieces), one cudaMallocAsync
     DistScratch sc{};
     size_t off = 0;
@@ -871,20 +883,25 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
     } else {
         filter_kernel<false><<<(unsigned)n_items, kTile, smem, st>>>(da);
         CK(cudaGetLastError());
-        const uint64_t v_lo = A.h_avoff[sel.tile0], v_hi = A.h_avoff[sel.tile1];
+        const uint64_t st0 = A.h_tile_st[sel.tile0], st1 = A.h_tile_st[sel.tile1 - 1] + 1;
+        const uint64_t v_lo = A.h_stvoff[st0], v_hi = A.h_stvoff[st1];
         const uint64_t n_vt = (v_hi - v_lo + kTile * kVertAPT - 1) / (kTile * kVertAPT);
         if (n_vt) {
             vertex_kernel<<<(unsigned)(n_vt * n_chunks), kTile, smem_f, st>>>(
-                VertArgs{A.averts, v_lo, v_hi, sel.tile0, A.d_tiles, B.fblocks, B.d_fhdr, stage_f, B.n, n_chunks, chunk,
+                VertArgs{A.averts, v_lo, v_hi, sel.tile0, sel.tile1, A.d_tiles, B.fblocks, B.d_fhdr, stage_f, B.n,
+                         n_chunks, chunk,
                          sel.obj0, (unsigned long long*)sc.itemmin, sc.objmin});
             CK(cudaGetLastError());
             ++launches;
         }
-        const uint64_t e_lo = A.h_aeoff[sel.tile0], e_hi = A.h_aeoff[sel.tile1];
+        // the super-tiles holding the selection's tiles (partial ones whole:
+        // edge_kernel attributes only to tiles inside the selection)
+        const uint64_t e_lo = A.h_steoff[st0], e_hi = A.h_steoff[st1];
         const uint64_t n_et = (e_hi - e_lo + kTile * kEdgeAPT - 1) / (kTile * kEdgeAPT);
         if (n_et) {
             edge_kernel<<<(unsigned)(n_et * n_chunks), kTile, smem_e, st>>>(
-                EdgeArgs{A.aedges, e_lo, e_hi, sel.tile0, A.d_tiles, B.fblocks, B.d_fhdr, stage_e, B.n, n_chunks, chunk,
+                EdgeArgs{A.aedges, e_lo, e_hi, sel.tile0, sel.tile1, A.d_tiles, B.fblocks, B.d_fhdr, stage_e, B.n,
+                         n_chunks, chunk,
                          sel.obj0, (unsigned long long*)sc.itemmin, sc.objmin});
             CK(cudaGetLastError());
             ++launches;

@@ -73,12 +73,14 @@ struct Geom {
     mutable uint32_t fblock_max_fv = 0; //   ... by its faces + vertices
     mutable uint32_t fblock_max_e = 0;  //   ... by its edges
     mutable uint32_t fblock_max_f = 0;  //   ... by its faces
-    // A edge tiles (tdb_internal.h kAER): built on first use as the A side of
-    // a distance filter (geom_edge_tiles); aeoff[t] = first entry of tile t
-    mutable double* aedges = nullptr;
-    mutable std::vector<uint64_t> h_aeoff;  // n_tiles + 1
-    mutable double* averts = nullptr;       // the tiles' distinct vertices (kAVR)
-    mutable std::vector<uint64_t> h_avoff;  // n_tiles + 1
+    // A side (tdb_internal.h kAER, kAVR): built on first use as the A side of
+    // a distance filter (geom_edge_tiles)
+    mutable double* aedges = nullptr;        // super-tiles' distinct edges
+    mutable std::vector<uint32_t> h_tile_st; // tile -> super-tile
+    mutable std::vector<uint64_t> h_steoff;  // n_super_tiles + 1: first entry of each
+    mutable double* averts = nullptr;        // super-tiles' distinct vertices
+    mutable std::vector<uint64_t> h_stvoff;  // n_super_tiles + 1: first entry of each
+    mutable bool atiles_built = false;
     std::shared_ptr<std::mutex> fmu = std::make_shared<std::mutex>();
 };
 
@@ -86,6 +88,8 @@ struct Geom {
 // device when these return).
 void geom_feature_blocks(const Geom& g, cudaStream_t st);
 void geom_edge_tiles(const Geom& g, cudaStream_t st);
+// atiles.cu: the super-tile edge and vertex lists (caller holds g.fmu)
+void geom_super_tiles(const Geom& g, cudaStream_t st);
 
 // tri9: 9 doubles per face (AoS), on the host unless tri9_on_device
 void geom_build(Geom* g, const double* tri9, uint64_t n, const uint64_t* host_off, uint64_t n_obj,

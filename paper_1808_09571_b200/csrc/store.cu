@@ -453,142 +453,14 @@ __global__ void __launch_bounds__(kFB) fblock_kernel(const double* __restrict__ 
     }
 }
 
-// One CTA (kTile threads, one per face) per A tile: its distinct edges and
-// vertices (first occurrence in face order represents one). Pass 0 counts
-// them (cnt[2t], cnt[2t + 1]); pass 1 writes them from eoff[t] / voff[t]
-// (tdb_internal.h kAER, kAVR).
-__global__ void __launch_bounds__(kTile) aedge_kernel(const double* __restrict__ planes, uint64_t n_pad,
-                                                      const Tile* __restrict__ tiles, int pass,
-                                                      unsigned* __restrict__ cnt, const uint64_t* __restrict__ eoff,
-                                                      double* __restrict__ out, const uint64_t* __restrict__ voff,
-                                                      double* __restrict__ vout) {
-    constexpr int R = 3 * kTile;
-    __shared__ unsigned long long vx[R], vy[R], vz[R];
-    __shared__ int rep[R];
-    __shared__ unsigned ekey[R];
-    __shared__ int live_s[kTile];
-    __shared__ int scan[kTile + 1], vscan[kTile + 1];
-    const int t = threadIdx.x;
-    const Tile T = tiles[blockIdx.x];
-    const uint64_t f = T.row0 + min((uint32_t)t, T.count - 1);
-    const bool live = (uint32_t)t < T.count && planes[(uint64_t)F_DEG * n_pad + f] == 0.0;
-    live_s[t] = live;
-    double v[9];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) v[k] = planes[(uint64_t)(F_V + k) * n_pad + f];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        vx[3 * t + k] = (unsigned long long)__double_as_longlong(v[3 * k]);
-        vy[3 * t + k] = (unsigned long long)__double_as_longlong(v[3 * k + 1]);
-        vz[3 * t + k] = (unsigned long long)__double_as_longlong(v[3 * k + 2]);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const int r = 3 * t + k;
-        int rr = r;
-        if (live)
-            for (int q = 0; q < r; ++q)
-                if (live_s[q / 3] && vx[q] == vx[r] && vy[q] == vy[r] && vz[q] == vz[r]) {
-                    rr = q;
-                    break;
-                }
-        rep[r] = rr;
-    }
-    __syncthreads();
-    int uv[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const unsigned a = (unsigned)rep[3 * t + k], b = (unsigned)rep[3 * t + (k == 2 ? 0 : k + 1)];
-        ekey[3 * t + k] = min(a, b) << 16 | max(a, b);
-        uv[k] = live && a == (unsigned)(3 * t + k);
-    }
-    __syncthreads();
-    int ue[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const int r = 3 * t + k;
-        bool first = live;
-        if (live)
-            for (int q = 0; q < r; ++q)
-                if (live_s[q / 3] && ekey[q] == ekey[r]) {
-                    first = false;
-                    break;
-                }
-        ue[k] = first;
-    }
-    scan[t + 1] = ue[0] + ue[1] + ue[2];
-    vscan[t + 1] = uv[0] + uv[1] + uv[2];
-    if (t == 0) scan[0] = vscan[0] = 0;
-    __syncthreads();
-    if (t == 0)
-        for (int q = 0; q < kTile; ++q) scan[q + 1] += scan[q], vscan[q + 1] += vscan[q];
-    __syncthreads();
-    if (pass == 0) {
-        if (t == 0) cnt[2 * blockIdx.x] = (unsigned)scan[kTile], cnt[2 * blockIdx.x + 1] = (unsigned)vscan[kTile];
-        return;
-    }
-    double* vb = vout + (voff[blockIdx.x] + vscan[t]) * (uint64_t)kAVR;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        if (!uv[k]) continue;
-        vb[0] = v[3 * k], vb[1] = v[3 * k + 1], vb[2] = v[3 * k + 2];
-        vb[3] = __longlong_as_double((long long)blockIdx.x);
-        vb += kAVR;
-    }
-    double* base = out + (eoff[blockIdx.x] + scan[t]) * (uint64_t)kAER;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        if (!ue[k]) continue;
-        double* p = base;
-        base += kAER;
-        p[AR_Q] = v[3 * k], p[AR_Q + 1] = v[3 * k + 1], p[AR_Q + 2] = v[3 * k + 2];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) p[AR_E + c] = planes[(uint64_t)(F_E + 3 * k + c) * n_pad + f];
-        p[AR_L] = planes[(uint64_t)(F_L + k) * n_pad + f];
-        p[AR_IL] = planes[(uint64_t)(F_IL + k) * n_pad + f];
-        p[AR_TILE] = __longlong_as_double((long long)blockIdx.x);
-        p[AR_TILE + 1] = 0.0;
-    }
-}
-
 }  // namespace
 
 void geom_edge_tiles(const Geom& g, cudaStream_t st) {
     std::lock_guard<std::mutex> lk(*g.fmu);
-    if (!g.h_aeoff.empty()) return;
-    const uint64_t nt = g.h_tiles.size();
-    std::vector<uint64_t> eoff(nt + 1, 0), voff(nt + 1, 0);
-    if (nt == 0) {
-        g.h_avoff = voff;
-        g.h_aeoff = eoff;
-        return;
-    }
-    unsigned* cnt = nullptr;
-    uint64_t* d_off = nullptr;
-    CK(cudaMallocAsync(&cnt, 2 * nt * sizeof(unsigned), st));
-    aedge_kernel<<<(unsigned)nt, kTile, 0, st>>>(g.planes, g.n_pad, g.d_tiles, 0, cnt, nullptr, nullptr, nullptr,
-                                                  nullptr);
-    CK(cudaGetLastError());
-    std::vector<unsigned> h(2 * nt);
-    CK(cudaMemcpyAsync(h.data(), cnt, 2 * nt * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    if (g.atiles_built) return;
+    geom_super_tiles(g, st);  // the super-tiles' distinct edges and vertices (atiles.cu)
     CK(cudaStreamSynchronize(st));
-    for (uint64_t t = 0; t < nt; ++t) eoff[t + 1] = eoff[t] + h[2 * t], voff[t + 1] = voff[t] + h[2 * t + 1];
-    double *eout = nullptr, *vout = nullptr;
-    CK(cudaMallocAsync(&eout, std::max<uint64_t>(eoff[nt], 1) * kAER * sizeof(double), st));
-    CK(cudaMallocAsync(&vout, std::max<uint64_t>(voff[nt], 1) * kAVR * sizeof(double), st));
-    CK(cudaMallocAsync(&d_off, 2 * nt * sizeof(uint64_t), st));
-    CK(cudaMemcpyAsync(d_off, eoff.data(), nt * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d_off + nt, voff.data(), nt * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
-    aedge_kernel<<<(unsigned)nt, kTile, 0, st>>>(g.planes, g.n_pad, g.d_tiles, 1, cnt, d_off, eout, d_off + nt, vout);
-    CK(cudaGetLastError());
-    CK(cudaFreeAsync(cnt, st));
-    CK(cudaFreeAsync(d_off, st));
-    CK(cudaStreamSynchronize(st));
-    g.aedges = eout;
-    g.averts = vout;
-    g.h_avoff = voff;
-    g.h_aeoff = eoff;
+    g.atiles_built = true;
 }
 
 void geom_feature_blocks(const Geom& g, cudaStream_t st) {
@@ -624,8 +496,10 @@ void geom_release(Geom* g, cudaStream_t st) {
     cudaFreeAsync(g->aedges, st);
     cudaFreeAsync(g->averts, st);
     g->aedges = g->averts = nullptr;
-    g->h_aeoff.clear();
-    g->h_avoff.clear();
+    g->h_steoff.clear();
+    g->h_stvoff.clear();
+    g->h_tile_st.clear();
+    g->atiles_built = false;
     g->fblocks = nullptr;
     g->d_fhdr = nullptr;
     cudaFreeAsync(g->planes, st);

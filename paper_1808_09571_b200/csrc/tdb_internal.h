@@ -69,14 +69,17 @@ enum : int { ER_P = 0, ER_E = 3, ER_L = 6, ER_IL = 7, kER = 8 };
 constexpr int kVR = 4;
 constexpr int kFBCap = kFB * (kFP + kFV + 3 * kVR + 3 * kER);  // doubles per block (28,672 B)
 
-// ---- A edge tiles (the distance filter's A side of the edge/edge candidates)
-// Per A tile (kTile faces), its distinct edges (unordered bitwise vertex pair,
-// non-degenerate faces only), concatenated in tile order; entry e of the list
-// is kAER doubles = start Q (3), E (3), |E|^2, 1/|E|^2, the tile's index (u64
-// bits), 0. The edge kernel runs kTile consecutive entries per CTA.
+// ---- A side of the shared candidates ----------------------
+// Edges: per super-tile (kSuperTile consecutive tiles of one object), its
+// distinct edges (unordered pair of bitwise-distinct vertices, non-degenerate
+// faces only), ordered by super-tile (csrc/atiles.cu); entry = kAER doubles =
+// start Q (3), E (3), |E|^2, 1/|E|^2, the two tiles that have it (u32 | u32
+// << 32, equal when one), 0. The edge kernel runs kEdgeAPT x kTile
+// consecutive entries per CTA.
 enum : int { AR_Q = 0, AR_E = 3, AR_L = 6, AR_IL = 7, AR_TILE = 8, kAER = 10 };
-// ... and its distinct vertices (bitwise, non-degenerate faces), likewise:
-// kAVR doubles = x y z, the tile's index (u64 bits).
+constexpr uint64_t kSuperTile = 128;
+// Vertices: likewise per super-tile, kAVR doubles = x y z, two tiles (u32 |
+// u32 << 32).
 constexpr int kAVR = 4;
 
 // per-object statistics (doubles): aabb lo xyz, hi xyz, max edge, max |coord|,

@@ -137,3 +137,40 @@ def test_feature_counts():
     soup = T.Mesh(np.random.default_rng(0).uniform(-1, 1, (1000, 9)))
     c = soup.feature_counts()
     assert c == {"faces": 1000, "vertices": 3000, "edges": 3000, "tile_edges": 3000, "tile_vertices": 3000}
+
+
+def _expected_counts(m, obj_faces):
+    """Numpy restatement of the A-side lists (csrc/atiles.cu): per super-tile
+    (128 tiles of 128 faces of one object) the distinct edges, one entry per
+    two faces sharing one; the distinct vertices, one entry per two of the
+    tiles having one. Meshes here have no degenerate faces."""
+    edges = verts = 0
+    f0 = 0
+    for nf in obj_faces:
+        for s0 in range(0, nf, 128 * 128):
+            s1 = min(nf, s0 + 128 * 128)
+            v = np.ascontiguousarray(m[f0 + s0:f0 + s1]).reshape(-1, 3)
+            _, vid = np.unique(v.view(np.dtype((np.void, 24))).ravel(), return_inverse=True)
+            vid = vid.reshape(-1, 3)
+            tile = (np.arange(s1 - s0) // 128)
+            e = np.stack([np.sort(np.stack([vid[:, k], vid[:, (k + 1) % 3]], 1), 1) for k in range(3)], 1).reshape(-1, 2)
+            _, cnt = np.unique(e, axis=0, return_counts=True)
+            edges += int(np.sum((cnt + 1) // 2))
+            vt = np.unique(np.stack([vid.ravel(), np.repeat(tile, 3)], 1), axis=0)
+            _, tcnt = np.unique(vt[:, 0], return_counts=True)
+            verts += int(np.sum((tcnt + 1) // 2))
+        f0 += nf
+    return edges, verts
+
+
+def test_super_tile_counts_match_restatement():
+    terrain = T.terrain(256, 160, 20.0, 7)          # 81,920 faces: rows of 512 faces (4 tiles)
+    sphere = T.unit_sphere(100_000)                 # 81,920 faces, subdivision order
+    for m in (terrain, sphere):
+        c = T.Mesh(m).feature_counts()
+        assert (c["tile_edges"], c["tile_vertices"]) == _expected_counts(m, [len(m)])
+    recs = [T.unit_sphere(1000) + 3 * k for k in range(5)]
+    tab = np.ascontiguousarray(np.concatenate(recs))
+    off = np.arange(6, dtype=np.uint64) * len(recs[0])
+    c = T.Table(tab, off).feature_counts()
+    assert (c["tile_edges"], c["tile_vertices"]) == _expected_counts(tab, [len(r) for r in recs])
