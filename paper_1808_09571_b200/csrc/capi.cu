@@ -149,6 +149,22 @@ void ensure_device() {
         CK(cudaDeviceGetDefaultMemPool(&pool, dev));
         uint64_t keep = UINT64_MAX;
         CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        // Reserve headroom once: stores rebuilt every call (the one-shot host
+        // path: ~1.2 GB of planes, feature blocks and staging per C2 batch)
+        // otherwise fragment a pool sized to the working set, and the pool
+        // then unmaps and maps memory inside cudaMallocAsync (0.1-0.9 s
+        // stalls). TDB_POOL_RESERVE_MB overrides (0 = none).
+        const char* e = getenv("TDB_POOL_RESERVE_MB");
+        const size_t mb = e ? (size_t)strtoull(e, nullptr, 10) : 8192;
+        if (mb) {
+            void* p = nullptr;
+            if (cudaMallocAsync(&p, mb << 20, g_streams[dev]) == cudaSuccess) {
+                cudaFreeAsync(p, g_streams[dev]);
+                cudaStreamSynchronize(g_streams[dev]);
+            } else {
+                cudaGetLastError();  // not enough memory: go without the headroom
+            }
+        }
     }
     t_device = dev;
 }

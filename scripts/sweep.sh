@@ -3,7 +3,7 @@
 # the raw JSON lines go to gpurun_out/sweep.jsonl. Used for DESIGN.md section 6.
 mkdir -p gpurun_out
 : > gpurun_out/sweep.jsonl
-for c in "--config c1" "--config c2" "--config c3 --steps 4" "--config c4 --steps 4 --e2e-steps 2" \
+for c in "--config c1" "--config c2" "--config c3 --steps 4" "--config c3s --steps 2" "--config c4 --steps 4 --e2e-steps 2" \
          "--config c5 --steps 2 --e2e-steps 1" "--config paper --steps 8" "--config paper --op intersects --steps 8" \
          "--config c2 --mode cull --steps 4 --no-cpu"; do
   timeout 900 python bench.py $c 2>/dev/null | tail -1 | tee -a gpurun_out/sweep.jsonl | python -c "
