@@ -55,6 +55,7 @@ struct DistArgs {
     const double* Bfb;
     const uint4* Bfhdr;
     uint32_t stage;  // doubles per SMEM stage (>= every block's used doubles, even)
+    const double4* Bsph;  // per block: bounding sphere of its vertices
 };
 
 __device__ __forceinline__ double warp_min_nn(double x) {
@@ -177,8 +178,19 @@ __global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MIN
             return sa;
         };
         unsigned long long smask = 0;
+        // FULL: no face of the block can straddle A's plane when the block's
+        // bounding sphere lies beyond it (margins >> the rounding of the
+        // heights below, so every face would test "no straddle" anyway)
+        bool maybe = true;
+        if (!kEdges) {
+            const double2* sp2 = reinterpret_cast<const double2*>(a.Bsph + blk0 + s);
+            const double2 c01 = __ldg(sp2), c2r = __ldg(sp2 + 1);
+            const double t = fabs(fma(A.n[0], c01.x, fma(A.n[1], c01.y, fma(A.n[2], c2r.x, -cA))));
+            maybe = !(t > c2r.y * (1.0 + 1e-9) +
+                              1e-9 * (fabs(c01.x) + fabs(c01.y) + fabs(c2r.x) + fabs(cA) + c2r.y));
+        }
 #pragma unroll kUF
-        for (int j = 0; j < (int)h.x; ++j) {
+        for (int j = 0; j < (maybe ? (int)h.x : 0); ++j) {
             const double2* q = reinterpret_cast<const double2*>(fv + kFV * j);
             const double2 q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3], q4 = q[4];
             const double g0 = fma(A.n[0], q0.x, fma(A.n[1], q0.y, fma(A.n[2], q1.x, -cA)));
@@ -876,7 +888,8 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
     CK(cudaFuncSetAttribute(vertex_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             2 * kFBCap * (int)sizeof(double)));
     DistArgs da{A.planes, A.n_pad, A.d_tiles, sel.tile0, sel.row_lo, sel.row_hi, B.planes, B.n_pad, B.n,
-                n_chunks, chunk, sel.obj0, sc.itemmin, sc.objmin, perm, lb2, ctr + 3, B.fblocks, B.d_fhdr, stage};
+                n_chunks, chunk, sel.obj0, sc.itemmin, sc.objmin, perm, lb2, ctr + 3, B.fblocks, B.d_fhdr, stage,
+                B.d_fsph};
     if (cx.mode == TDB_MODE_CULL) {
         filter_kernel<true><<<(unsigned)n_items, kTile, smem, st>>>(da);
         CK(cudaGetLastError());

@@ -68,6 +68,7 @@ struct Geom {
     // of a distance filter (geom_feature_blocks), kept until release
     mutable double* fblocks = nullptr;  // n_fblocks x kFBCap doubles
     mutable uint4* d_fhdr = nullptr;    // per block: faces, vertices, edges, doubles used
+    mutable double4* d_fsph = nullptr;  // per block: bounding sphere of its live vertices (x, y, z, r)
     mutable uint64_t n_fblocks = 0;
     mutable uint32_t fblock_max = 0;    // max doubles used by one block
     mutable uint32_t fblock_max_fv = 0; //   ... by its faces + vertices

@@ -16,6 +16,8 @@ namespace tdb {
 
 namespace {
 
+__device__ __forceinline__ double pos_inf_h_d() { return __longlong_as_double(0x7ff0000000000000LL); }
+
 // Order-preserving u64 encoding of doubles for atomicMin/atomicMax.
 __device__ __forceinline__ unsigned long long ord(double d) {
     const unsigned long long u = (unsigned long long)__double_as_longlong(d);
@@ -338,7 +340,7 @@ namespace {
 // edge is represented by its first occurrence in face order.
 __global__ void __launch_bounds__(kFB) fblock_kernel(const double* __restrict__ planes, uint64_t n, uint64_t n_pad,
                                                      double* __restrict__ out, uint4* __restrict__ hdr,
-                                                     unsigned* __restrict__ max_used) {
+                                                     double4* __restrict__ sph, unsigned* __restrict__ max_used) {
     constexpr int R = 3 * kFB;  // vertex / edge references of the block
     __shared__ unsigned long long vx[R], vy[R], vz[R];
     __shared__ int rep[R];
@@ -443,6 +445,39 @@ __global__ void __launch_bounds__(kFB) fblock_kernel(const double* __restrict__ 
             }
         }
     }
+    // bounding sphere of the block's live vertices (the filter's "can any
+    // face of this block straddle the plane" test): box centre, max distance
+    // rounded up
+    {
+        __shared__ double red[6][kFB];
+        double lo[3] = {pos_inf_h_d(), pos_inf_h_d(), pos_inf_h_d()}, hi[3] = {-lo[0], -lo[0], -lo[0]};
+        if (live)
+            for (int k = 0; k < 9; ++k) lo[k % 3] = fmin(lo[k % 3], v[k]), hi[k % 3] = fmax(hi[k % 3], v[k]);
+        for (int c = 0; c < 3; ++c) red[c][t] = lo[c], red[3 + c][t] = hi[c];
+        __syncthreads();
+        for (int w = kFB / 2; w > 0; w >>= 1) {
+            if (t < w)
+                for (int c = 0; c < 3; ++c)
+                    red[c][t] = fmin(red[c][t], red[c][t + w]), red[3 + c][t] = fmax(red[3 + c][t], red[3 + c][t + w]);
+            __syncthreads();
+        }
+        const double cx = 0.5 * (red[0][0] + red[3][0]), cy = 0.5 * (red[1][0] + red[4][0]),
+                     cz = 0.5 * (red[2][0] + red[5][0]);
+        __syncthreads();
+        double r = 0.0;
+        if (live)
+            for (int k = 0; k < 3; ++k) {
+                const double dx = v[3 * k] - cx, dy = v[3 * k + 1] - cy, dz = v[3 * k + 2] - cz;
+                r = fmax(r, sqrt(dx * dx + dy * dy + dz * dz));
+            }
+        red[0][t] = r;
+        __syncthreads();
+        for (int w = kFB / 2; w > 0; w >>= 1) {
+            if (t < w) red[0][t] = fmax(red[0][t], red[0][t + w]);
+            __syncthreads();
+        }
+        if (t == 0) sph[blk] = make_double4(cx, cy, cz, red[0][0] * (1.0 + 1e-12));  // NaN / +inf when no live face
+    }
     if (t == 0) {
         const unsigned used = (unsigned)((kFP + kFV) * NF + kVR * NV + kER * NE);
         hdr[blk] = make_uint4((unsigned)NF, (unsigned)NV, (unsigned)NE, used);
@@ -474,7 +509,9 @@ void geom_feature_blocks(const Geom& g, cudaStream_t st) {
     CK(cudaMallocAsync(&hdr, nb * sizeof(uint4), st));
     CK(cudaMallocAsync(&mx, 4 * sizeof(unsigned), st));
     CK(cudaMemsetAsync(mx, 0, 4 * sizeof(unsigned), st));
-    fblock_kernel<<<(unsigned)nb, kFB, 0, st>>>(g.planes, g.n, g.n_pad, blocks, hdr, mx);
+    double4* sph = nullptr;
+    CK(cudaMallocAsync(&sph, nb * sizeof(double4), st));
+    fblock_kernel<<<(unsigned)nb, kFB, 0, st>>>(g.planes, g.n, g.n_pad, blocks, hdr, sph, mx);
     CK(cudaGetLastError());
     unsigned used[4] = {0, 0, 0, 0};
     CK(cudaMemcpyAsync(used, mx, sizeof used, cudaMemcpyDeviceToHost, st));
@@ -482,6 +519,7 @@ void geom_feature_blocks(const Geom& g, cudaStream_t st) {
     CK(cudaStreamSynchronize(st));
     g.fblocks = blocks;
     g.d_fhdr = hdr;
+    g.d_fsph = sph;
     g.n_fblocks = nb;
     g.fblock_max = used[0];
     g.fblock_max_fv = used[1];
@@ -493,6 +531,8 @@ void geom_release(Geom* g, cudaStream_t st) {
     if (!g) return;
     cudaFreeAsync(g->fblocks, st);
     cudaFreeAsync(g->d_fhdr, st);
+    cudaFreeAsync(g->d_fsph, st);
+    g->d_fsph = nullptr;
     cudaFreeAsync(g->aedges, st);
     cudaFreeAsync(g->averts, st);
     g->aedges = g->averts = nullptr;
