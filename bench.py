@@ -717,7 +717,17 @@ def main():
     if wl.op == "distance" and wl.name != "paper":
         fb = (wl.dQ if wl.table else wl.dB).feature_counts()
         fa = (wl.dT if wl.table else wl.dA).feature_counts()
-        per_face_v, per_face_e = fb["vertices"] / fb["faces"], fb["edges"] / fb["faces"]
+        per_face_v = fb["vertices"] / fb["faces"]
+        # the library's B-chunk choice (runtime.h pick_chunk): B's edges come
+        # per 1,024 faces when the chunk is a multiple of that, else per block
+        units = wl.batch_units if wl.table else wl.BR
+        tiles = -(-units * (wl.nf if wl.table else 1) // 128)
+        nb = len(wl.Q) if wl.table else wl.M
+        chunk, target = 8192, torch.cuda.get_device_properties(local).multi_processor_count * 12
+        while chunk > 64 and tiles * -(-nb // chunk) < target:
+            chunk //= 2
+        r_chunk_super = chunk % 1024 == 0
+        per_face_e = (fb["super_edges"] if r_chunk_super else fb["edges"]) / fb["faces"]
         a_edges, a_verts = fa["tile_edges"] / fa["faces"], fa["tile_vertices"] / fa["faces"]
         ep = a_edges * per_face_e  # edge pairs per face pair
         instr = (FILTER_LOOP_FACE[0] + per_face_v * FILTER_LOOP_VERTEX[0] + a_verts * FILTER_VERT_PAIR[0]

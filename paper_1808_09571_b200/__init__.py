@@ -108,7 +108,7 @@ _SIGS = [
     ("tdb_mesh_upload", ct.c_int, [_D, ct.c_uint64, ct.POINTER(ct.c_void_p)]),
     ("tdb_table_upload", ct.c_int, [_D, _U64, ct.c_uint64, ct.POINTER(ct.c_void_p)]),
     ("tdb_geom_info", ct.c_int, [ct.c_void_p, _U64, _U64, _U64, _D]),
-    ("tdb_geom_feature_counts", ct.c_int, [ct.c_void_p, _U64, _U64, _U64, _U64, _U64]),
+    ("tdb_geom_feature_counts", ct.c_int, [ct.c_void_p, _U64, _U64, _U64, _U64, _U64, _U64]),
     ("tdb_mesh_from_wkt", ct.c_int, [ct.c_char_p, ct.c_uint64, ct.POINTER(ct.c_void_p), _U64]),
     ("tdb_table_from_wkt", ct.c_int, [ct.c_char_p, _U64, ct.c_uint64, ct.POINTER(ct.c_void_p), _U64, _U64]),
     ("tdb_geom_download", ct.c_int, [ct.c_void_p, _D]),
@@ -261,12 +261,13 @@ class _Geom:
         """The distance filter's shared candidates: as the B
         side, total non-degenerate faces, distinct vertices and distinct edges
         over the store's 64-face blocks; as the A side, the distinct edges and
-        vertices of its 128-face tiles (tile_edges, tile_vertices)."""
-        f, v, e, te, tv = (ct.c_uint64() for _ in range(5))
+        vertices of its super-tiles (tile_edges, tile_vertices); the distinct
+        edges per 1,024 faces (super_edges, B's lists in large calls)."""
+        f, v, e, te, tv, se = (ct.c_uint64() for _ in range(6))
         _check(lib().tdb_geom_feature_counts(self._h, ct.byref(f), ct.byref(v), ct.byref(e), ct.byref(te),
-                                             ct.byref(tv)))
+                                             ct.byref(tv), ct.byref(se)))
         return {"faces": f.value, "vertices": v.value, "edges": e.value, "tile_edges": te.value,
-                "tile_vertices": tv.value}
+                "tile_vertices": tv.value, "super_edges": se.value}
 
     def download(self) -> np.ndarray:
         """The stored faces as (n, 9) float64, face order (the AoS the store was built from)."""

@@ -197,20 +197,30 @@ struct MaxOp {
 
 }  // namespace
 
-void geom_super_tiles(const Geom& g, cudaStream_t st) {
-    // caller holds g.fmu
+namespace {
+
+// The lists of one grouping: groups of `group_tiles` consecutive tiles of one
+// object; distinct edges (and, when asked, vertices) per group, each entry
+// carrying two of its tiles; entries ordered by group.
+struct SuperLists {
+    std::vector<uint32_t> tile_grp;
+    std::vector<uint64_t> eoff, voff;  // per group: first entry
+    double* edges = nullptr;
+    double* verts = nullptr;
+};
+
+void build_super(const Geom& g, uint64_t group_tiles, bool with_vertices, cudaStream_t st, SuperLists& L) {
     const uint64_t nt = g.h_tiles.size(), n = g.n, m = 3 * n;
-    // super-tiles: kSuperTile consecutive tiles of one object
     std::vector<uint32_t> tile_st(nt);
     uint32_t n_st = 0;
     for (uint64_t o = 0; o + 1 < g.obj_tile0.size(); ++o) {
         const uint64_t t0 = g.obj_tile0[o], t1 = g.obj_tile0[o + 1];
-        for (uint64_t t = t0; t < t1; ++t) tile_st[t] = n_st + (uint32_t)((t - t0) / kSuperTile);
-        n_st += (uint32_t)((t1 - t0 + kSuperTile - 1) / kSuperTile);
+        for (uint64_t t = t0; t < t1; ++t) tile_st[t] = n_st + (uint32_t)((t - t0) / group_tiles);
+        n_st += (uint32_t)((t1 - t0 + group_tiles - 1) / group_tiles);
     }
-    g.h_tile_st = tile_st;
-    g.h_steoff.assign(n_st + 1, 0);
-    g.h_stvoff.assign(n_st + 1, 0);
+    L.tile_grp = tile_st;
+    L.eoff.assign(n_st + 1, 0);
+    L.voff.assign(n_st + 1, 0);
     if (nt == 0 || m == 0) return;
     if (m >= 0xffffffffull) throw std::invalid_argument("edge super-tiles: more than 2^32 face corners");
     DevBuf<uint32_t> d_tile_st(nt, st), face_tile(n, st);
@@ -260,7 +270,7 @@ void geom_super_tiles(const Geom& g, cudaStream_t st) {
     }
     vid_scatter_kernel<<<grid, 256, 0, st>>>(cur, nxt, m, vid.p);
     CK(cudaGetLastError());
-    {  // vertex entries (tmp32 still holds the vertex-start flags)
+    if (with_vertices) {  // vertex entries (tmp32 still holds the vertex-start flags)
         DevBuf<uint32_t> vs0(m, st), vstart(m, st), tnew(m, st), rank(m, st), vent(m, st), vpos(m, st);
         vstart_kernel<<<grid, 256, 0, st>>>(tmp32.p, m, vs0.p);
         CK(cudaGetLastError());
@@ -289,9 +299,8 @@ void geom_super_tiles(const Geom& g, cudaStream_t st) {
         std::vector<unsigned long long> cnt(n_st);
         CK(cudaMemcpyAsync(cnt.data(), vcount.p, n_st * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        g.h_stvoff.assign(n_st + 1, 0);
-        for (uint32_t q = 0; q < n_st; ++q) g.h_stvoff[q + 1] = g.h_stvoff[q] + cnt[q];
-        g.averts = vout;
+        for (uint32_t q = 0; q < n_st; ++q) L.voff[q + 1] = L.voff[q] + cnt[q];
+        L.verts = vout;
     }
     // edges
     DevBuf<unsigned long long> ekey(m, st);
@@ -330,8 +339,30 @@ void geom_super_tiles(const Geom& g, cudaStream_t st) {
     std::vector<unsigned long long> cnt(n_st);
     CK(cudaMemcpyAsync(cnt.data(), st_count.p, n_st * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    for (uint32_t s = 0; s < n_st; ++s) g.h_steoff[s + 1] = g.h_steoff[s] + cnt[s];
-    g.aedges = out;
+    for (uint32_t s = 0; s < n_st; ++s) L.eoff[s + 1] = L.eoff[s] + cnt[s];
+    L.edges = out;
+}
+
+}  // namespace
+
+void geom_super_tiles(const Geom& g, cudaStream_t st) {
+    SuperLists L;
+    build_super(g, kSuperTile, true, st, L);
+    g.h_tile_st = std::move(L.tile_grp);
+    g.h_steoff = std::move(L.eoff);
+    g.h_stvoff = std::move(L.voff);
+    g.aedges = L.edges;
+    g.averts = L.verts;
+}
+
+void geom_super_bedges(const Geom& g, cudaStream_t st) {
+    SuperLists L;
+    build_super(g, kBSuper / kTile, false, st, L);
+    g.h_bseoff = std::move(L.eoff);
+    g.bedges = L.edges;
+    CK(cudaMallocAsync(&g.d_bseoff, g.h_bseoff.size() * sizeof(uint64_t), st));
+    CK(cudaMemcpyAsync(g.d_bseoff, g.h_bseoff.data(), g.h_bseoff.size() * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                       st));
 }
 
 }  // namespace tdb

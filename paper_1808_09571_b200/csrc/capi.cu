@@ -387,7 +387,7 @@ int tdb_geom_set_has_degenerate_faces(tdb_mesh g, const uint8_t* flags, uint64_t
 }
 
 int tdb_geom_feature_counts(tdb_mesh g, uint64_t* faces, uint64_t* vertices, uint64_t* edges,
-                            uint64_t* tile_edges, uint64_t* tile_vertices) {
+                            uint64_t* tile_edges, uint64_t* tile_vertices, uint64_t* super_edges) {
     return guarded([&] {
         need(g != nullptr, "null handle");
         cudaSetDevice(g->g.device);
@@ -407,6 +407,10 @@ int tdb_geom_feature_counts(tdb_mesh g, uint64_t* faces, uint64_t* vertices, uin
             tdb::geom_edge_tiles(g->g, st);
             if (tile_edges) *tile_edges = g->g.h_steoff.empty() ? 0 : g->g.h_steoff.back();
             if (tile_vertices) *tile_vertices = g->g.h_stvoff.empty() ? 0 : g->g.h_stvoff.back();
+        }
+        if (super_edges) {
+            tdb::geom_bedges(g->g, st);
+            *super_edges = g->g.h_bseoff.empty() ? 0 : g->g.h_bseoff.back();
         }
     });
 }

@@ -258,6 +258,8 @@ struct EdgeArgs {
     uint64_t Bn, n_chunks, chunk, obj0;
     unsigned long long* itemmin;  // the filter's item minima (non-negative doubles as u64)
     unsigned long long* objmin;
+    const double* Bse;            // B's super-block edges (kSuper) and their per-group offsets
+    const uint64_t* Bse_off;
 };
 
 // Edge/edge candidates of FULL mode: one A distinct edge per thread (kTile
@@ -274,9 +276,13 @@ struct EdgeArgs {
 #endif
 constexpr int kEdgeAPT = TDB_EDGE_APT;  // A edges per thread (a B edge loaded once feeds kEdgeAPT pairs)
 
+// kSuper: B's distinct edges per kBSuper faces (the chunk is a multiple of
+// kBSuper), streamed kEdgePiece entries per stage; else per 64-face block.
+template <bool kSuper>
 __global__ void __launch_bounds__(kTile, TDB_EDGE_MINB) edge_kernel(EdgeArgs a) {
     extern __shared__ __align__(128) double dsm[];
     __shared__ alignas(8) uint64_t bar[2];
+    constexpr int kStride = kSuper ? kAER : kER;  // doubles per staged B edge (P, E, |E|^2, 1/|E|^2 first)
     const uint64_t et = blockIdx.x / a.n_chunks, ch = blockIdx.x - et * a.n_chunks;
     double Q[kEdgeAPT][8];
     uint64_t tile[kEdgeAPT];
@@ -298,7 +304,19 @@ __global__ void __launch_bounds__(kTile, TDB_EDGE_MINB) edge_kernel(EdgeArgs a) 
 
     const uint64_t b0 = ch * a.chunk, b1 = min(a.Bn, b0 + a.chunk);
     const uint64_t blk0 = b0 / kFB;
-    const int nblk = (int)((b1 - b0 + kFB - 1) / kFB);
+    uint64_t se0 = 0, se1 = 0;
+    int nunits;
+    if (kSuper) {
+        se0 = __ldg(a.Bse_off + b0 / kBSuper);
+        se1 = __ldg(a.Bse_off + (b1 + kBSuper - 1) / kBSuper);
+        nunits = (int)((se1 - se0 + kEdgePiece - 1) / kEdgePiece);
+    } else {
+        nunits = (int)((b1 - b0 + kFB - 1) / kFB);
+    }
+    auto unit_count = [&](int s) -> int {
+        return kSuper ? (int)min((uint64_t)kEdgePiece, se1 - se0 - (uint64_t)s * kEdgePiece)
+                      : (int)__ldg(&a.Bfhdr[blk0 + s].z);
+    };
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -307,33 +325,38 @@ __global__ void __launch_bounds__(kTile, TDB_EDGE_MINB) edge_kernel(EdgeArgs a) 
     __syncthreads();
     auto issue = [&](int s) {
         const int st = s & 1;
-        const uint4 hb = __ldg(&a.Bfhdr[blk0 + s]);
-        const uint32_t bytes = kER * hb.z * (uint32_t)sizeof(double);
+        const uint32_t bytes = (uint32_t)(kStride * unit_count(s)) * (uint32_t)sizeof(double);
+        const double* src;
+        if (kSuper) {
+            src = a.Bse + (se0 + (uint64_t)s * kEdgePiece) * kAER;
+        } else {
+            const uint4 hb = __ldg(&a.Bfhdr[blk0 + s]);
+            src = a.Bfb + (blk0 + s) * (uint64_t)kFBCap + (kFP + kFV) * hb.x + kVR * hb.y;
+        }
         mbar_expect_tx(&bar[st], bytes);
-        if (bytes)
-            bulk_g2s(dsm + (size_t)st * a.stage, a.Bfb + (blk0 + s) * (uint64_t)kFBCap + (kFP + kFV) * hb.x + kVR * hb.y, bytes,
-                     &bar[st]);
+        if (bytes) bulk_g2s(dsm + (size_t)st * a.stage, src, bytes, &bar[st]);
     };
     if (threadIdx.x == 0) {
         issue(0);
-        if (nblk > 1) issue(1);
+        if (nunits > 1) issue(1);
     }
 #pragma unroll 1
-    for (int s = 0; s < nblk; ++s) {
+    for (int s = 0; s < nunits; ++s) {
         const int st = s & 1;
-        const int ne = (int)__ldg(&a.Bfhdr[blk0 + s].z);
+        const int ne = unit_count(s);
         mbar_wait(&bar[st], (uint32_t)((s >> 1) & 1));
-        const double2* er = reinterpret_cast<const double2*>(dsm + (size_t)st * a.stage);
+        const double* er = dsm + (size_t)st * a.stage;
 #pragma unroll kUEE
         for (int j = 0; j < ne; ++j) {
-            const double2 p0 = er[4 * j], p1 = er[4 * j + 1], p2 = er[4 * j + 2], p3 = er[4 * j + 3];
+            const double2* r = reinterpret_cast<const double2*>(er + (size_t)kStride * j);
+            const double2 p0 = r[0], p1 = r[1], p2 = r[2], p3 = r[3];
 #pragma unroll
             for (int i = 0; i < kEdgeAPT; ++i)
                 best[i] = min(best[i], edge_pair(Q[i][0], Q[i][1], Q[i][2], Q[i][3], Q[i][4], Q[i][5], Q[i][6], Q[i][7],
                                                  p0.x, p0.y, p1.x, p1.y, p2.x, p2.y, p3.x, p3.y));
         }
         __syncthreads();
-        if (threadIdx.x == 0 && s + 2 < nblk) issue(s + 2);
+        if (threadIdx.x == 0 && s + 2 < nunits) issue(s + 2);
     }
 #pragma unroll
     for (int i = 0; i < kEdgeAPT; ++i)
@@ -806,7 +829,10 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
 
     const Geom& A = *sel.A;
     geom_feature_blocks(B, st);  // B's feature blocks, once per store
-    if (cx.mode != TDB_MODE_CULL) geom_edge_tiles(A, st);  // A's super-tile lists, once per store
+    if (cx.mode != TDB_MODE_CULL) {
+        geom_edge_tiles(A, st);  // A's super-tile lists, once per store
+        if (pick_chunk(sel.tile1 - sel.tile0, B.n, cx.sms, 12, kFB) % kBSuper == 0) geom_bedges(B, st);  // B's, once
+    }
     // ---- scratch layout (256-byte aligned pieces), one cudaMallocAsync
     DistScratch sc{};
     size_t off = 0;
@@ -883,8 +909,10 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
                             2 * kFBCap * (int)sizeof(double)));
     CK(cudaFuncSetAttribute(filter_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             2 * kFBCap * (int)sizeof(double)));
-    CK(cudaFuncSetAttribute(edge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(edge_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             2 * kFBCap * (int)sizeof(double)));
+    CK(cudaFuncSetAttribute(edge_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            2 * kEdgePiece * kAER * (int)sizeof(double)));
     CK(cudaFuncSetAttribute(vertex_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             2 * kFBCap * (int)sizeof(double)));
     DistArgs da{A.planes, A.n_pad, A.d_tiles, sel.tile0, sel.row_lo, sel.row_hi, B.planes, B.n_pad, B.n,
@@ -912,10 +940,17 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
         const uint64_t e_lo = A.h_steoff[st0], e_hi = A.h_steoff[st1];
         const uint64_t n_et = (e_hi - e_lo + kTile * kEdgeAPT - 1) / (kTile * kEdgeAPT);
         if (n_et) {
-            edge_kernel<<<(unsigned)(n_et * n_chunks), kTile, smem_e, st>>>(
-                EdgeArgs{A.aedges, e_lo, e_hi, sel.tile0, sel.tile1, A.d_tiles, B.fblocks, B.d_fhdr, stage_e, B.n,
-                         n_chunks, chunk,
-                         sel.obj0, (unsigned long long*)sc.itemmin, sc.objmin});
+            // B's edges per kBSuper faces when the chunk allows (fewer edge pairs), else per feature block
+            const bool super = chunk % kBSuper == 0 && B.d_bseoff;
+            const uint32_t stg = super ? (uint32_t)(kEdgePiece * kAER) : stage_e;
+            const EdgeArgs ea{A.aedges, e_lo, e_hi, sel.tile0, sel.tile1, A.d_tiles, B.fblocks, B.d_fhdr, stg, B.n,
+                              n_chunks, chunk, sel.obj0, (unsigned long long*)sc.itemmin, sc.objmin, B.bedges,
+                              B.d_bseoff};
+            const size_t smem_x = 2 * (size_t)stg * sizeof(double);
+            if (super)
+                edge_kernel<true><<<(unsigned)(n_et * n_chunks), kTile, smem_x, st>>>(ea);
+            else
+                edge_kernel<false><<<(unsigned)(n_et * n_chunks), kTile, smem_x, st>>>(ea);
             CK(cudaGetLastError());
             ++launches;
         }

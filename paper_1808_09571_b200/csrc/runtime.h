@@ -82,6 +82,10 @@ struct Geom {
     mutable double* averts = nullptr;        // super-tiles' distinct vertices
     mutable std::vector<uint64_t> h_stvoff;  // n_super_tiles + 1: first entry of each
     mutable bool atiles_built = false;
+    // B side: distinct edges per kBSuper faces (geom_super_bedges)
+    mutable double* bedges = nullptr;
+    mutable std::vector<uint64_t> h_bseoff;  // per group of kBSuper faces: first entry
+    mutable uint64_t* d_bseoff = nullptr;     // device copy
     std::shared_ptr<std::mutex> fmu = std::make_shared<std::mutex>();
 };
 
@@ -91,6 +95,9 @@ void geom_feature_blocks(const Geom& g, cudaStream_t st);
 void geom_edge_tiles(const Geom& g, cudaStream_t st);
 // atiles.cu: the super-tile edge and vertex lists (caller holds g.fmu)
 void geom_super_tiles(const Geom& g, cudaStream_t st);
+void geom_super_bedges(const Geom& g, cudaStream_t st);
+// B's super-block edge lists, once (thread-safe)
+void geom_bedges(const Geom& g, cudaStream_t st);
 
 // tri9: 9 doubles per face (AoS), on the host unless tri9_on_device
 void geom_build(Geom* g, const double* tri9, uint64_t n, const uint64_t* host_off, uint64_t n_obj,

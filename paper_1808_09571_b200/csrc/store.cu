@@ -498,6 +498,13 @@ void geom_edge_tiles(const Geom& g, cudaStream_t st) {
     g.atiles_built = true;
 }
 
+void geom_bedges(const Geom& g, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(*g.fmu);
+    if (!g.h_bseoff.empty()) return;
+    geom_super_bedges(g, st);
+    CK(cudaStreamSynchronize(st));
+}
+
 void geom_feature_blocks(const Geom& g, cudaStream_t st) {
     std::lock_guard<std::mutex> lk(*g.fmu);
     if (g.fblocks || g.n == 0) return;
@@ -536,6 +543,11 @@ void geom_release(Geom* g, cudaStream_t st) {
     cudaFreeAsync(g->aedges, st);
     cudaFreeAsync(g->averts, st);
     g->aedges = g->averts = nullptr;
+    cudaFreeAsync(g->bedges, st);
+    cudaFreeAsync(g->d_bseoff, st);
+    g->bedges = nullptr;
+    g->d_bseoff = nullptr;
+    g->h_bseoff.clear();
     g->h_steoff.clear();
     g->h_stvoff.clear();
     g->h_tile_st.clear();

@@ -78,6 +78,12 @@ constexpr int kFBCap = kFB * (kFP + kFV + 3 * kVR + 3 * kER);  // doubles per bl
 // consecutive entries per CTA.
 enum : int { AR_Q = 0, AR_E = 3, AR_L = 6, AR_IL = 7, AR_TILE = 8, kAER = 10 };
 constexpr uint64_t kSuperTile = 128;
+// B side of the edge/edge candidates when the chunk allows (FULL mode, chunk
+// % kBSuper == 0): B's distinct edges per kBSuper consecutive faces (the same
+// builder, csrc/atiles.cu), streamed by edge_kernel kEdgePiece entries per
+// TMA stage.
+constexpr uint64_t kBSuper = 1024;
+constexpr int kEdgePiece = 256;
 // Vertices: likewise per super-tile, kAVR doubles = x y z, two tiles (u32 |
 // u32 << 32).
 constexpr int kAVR = 4;

@@ -136,7 +136,22 @@ def test_feature_counts():
     assert c["tile_edges"] < 2.2 * 81920 and c["tile_vertices"] < 1.2 * 81920
     soup = T.Mesh(np.random.default_rng(0).uniform(-1, 1, (1000, 9)))
     c = soup.feature_counts()
-    assert c == {"faces": 1000, "vertices": 3000, "edges": 3000, "tile_edges": 3000, "tile_vertices": 3000}
+    assert c == {"faces": 1000, "vertices": 3000, "edges": 3000, "tile_edges": 3000, "tile_vertices": 3000,
+                 "super_edges": 3000}
+
+
+def _expected_super_edges(m, group=1024):
+    """B's distinct edges per `group` consecutive faces of a one-object
+    store, one entry per two faces sharing one (csrc/atiles.cu)."""
+    total = 0
+    for s0 in range(0, len(m), group):
+        v = np.ascontiguousarray(m[s0:s0 + group]).reshape(-1, 3)
+        _, vid = np.unique(v.view(np.dtype((np.void, 24))).ravel(), return_inverse=True)
+        vid = vid.reshape(-1, 3)
+        e = np.stack([np.sort(np.stack([vid[:, k], vid[:, (k + 1) % 3]], 1), 1) for k in range(3)], 1).reshape(-1, 2)
+        _, cnt = np.unique(e, axis=0, return_counts=True)
+        total += int(np.sum((cnt + 1) // 2))
+    return total
 
 
 def _expected_counts(m, obj_faces):
@@ -169,6 +184,7 @@ def test_super_tile_counts_match_restatement():
     for m in (terrain, sphere):
         c = T.Mesh(m).feature_counts()
         assert (c["tile_edges"], c["tile_vertices"]) == _expected_counts(m, [len(m)])
+        assert c["super_edges"] == _expected_super_edges(m)
     recs = [T.unit_sphere(1000) + 3 * k for k in range(5)]
     tab = np.ascontiguousarray(np.concatenate(recs))
     off = np.arange(6, dtype=np.uint64) * len(recs[0])
