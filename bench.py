@@ -706,9 +706,11 @@ def main():
     roofline = {
         "bound": "fp64", "achieved": achieved_tf, "peak": fp64_tf, "unit": "TFLOP/s",
         "frac": achieved_tf / fp64_tf, "traffic": traffic,
-        "traffic_note": "dram__bytes_read+write per launch from profiles/traffic.json (ncu --set full), "
-                        "scaled to this launch's pairs; algorithmic bytes = 288 B per B face per 128-row tile",
-        "kernel": kname,
+        "traffic_note": "dram__bytes_read+write per launch from profiles/traffic.json (ncu --set full; the "
+                        "three filter-stage kernels summed for distance), scaled to this launch's pairs",
+        "kernel": (kname if wl.op != "distance" or wl.name == "paper" else
+                   "filter stage: edge_kernel (dominant, ~74% of it) + vertex_kernel + filter_kernel<false>, "
+                   "timed together (events around the three launches)"),
         "work_per_pair_flops": w,
         "peak_source": "measured in this run: DFMA issue-rate microbenchmark (tdb_fp64_peak); "
                        "spec 148 SM x 64 FMA x 2 x 1.965 GHz = 37.2",
