@@ -48,7 +48,7 @@ constexpr int kHitPlanes = 15;  // V (9), N (3), C, DEG, K
 __device__ __constant__ int kHitPlaneOf[kHitPlanes] = {0,   1,   2,       3,       4,   5,     6,  7,
                                                        8,   F_N, F_N + 1, F_N + 2, F_C, F_DEG, F_K};
 enum { HS_V = 0, HS_N = 9, HS_C = 12, HS_DEG = 13, HS_K = 14 };
-constexpr int kSBH = 128;          // B faces per staged sub-tile
+constexpr int kSBH = kHitGroup;    // B faces per staged sub-tile (one bounding sphere each)
 constexpr int kRows = 4;           // A rows per lane
 constexpr int kWarps = 4;          // tiles per CTA (one per warp)
 
@@ -72,6 +72,7 @@ struct HitArgs {
     // the origin, and a bound on |v - origin| over B
     const float* Bf;
     double ox, oy, oz, RB;
+    const double4* Bsph;  // per kHitGroup B faces: bounding sphere (x, y, z, r)
 };
 
 __device__ __forceinline__ exact::tri load_tri(const double* P, uint64_t pad, uint64_t i) {
@@ -177,6 +178,7 @@ __global__ void __launch_bounds__(32 * kWarps, TDB_HIT_MINB) hit_kernel(HitArgs 
         diag2 += (hi - lo) * (hi - lo);
     }
     const double D = sqrt(diag2), abs_tol = kCullAbs * fmax(As[7], Bs[7]);
+    const double tau_blk = (kCullOne + As[8]) * D + abs_tol;  // >= every live row's one-way margin
     const double gap = kApart * D + abs_tol;
 #pragma unroll
     for (int k = 0; k < 3; ++k) apart |= (As[k] > Bs[3 + k] + gap) || (Bs[k] > As[3 + k] + gap);
@@ -278,7 +280,22 @@ __global__ void __launch_bounds__(32 * kWarps, TDB_HIT_MINB) hit_kernel(HitArgs 
                     if (h < row_pmin(r, f0)) live &= ~(1u << r);
             }
         }
-        if (__any_sync(0xffffffffu, live != 0)) {
+        // rows whose one-way margin clears the sub-tile's bounding sphere: every
+        // face of it is culled one-way (the object-level kappa_max bounds the
+        // row's; the slack covers the heights' rounding)
+        unsigned bc = 0;
+        {
+            const double2* sp = reinterpret_cast<const double2*>(a.Bsph + f0 / kHitGroup);
+            const double2 c01 = __ldg(sp), c2r = __ldg(sp + 1);
+            const double reach = c2r.y * (1.0 + 1e-9) + tau_blk + 1e-12 * (fabs(c01.x) + fabs(c01.y) + fabs(c2r.x));
+#pragma unroll
+            for (int r = 0; r < kRows; ++r) {
+                const double t = fma(an[r][0], c01.x, fma(an[r][1], c01.y, fma(an[r][2], c2r.x, -ac[r])));
+                const double rr = reach + 1e-12 * fabs(ac[r]);
+                bc |= (t > rr || t < -rr) ? 1u << r : 0u;
+            }
+        }
+        if (__any_sync(0xffffffffu, (live & ~bc) != 0)) {
             const float4* fb = smf[st];
             const int* degw = reinterpret_cast<const int*>(sb + HS_DEG * kSBH) + 1;  // high words
 #pragma unroll 1
@@ -303,7 +320,7 @@ __global__ void __launch_bounds__(32 * kWarps, TDB_HIT_MINB) hit_kernel(HitArgs 
                 unsigned need = 0;
 #pragma unroll
                 for (int r = 0; r < kRows; ++r) need |= sep[r] ? 0u : 1u << r;
-                need &= live;
+                need &= live & ~bc;
                 while (need) {  // rare: FP64 plane test, second plane, exact predicate
                     const int r = __ffs(need) - 1;
                     need &= need - 1;
@@ -430,6 +447,7 @@ void run_intersects_batch(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t
         CK(cudaMemcpyAsync(Bstats_copy, B.stats, kObjStats * sizeof(double), cudaMemcpyHostToDevice, st));
         Bstats = Bstats_copy;
     }
+    geom_hit_spheres(B, st);  // B's sub-tile spheres, once per store
     EventPair& evs = thread_events();
     cudaEvent_t e0 = evs.e[0], e1 = evs.e[1], e2 = evs.e[2];
     double* caabb = nullptr;
@@ -447,7 +465,7 @@ void run_intersects_batch(const Ctx& cx, const ASel& sel, const Geom& B, uint8_t
                                                                   n_chunks, chunk, sel.obj0, A.d_obj_stats, Bstats,
                                                                   objhit, nex, caabb ? A.d_tile_aabb : nullptr,
                                                                   caabb, nlog, B.fplanes, B.origin[0],
-                                                                  B.origin[1], B.origin[2], rb});
+                                                                  B.origin[1], B.origin[2], rb, B.d_hsph});
     CK(cudaGetLastError());
     CK(cudaEventRecord(e1, st));
     thread_local std::vector<unsigned long long> hres;

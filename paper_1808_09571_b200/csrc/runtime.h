@@ -86,6 +86,8 @@ struct Geom {
     mutable double* bedges = nullptr;
     mutable std::vector<uint64_t> h_bseoff;  // per group of kBSuper faces: first entry
     mutable uint64_t* d_bseoff = nullptr;     // device copy
+    // intersects (as B): bounding sphere of each kHitGroup faces (geom_hit_spheres)
+    mutable double4* d_hsph = nullptr;
     std::shared_ptr<std::mutex> fmu = std::make_shared<std::mutex>();
 };
 
@@ -98,6 +100,8 @@ void geom_super_tiles(const Geom& g, cudaStream_t st);
 void geom_super_bedges(const Geom& g, cudaStream_t st);
 // B's super-block edge lists, once (thread-safe)
 void geom_bedges(const Geom& g, cudaStream_t st);
+// B's per-kHitGroup-faces bounding spheres for the intersects block cull, once
+void geom_hit_spheres(const Geom& g, cudaStream_t st);
 
 // tri9: 9 doubles per face (AoS), on the host unless tri9_on_device
 void geom_build(Geom* g, const double* tri9, uint64_t n, const uint64_t* host_off, uint64_t n_obj,

@@ -498,6 +498,66 @@ void geom_edge_tiles(const Geom& g, cudaStream_t st) {
     g.atiles_built = true;
 }
 
+namespace {
+// Bounding sphere of each group of `group` consecutive faces (all faces,
+// degenerate ones included): box centre, max vertex distance rounded up.
+__global__ void group_sphere_kernel(const double* __restrict__ planes, uint64_t n, uint64_t n_pad, int group,
+                                    double4* __restrict__ out) {
+    __shared__ double red[6][128];
+    const int t = threadIdx.x;
+    const uint64_t g0 = (uint64_t)blockIdx.x * group;
+    double lo[3] = {pos_inf_h_d(), pos_inf_h_d(), pos_inf_h_d()}, hi[3] = {-lo[0], -lo[0], -lo[0]};
+    for (int i = t; i < group; i += blockDim.x) {
+        const uint64_t f = g0 + i;
+        if (f >= n) break;
+        for (int k = 0; k < 9; ++k) {
+            const double x = planes[(uint64_t)(F_V + k) * n_pad + f];
+            lo[k % 3] = fmin(lo[k % 3], x), hi[k % 3] = fmax(hi[k % 3], x);
+        }
+    }
+    for (int c = 0; c < 3; ++c) red[c][t] = lo[c], red[3 + c][t] = hi[c];
+    __syncthreads();
+    for (int w = 64; w > 0; w >>= 1) {
+        if (t < w)
+            for (int c = 0; c < 3; ++c)
+                red[c][t] = fmin(red[c][t], red[c][t + w]), red[3 + c][t] = fmax(red[3 + c][t], red[3 + c][t + w]);
+        __syncthreads();
+    }
+    const double cx = 0.5 * (red[0][0] + red[3][0]), cy = 0.5 * (red[1][0] + red[4][0]), cz = 0.5 * (red[2][0] + red[5][0]);
+    __syncthreads();
+    double r = 0.0;
+    for (int i = t; i < group; i += blockDim.x) {
+        const uint64_t f = g0 + i;
+        if (f >= n) break;
+        for (int k = 0; k < 3; ++k) {
+            const double dx = planes[(uint64_t)(F_V + 3 * k) * n_pad + f] - cx;
+            const double dy = planes[(uint64_t)(F_V + 3 * k + 1) * n_pad + f] - cy;
+            const double dz = planes[(uint64_t)(F_V + 3 * k + 2) * n_pad + f] - cz;
+            r = fmax(r, sqrt(dx * dx + dy * dy + dz * dz));
+        }
+    }
+    red[0][t] = r;
+    __syncthreads();
+    for (int w = 64; w > 0; w >>= 1) {
+        if (t < w) red[0][t] = fmax(red[0][t], red[0][t + w]);
+        __syncthreads();
+    }
+    if (t == 0) out[blockIdx.x] = make_double4(cx, cy, cz, red[0][0] * (1.0 + 1e-12));
+}
+}  // namespace
+
+void geom_hit_spheres(const Geom& g, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(*g.fmu);
+    if (g.d_hsph || g.n == 0) return;
+    const uint64_t ng = (g.n + kHitGroup - 1) / kHitGroup;
+    double4* out = nullptr;
+    CK(cudaMallocAsync(&out, ng * sizeof(double4), st));
+    group_sphere_kernel<<<(unsigned)ng, 128, 0, st>>>(g.planes, g.n, g.n_pad, kHitGroup, out);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    g.d_hsph = out;
+}
+
 void geom_bedges(const Geom& g, cudaStream_t st) {
     std::lock_guard<std::mutex> lk(*g.fmu);
     if (!g.h_bseoff.empty()) return;
@@ -545,6 +605,8 @@ void geom_release(Geom* g, cudaStream_t st) {
     g->aedges = g->averts = nullptr;
     cudaFreeAsync(g->bedges, st);
     cudaFreeAsync(g->d_bseoff, st);
+    cudaFreeAsync(g->d_hsph, st);
+    g->d_hsph = nullptr;
     g->bedges = nullptr;
     g->d_bseoff = nullptr;
     g->h_bseoff.clear();

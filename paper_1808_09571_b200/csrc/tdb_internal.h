@@ -123,5 +123,9 @@ constexpr double kCullOne = 2.5e-2;
 constexpr double kCullTwo = 1.01e-12;
 constexpr double kApart = 5e-2;
 constexpr double kCullAbs = 1e-13;
+// hit_kernel's B sub-tile (and its bounding sphere: csrc/store.cu
+// geom_hit_spheres); a row whose one-way margin clears the whole sphere skips
+// the sub-tile (every face of it would be culled one-way).
+constexpr int kHitGroup = 128;
 
 }  // namespace tdb
