@@ -147,8 +147,8 @@ int tdb_geom_set_has_degenerate_faces(tdb_mesh g, const uint8_t* flags, uint64_t
 /* The distance filter's shared candidates (built on first use,
  * or here): as the B side, totals over the store's 64-face feature blocks of
  * non-degenerate faces, distinct vertices and distinct edges; as the A side,
- * the totals of the distinct edges and vertices of its super-tiles (128
- * tiles of 128 faces); super_edges: the distinct edges per 1,024 faces (B's
+ * the totals of the distinct edges and vertices of its super-tiles (256
+ * tiles of 128 faces); super_edges: the distinct edges per 8,192 faces (B's
  * edge lists when a call's chunk allows them). No
  * reference counterpart (instrumentation for the roofline accounting). */
 int tdb_geom_feature_counts(tdb_mesh g, uint64_t* faces, uint64_t* vertices, uint64_t* edges,

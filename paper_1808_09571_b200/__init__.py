@@ -262,7 +262,7 @@ class _Geom:
         side, total non-degenerate faces, distinct vertices and distinct edges
         over the store's 64-face blocks; as the A side, the distinct edges and
         vertices of its super-tiles (tile_edges, tile_vertices); the distinct
-        edges per 1,024 faces (super_edges, B's lists in large calls)."""
+        edges per 8,192 faces (super_edges, B's lists in large calls)."""
         f, v, e, te, tv, se = (ct.c_uint64() for _ in range(6))
         _check(lib().tdb_geom_feature_counts(self._h, ct.byref(f), ct.byref(v), ct.byref(e), ct.byref(te),
                                              ct.byref(tv), ct.byref(se)))

@@ -6,7 +6,7 @@
 // Deduplicating within a super-tile instead of within a tile shares the
 // edges between tiles too: a 1024-wide terrain's 128-face tiles are strips
 // of one grid row, 2.0 distinct edges per face each, while a super-tile of
-// 128 tiles (8 rows) has 1.56. The edge kernel attributes an entry's
+// 256 tiles (16 rows) has 1.53. The edge kernel attributes an entry's
 // candidate to both of its tiles' items.
 //
 // Build (once per store, on the device): corner keys (super-tile, x, y, z

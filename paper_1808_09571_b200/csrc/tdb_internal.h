@@ -77,12 +77,18 @@ constexpr int kFBCap = kFB * (kFP + kFV + 3 * kVR + 3 * kER);  // doubles per bl
 // << 32, equal when one), 0. The edge kernel runs kEdgeAPT x kTile
 // consecutive entries per CTA.
 enum : int { AR_Q = 0, AR_E = 3, AR_L = 6, AR_IL = 7, AR_TILE = 8, kAER = 10 };
-constexpr uint64_t kSuperTile = 128;
+#ifndef TDB_SUPERTILE
+#define TDB_SUPERTILE 256
+#endif
+constexpr uint64_t kSuperTile = TDB_SUPERTILE;
 // B side of the edge/edge candidates when the chunk allows (FULL mode, chunk
-// % kBSuper == 0): B's distinct edges per kBSuper consecutive faces (the same
-// builder, csrc/atiles.cu), streamed by edge_kernel kEdgePiece entries per
-// TMA stage.
-constexpr uint64_t kBSuper = 1024;
+// % kBSuper == 0, i.e. full 8,192-face chunks): B's distinct edges per kBSuper
+// consecutive faces (the same builder, csrc/atiles.cu), streamed by
+// edge_kernel kEdgePiece entries per TMA stage.
+#ifndef TDB_BSUPER
+#define TDB_BSUPER 8192
+#endif
+constexpr uint64_t kBSuper = TDB_BSUPER;
 constexpr int kEdgePiece = 256;
 // Vertices: likewise per super-tile, kAVR doubles = x y z, two tiles (u32 |
 // u32 << 32).

@@ -140,7 +140,7 @@ def test_feature_counts():
                  "super_edges": 3000}
 
 
-def _expected_super_edges(m, group=1024):
+def _expected_super_edges(m, group=8192):
     """B's distinct edges per `group` consecutive faces of a one-object
     store, one entry per two faces sharing one (csrc/atiles.cu)."""
     total = 0
@@ -154,16 +154,16 @@ def _expected_super_edges(m, group=1024):
     return total
 
 
-def _expected_counts(m, obj_faces):
+def _expected_counts(m, obj_faces, tiles_per_group=256):
     """Numpy restatement of the A-side lists (csrc/atiles.cu): per super-tile
-    (128 tiles of 128 faces of one object) the distinct edges, one entry per
+    (256 tiles of 128 faces of one object) the distinct edges, one entry per
     two faces sharing one; the distinct vertices, one entry per two of the
     tiles having one. Meshes here have no degenerate faces."""
     edges = verts = 0
     f0 = 0
     for nf in obj_faces:
-        for s0 in range(0, nf, 128 * 128):
-            s1 = min(nf, s0 + 128 * 128)
+        for s0 in range(0, nf, 128 * tiles_per_group):
+            s1 = min(nf, s0 + 128 * tiles_per_group)
             v = np.ascontiguousarray(m[f0 + s0:f0 + s1]).reshape(-1, 3)
             _, vid = np.unique(v.view(np.dtype((np.void, 24))).ravel(), return_inverse=True)
             vid = vid.reshape(-1, 3)
