@@ -181,6 +181,31 @@ __global__ void ventry_kernel(const double* __restrict__ planes, uint64_t n_pad,
     atomicAdd(st_count + tile_st[ta], 1ull);
 }
 
+// A-side entries reordered by their first tile, so that any tile range is
+// (almost) a contiguous range: keys, per-tile counts, per-super-tile span of
+// (second tile - first tile).
+__global__ void tkey_kernel(const double* __restrict__ rec, uint64_t n, int stride, int field,
+                            const uint32_t* __restrict__ tile_st, uint32_t* __restrict__ key,
+                            uint32_t* __restrict__ idx, unsigned long long* __restrict__ tcount,
+                            unsigned* __restrict__ span) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    const unsigned long long t = (unsigned long long)__double_as_longlong(rec[e * stride + field]);
+    const uint32_t ta = (uint32_t)t, tb = (uint32_t)(t >> 32);
+    key[e] = ta;
+    idx[e] = (uint32_t)e;
+    atomicAdd(tcount + ta, 1ull);
+    atomicMax(span + tile_st[ta], tb - ta);
+}
+
+__global__ void rgather_kernel(const double* __restrict__ in, const uint32_t* __restrict__ idx, uint64_t n,
+                               int stride, double* __restrict__ out) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * stride) return;
+    const uint64_t e = i / stride, k = i - e * stride;
+    out[i] = in[(uint64_t)idx[e] * stride + k];
+}
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;
@@ -345,14 +370,51 @@ void build_super(const Geom& g, uint64_t group_tiles, bool with_vertices, cudaSt
 
 }  // namespace
 
+// Reorders n records (stride doubles, tiles in `field`) by their first tile;
+// returns per-tile offsets (n_tiles + 1) and per-super-tile spans.
+static double* by_tile(double* rec, uint64_t n, int stride, int field, const std::vector<uint32_t>& tile_st,
+                       uint32_t n_st, cudaStream_t st, std::vector<uint64_t>& toff, std::vector<uint32_t>& span) {
+    const uint64_t nt = tile_st.size();
+    toff.assign(nt + 1, 0);
+    span.assign(n_st, 0);
+    if (n == 0) return rec;
+    DevBuf<uint32_t> d_tst(nt, st), key(n, st), key2(n, st), idx(n, st), idx2(n, st);
+    DevBuf<unsigned long long> cnt(nt, st);
+    DevBuf<unsigned> d_span(n_st, st);
+    CK(cudaMemcpyAsync(d_tst.p, tile_st.data(), nt * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(cnt.p, 0, nt * sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(d_span.p, 0, std::max<uint32_t>(n_st, 1) * sizeof(unsigned), st));
+    tkey_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(rec, n, stride, field, d_tst.p, key.p, idx.p, cnt.p,
+                                                             d_span.p);
+    CK(cudaGetLastError());
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, key2.p, idx.p, idx2.p, (int)n, 0, 32, st));
+    DevBuf<unsigned char> temp(tb, st);
+    CK(cub::DeviceRadixSort::SortPairs(temp.p, tb, key.p, key2.p, idx.p, idx2.p, (int)n, 0, 32, st));
+    double* out = nullptr;
+    CK(cudaMallocAsync(&out, n * stride * sizeof(double), st));
+    rgather_kernel<<<(unsigned)((n * stride + 255) / 256), 256, 0, st>>>(rec, idx2.p, n, stride, out);
+    CK(cudaGetLastError());
+    CK(cudaFreeAsync(rec, st));
+    std::vector<unsigned long long> c(nt);
+    std::vector<unsigned> sp(n_st);
+    CK(cudaMemcpyAsync(c.data(), cnt.p, nt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(sp.data(), d_span.p, n_st * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (uint64_t t = 0; t < nt; ++t) toff[t + 1] = toff[t] + c[t];
+    span.assign(sp.begin(), sp.end());
+    return out;
+}
+
 void geom_super_tiles(const Geom& g, cudaStream_t st) {
     SuperLists L;
     build_super(g, kSuperTile, true, st, L);
+    const uint32_t n_st = (uint32_t)(L.eoff.size() - 1);
+    g.aedges = by_tile(L.edges, L.eoff.back(), kAER, AR_TILE, L.tile_grp, n_st, st, g.h_tile_eoff, g.h_st_espan);
+    g.averts = by_tile(L.verts, L.voff.back(), kAVR, 3, L.tile_grp, n_st, st, g.h_tile_voff, g.h_st_vspan);
     g.h_tile_st = std::move(L.tile_grp);
-    g.h_steoff = std::move(L.eoff);
-    g.h_stvoff = std::move(L.voff);
-    g.aedges = L.edges;
-    g.averts = L.verts;
+    g.h_st_tile0.assign(n_st + 1, (uint64_t)g.h_tile_st.size());
+    for (uint64_t t = g.h_tile_st.size(); t-- > 0;) g.h_st_tile0[g.h_tile_st[t]] = t;
 }
 
 void geom_super_bedges(const Geom& g, cudaStream_t st) {

@@ -405,8 +405,8 @@ int tdb_geom_feature_counts(tdb_mesh g, uint64_t* faces, uint64_t* vertices, uin
         if (edges) *edges = t[2];
         if (tile_edges || tile_vertices) {
             tdb::geom_edge_tiles(g->g, st);
-            if (tile_edges) *tile_edges = g->g.h_steoff.empty() ? 0 : g->g.h_steoff.back();
-            if (tile_vertices) *tile_vertices = g->g.h_stvoff.empty() ? 0 : g->g.h_stvoff.back();
+            if (tile_edges) *tile_edges = g->g.h_tile_eoff.empty() ? 0 : g->g.h_tile_eoff.back();
+            if (tile_vertices) *tile_vertices = g->g.h_tile_voff.empty() ? 0 : g->g.h_tile_voff.back();
         }
         if (super_edges) {
             tdb::geom_bedges(g->g, st);

@@ -924,8 +924,12 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
     } else {
         filter_kernel<false><<<(unsigned)n_items, kTile, smem, st>>>(da);
         CK(cudaGetLastError());
-        const uint64_t st0 = A.h_tile_st[sel.tile0], st1 = A.h_tile_st[sel.tile1 - 1] + 1;
-        const uint64_t v_lo = A.h_stvoff[st0], v_hi = A.h_stvoff[st1];
+        // entries are ordered by their first tile: those of tiles [tile0, tile1)
+        // lie in [first tile >= tile0 - span, first tile < tile1), span = the
+        // largest (second - first tile) of tile0's super-tile
+        const uint64_t st0 = A.h_tile_st[sel.tile0], t_st = A.h_st_tile0[st0];
+        auto lo_tile = [&](uint32_t span) { return std::max<uint64_t>(t_st, sel.tile0 >= span ? sel.tile0 - span : 0); };
+        const uint64_t v_lo = A.h_tile_voff[lo_tile(A.h_st_vspan[st0])], v_hi = A.h_tile_voff[sel.tile1];
         const uint64_t n_vt = (v_hi - v_lo + kTile * kVertAPT - 1) / (kTile * kVertAPT);
         if (n_vt) {
             vertex_kernel<<<(unsigned)(n_vt * n_chunks), kTile, smem_f, st>>>(
@@ -935,9 +939,9 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
             CK(cudaGetLastError());
             ++launches;
         }
-        // the super-tiles holding the selection's tiles (partial ones whole:
-        // edge_kernel attributes only to tiles inside the selection)
-        const uint64_t e_lo = A.h_steoff[st0], e_hi = A.h_steoff[st1];
+        // (entries reaching back into tiles before tile0 are evaluated too;
+        // the kernels attribute only to tiles inside the selection)
+        const uint64_t e_lo = A.h_tile_eoff[lo_tile(A.h_st_espan[st0])], e_hi = A.h_tile_eoff[sel.tile1];
         const uint64_t n_et = (e_hi - e_lo + kTile * kEdgeAPT - 1) / (kTile * kEdgeAPT);
         if (n_et) {
             // B's edges per kBSuper faces when the chunk allows (fewer edge pairs), else per feature block

@@ -76,11 +76,12 @@ struct Geom {
     mutable uint32_t fblock_max_f = 0;  //   ... by its faces
     // A side (tdb_internal.h kAER, kAVR): built on first use as the A side of
     // a distance filter (geom_edge_tiles)
-    mutable double* aedges = nullptr;        // super-tiles' distinct edges
+    mutable double* aedges = nullptr;        // super-tiles' distinct edges, ordered by first tile
+    mutable double* averts = nullptr;        // super-tiles' distinct vertices, ordered by first tile
     mutable std::vector<uint32_t> h_tile_st; // tile -> super-tile
-    mutable std::vector<uint64_t> h_steoff;  // n_super_tiles + 1: first entry of each
-    mutable double* averts = nullptr;        // super-tiles' distinct vertices
-    mutable std::vector<uint64_t> h_stvoff;  // n_super_tiles + 1: first entry of each
+    mutable std::vector<uint64_t> h_st_tile0;  // super-tile -> its first tile
+    mutable std::vector<uint64_t> h_tile_eoff, h_tile_voff;  // n_tiles + 1: first entry with that first tile
+    mutable std::vector<uint32_t> h_st_espan, h_st_vspan;    // per super-tile: max (second - first tile)
     mutable bool atiles_built = false;
     // B side: distinct edges per kBSuper faces (geom_super_bedges)
     mutable double* bedges = nullptr;

@@ -610,8 +610,8 @@ void geom_release(Geom* g, cudaStream_t st) {
     g->bedges = nullptr;
     g->d_bseoff = nullptr;
     g->h_bseoff.clear();
-    g->h_steoff.clear();
-    g->h_stvoff.clear();
+    g->h_tile_eoff.clear();
+    g->h_tile_voff.clear();
     g->h_tile_st.clear();
     g->atiles_built = false;
     g->fblocks = nullptr;
