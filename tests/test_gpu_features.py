@@ -190,3 +190,18 @@ def test_super_tile_counts_match_restatement():
     off = np.arange(6, dtype=np.uint64) * len(recs[0])
     c = T.Table(tab, off).feature_counts()
     assert (c["tile_edges"], c["tile_vertices"]) == _expected_counts(tab, [len(r) for r in recs])
+
+
+def test_row_selections_cutting_super_tiles():
+    """A terrain of 327,680 faces (160 rows of 2,048 faces, 16 tiles per row:
+    its super-tiles of 256 tiles are 16 rows, and an edge's two tiles are up
+    to 16 tiles apart) against a small body: selections that start and end
+    inside super-tiles read their tiles' entries plus the span before them,
+    and must give the oracle's answer; so must the two-way shard split."""
+    a = T.terrain(1024, 160, 20.0, 3)
+    b = np.ascontiguousarray(T.ore_body(2000) * 0.05 + np.tile([500.0, 40.0, -30.0], 3))
+    ma, mb = T.Mesh(a), T.Mesh(b)
+    for r0, r1 in [(33_000, 70_001), (32_768, 65_536), (100, 40_000), (200_000, 327_680), (65_535, 65_537)]:
+        r = T.mesh_mesh_distance(ma, mb, rows=(r0, r1))
+        d, p, found, *_ = O.mesh_mesh_distance(a, b, rows=(r0, r1, 1))
+        assert found and bits(r.distance) == bits(d) and r.pair_index == p, (r0, r1, r, d, p)
