@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MIN
 }
 
 #ifndef TDB_EDGE_MINB
-#define TDB_EDGE_MINB 4
+#define TDB_EDGE_MINB 3
 #endif
 #ifndef TDB_UEE
 #define TDB_UEE 4
@@ -272,7 +272,7 @@ struct EdgeArgs {
 // [row_lo, row_hi) contributes all its edges: a lower item minimum only
 // widens the band (check_kernel), never drops a pair.
 #ifndef TDB_EDGE_APT
-#define TDB_EDGE_APT 2
+#define TDB_EDGE_APT 3
 #endif
 constexpr int kEdgeAPT = TDB_EDGE_APT;  // A edges per thread (a B edge loaded once feeds kEdgeAPT pairs)
 
