@@ -97,3 +97,23 @@ def test_literal_over_mesh_column_uses_each_records_flag():
         for o, mo in enumerate(objs):
             rd, rf = O.ref_queries_mesh_distance_flag(lit[None, :], mo, flags[o], points=is_pt)
             assert bits(d[o]) == bits(rd[0]) and f[o] == rf[0], (o, flags[o], d[o], rd, f[o], rf)
+
+
+@pytest.mark.parametrize("mesh", ["soup", "sphere"])
+def test_fused_query_paths_follow_the_flag(mesh):
+    """40,000 queries against one small mesh: the fused kernel (the whole mesh
+    in one chunk, q_fused_kernel), flag cleared and set, on a soup with
+    degenerate faces and on a clean sphere; bit-exact against the reference."""
+    rng = np.random.default_rng(77)
+    m = _degenerate_soup(rng, 500) if mesh == "soup" else T.unit_sphere(1000)
+    pts = rng.uniform(-1.2, 1.2, (40_000, 3))
+    segs = np.concatenate([pts, pts + rng.normal(scale=0.3, size=pts.shape)], 1)
+    segs[::7, 3:6] = segs[::7, 0:3]
+    for flag in (False, True):
+        dm = T.Mesh(m).set_has_degenerate_faces(flag)
+        for q, is_pt in ((pts, True), (segs, False)):
+            d, f = T.points_mesh_distance(q, dm) if is_pt else T.segments_mesh_distance(q, dm)
+            rd, rf = O.ref_queries_mesh_distance_flag(q, m, flag, points=is_pt)
+            bad = np.flatnonzero((bits(d) != bits(rd)) | (f != rf))
+            assert len(bad) == 0, (mesh, flag, is_pt, len(bad), q[bad[:3]], d[bad[:3]], rd[bad[:3]], f[bad[:3]],
+                                   rf[bad[:3]])
