@@ -247,7 +247,8 @@ void build_super(const Geom& g, uint64_t group_tiles, bool with_vertices, cudaSt
     L.eoff.assign(n_st + 1, 0);
     L.voff.assign(n_st + 1, 0);
     if (nt == 0 || m == 0) return;
-    if (m >= 0xffffffffull) throw std::invalid_argument("edge super-tiles: more than 2^32 face corners");
+    if (m >= 0x7fffffffull)  // cub sorts / scans take int counts
+        throw std::invalid_argument("shared-candidate lists: more than 2^31 face corners (715M faces) in one store");
     DevBuf<uint32_t> d_tile_st(nt, st), face_tile(n, st);
     CK(cudaMemcpyAsync(d_tile_st.p, tile_st.data(), nt * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
     face_tile_kernel<<<(unsigned)nt, 128, 0, st>>>(g.d_tiles, nt, face_tile.p);
