@@ -121,13 +121,19 @@ __global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MIN
         mbar_fence_init();
     }
     __syncthreads();
+    // per stage, beside the block's records: its header and bounds, staged by
+    // the same TMA transaction (the consumers then never wait on global loads)
+    __shared__ alignas(16) uint4 shdr[2];
+    __shared__ alignas(16) double4 ssph[2];
     auto issue = [&](int s) {
         const int st = s & 1;
         const uint4 hb = __ldg(&a.Bfhdr[blk0 + s]);
         // CULL: the whole block; FULL: [vertices of faces | distinct vertices]
         const uint32_t off = kEdges ? 0u : kFP * hb.x;
         const uint32_t bytes = (kEdges ? hb.w : kFV * hb.x + kVR * hb.y) * (uint32_t)sizeof(double);
-        mbar_expect_tx(&bar[st], bytes);
+        mbar_expect_tx(&bar[st], bytes + (uint32_t)sizeof(uint4) + (kEdges ? 0u : (uint32_t)sizeof(double4)));
+        bulk_g2s(&shdr[st], &a.Bfhdr[blk0 + s], sizeof(uint4), &bar[st]);
+        if (!kEdges) bulk_g2s(&ssph[st], a.Bsph + blk0 + s, sizeof(double4), &bar[st]);
         if (bytes) bulk_g2s(dsm + (size_t)st * a.stage, a.Bfb + (blk0 + s) * (uint64_t)kFBCap + off, bytes, &bar[st]);
     };
     if (threadIdx.x == 0) {
@@ -143,8 +149,8 @@ __global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MIN
 #pragma unroll 1
     for (int s = 0; s < nblk; ++s) {
         const int st = s & 1;
-        const uint4 h = __ldg(&a.Bfhdr[blk0 + s]);
         mbar_wait(&bar[st], (uint32_t)((s >> 1) & 1));
+        const uint4 h = shdr[st];
         const double* base = dsm + (size_t)st * a.stage;
         const double* fp = base;                                // face planes (CULL only)
         const double* fv = kEdges ? base + kFP * h.x : base;    // vertices of faces
@@ -183,11 +189,9 @@ __global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MIN
         // heights below, so every face would test "no straddle" anyway)
         bool maybe = true;
         if (!kEdges) {
-            const double2* sp2 = reinterpret_cast<const double2*>(a.Bsph + blk0 + s);
-            const double2 c01 = __ldg(sp2), c2r = __ldg(sp2 + 1);
-            const double t = fabs(fma(A.n[0], c01.x, fma(A.n[1], c01.y, fma(A.n[2], c2r.x, -cA))));
-            maybe = !(t > c2r.y * (1.0 + 1e-9) +
-                              1e-9 * (fabs(c01.x) + fabs(c01.y) + fabs(c2r.x) + fabs(cA) + c2r.y));
+            const double4 sp = ssph[st];
+            const double t = fabs(fma(A.n[0], sp.x, fma(A.n[1], sp.y, fma(A.n[2], sp.z, -cA))));
+            maybe = !(t > sp.w * (1.0 + 1e-9) + 1e-9 * (fabs(sp.x) + fabs(sp.y) + fabs(sp.z) + fabs(cA) + sp.w));
         }
 #pragma unroll kUF
         for (int j = 0; j < (maybe ? (int)h.x : 0); ++j) {
