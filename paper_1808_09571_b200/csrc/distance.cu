@@ -128,13 +128,14 @@ __global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MIN
     auto issue = [&](int s) {
         const int st = s & 1;
         const uint4 hb = __ldg(&a.Bfhdr[blk0 + s]);
-        // CULL: the whole block; FULL: [vertices of faces | distinct vertices]
-        const uint32_t off = kEdges ? 0u : kFP * hb.x;
-        const uint32_t bytes = (kEdges ? hb.w : kFV * hb.x + kVR * hb.y) * (uint32_t)sizeof(double);
+        // CULL: the whole block; FULL: [face planes | vertices of faces |
+        // distinct vertices] (the planes for the rare straddling faces: read
+        // from L2 they stalled the warp, and the CTA at its barrier)
+        const uint32_t bytes = (kEdges ? hb.w : (kFP + kFV) * hb.x + kVR * hb.y) * (uint32_t)sizeof(double);
         mbar_expect_tx(&bar[st], bytes + (uint32_t)sizeof(uint4) + (kEdges ? 0u : (uint32_t)sizeof(double4)));
         bulk_g2s(&shdr[st], &a.Bfhdr[blk0 + s], sizeof(uint4), &bar[st]);
         if (!kEdges) bulk_g2s(&ssph[st], a.Bsph + blk0 + s, sizeof(double4), &bar[st]);
-        if (bytes) bulk_g2s(dsm + (size_t)st * a.stage, a.Bfb + (blk0 + s) * (uint64_t)kFBCap + off, bytes, &bar[st]);
+        if (bytes) bulk_g2s(dsm + (size_t)st * a.stage, a.Bfb + (blk0 + s) * (uint64_t)kFBCap, bytes, &bar[st]);
     };
     if (threadIdx.x == 0) {
         issue(0);
@@ -152,8 +153,8 @@ __global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MIN
         mbar_wait(&bar[st], (uint32_t)((s >> 1) & 1));
         const uint4 h = shdr[st];
         const double* base = dsm + (size_t)st * a.stage;
-        const double* fp = base;                                // face planes (CULL only)
-        const double* fv = kEdges ? base + kFP * h.x : base;    // vertices of faces
+        const double* fp = base;                                // face planes
+        const double* fv = base + kFP * h.x;                    // vertices of faces
         const double* vr = fv + kFV * h.x;                      // distinct vertices
         const double* er = vr + kVR * h.y;                      // distinct edges (CULL only)
         // B's distinct vertices against A's face
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MIN
         // distinct vertices, and here only on the (rare) straddling faces, to
         // decide the piercing test: the face loop collects them in a mask
         // and stays branch-free.
-        const double* fpl = kEdges ? fp : a.Bfb + (blk0 + s) * (uint64_t)kFBCap;  // FULL: planes from L2
+        const double* fpl = fp;
         auto straddling = [&](int j) {  // A's vertices against face j (+ hmin in CULL), piercing test
             const double2* q = reinterpret_cast<const double2*>(fv + kFV * j);
             const double2 q0 = q[0], q1 = q[1], q4 = q[4];
@@ -904,7 +905,7 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
     // SMEM stages (128-byte aligned): a whole block (CULL), or only the part
     // each FULL kernel stages
     auto stage_of = [](uint32_t doubles) { return (std::max<uint32_t>(doubles, 2) + 15) & ~15u; };
-    const uint32_t stage = stage_of(cx.mode == TDB_MODE_CULL ? B.fblock_max : B.fblock_max_fv);
+    const uint32_t stage = stage_of(cx.mode == TDB_MODE_CULL ? B.fblock_max : B.fblock_max_pfv);
     const uint32_t stage_e = stage_of(B.fblock_max_e), stage_f = stage_of(B.fblock_max_f);
     const size_t smem = 2 * (size_t)stage * sizeof(double), smem_e = 2 * (size_t)stage_e * sizeof(double),
                  smem_f = 2 * (size_t)stage_f * sizeof(double);

@@ -71,7 +71,7 @@ struct Geom {
     mutable double4* d_fsph = nullptr;  // per block: bounding sphere of its live vertices (x, y, z, r)
     mutable uint64_t n_fblocks = 0;
     mutable uint32_t fblock_max = 0;    // max doubles used by one block
-    mutable uint32_t fblock_max_fv = 0; //   ... by its faces + vertices
+    mutable uint32_t fblock_max_pfv = 0;  //   ... by its face planes, face vertices and vertices
     mutable uint32_t fblock_max_e = 0;  //   ... by its edges
     mutable uint32_t fblock_max_f = 0;  //   ... by its faces
     // A side (tdb_internal.h kAER, kAVR): built on first use as the A side of

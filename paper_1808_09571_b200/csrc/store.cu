@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(kFB) fblock_kernel(const double* __restrict__ 
         const unsigned used = (unsigned)((kFP + kFV) * NF + kVR * NV + kER * NE);
         hdr[blk] = make_uint4((unsigned)NF, (unsigned)NV, (unsigned)NE, used);
         atomicMax(max_used, used);
-        atomicMax(max_used + 1, (unsigned)(kFV * NF + kVR * NV));  // filter_kernel (FULL)
+        atomicMax(max_used + 1, (unsigned)((kFP + kFV) * NF + kVR * NV));  // filter_kernel (FULL)
         atomicMax(max_used + 2, (unsigned)(kER * NE));             // edge_kernel
         atomicMax(max_used + 3, (unsigned)((kFP + kFV) * NF));     // vertex_kernel
     }
@@ -589,7 +589,7 @@ void geom_feature_blocks(const Geom& g, cudaStream_t st) {
     g.d_fsph = sph;
     g.n_fblocks = nb;
     g.fblock_max = used[0];
-    g.fblock_max_fv = used[1];
+    g.fblock_max_pfv = used[1];
     g.fblock_max_e = used[2];
     g.fblock_max_f = used[3];
 }
