@@ -211,13 +211,10 @@ __global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MIN
                 smask |= (unsigned long long)sb << j;
             }
         }
-        while (smask) {  // FULL, rare
+        while (smask) {  // FULL, rare (B's face from the staged records)
             const int j = __ffsll((long long)smask) - 1;
             smask &= smask - 1;
-            if (straddling(j)) {
-                const double idx = fv[kFV * j + FV_IDX];
-                pierce |= pierce_slow(a.Ap + row, a.An_pad, a.Bp + (uint64_t)__double_as_longlong(idx), a.Bn_pad);
-            }
+            if (straddling(j)) pierce |= pierce_t(a.Ap + row, a.An_pad, FaceRec{fv + kFV * j, fp + kFP * j});
         }
         // B's distinct edges against A's edges (CULL; FULL: edge_kernel)
 #pragma unroll kUE

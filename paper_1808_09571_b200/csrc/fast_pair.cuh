@@ -133,10 +133,22 @@ __device__ __forceinline__ bool edges_pierce(const double h[3], const double u[3
     return hit;
 }
 
+// B's face as the filter stages it (tdb_internal.h): its face-vertices record
+// (V at FV_V) and its face-planes record (N, U, W at FP_N, FP_U, FP_W), read
+// through the plane field numbers F_V / F_N / F_U / F_W.
+struct FaceRec {
+    const double* fv;
+    const double* fp;
+    __device__ __forceinline__ double operator()(int f) const {
+        return f < F_E ? fv[FV_V + f] : f < F_U ? fp[FP_N + f - F_N] : f < F_W ? fp[FP_U + f - F_U] : fp[FP_W + f - F_W];
+    }
+};
+
 // Out-of-line (rare) piercing test for a pair whose triangles both straddle
 // the other's plane; reloads both faces so the hot path keeps no state.
-static __device__ __noinline__ bool pierce_slow(const double* ap, uint64_t as, const double* bp, uint64_t bs) {
-    const FaceRef A{ap, as}, B{bp, bs};
+template <class PB>
+static __device__ __noinline__ bool pierce_t(const double* ap, uint64_t as, PB B) {
+    const FaceRef A{ap, as};
     double hb[3], ub[3], vb[3], ha[3], ua[3], va[3];
     const double a0x = A(F_V), a0y = A(F_V + 1), a0z = A(F_V + 2);
     const double b0x = B(F_V), b0y = B(F_V + 1), b0z = B(F_V + 2);
@@ -155,6 +167,10 @@ static __device__ __noinline__ bool pierce_slow(const double* ap, uint64_t as, c
         va[k] = dot3(Wb, qx, qy, qz);
     }
     return edges_pierce(hb, ub, vb) || edges_pierce(ha, ua, va);
+}
+
+static __device__ __forceinline__ bool pierce_slow(const double* ap, uint64_t as, const double* bp, uint64_t bs) {
+    return pierce_t(ap, as, FaceRef{bp, bs});
 }
 
 constexpr int kInfHi = 0x7ff00000;  // high word of +inf
