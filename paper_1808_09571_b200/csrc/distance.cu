@@ -315,10 +315,11 @@ __global__ void __launch_bounds__(kTile, TDB_EDGE_MINB) edge_kernel(EdgeArgs a) 
     } else {
         nunits = (int)((b1 - b0 + kFB - 1) / kFB);
     }
-    auto unit_count = [&](int s) -> int {
+    auto unit_count = [&](int s) -> int {  // the producer's view (the consumers read the staged header)
         return kSuper ? (int)min((uint64_t)kEdgePiece, se1 - se0 - (uint64_t)s * kEdgePiece)
                       : (int)__ldg(&a.Bfhdr[blk0 + s].z);
     };
+    __shared__ alignas(16) uint4 shdr[2];
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -335,7 +336,8 @@ __global__ void __launch_bounds__(kTile, TDB_EDGE_MINB) edge_kernel(EdgeArgs a) 
             const uint4 hb = __ldg(&a.Bfhdr[blk0 + s]);
             src = a.Bfb + (blk0 + s) * (uint64_t)kFBCap + (kFP + kFV) * hb.x + kVR * hb.y;
         }
-        mbar_expect_tx(&bar[st], bytes);
+        mbar_expect_tx(&bar[st], bytes + (kSuper ? 0u : (uint32_t)sizeof(uint4)));
+        if (!kSuper) bulk_g2s(&shdr[st], &a.Bfhdr[blk0 + s], sizeof(uint4), &bar[st]);
         if (bytes) bulk_g2s(dsm + (size_t)st * a.stage, src, bytes, &bar[st]);
     };
     if (threadIdx.x == 0) {
@@ -345,8 +347,8 @@ __global__ void __launch_bounds__(kTile, TDB_EDGE_MINB) edge_kernel(EdgeArgs a) 
 #pragma unroll 1
     for (int s = 0; s < nunits; ++s) {
         const int st = s & 1;
-        const int ne = unit_count(s);
         mbar_wait(&bar[st], (uint32_t)((s >> 1) & 1));
+        const int ne = kSuper ? unit_count(s) : (int)shdr[st].z;
         const double* er = dsm + (size_t)st * a.stage;
 #pragma unroll kUEE
         for (int j = 0; j < ne; ++j) {
@@ -408,6 +410,7 @@ constexpr int kVertAPT = TDB_VERT_APT;  // A vertices per thread (a B face loade
 __global__ void __launch_bounds__(kTile, TDB_VERT_MINB) vertex_kernel(VertArgs a) {
     extern __shared__ __align__(128) double dsm[];
     __shared__ alignas(8) uint64_t bar[2];
+    __shared__ alignas(16) uint4 shdr[2];
     const uint64_t vt = blockIdx.x / a.n_chunks, ch = blockIdx.x - vt * a.n_chunks;
     double ax[kVertAPT], ay[kVertAPT], az[kVertAPT];
     uint64_t tile[kVertAPT];
@@ -436,7 +439,8 @@ __global__ void __launch_bounds__(kTile, TDB_VERT_MINB) vertex_kernel(VertArgs a
     auto issue = [&](int s) {
         const int st = s & 1;
         const uint32_t bytes = (kFP + kFV) * __ldg(&a.Bfhdr[blk0 + s].x) * (uint32_t)sizeof(double);
-        mbar_expect_tx(&bar[st], bytes);
+        mbar_expect_tx(&bar[st], bytes + (uint32_t)sizeof(uint4));
+        bulk_g2s(&shdr[st], &a.Bfhdr[blk0 + s], sizeof(uint4), &bar[st]);  // the header rides along
         if (bytes) bulk_g2s(dsm + (size_t)st * a.stage, a.Bfb + (blk0 + s) * (uint64_t)kFBCap, bytes, &bar[st]);
     };
     if (threadIdx.x == 0) {
@@ -446,8 +450,8 @@ __global__ void __launch_bounds__(kTile, TDB_VERT_MINB) vertex_kernel(VertArgs a
 #pragma unroll 1
     for (int s = 0; s < nblk; ++s) {
         const int st = s & 1;
-        const int nf = (int)__ldg(&a.Bfhdr[blk0 + s].x);
         mbar_wait(&bar[st], (uint32_t)((s >> 1) & 1));
+        const int nf = (int)shdr[st].x;
         const double2* fp = reinterpret_cast<const double2*>(dsm + (size_t)st * a.stage);  // face planes
         const double2* fv = fp + (kFP / 2) * nf;                                           // vertices of faces
 #pragma unroll kUVF
