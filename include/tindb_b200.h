@@ -274,6 +274,11 @@ int tdb_pairs_intersects(const double* a9, const double* b9, uint64_t n, uint8_t
 /* Filter value d~^2 of the FP64 roofline path for aligned pairs (testing the
  * filter's error bound against the exact composition). */
 int tdb_pairs_filter(const double* a9, const double* b9, uint64_t n, double* d2_out);
+/* The candidate set FULL mode evaluates (FP64 vertex/face and piercing, FP32
+ * edge/edge relative to b's box centre o, as edge32_kernel does): d~^2 per
+ * pair, and o (3) and the half-diagonal rB of b's box in origin_rb_out[4]
+ * (testing eta_f32). */
+int tdb_pairs_filter_f32(const double* a9, const double* b9, uint64_t n, double* d2_out, double* origin_rb_out);
 
 /* ---- mesh generators ("mesh/geometry loader"; dataset.cpp:85-139). Return
  * the face count; write faces when out != NULL. Bit-identical to the

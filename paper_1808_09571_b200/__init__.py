@@ -130,6 +130,7 @@ _SIGS = [
     ("tdb_pairs_distance", ct.c_int, [_D, _D, ct.c_uint64, _D]),
     ("tdb_pairs_intersects", ct.c_int, [_D, _D, ct.c_uint64, _U8]),
     ("tdb_pairs_filter", ct.c_int, [_D, _D, ct.c_uint64, _D]),
+    ("tdb_pairs_filter_f32", ct.c_int, [_D, _D, ct.c_uint64, _D, _D]),
     ("tdb_gen_unit_sphere", ct.c_uint64, [ct.c_uint64, _D]),
     ("tdb_gen_ore_body", ct.c_uint64, [ct.c_uint64, _D]),
     ("tdb_gen_terrain", ct.c_uint64, [ct.c_uint32, ct.c_uint32, ct.c_double, ct.c_uint64, _D]),
@@ -498,6 +499,16 @@ def pairs_filter(a, b) -> np.ndarray:
     out = np.empty(len(a), np.float64)
     _check(lib().tdb_pairs_filter(_dp(a), _dp(b), len(a), _dp(out)))
     return out
+
+
+def pairs_filter_f32(a, b):
+    """FULL mode's candidate set for aligned pairs (FP64 vertex/face, FP32
+    edge/edge relative to b's box centre): (d~^2 per pair, origin, rB)."""
+    a, b = _f64(a), _f64(b)
+    out = np.empty(len(a), np.float64)
+    orb = np.empty(4, np.float64)
+    _check(lib().tdb_pairs_filter_f32(_dp(a), _dp(b), len(a), _dp(out), _dp(orb)))
+    return out, orb[:3].copy(), float(orb[3])
 
 
 def _qarr(q, width):

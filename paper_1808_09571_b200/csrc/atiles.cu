@@ -16,6 +16,7 @@
 // run of two). Ids are ordered by super-tile, so the entries of a super-tile
 // are contiguous: per-super-tile offsets select a call's tiles.
 #include <algorithm>
+#include <cmath>
 #include <vector>
 
 #include <cub/cub.cuh>
@@ -418,11 +419,40 @@ void geom_super_tiles(const Geom& g, cudaStream_t st) {
     for (uint64_t t = g.h_tile_st.size(); t-- > 0;) g.h_st_tile0[g.h_tile_st[t]] = t;
 }
 
+// FP64 entries (kAER) -> FP32 records (kBER) relative to o.
+__global__ void bedge_f32_kernel(const double* __restrict__ e, uint64_t n, double ox, double oy, double oz,
+                                 float4* __restrict__ out) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double* r = e + i * kAER;
+    out[2 * i] = make_float4((float)(r[AR_Q] - ox), (float)(r[AR_Q + 1] - oy), (float)(r[AR_Q + 2] - oz),
+                             (float)r[AR_E]);
+    out[2 * i + 1] = make_float4((float)r[AR_E + 1], (float)r[AR_E + 2], (float)r[AR_L], (float)r[AR_IL]);
+}
+
 void geom_super_bedges(const Geom& g, cudaStream_t st) {
     SuperLists L;
     build_super(g, kBSuper / kTile, false, st, L);
     g.h_bseoff = std::move(L.eoff);
-    g.bedges = L.edges;
+    const uint64_t n = g.h_bseoff.back();
+    // origin: B's box centre (its non-degenerate faces); every start point is
+    // within the half-diagonal of it
+    const double* s = g.stats;
+    const bool box = std::isfinite(s[0]) && std::isfinite(s[1]) && std::isfinite(s[2]) && std::isfinite(s[3]) &&
+                     std::isfinite(s[4]) && std::isfinite(s[5]);
+    double r2 = 0.0;
+    for (int k = 0; k < 3; ++k) {
+        g.bse_org[k] = box ? 0.5 * (s[k] + s[3 + k]) : 0.0;
+        r2 += box ? (s[3 + k] - s[k]) * (s[3 + k] - s[k]) : 0.0;
+    }
+    g.bse_rB = 0.5 * std::sqrt(r2) * (1.0 + 1e-12);
+    CK(cudaMallocAsync(&g.bedges, std::max<uint64_t>(n, 1) * 2 * sizeof(float4), st));
+    if (n) {
+        bedge_f32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(L.edges, n, g.bse_org[0], g.bse_org[1],
+                                                                       g.bse_org[2], g.bedges);
+        CK(cudaGetLastError());
+    }
+    CK(cudaFreeAsync(L.edges, st));
     CK(cudaMallocAsync(&g.d_bseoff, g.h_bseoff.size() * sizeof(uint64_t), st));
     CK(cudaMemcpyAsync(g.d_bseoff, g.h_bseoff.data(), g.h_bseoff.size() * sizeof(uint64_t), cudaMemcpyHostToDevice,
                        st));

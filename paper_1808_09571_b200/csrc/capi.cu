@@ -551,6 +551,29 @@ int tdb_pairs_filter(const double* a9, const double* b9, uint64_t n, double* d2)
     return rc;
 }
 
+int tdb_pairs_filter_f32(const double* a9, const double* b9, uint64_t n, double* d2, double* origin_rb) {
+    tdb_mesh a = nullptr, b = nullptr;
+    int rc = tdb_mesh_upload(a9, n, &a);
+    if (rc == TDB_OK) rc = tdb_mesh_upload(b9, n, &b);
+    if (rc == TDB_OK)
+        rc = guarded([&] {
+            need(origin_rb != nullptr, "null origin output");
+            const double* s = b->g.stats;  // as geom_super_bedges: B's box centre and half-diagonal
+            double r2 = 0.0;
+            for (int k = 0; k < 3; ++k) {
+                origin_rb[k] = 0.5 * (s[k] + s[3 + k]);
+                r2 += (s[3 + k] - s[k]) * (s[3 + k] - s[k]);
+            }
+            origin_rb[3] = 0.5 * std::sqrt(r2) * (1.0 + 1e-12);
+            tdb::run_pairs_filter(ctx(), a->g, b->g, d2, origin_rb);
+        });
+    const std::string err = t_err;
+    tdb_mesh_free(a);
+    tdb_mesh_free(b);
+    t_err = err;
+    return rc;
+}
+
 int tdb_query_face_result(int op, int kind, const double* q, const double* tri9, tdb_face_result* out) {
     return guarded([&] {
         need(q && tri9 && out, "null argument");

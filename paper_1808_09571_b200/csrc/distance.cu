@@ -260,9 +260,24 @@ struct EdgeArgs {
     uint64_t Bn, n_chunks, chunk, obj0;
     unsigned long long* itemmin;  // the filter's item minima (non-negative doubles as u64)
     unsigned long long* objmin;
-    const double* Bse;            // B's super-block edges (kSuper) and their per-group offsets
+    const float4* Bse;            // B's super-block edges (FP32 records, kBER) and their per-group offsets
     const uint64_t* Bse_off;
+    double ox, oy, oz;            // their origin
 };
+
+// An edge's minimum into the (tile, chunk) items of its tiles inside the
+// selection and into its object.
+__device__ __forceinline__ void edge_min_out(const EdgeArgs& a, uint64_t tile, uint64_t ch,
+                                             unsigned long long bits) {
+    const uint64_t t2[2] = {tile & 0xffffffffull, tile >> 32};  // the edge's tiles
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const uint64_t t = t2[q];
+        if ((q == 1 && t == t2[0]) || t < a.tile0 || t >= a.tile1) continue;  // outside the selection
+        atomicMin(a.itemmin + (t - a.tile0) * a.n_chunks + ch, bits);
+        atomicMin(a.objmin + (a.tiles[t].obj - a.obj0), bits);
+    }
+}
 
 // Edge/edge candidates of FULL mode: one A distinct edge per thread (kTile
 // consecutive entries of A's edge tiles per CTA) against every distinct edge
@@ -272,19 +287,16 @@ struct EdgeArgs {
 // item minimum is the minimum over its pairs of pair_d2 (up to the edge
 // direction of a shared edge). A tile partly outside
 // [row_lo, row_hi) contributes all its edges: a lower item minimum only
-// widens the band (check_kernel), never drops a pair.
+// widens the band (check_kernel), never drops a pair. This FP64 kernel runs
+// when the chunk is not a multiple of kBSuper; edge32_kernel otherwise.
 #ifndef TDB_EDGE_APT
 #define TDB_EDGE_APT 3
 #endif
 constexpr int kEdgeAPT = TDB_EDGE_APT;  // A edges per thread (a B edge loaded once feeds kEdgeAPT pairs)
 
-// kSuper: B's distinct edges per kBSuper faces (the chunk is a multiple of
-// kBSuper), streamed kEdgePiece entries per stage; else per 64-face block.
-template <bool kSuper>
 __global__ void __launch_bounds__(kTile, TDB_EDGE_MINB) edge_kernel(EdgeArgs a) {
     extern __shared__ __align__(128) double dsm[];
     __shared__ alignas(8) uint64_t bar[2];
-    constexpr int kStride = kSuper ? kAER : kER;  // doubles per staged B edge (P, E, |E|^2, 1/|E|^2 first)
     const uint64_t et = blockIdx.x / a.n_chunks, ch = blockIdx.x - et * a.n_chunks;
     double Q[kEdgeAPT][8];
     uint64_t tile[kEdgeAPT];
@@ -306,19 +318,7 @@ __global__ void __launch_bounds__(kTile, TDB_EDGE_MINB) edge_kernel(EdgeArgs a) 
 
     const uint64_t b0 = ch * a.chunk, b1 = min(a.Bn, b0 + a.chunk);
     const uint64_t blk0 = b0 / kFB;
-    uint64_t se0 = 0, se1 = 0;
-    int nunits;
-    if (kSuper) {
-        se0 = __ldg(a.Bse_off + b0 / kBSuper);
-        se1 = __ldg(a.Bse_off + (b1 + kBSuper - 1) / kBSuper);
-        nunits = (int)((se1 - se0 + kEdgePiece - 1) / kEdgePiece);
-    } else {
-        nunits = (int)((b1 - b0 + kFB - 1) / kFB);
-    }
-    auto unit_count = [&](int s) -> int {  // the producer's view (the consumers read the staged header)
-        return kSuper ? (int)min((uint64_t)kEdgePiece, se1 - se0 - (uint64_t)s * kEdgePiece)
-                      : (int)__ldg(&a.Bfhdr[blk0 + s].z);
-    };
+    const int nunits = (int)((b1 - b0 + kFB - 1) / kFB);
     __shared__ alignas(16) uint4 shdr[2];
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
@@ -328,16 +328,11 @@ __global__ void __launch_bounds__(kTile, TDB_EDGE_MINB) edge_kernel(EdgeArgs a) 
     __syncthreads();
     auto issue = [&](int s) {
         const int st = s & 1;
-        const uint32_t bytes = (uint32_t)(kStride * unit_count(s)) * (uint32_t)sizeof(double);
-        const double* src;
-        if (kSuper) {
-            src = a.Bse + (se0 + (uint64_t)s * kEdgePiece) * kAER;
-        } else {
-            const uint4 hb = __ldg(&a.Bfhdr[blk0 + s]);
-            src = a.Bfb + (blk0 + s) * (uint64_t)kFBCap + (kFP + kFV) * hb.x + kVR * hb.y;
-        }
-        mbar_expect_tx(&bar[st], bytes + (kSuper ? 0u : (uint32_t)sizeof(uint4)));
-        if (!kSuper) bulk_g2s(&shdr[st], &a.Bfhdr[blk0 + s], sizeof(uint4), &bar[st]);
+        const uint4 hb = __ldg(&a.Bfhdr[blk0 + s]);
+        const uint32_t bytes = (uint32_t)(kER * hb.z) * (uint32_t)sizeof(double);
+        const double* src = a.Bfb + (blk0 + s) * (uint64_t)kFBCap + (kFP + kFV) * hb.x + kVR * hb.y;
+        mbar_expect_tx(&bar[st], bytes + (uint32_t)sizeof(uint4));
+        bulk_g2s(&shdr[st], &a.Bfhdr[blk0 + s], sizeof(uint4), &bar[st]);
         if (bytes) bulk_g2s(dsm + (size_t)st * a.stage, src, bytes, &bar[st]);
     };
     if (threadIdx.x == 0) {
@@ -348,11 +343,11 @@ __global__ void __launch_bounds__(kTile, TDB_EDGE_MINB) edge_kernel(EdgeArgs a) 
     for (int s = 0; s < nunits; ++s) {
         const int st = s & 1;
         mbar_wait(&bar[st], (uint32_t)((s >> 1) & 1));
-        const int ne = kSuper ? unit_count(s) : (int)shdr[st].z;
+        const int ne = (int)shdr[st].z;
         const double* er = dsm + (size_t)st * a.stage;
 #pragma unroll kUEE
         for (int j = 0; j < ne; ++j) {
-            const double2* r = reinterpret_cast<const double2*>(er + (size_t)kStride * j);
+            const double2* r = reinterpret_cast<const double2*>(er + (size_t)kER * j);
             const double2 p0 = r[0], p1 = r[1], p2 = r[2], p3 = r[3];
 #pragma unroll
             for (int i = 0; i < kEdgeAPT; ++i)
@@ -364,17 +359,86 @@ __global__ void __launch_bounds__(kTile, TDB_EDGE_MINB) edge_kernel(EdgeArgs a) 
     }
 #pragma unroll
     for (int i = 0; i < kEdgeAPT; ++i)
-        if (active[i] && best[i] < kInfHi) {
-            const unsigned long long bits = (unsigned long long)__double_as_longlong(__hiloint2double(best[i], 0));
-            const uint64_t t2[2] = {tile[i] & 0xffffffffull, tile[i] >> 32};  // the edge's tiles
+        if (active[i] && best[i] < kInfHi)
+            edge_min_out(a, tile[i], ch, (unsigned long long)__double_as_longlong(__hiloint2double(best[i], 0)));
+}
+
+// The same candidates on B's distinct edges per kBSuper faces (the chunk is a
+// multiple of kBSuper), in FP32 (fast_pair.cuh edge_pair32; the band adds
+// eta_f32): kEdge32APT A edges per thread, B's FP32 records streamed
+// kEdgePiece per TMA stage (8 KB).
+#ifndef TDB_E32_APT
+#define TDB_E32_APT 4
+#endif
+#ifndef TDB_E32_MINB
+#define TDB_E32_MINB 6
+#endif
+#ifndef TDB_UE32
+#define TDB_UE32 2
+#endif
+constexpr int kEdge32APT = TDB_E32_APT;
+constexpr int kUE32 = TDB_UE32;
+
+__global__ void __launch_bounds__(kTile, TDB_E32_MINB) edge32_kernel(EdgeArgs a) {
+    __shared__ alignas(128) float4 rec[2][2 * kEdgePiece];
+    __shared__ alignas(8) uint64_t bar[2];
+    const uint64_t et = blockIdx.x / a.n_chunks, ch = blockIdx.x - et * a.n_chunks;
+    float Q[kEdge32APT][8];
+    uint64_t tile[kEdge32APT];
+    bool active[kEdge32APT];
+    float best[kEdge32APT];
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const uint64_t t = t2[q];
-                if ((q == 1 && t == t2[0]) || t < a.tile0 || t >= a.tile1) continue;  // outside the selection
-                atomicMin(a.itemmin + (t - a.tile0) * a.n_chunks + ch, bits);
-                atomicMin(a.objmin + (a.tiles[t].obj - a.obj0), bits);
-            }
+    for (int i = 0; i < kEdge32APT; ++i) {
+        const uint64_t e = a.e_lo + (et * kEdge32APT + i) * kTile + threadIdx.x;
+        active[i] = e < a.e_hi;
+        const double* q = a.Ae + min(e, a.e_hi - 1) * kAER;
+        const double2 v0 = __ldg(reinterpret_cast<const double2*>(q)), v1 = __ldg(reinterpret_cast<const double2*>(q) + 1),
+                      v2 = __ldg(reinterpret_cast<const double2*>(q) + 2), v3 = __ldg(reinterpret_cast<const double2*>(q) + 3);
+        Q[i][0] = (float)(v0.x - a.ox), Q[i][1] = (float)(v0.y - a.oy), Q[i][2] = (float)(v1.x - a.oz);
+        Q[i][3] = (float)v1.y, Q[i][4] = (float)v2.x, Q[i][5] = (float)v2.y;
+        Q[i][6] = (float)v3.x, Q[i][7] = (float)v3.y;
+        tile[i] = (uint64_t)__double_as_longlong(__ldg(q + AR_TILE));
+        best[i] = __int_as_float(0x7f800000);
+    }
+
+    const uint64_t b0 = ch * a.chunk, b1 = min(a.Bn, b0 + a.chunk);
+    const uint64_t se0 = __ldg(a.Bse_off + b0 / kBSuper), se1 = __ldg(a.Bse_off + (b1 + kBSuper - 1) / kBSuper);
+    const int nunits = (int)((se1 - se0 + kEdgePiece - 1) / kEdgePiece);
+    auto unit_count = [&](int s) -> int { return (int)min((uint64_t)kEdgePiece, se1 - se0 - (uint64_t)s * kEdgePiece); };
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    auto issue = [&](int s) {
+        const int st = s & 1;
+        const uint32_t bytes = (uint32_t)unit_count(s) * 2u * (uint32_t)sizeof(float4);
+        mbar_expect_tx(&bar[st], bytes);
+        bulk_g2s(&rec[st][0], a.Bse + 2 * (se0 + (uint64_t)s * kEdgePiece), bytes, &bar[st]);
+    };
+    if (threadIdx.x == 0) {
+        if (nunits > 0) issue(0);
+        if (nunits > 1) issue(1);
+    }
+#pragma unroll 1
+    for (int s = 0; s < nunits; ++s) {
+        const int st = s & 1;
+        mbar_wait(&bar[st], (uint32_t)((s >> 1) & 1));
+        const int ne = unit_count(s);
+        const float4* r = &rec[st][0];
+#pragma unroll kUE32
+        for (int j = 0; j < ne; ++j) {
+            const float4 p0 = r[2 * j], p1 = r[2 * j + 1];
+#pragma unroll
+            for (int i = 0; i < kEdge32APT; ++i) best[i] = fminf(best[i], edge_pair32(Q[i], p0, p1));
         }
+        __syncthreads();
+        if (threadIdx.x == 0 && s + 2 < nunits) issue(s + 2);
+    }
+#pragma unroll
+    for (int i = 0; i < kEdge32APT; ++i)
+        if (active[i] && best[i] < __int_as_float(0x7f800000)) edge_min_out(a, tile[i], ch, f32_as_f64_bits(best[i]));
 }
 
 struct VertArgs {
@@ -497,14 +561,20 @@ struct BandArgs {
     double* band;
     unsigned long long* objD;
     unsigned long long* objP;
+    double rB;  // the FP32 edge lists' origin radius (eta_f32) when they ran, else < 0
 };
 
 // eta(m) (tdb_internal.h) for objects A and B. The round is complete when the
 // exact minimum D satisfies D + eta(D) <= band: every pair the reference can
 // rank at or below D has d~ <= d_true + eta(d_true) <= D + eta(D) (eta grows
 // with m), so it was flagged.
-__device__ __forceinline__ double band_eta(const double* As, const double* Bs, double m) {
-    return band_eta_of(fmax(As[6], Bs[6]), fmax(As[8], Bs[8]), fmax(As[7], Bs[7]), m);
+// With the FP32 edge lists (rB >= 0) eta_f32 is added: it bounds those
+// candidates' excess (its supremum over d <= m, so the check still reads
+// "D + eta(D) <= band").
+__device__ __forceinline__ double band_eta(const double* As, const double* Bs, double m, double rB) {
+    const double L = fmax(As[6], Bs[6]);
+    const double e = band_eta_of(L, fmax(As[8], Bs[8]), fmax(As[7], Bs[7]), m);
+    return rB >= 0.0 ? e + eta_f32(L, rB, m) : e;
 }
 
 __global__ void band_kernel(BandArgs a) {
@@ -519,7 +589,7 @@ __global__ void band_kernel(BandArgs a) {
         return;
     }
     const double m = sqrt(__longlong_as_double((long long)e));
-    const double b = m * (1.0 + kBandRel) + 2.0 * band_eta(a.Astats + (a.obj0 + o) * kObjStats, a.Bstats, m);
+    const double b = m * (1.0 + kBandRel) + 2.0 * band_eta(a.Astats + (a.obj0 + o) * kObjStats, a.Bstats, m, a.rB);
     a.band[o] = b;
     a.band2[o] = b * b * (1.0 + 4e-16);
 }
@@ -641,6 +711,7 @@ struct CheckArgs {
     unsigned long long* objD;
     unsigned long long* objP;
     unsigned long long* retry;
+    double rB;  // as BandArgs
 };
 
 // After a round: objects whose exact minimum lies outside the band get the
@@ -659,8 +730,8 @@ __global__ void check_kernel(CheckArgs a) {
     // NaN/inf; treat as done.
     const double* As = a.Astats + (a.obj0 + o) * kObjStats;
     const double m = d != kNone ? __longlong_as_double((long long)d) : 0.0;
-    if (d != kNone && m + band_eta(As, a.Bstats, m) > b) {
-        const double nb = m * (1.0 + kBandRel) + 2.0 * band_eta(As, a.Bstats, m);
+    if (d != kNone && m + band_eta(As, a.Bstats, m, a.rB) > b) {
+        const double nb = m * (1.0 + kBandRel) + 2.0 * band_eta(As, a.Bstats, m, a.rB);
         a.band[o] = nb;
         a.band2[o] = nb * nb * (1.0 + 4e-16);
         a.objD[o] = kNone;
@@ -882,6 +953,7 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
     EventPair& ev = thread_events();
     CK(cudaEventRecord(ev.e[0], st));
     uint64_t launches = 1;
+    double rB = -1.0;  // >= 0 when the FP32 edge lists ran (band_eta adds eta_f32)
     unsigned long long *perm = nullptr, *lb2 = nullptr;
     void* cull_mem[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     if (cx.mode == TDB_MODE_CULL) {
@@ -915,10 +987,8 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
                             2 * kFBCap * (int)sizeof(double)));
     CK(cudaFuncSetAttribute(filter_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             2 * kFBCap * (int)sizeof(double)));
-    CK(cudaFuncSetAttribute(edge_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(edge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             2 * kFBCap * (int)sizeof(double)));
-    CK(cudaFuncSetAttribute(edge_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            2 * kEdgePiece * kAER * (int)sizeof(double)));
     CK(cudaFuncSetAttribute(vertex_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             2 * kFBCap * (int)sizeof(double)));
     DistArgs da{A.planes, A.n_pad, A.d_tiles, sel.tile0, sel.row_lo, sel.row_hi, B.planes, B.n_pad, B.n,
@@ -948,19 +1018,22 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
         // (entries reaching back into tiles before tile0 are evaluated too;
         // the kernels attribute only to tiles inside the selection)
         const uint64_t e_lo = A.h_tile_eoff[lo_tile(A.h_st_espan[st0])], e_hi = A.h_tile_eoff[sel.tile1];
-        const uint64_t n_et = (e_hi - e_lo + kTile * kEdgeAPT - 1) / (kTile * kEdgeAPT);
+        // B's edges per kBSuper faces in FP32 when the chunk allows (fewer edge
+        // pairs; coordinates within 1e15 so no FP32 value overflows), else per
+        // feature block in FP64
+        const bool super = chunk % kBSuper == 0 && B.d_bseoff && std::max(A.stats[7], B.stats[7]) < 1e15;
+        const int apt = super ? kEdge32APT : kEdgeAPT;
+        const uint64_t n_et = (e_hi - e_lo + (uint64_t)kTile * apt - 1) / ((uint64_t)kTile * apt);
         if (n_et) {
-            // B's edges per kBSuper faces when the chunk allows (fewer edge pairs), else per feature block
-            const bool super = chunk % kBSuper == 0 && B.d_bseoff;
-            const uint32_t stg = super ? (uint32_t)(kEdgePiece * kAER) : stage_e;
-            const EdgeArgs ea{A.aedges, e_lo, e_hi, sel.tile0, sel.tile1, A.d_tiles, B.fblocks, B.d_fhdr, stg, B.n,
-                              n_chunks, chunk, sel.obj0, (unsigned long long*)sc.itemmin, sc.objmin, B.bedges,
-                              B.d_bseoff};
-            const size_t smem_x = 2 * (size_t)stg * sizeof(double);
-            if (super)
-                edge_kernel<true><<<(unsigned)(n_et * n_chunks), kTile, smem_x, st>>>(ea);
-            else
-                edge_kernel<false><<<(unsigned)(n_et * n_chunks), kTile, smem_x, st>>>(ea);
+            const EdgeArgs ea{A.aedges, e_lo, e_hi, sel.tile0, sel.tile1, A.d_tiles, B.fblocks, B.d_fhdr, stage_e,
+                              B.n, n_chunks, chunk, sel.obj0, (unsigned long long*)sc.itemmin, sc.objmin, B.bedges,
+                              B.d_bseoff, B.bse_org[0], B.bse_org[1], B.bse_org[2]};
+            if (super) {
+                edge32_kernel<<<(unsigned)(n_et * n_chunks), kTile, 0, st>>>(ea);
+                rB = B.bse_rB;
+            } else {
+                edge_kernel<<<(unsigned)(n_et * n_chunks), kTile, smem_e, st>>>(ea);
+            }
             CK(cudaGetLastError());
             ++launches;
         }
@@ -970,7 +1043,7 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
 
     const unsigned ob = (unsigned)((nobj + 255) / 256);
     band_kernel<<<ob, 256, 0, st>>>(BandArgs{sc.objmin, A.d_obj_stats, Bstats, sel.obj0, nobj, sc.band2, sc.band,
-                                             sc.objD, sc.objP});
+                                             sc.objD, sc.objP, rB});
     CK(cudaGetLastError());
     ++launches;
 
@@ -996,7 +1069,7 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
             CK(cudaGetLastError());
         }
         check_kernel<<<ob, 256, 0, st>>>(CheckArgs{nobj, sel.obj0, A.d_obj_stats, Bstats, sc.band2, sc.band,
-                                                   sc.objD, sc.objP, retry});
+                                                   sc.objD, sc.objP, retry, rB});
         CK(cudaGetLastError());
         launches += 4;
         if (want_witness) {  // for this round's winner; recomputed if the band widens

@@ -255,6 +255,66 @@ __device__ __forceinline__ int edge_pair(double qx, double qy, double qz, double
     return __double2hiint(fma(dx, dx, fma(dy, dy, dz * dz)));
 }
 
+// ---- FP32 edge/edge candidate (FULL mode's shared edge lists, DESIGN.md 4.1/4.2)
+// The same clamped solve as edge_pair on FP32 copies of the edges, with both
+// start points relative to one origin o (B's box centre): Q' = fl(Q - o),
+// P' = fl(P - o), E = fl(E), |E|^2, 1/|E|^2 rounded once. Every value is
+// still the distance between two points of (float-rounded) edges; its excess
+// over the true edge/edge distance is bounded by eta_f32 (below). The FP64
+// exact pass is unchanged: this only decides which items it re-scans.
+__device__ __forceinline__ float rcp_approx_f32(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// A edge: Q' (3), E (3), |E|^2, 1/|E|^2; B edge record p0 = P'x P'y P'z Ebx,
+// p1 = Eby Ebz Lb ILb. Returns d~^2.
+__device__ __forceinline__ float edge_pair32(const float (&q)[8], float4 p0, float4 p1) {
+    const float wx = p0.x - q[0], wy = p0.y - q[1], wz = p0.z - q[2];  // w = P - Q
+    const float fw = fmaf(p0.w, wx, fmaf(p1.x, wy, p1.y * wz));
+    const float bb = fmaf(q[3], p0.w, fmaf(q[4], p1.x, q[5] * p1.y));
+    const float cw = fmaf(q[3], wx, fmaf(q[4], wy, q[5] * wz));
+    const float bbI = bb * p1.w;
+    const float den = fmaf(-bbI, bb, q[6]);
+    const float num = fmaf(-bbI, fw, cw);
+    float s = __saturatef(num * rcp_approx_f32(den));  // NaN -> 0: any s in [0, 1] is a point of the edge
+    const float t = __saturatef(fmaf(bb, s, -fw) * p1.w);
+    s = __saturatef(fmaf(bb, t, cw) * q[7]);
+    const float dx = fmaf(s, q[3], fmaf(-t, p0.w, -wx));
+    const float dy = fmaf(s, q[4], fmaf(-t, p1.x, -wy));
+    const float dz = fmaf(s, q[5], fmaf(-t, p1.y, -wz));
+    return fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+}
+
+// A non-negative float as the double of the same value, by integer ops
+// (no F2F): the item minima are non-negative doubles compared as u64.
+__device__ __forceinline__ unsigned long long f32_as_f64_bits(float x) {
+    const unsigned u = __float_as_uint(x);
+    if (u == 0u) return 0ull;
+    if (u >= 0x7f800000u) return 0x7ff0000000000000ull;  // +inf (NaN never reaches here: fminf drops it)
+    if (u < 0x00800000u) return (unsigned long long)__double_as_longlong((double)x);  // subnormal (rare)
+    return ((unsigned long long)((u >> 3) + 0x38000000u) << 32) | ((unsigned long long)(u << 29));
+}
+
+// eta of the FP32 edge/edge candidate, added to eta(m) when the FP32 lists
+// ran. u = 2^-24; L = max edge; rB = B's box half-diagonal.
+//   solve: squared excess X = 12 u L (|w| + L) <= kF32Solve L (m + 4L): the
+//          excess in d is <= min(sqrt X, X / 2d) (sqrt(d^2 + X) - d);
+//   data:  the float start points / edges / w and the evaluation move the
+//          point pair by <= u (2 rB + 10 (m + 4L)).
+// Margins 4x. The sqrt / (X / 2d) pair is not monotone in d, so the value
+// used is its supremum over d <= m: max(4 min(sqrt X, X / 2m), 4.5 sqrt X - m).
+constexpr double kF32Solve = 12.0 * 5.9604644775390625e-8;
+constexpr double kF32Lin = 4.0 * 10.0 * 5.9604644775390625e-8;
+constexpr double kF32Org = 4.0 * 2.0 * 5.9604644775390625e-8;
+__device__ __forceinline__ double eta_f32(double L, double rB, double m) {
+    const double w = m + 4.0 * L;
+    const double X = kF32Solve * L * w, sx = sqrt(X);
+    const double solve = m > 0.5 * sx ? X / (2.0 * m) : sx;
+    return fmax(4.0 * solve, 4.5 * sx - m) + kF32Lin * w + kF32Org * rB;
+}
+
 // Edge P -> P + Eb of B (|Eb|^2 = Lb, 1/|Eb|^2 = ILb) against A's three edges.
 __device__ __forceinline__ int edge_cand(const AFace& A, double px, double py, double pz, double ebx, double eby,
                                          double ebz, double Lb, double ILb) {
@@ -278,7 +338,9 @@ __device__ __forceinline__ int hmin_sq(int hmin) {
 // face. The filter kernel evaluates the same candidates, each shared vertex
 // and edge once per feature block (distance.cu). `ap`/`as` locate A's fields
 // for the out-of-line piercing test.
-template <class P>
+// kEdges = false leaves out the edge/edge candidates (tdb_pairs_filter_f32
+// adds them in FP32, as FULL mode does).
+template <class P, bool kEdges = true>
 __device__ __forceinline__ double pair_d2(const AFace& A, const P& bt, const double* ap, uint64_t as) {
     double b[9], nb[3], ub[3], vb[3];
 #pragma unroll
@@ -292,7 +354,8 @@ __device__ __forceinline__ double pair_d2(const AFace& A, const P& bt, const dou
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         hmin = min(hmin, vertex_cand(A, b[3 * k], b[3 * k + 1], b[3 * k + 2], hs));
-        best = min(best, edge_cand(A, b[3 * k], b[3 * k + 1], b[3 * k + 2], bt(F_E + 3 * k), bt(F_E + 3 * k + 1),
+        if (kEdges)
+            best = min(best, edge_cand(A, b[3 * k], b[3 * k + 1], b[3 * k + 2], bt(F_E + 3 * k), bt(F_E + 3 * k + 1),
                                    bt(F_E + 3 * k + 2), bt(F_L + k), bt(F_IL + k)));
     }
     best = min(best, hmin_sq(hmin));

@@ -37,6 +37,40 @@ __global__ void filter_pairs_kernel(const double* __restrict__ pa, const double*
     }
 }
 
+// FULL mode's candidate set per pair: the FP64 vertex/face candidates and
+// piercing test, the nine edge/edge candidates in FP32 relative to o
+// (edge32_kernel's arithmetic, fast_pair.cuh edge_pair32).
+__global__ void filter_pairs_f32_kernel(const double* __restrict__ pa, const double* __restrict__ pb, uint64_t n,
+                                        double ox, double oy, double oz, double* __restrict__ d2) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const double* fa = pa + NF * k;
+        const double* fb = pb + NF * k;
+        AFace A;
+        load_aface(A, FaceRef{fa, 1});
+        if (fa[F_DEG] != 0.0 || fb[F_DEG] != 0.0) {
+            d2[k] = pos_inf();
+            continue;
+        }
+        const double v = pair_d2<FaceRef, false>(A, FaceRef{fb, 1}, fa, 1);
+        float best = __int_as_float(0x7f800000);
+        for (int i = 0; i < 3; ++i) {
+            const float q[8] = {(float)(fa[F_V + 3 * i] - ox), (float)(fa[F_V + 3 * i + 1] - oy),
+                                (float)(fa[F_V + 3 * i + 2] - oz), (float)fa[F_E + 3 * i], (float)fa[F_E + 3 * i + 1],
+                                (float)fa[F_E + 3 * i + 2], (float)fa[F_L + i], (float)fa[F_IL + i]};
+            for (int j = 0; j < 3; ++j) {
+                const float4 p0 = make_float4((float)(fb[F_V + 3 * j] - ox), (float)(fb[F_V + 3 * j + 1] - oy),
+                                              (float)(fb[F_V + 3 * j + 2] - oz), (float)fb[F_E + 3 * j]);
+                const float4 p1 = make_float4((float)fb[F_E + 3 * j + 1], (float)fb[F_E + 3 * j + 2],
+                                              (float)fb[F_L + j], (float)fb[F_IL + j]);
+                best = fminf(best, edge_pair32(q, p0, p1));
+            }
+        }
+        const double e = __longlong_as_double((long long)f32_as_f64_bits(best));
+        d2[k] = min_nn(v, e);
+    }
+}
+
 // gather planes of a Geom into per-face AoS records
 __global__ void planes_to_aos(const double* __restrict__ planes, uint64_t n, uint64_t n_pad, double* __restrict__ out) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -86,7 +120,7 @@ void run_pairs(const Ctx& cx, const double* a9, const double* b9, uint64_t n, do
     CK(cudaStreamSynchronize(st));
 }
 
-void run_pairs_filter(const Ctx& cx, const Geom& A, const Geom& B, double* d2) {
+void run_pairs_filter(const Ctx& cx, const Geom& A, const Geom& B, double* d2, const double* origin) {
     const cudaStream_t st = cx.stream;
     const uint64_t n = A.n;
     if (n == 0) return;
@@ -96,7 +130,11 @@ void run_pairs_filter(const Ctx& cx, const Geom& A, const Geom& B, double* d2) {
     CK(cudaMallocAsync(&dd, n * sizeof(double), st));
     planes_to_aos<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(A.planes, n, A.n_pad, pa);
     planes_to_aos<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(B.planes, n, B.n_pad, pb);
-    filter_pairs_kernel<<<(unsigned)std::min<uint64_t>((n + 127) / 128, 148 * 16), 128, 0, st>>>(pa, pb, n, dd);
+    const unsigned grid = (unsigned)std::min<uint64_t>((n + 127) / 128, 148 * 16);
+    if (origin)
+        filter_pairs_f32_kernel<<<grid, 128, 0, st>>>(pa, pb, n, origin[0], origin[1], origin[2], dd);
+    else
+        filter_pairs_kernel<<<grid, 128, 0, st>>>(pa, pb, n, dd);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(d2, dd, n * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaFreeAsync(pa, st));

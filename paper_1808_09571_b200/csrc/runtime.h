@@ -83,8 +83,12 @@ struct Geom {
     mutable std::vector<uint64_t> h_tile_eoff, h_tile_voff;  // n_tiles + 1: first entry with that first tile
     mutable std::vector<uint32_t> h_st_espan, h_st_vspan;    // per super-tile: max (second - first tile)
     mutable bool atiles_built = false;
-    // B side: distinct edges per kBSuper faces (geom_super_bedges)
-    mutable double* bedges = nullptr;
+    // B side: distinct edges per kBSuper faces (geom_super_bedges), as FP32
+    // records (tdb_internal.h kBER) relative to bse_org = B's box centre;
+    // bse_rB = the box's half-diagonal (bounds |P - bse_org|, eta_f32)
+    mutable float4* bedges = nullptr;
+    mutable double bse_org[3] = {0.0, 0.0, 0.0};
+    mutable double bse_rB = 0.0;
     mutable std::vector<uint64_t> h_bseoff;  // per group of kBSuper faces: first entry
     mutable uint64_t* d_bseoff = nullptr;     // device copy
     // intersects (as B): bounding sphere of each kHitGroup faces (geom_hit_spheres)
@@ -289,7 +293,9 @@ void run_queries_direct(const Ctx& cx, int op, const double* q, uint64_t n, int 
 void run_pairs(const Ctx& cx, const double* a9, const double* b9, uint64_t n, double* dist,
                uint8_t* hit);
 
-void run_pairs_filter(const Ctx& cx, const Geom& A, const Geom& B, double* d2);
+// origin != nullptr: FULL mode's candidate set (FP32 edge/edge relative to
+// origin); else the FP64 per-pair filter
+void run_pairs_filter(const Ctx& cx, const Geom& A, const Geom& B, double* d2, const double* origin = nullptr);
 
 double fp64_peak(const Ctx& cx, double* ms);
 

@@ -90,6 +90,10 @@ constexpr uint64_t kSuperTile = TDB_SUPERTILE;
 #endif
 constexpr uint64_t kBSuper = TDB_BSUPER;
 constexpr int kEdgePiece = 256;
+// Those B entries as FP32 records of kBER floats (two float4): P - o (3), E
+// (3), |E|^2, 1/|E|^2, o = B's box centre; the FP32 edge/edge candidate
+// (fast_pair.cuh edge_pair32, eta_f32).
+constexpr int kBER = 8;
 // Vertices: likewise per super-tile, kAVR doubles = x y z, two tiles (u32 |
 // u32 << 32).
 constexpr int kAVR = 4;

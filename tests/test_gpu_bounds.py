@@ -172,6 +172,42 @@ def test_filter_error_within_eta_at_scale(seed):
           f"{overshoot} pairs where the reference overshoots the exact distance (d~ matches the exact one)")
 
 
+@pytest.mark.parametrize("seed", [13, 14])
+def test_filter_f32_error_within_eta_at_scale(seed):
+    """FULL mode's candidate set with the FP32 edge/edge candidates
+    (tdb_pairs_filter_f32: edge32_kernel's arithmetic relative to b's box
+    centre) on 10M adversarial pairs per seed: d~ never above d + eta_proven +
+    eta_f32_proven. Each pair is centred on its b triangle and
+    the pairs are grouped by edge-length decade, so the origin radius rB of a
+    call is that of its own pairs (production: B's box)."""
+    u = 2.0 ** -24
+    worst = 0.0
+    for part in range(5):
+        a, b = adversarial_pairs(seed * 100 + part, 2_000_000)
+        c = np.tile(b.reshape(-1, 3, 3).mean(1), 3)
+        a, b = np.ascontiguousarray(a - c), np.ascontiguousarray(b - c)
+        ref = T.pairs_distance(a, b)
+        fin = np.isfinite(ref)
+        A3, B3 = a.reshape(-1, 3, 3), b.reshape(-1, 3, 3)
+        edge = np.maximum(np.linalg.norm(A3 - np.roll(A3, -1, 1), axis=2).max(1),
+                          np.linalg.norm(B3 - np.roll(B3, -1, 1), axis=2).max(1))
+        dec = np.floor(np.log10(np.maximum(edge, 1e-300)))
+        for dv in np.unique(dec[fin]):
+            idx = np.nonzero(fin & (dec == dv))[0]
+            d2, _, rB = T.pairs_filter_f32(a[idx], b[idx])
+            assert np.isfinite(d2).all()
+            dt, r = np.sqrt(d2), ref[idx]
+            eta, e, _ = _proven_eta(A3[idx], B3[idx], r)
+            X = 12 * u * e * (r + 3 * e)              # the FP32 solve's squared excess, |w| <= d + 2L
+            solve = np.where(r > 0.5 * np.sqrt(X), X / (2 * np.maximum(r, 1e-300)), np.sqrt(X))
+            lin = u * (2 * rB + 10 * (r + 4 * e))     # float data, w and the evaluation
+            hi = (dt - r) / (eta + solve + lin)
+            k = int(np.argmax(hi))
+            assert hi[k] <= 1.0, (hi[k], dv, a[idx][k], b[idx][k], r[k], dt[k])
+            worst = max(worst, float(hi[k]))
+    print(f"seed {seed}: 10M pairs, max (d~ - d)/(eta_proven + eta_f32_proven) = {worst:.3g}")
+
+
 @pytest.mark.parametrize("seed", [21, 22])
 def test_intersects_cull_margin_at_scale(seed):
     """hit_kernel (plane cull + exact survivors) == the exact predicate on
