@@ -61,6 +61,8 @@ FILTER_LOOP_FACE = (0, 0)      # filter_kernel<false> face loop (straddle test):
 FILTER_LOOP_VERTEX = (13, 19)  # filter_kernel<false> vertex loop: a B vertex against the A face
 FILTER_VERT_PAIR = (13, 19)    # vertex_kernel: an A tile vertex against a B face
 FILTER_EDGE_PAIR = (31, 51)    # edge_kernel: an A tile edge against a B block edge
+FILTER_EDGE_PAIR32 = (30, 47)  # edge32_kernel (FP32, the chunk a multiple of 1,024 faces): 18 FFMA + 5 FMUL +
+                               # 3 FADD + 3 FMUL.SAT + 1 FMNMX per edge pair, + 1 MUFU.RCP (cuobjdump -sass)
 U64_MAX = (1 << 64) - 1
 C3S_AXIS, C3S_ANGLE = (1.0, 2.0, 3.0), 0.37  # C3 stress variant rotation
 
@@ -733,9 +735,11 @@ def main():
         a_edges, a_verts = fa["tile_edges"] / fa["faces"], fa["tile_vertices"] / fa["faces"]
         ep = a_edges * per_face_e  # edge pairs per face pair
         instr = (FILTER_LOOP_FACE[0] + per_face_v * FILTER_LOOP_VERTEX[0] + a_verts * FILTER_VERT_PAIR[0]
-                 + ep * FILTER_EDGE_PAIR[0])
+                 + (0 if r_chunk_super else ep * FILTER_EDGE_PAIR[0]))
         flops = (FILTER_LOOP_FACE[1] + per_face_v * FILTER_LOOP_VERTEX[1] + a_verts * FILTER_VERT_PAIR[1]
-                 + ep * FILTER_EDGE_PAIR[1])
+                 + (0 if r_chunk_super else ep * FILTER_EDGE_PAIR[1]))
+        instr32 = ep * FILTER_EDGE_PAIR32[0] if r_chunk_super else 0.0  # FP32 pipe (edge32_kernel)
+        flops32 = ep * FILTER_EDGE_PAIR32[1] if r_chunk_super else 0.0
         roofline["features_per_face"] = {"b_vertices": per_face_v, "b_edges": per_face_e, "a_tile_edges": a_edges,
                                          "a_tile_vertices": a_verts}
         roofline["fp64_instr_per_pair"] = instr
@@ -745,6 +749,18 @@ def main():
                             "algorithmic; fp64_pipe_frac is the hardware fraction (FP64-pipe issue / peak)")
         roofline["fp64_pipe_frac"] = instr * f_pairs / (f_ms * 1e-3) / (fp64_tf * 1e12 / 2)
         roofline["executed_fp64_tflops"] = flops * f_pairs / (f_ms * 1e-3) / 1e12
+        if r_chunk_super:  # the edge/edge candidates run on the FP32 pipe (128 lanes per SM per clock)
+            sm_mhz = (clk or {}).get("sm_mhz") or 1965.0
+            fp32_rate = torch.cuda.get_device_properties(local).multi_processor_count * 128 * sm_mhz * 1e6
+            roofline["fp32_instr_per_pair"] = instr32
+            roofline["fp32_pipe_frac"] = instr32 * f_pairs / (f_ms * 1e-3) / fp32_rate
+            roofline["executed_fp32_tflops"] = flops32 * f_pairs / (f_ms * 1e-3) / 1e12
+            roofline["pipe_busy_frac"] = roofline["fp64_pipe_frac"] + roofline["fp32_pipe_frac"]
+            roofline["kernel"] = ("filter stage: edge32_kernel (FP32 edge/edge candidates) + vertex_kernel + "
+                                  "filter_kernel<false> (FP64), timed together (events around the three launches)")
+            roofline["note"] += ("; the edge/edge candidates run in FP32 (edge32_kernel, band widened by eta_f32), "
+                                 "so fp64_pipe_frac + fp32_pipe_frac = pipe_busy_frac is the stage's hardware "
+                                 "fraction (the kernels run one after another)")
     elif wl.op == "intersects":
         roofline["note"] = ("culled pairs skip the W_i work (conservative FP32/FP64 separating-plane test, "
                             "DESIGN.md 4.3): frac > 1 is algorithmic, not hardware")

@@ -1,0 +1,14 @@
+# round-2 final evidence for the FP32 edge build (edge32_kernel): GPU suite, sweep, default bench + reference arm,
+# launch list, ncu --set full of each FULL-mode distance kernel (bench launch)
+timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=5 > gpurun_out/r2k_gputest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r2k_gputest.log
+tail -3 gpurun_out/r2k_gputest.log
+bash scripts/sweep.sh; python scripts/hit_probe.py > gpurun_out/r2k_hit_probe.txt 2>&1; cat gpurun_out/r2k_hit_probe.txt
+cp gpurun_out/sweep.jsonl gpurun_out/r2k_sweep.jsonl
+timeout 900 python bench.py > gpurun_out/r2k_bench_default.json 2> gpurun_out/r2k_bench_default.err; echo "bench rc=$?"
+timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/r2k_bench_reference.json 2> gpurun_out/r2k_bench_reference.err; echo "ref rc=$?"
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2k_launches_bench_default.csv python bench.py --steps 2 --warmup 1 --no-cpu --e2e-steps 1 > gpurun_out/r2k_launches.log 2>&1; echo "launches rc=$?"
+for k in edge32_kernel vertex_kernel filter_kernel; do
+  ncu --set full --clock-control none --import-source on -k regex:"^$k" -c 1 -o gpurun_out/r2k_c2_$k -f python bench.py --steps 1 --warmup 0 --no-cpu --e2e-steps 0 > gpurun_out/r2k_prof_$k.log 2>&1; echo "$k rc=$?"
+done
+timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_features.py tests/test_gpu_direct.py -q -p no:cacheprovider -x -k "not cutting_super" > gpurun_out/r2k_memcheck.log 2>&1; echo "memcheck rc=$?" >> gpurun_out/r2k_memcheck.log
+tail -3 gpurun_out/r2k_memcheck.log
