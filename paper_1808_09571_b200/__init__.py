@@ -503,7 +503,9 @@ def pairs_filter(a, b) -> np.ndarray:
 
 def pairs_filter_f32(a, b):
     """FULL mode's candidate set for aligned pairs (FP64 vertex/face, FP32
-    edge/edge relative to b's box centre): (d~^2 per pair, origin, rB)."""
+    edge/edge relative to b's box centre): (d~^2 per pair, origin, rB).
+    A pair whose packed FP32 candidates (edge_pair32x2) differ from the scalar
+    ones in any bit gets NaN."""
     a, b = _f64(a), _f64(b)
     out = np.empty(len(a), np.float64)
     orb = np.empty(4, np.float64)

@@ -85,13 +85,39 @@ constexpr int kUV = TDB_UV, kUF = TDB_UF, kUE = TDB_UE;
 #define TDB_FACE_MINB 4
 #endif
 static_assert(kFB <= 64, "the face loop's straddle mask is 64 bits");
+// SMEM stages of filter_kernel: FULL keeps kFStages blocks in flight, each
+// released per warp (an "empty" mbarrier per stage), so a warp whose rows meet
+// straddling faces no longer holds the CTA at a per-block barrier: warps may
+// drift kFStages - 2 blocks apart. CULL (whole blocks) keeps two.
+#ifndef TDB_FSTAGES
+#define TDB_FSTAGES 4
+#endif
+#ifndef TDB_FCHUNK_MAJOR
+#define TDB_FCHUNK_MAJOR 1
+#endif
+template <bool kEdges>
+constexpr int filter_stages() { return kEdges ? 2 : TDB_FSTAGES; }
 template <bool kEdges>
 __global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MINB) filter_kernel(DistArgs a) {
-    extern __shared__ __align__(128) double dsm[];  // 2 stages of a.stage doubles: one feature block each
-    __shared__ alignas(8) uint64_t bar[2];
+    constexpr int NS = filter_stages<kEdges>();
+    static_assert(NS >= 2, "at least double buffering");
+    extern __shared__ __align__(128) double dsm[];  // NS stages of a.stage doubles: one feature block each
+    __shared__ alignas(8) uint64_t bar[NS];         // full: the stage's TMA transaction landed
+    __shared__ alignas(8) uint64_t ebar[NS];        // empty: every warp is done with the stage
     __shared__ double red[kTile / 32];
 
-    const uint64_t item = a.perm ? a.perm[blockIdx.x] : blockIdx.x;
+    // FULL: CTAs in chunk-major order (TDB_FCHUNK_MAJOR), so the CTAs resident
+    // at a time share one or two B chunks and read them from L2, not HBM (the
+    // item index, and so every output, is the same either way)
+    uint64_t item;
+    if (a.perm) {
+        item = a.perm[blockIdx.x];
+    } else if (TDB_FCHUNK_MAJOR) {
+        const uint64_t nt = gridDim.x / a.n_chunks, c = blockIdx.x / nt;
+        item = (blockIdx.x - c * nt) * a.n_chunks + c;
+    } else {
+        item = blockIdx.x;
+    }
     const uint64_t tl = item / a.n_chunks, ch = item - tl * a.n_chunks;
     const Tile T = a.tiles[a.tile0 + tl];
     if (a.perm) {  // CULL: no pair of this item can beat the object's current minimum
@@ -116,17 +142,20 @@ __global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MIN
     const uint64_t blk0 = b0 / kFB;
     const int nblk = (int)((b1 - b0 + kFB - 1) / kFB);
     if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+#pragma unroll
+        for (int i = 0; i < NS; ++i) {
+            mbar_init(&bar[i], 1);
+            mbar_init(&ebar[i], kTile / 32);
+        }
         mbar_fence_init();
     }
     __syncthreads();
     // per stage, beside the block's records: its header and bounds, staged by
     // the same TMA transaction (the consumers then never wait on global loads)
-    __shared__ alignas(16) uint4 shdr[2];
-    __shared__ alignas(16) double4 ssph[2];
+    __shared__ alignas(16) uint4 shdr[NS];
+    __shared__ alignas(16) double4 ssph[NS];
     auto issue = [&](int s) {
-        const int st = s & 1;
+        const int st = s % NS;
         const uint4 hb = __ldg(&a.Bfhdr[blk0 + s]);
         // CULL: the whole block; FULL: [face planes | vertices of faces |
         // distinct vertices] (the planes for the rare straddling faces: read
@@ -137,10 +166,8 @@ __global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MIN
         if (!kEdges) bulk_g2s(&ssph[st], a.Bsph + blk0 + s, sizeof(double4), &bar[st]);
         if (bytes) bulk_g2s(dsm + (size_t)st * a.stage, a.Bfb + (blk0 + s) * (uint64_t)kFBCap, bytes, &bar[st]);
     };
-    if (threadIdx.x == 0) {
-        issue(0);
-        if (nblk > 1) issue(1);
-    }
+    if (threadIdx.x == 0)
+        for (int s = 0; s < min(NS, nblk); ++s) issue(s);
     int best = kInfHi, hmin = kInfHi;
     bool pierce = false;
     // A's plane n.x = c, for the signs of B's vertex heights (the straddle
@@ -149,8 +176,8 @@ __global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MIN
     const double cA = dot3(A.n, A.v[0], A.v[1], A.v[2]);
 #pragma unroll 1
     for (int s = 0; s < nblk; ++s) {
-        const int st = s & 1;
-        mbar_wait(&bar[st], (uint32_t)((s >> 1) & 1));
+        const int st = s % NS;
+        mbar_wait(&bar[st], (uint32_t)((s / NS) & 1));
         const uint4 h = shdr[st];
         const double* base = dsm + (size_t)st * a.stage;
         const double* fp = base;                                // face planes
@@ -223,8 +250,15 @@ __global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MIN
             const double2 q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3];
             best = min(best, edge_cand(A, q0.x, q0.y, q1.x, q1.y, q2.x, q2.y, q3.x, q3.y));
         }
-        __syncthreads();
-        if (threadIdx.x == 0 && s + 2 < nblk) issue(s + 2);
+        // release the stage (each warp), then refill the one every warp
+        // released NS - 2 blocks ago: block q + NS into q's buffer
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(&ebar[st]);
+        const int q = s - (NS - 2);
+        if (threadIdx.x == 0 && q >= 0 && q + NS < nblk) {
+            mbar_wait(&ebar[q % NS], (uint32_t)((q / NS) & 1));
+            issue(q + NS);
+        }
     }
     double m = __hiloint2double(pierce ? 0 : min(best, hmin_sq(hmin)), 0);
     if (!active || b1 <= b0) m = pos_inf();
@@ -371,10 +405,14 @@ __global__ void __launch_bounds__(kTile, TDB_EDGE_MINB) edge_kernel(EdgeArgs a) 
 #define TDB_E32_APT 4
 #endif
 #ifndef TDB_E32_MINB
-#define TDB_E32_MINB 6
+#define TDB_E32_MINB 5
 #endif
 #ifndef TDB_UE32
 #define TDB_UE32 2
+#endif
+// two A edges per packed FP32 pair (fast_pair.cuh edge_pair32x2; bit-identical values)
+#ifndef TDB_E32_PACKED
+#define TDB_E32_PACKED 1
 #endif
 constexpr int kEdge32APT = TDB_E32_APT;
 constexpr int kUE32 = TDB_UE32;
@@ -400,6 +438,24 @@ __global__ void __launch_bounds__(kTile, TDB_E32_MINB) edge32_kernel(EdgeArgs a)
         tile[i] = (uint64_t)__double_as_longlong(__ldg(q + AR_TILE));
         best[i] = __int_as_float(0x7f800000);
     }
+
+#if TDB_E32_PACKED
+    static_assert(kEdge32APT % 2 == 0, "A edges in packed pairs");
+    AEdge32x2 A2[kEdge32APT / 2];
+#pragma unroll
+    for (int i = 0; i < kEdge32APT / 2; ++i) {
+        const float* x = Q[2 * i];
+        const float* y = Q[2 * i + 1];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            A2[i].q[k] = pk2f(x[k], y[k]);
+            A2[i].e[k] = pk2f(x[3 + k], y[3 + k]);
+            A2[i].ne[k] = pk2f(-x[3 + k], -y[3 + k]);
+        }
+        A2[i].L = pk2f(x[6], y[6]);
+        A2[i].il[0] = x[7], A2[i].il[1] = y[7];
+    }
+#endif
 
     const uint64_t b0 = ch * a.chunk, b1 = min(a.Bn, b0 + a.chunk);
     const uint64_t se0 = __ldg(a.Bse_off + b0 / kBSuper), se1 = __ldg(a.Bse_off + (b1 + kBSuper - 1) / kBSuper);
@@ -427,12 +483,27 @@ __global__ void __launch_bounds__(kTile, TDB_E32_MINB) edge32_kernel(EdgeArgs a)
         mbar_wait(&bar[st], (uint32_t)((s >> 1) & 1));
         const int ne = unit_count(s);
         const float4* r = &rec[st][0];
+#if TDB_E32_PACKED
+#pragma unroll kUE32
+        for (int j = 0; j < ne; ++j) {
+            const float4 p0 = r[2 * j], p1 = r[2 * j + 1];
+            const float nIL = -p1.w;
+#pragma unroll
+            for (int i = 0; i < kEdge32APT / 2; ++i) {
+                float d0, d1;
+                edge_pair32x2(A2[i], p0, p1, nIL, d0, d1);
+                best[2 * i] = fminf(best[2 * i], d0);
+                best[2 * i + 1] = fminf(best[2 * i + 1], d1);
+            }
+        }
+#else
 #pragma unroll kUE32
         for (int j = 0; j < ne; ++j) {
             const float4 p0 = r[2 * j], p1 = r[2 * j + 1];
 #pragma unroll
             for (int i = 0; i < kEdge32APT; ++i) best[i] = fminf(best[i], edge_pair32(Q[i], p0, p1));
         }
+#endif
         __syncthreads();
         if (threadIdx.x == 0 && s + 2 < nunits) issue(s + 2);
     }
@@ -475,7 +546,10 @@ __global__ void __launch_bounds__(kTile, TDB_VERT_MINB) vertex_kernel(VertArgs a
     extern __shared__ __align__(128) double dsm[];
     __shared__ alignas(8) uint64_t bar[2];
     __shared__ alignas(16) uint4 shdr[2];
-    const uint64_t vt = blockIdx.x / a.n_chunks, ch = blockIdx.x - vt * a.n_chunks;
+    // chunk-major CTA order (as filter_kernel): resident CTAs share B chunks in L2
+    const uint64_t n_vt = gridDim.x / a.n_chunks;
+    const uint64_t ch = TDB_FCHUNK_MAJOR ? blockIdx.x / n_vt : blockIdx.x % a.n_chunks;
+    const uint64_t vt = TDB_FCHUNK_MAJOR ? blockIdx.x - ch * n_vt : blockIdx.x / a.n_chunks;
     double ax[kVertAPT], ay[kVertAPT], az[kVertAPT];
     uint64_t tile[kVertAPT];
     bool active[kVertAPT];
@@ -986,7 +1060,7 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
     CK(cudaFuncSetAttribute(filter_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             2 * kFBCap * (int)sizeof(double)));
     CK(cudaFuncSetAttribute(filter_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            2 * kFBCap * (int)sizeof(double)));
+                            filter_stages<false>() * kFBCap * (int)sizeof(double)));
     CK(cudaFuncSetAttribute(edge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             2 * kFBCap * (int)sizeof(double)));
     CK(cudaFuncSetAttribute(vertex_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -998,7 +1072,7 @@ void run_distance_batch(const Ctx& cx, const ASel& sel, const Geom& B, double* d
         filter_kernel<true><<<(unsigned)n_items, kTile, smem, st>>>(da);
         CK(cudaGetLastError());
     } else {
-        filter_kernel<false><<<(unsigned)n_items, kTile, smem, st>>>(da);
+        filter_kernel<false><<<(unsigned)n_items, kTile, filter_stages<false>() * (size_t)stage * sizeof(double), st>>>(da);
         CK(cudaGetLastError());
         // entries are ordered by their first tile: those of tiles [tile0, tile1)
         // lie in [first tile >= tile0 - span, first tile < tile1), span = the

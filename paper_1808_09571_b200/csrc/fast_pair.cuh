@@ -287,6 +287,77 @@ __device__ __forceinline__ float edge_pair32(const float (&q)[8], float4 p0, flo
     return fmaf(dx, dx, fmaf(dy, dy, dz * dz));
 }
 
+// The same candidate for two A edges at once on packed FP32 pairs
+// (fma/mul/sub .rn.f32x2, SASS FFMA2/FMUL2/FADD2): lane k of every packed
+// operation is the IEEE operation edge_pair32 performs for A edge k, or its
+// exact negation (x * -y = -(x * y), fma(a, -b, c) = c - a b, rounded
+// alike), so each half returns edge_pair32's value bit for bit and eta_f32
+// is unchanged. B's components enter as {x, x} broadcasts (ptxas folds them
+// into the FFMA2 scalar operand). Q2[k] = {A edge 0's field k, A edge 1's};
+// Q2[3..5] are passed negated (nE = -E_A) beside E_A itself.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2f(float a, float b) {
+    f32x2 d;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(a), "f"(b));
+    return d;
+}
+__device__ __forceinline__ float lo_f(f32x2 x) { return __uint_as_float((unsigned)x); }
+__device__ __forceinline__ float hi_f(f32x2 x) { return __uint_as_float((unsigned)(x >> 32)); }
+__device__ __forceinline__ f32x2 fma2f(f32x2 a, f32x2 b, f32x2 c) {
+    f32x2 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f32x2 mul2f(f32x2 a, f32x2 b) {
+    f32x2 d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f32x2 sub2f(f32x2 a, f32x2 b) {
+    f32x2 d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+struct AEdge32x2 {
+    f32x2 q[3];   // Q' (start point about o)
+    f32x2 e[3];   // E_A
+    f32x2 ne[3];  // -E_A
+    f32x2 L;      // |E_A|^2
+    float il[2];  // 1/|E_A|^2
+};
+
+// B edge record p0 = P'x P'y P'z Ebx, p1 = Eby Ebz Lb ILb (nILb = -ILb).
+// Returns {d~^2 for A edge 0, for A edge 1}.
+__device__ __forceinline__ void edge_pair32x2(const AEdge32x2& A, float4 p0, float4 p1, float nILb, float& d0,
+                                              float& d1) {
+    const f32x2 Px = pk2f(p0.x, p0.x), Py = pk2f(p0.y, p0.y), Pz = pk2f(p0.z, p0.z);
+    const f32x2 Ex = pk2f(p0.w, p0.w), Ey = pk2f(p1.x, p1.x), Ez = pk2f(p1.y, p1.y);
+    const f32x2 nIL = pk2f(nILb, nILb);
+    const f32x2 wx = sub2f(Px, A.q[0]), wy = sub2f(Py, A.q[1]), wz = sub2f(Pz, A.q[2]);  // w = P - Q
+    const f32x2 fw = fma2f(Ex, wx, fma2f(Ey, wy, mul2f(Ez, wz)));
+    const f32x2 bb = fma2f(A.e[0], Ex, fma2f(A.e[1], Ey, mul2f(A.e[2], Ez)));
+    const f32x2 cw = fma2f(A.e[0], wx, fma2f(A.e[1], wy, mul2f(A.e[2], wz)));
+    const f32x2 nbbI = mul2f(bb, nIL);                       // -(bb * ILb)
+    const f32x2 den = fma2f(nbbI, bb, A.L);                  // fmaf(-bbI, bb, |E_A|^2)
+    const f32x2 num = fma2f(nbbI, fw, cw);                   // fmaf(-bbI, fw, cw)
+    const float s0 = __saturatef(lo_f(num) * rcp_approx_f32(lo_f(den)));
+    const float s1 = __saturatef(hi_f(num) * rcp_approx_f32(hi_f(den)));
+    const f32x2 nfw = mul2f(fw, pk2f(-1.0f, -1.0f));         // exact
+    const f32x2 tp = fma2f(bb, pk2f(s0, s1), nfw);           // fmaf(bb, s, -fw)
+    const float t0 = __saturatef(lo_f(tp) * p1.w), t1 = __saturatef(hi_f(tp) * p1.w);
+    const f32x2 t = pk2f(t0, t1);
+    const f32x2 sp = fma2f(bb, t, cw);                       // fmaf(bb, t, cw)
+    const f32x2 s = pk2f(__saturatef(lo_f(sp) * A.il[0]), __saturatef(hi_f(sp) * A.il[1]));
+    // -d: -dx = fmaf(s, -q3, fmaf(t, Ebx, wx)) (fmaf(-t, Ebx, -wx) negated)
+    const f32x2 dx = fma2f(s, A.ne[0], fma2f(t, Ex, wx));
+    const f32x2 dy = fma2f(s, A.ne[1], fma2f(t, Ey, wy));
+    const f32x2 dz = fma2f(s, A.ne[2], fma2f(t, Ez, wz));
+    const f32x2 d2 = fma2f(dx, dx, fma2f(dy, dy, mul2f(dz, dz)));
+    d0 = lo_f(d2);
+    d1 = hi_f(d2);
+}
+
 // A non-negative float as the double of the same value, by integer ops
 // (no F2F): the item minima are non-negative doubles compared as u64.
 __device__ __forceinline__ unsigned long long f32_as_f64_bits(float x) {

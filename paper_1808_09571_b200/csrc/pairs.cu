@@ -54,20 +54,45 @@ __global__ void filter_pairs_f32_kernel(const double* __restrict__ pa, const dou
         }
         const double v = pair_d2<FaceRef, false>(A, FaceRef{fb, 1}, fa, 1);
         float best = __int_as_float(0x7f800000);
+        float q[3][8];
         for (int i = 0; i < 3; ++i) {
-            const float q[8] = {(float)(fa[F_V + 3 * i] - ox), (float)(fa[F_V + 3 * i + 1] - oy),
-                                (float)(fa[F_V + 3 * i + 2] - oz), (float)fa[F_E + 3 * i], (float)fa[F_E + 3 * i + 1],
-                                (float)fa[F_E + 3 * i + 2], (float)fa[F_L + i], (float)fa[F_IL + i]};
-            for (int j = 0; j < 3; ++j) {
-                const float4 p0 = make_float4((float)(fb[F_V + 3 * j] - ox), (float)(fb[F_V + 3 * j + 1] - oy),
-                                              (float)(fb[F_V + 3 * j + 2] - oz), (float)fb[F_E + 3 * j]);
-                const float4 p1 = make_float4((float)fb[F_E + 3 * j + 1], (float)fb[F_E + 3 * j + 2],
-                                              (float)fb[F_L + j], (float)fb[F_IL + j]);
-                best = fminf(best, edge_pair32(q, p0, p1));
+            const float qi[8] = {(float)(fa[F_V + 3 * i] - ox), (float)(fa[F_V + 3 * i + 1] - oy),
+                                 (float)(fa[F_V + 3 * i + 2] - oz), (float)fa[F_E + 3 * i], (float)fa[F_E + 3 * i + 1],
+                                 (float)fa[F_E + 3 * i + 2], (float)fa[F_L + i], (float)fa[F_IL + i]};
+            for (int f = 0; f < 8; ++f) q[i][f] = qi[f];
+        }
+        // the packed form (edge_pair32x2) on A edges {0, 1} and {2, 2}: any
+        // bit difference from the scalar one is reported as NaN
+        AEdge32x2 A2[2];
+        for (int h = 0; h < 2; ++h) {
+            const float* x = q[2 * h];
+            const float* y = q[h == 0 ? 1 : 2];
+            for (int c = 0; c < 3; ++c)
+                A2[h].q[c] = pk2f(x[c], y[c]), A2[h].e[c] = pk2f(x[3 + c], y[3 + c]),
+                A2[h].ne[c] = pk2f(-x[3 + c], -y[3 + c]);
+            A2[h].L = pk2f(x[6], y[6]);
+            A2[h].il[0] = x[7], A2[h].il[1] = y[7];
+        }
+        bool same = true;
+        for (int j = 0; j < 3; ++j) {
+            const float4 p0 = make_float4((float)(fb[F_V + 3 * j] - ox), (float)(fb[F_V + 3 * j + 1] - oy),
+                                          (float)(fb[F_V + 3 * j + 2] - oz), (float)fb[F_E + 3 * j]);
+            const float4 p1 = make_float4((float)fb[F_E + 3 * j + 1], (float)fb[F_E + 3 * j + 2],
+                                          (float)fb[F_L + j], (float)fb[F_IL + j]);
+            float e[3];
+            for (int i = 0; i < 3; ++i) {
+                e[i] = edge_pair32(q[i], p0, p1);
+                best = fminf(best, e[i]);
             }
+            float d[4];
+            edge_pair32x2(A2[0], p0, p1, -p1.w, d[0], d[1]);
+            edge_pair32x2(A2[1], p0, p1, -p1.w, d[2], d[3]);
+            same = same && __float_as_uint(d[0]) == __float_as_uint(e[0]) &&
+                   __float_as_uint(d[1]) == __float_as_uint(e[1]) && __float_as_uint(d[2]) == __float_as_uint(e[2]) &&
+                   __float_as_uint(d[3]) == __float_as_uint(e[2]);
         }
         const double e = __longlong_as_double((long long)f32_as_f64_bits(best));
-        d2[k] = min_nn(v, e);
+        d2[k] = same ? min_nn(v, e) : __longlong_as_double(0x7ff8000000000000ll);
     }
 }
 

@@ -179,7 +179,10 @@ def test_filter_f32_error_within_eta_at_scale(seed):
     centre) on 10M adversarial pairs per seed: d~ never above d + eta_proven +
     eta_f32_proven. Each pair is centred on its b triangle and
     the pairs are grouped by edge-length decade, so the origin radius rB of a
-    call is that of its own pairs (production: B's box)."""
+    call is that of its own pairs (production: B's box). The library also
+    evaluates the packed form (edge_pair32x2, two A edges per f32x2 op) and
+    returns NaN for a pair whose packed values differ from the scalar ones in
+    any bit, so the isfinite assertion pins the packed kernel to this bound."""
     u = 2.0 ** -24
     worst = 0.0
     for part in range(5):
