@@ -63,24 +63,34 @@ __device__ __forceinline__ bool skip_face(const QArgs& a, const double* sb, int 
 // ---- TMA-staged streaming of B faces [b0, b1) through 2 SMEM stages ------
 // `g` counts sub-tiles across calls so the mbarrier phases stay consistent
 // when one kernel streams the same range several times.
-template <int NP>
+template <int NP, int NS = 2>
 struct Stream {
+    // NS staged sub-tiles in flight. NS == 2: a CTA barrier per sub-tile.
+    // NS > 2: each warp releases a stage through an "empty" mbarrier
+    // (blockDim / 32 arrivals) and thread 0 refills the stage every warp
+    // released NS - 2 sub-tiles earlier, so warps whose lanes meet exact
+    // predicates may drift NS - 2 sub-tiles apart instead of meeting at a
+    // barrier per sub-tile (one CTA barrier at the end of run()).
     double (*sm)[NP * kSB];
-    uint64_t* bar;
+    uint64_t* bar;   // NS full barriers
+    uint64_t* ebar;  // NS empty barriers (NS > 2)
     const int* plane;
     uint32_t g = 0;
 
     __device__ void init() {
         if (threadIdx.x == 0) {
-            mbar_init(&bar[0], 1);
-            mbar_init(&bar[1], 1);
+#pragma unroll
+            for (int i = 0; i < NS; ++i) {
+                mbar_init(&bar[i], 1);
+                if (NS > 2) mbar_init(&ebar[i], blockDim.x / 32);
+            }
             mbar_fence_init();
         }
         __syncthreads();
     }
 
     __device__ void issue(const double* Bp, uint64_t pad, uint64_t b0, uint64_t b1, uint32_t s) {
-        const int st = (g + s) & 1;
+        const int st = (g + s) % NS;
         const uint64_t f0 = b0 + (uint64_t)s * kSB;
         const int cnt = (int)min((uint64_t)kSB, b1 - f0);
         const uint32_t bytes = (uint32_t)(((cnt + 1) & ~1) * sizeof(double));
@@ -93,19 +103,28 @@ struct Stream {
     template <class F>
     __device__ void run(const double* Bp, uint64_t pad, uint64_t b0, uint64_t b1, F&& fn) {
         const uint32_t nsub = (uint32_t)((b1 - b0 + kSB - 1) / kSB);
-        if (threadIdx.x == 0) {
-            if (nsub > 0) issue(Bp, pad, b0, b1, 0);
-            if (nsub > 1) issue(Bp, pad, b0, b1, 1);
-        }
+        if (threadIdx.x == 0)
+            for (uint32_t s = 0; s < min((uint32_t)NS, nsub); ++s) issue(Bp, pad, b0, b1, s);
 #pragma unroll 1
         for (uint32_t s = 0; s < nsub; ++s) {
-            const int st = (g + s) & 1;
-            mbar_wait(&bar[st], ((g + s) >> 1) & 1);
+            const int st = (g + s) % NS;
+            mbar_wait(&bar[st], ((g + s) / NS) & 1);
             const uint64_t f0 = b0 + (uint64_t)s * kSB;
             fn(sm[st], (int)min((uint64_t)kSB, b1 - f0), f0);
-            __syncthreads();
-            if (threadIdx.x == 0 && s + 2 < nsub) issue(Bp, pad, b0, b1, s + 2);
+            if (NS == 2) {
+                __syncthreads();
+                if (threadIdx.x == 0 && s + 2 < nsub) issue(Bp, pad, b0, b1, s + 2);
+            } else {
+                __syncwarp();
+                if ((threadIdx.x & 31) == 0) mbar_arrive(&ebar[st]);
+                const int q = (int)s - (NS - 2);
+                if (threadIdx.x == 0 && q >= 0 && (uint32_t)q + NS < nsub) {
+                    mbar_wait(&ebar[(g + q) % NS], ((g + q) / NS) & 1);
+                    issue(Bp, pad, b0, b1, q + NS);
+                }
+            }
         }
+        if (NS > 2) __syncthreads();  // every stage released before a later run() refills it
         g += nsub;
     }
 };
@@ -288,7 +307,7 @@ __global__ void __launch_bounds__(kTile, TDB_QF_MINB) q_fused_kernel(QArgs a, co
                                                            unsigned long long* nrounds, NearLog near) {
     __shared__ alignas(128) double sm[2][kFilterPlanes * kSB];
     __shared__ alignas(8) uint64_t bar[2];
-    Stream<kFilterPlanes> S{sm, bar, kDistPlaneIds};
+    Stream<kFilterPlanes> S{sm, bar, nullptr, kDistPlaneIds};
     S.init();
     // per-thread candidate list (SMEM, column per thread): faces whose filter
     // value lies inside the band of the running minimum
@@ -403,7 +422,7 @@ __global__ void __launch_bounds__(kTile, 4) q_filter_kernel(QArgs a) {
     __shared__ alignas(128) double sm[2][kFilterPlanes * kSB];
     __shared__ alignas(8) uint64_t bar[2];
     __shared__ double red[kTile / 32];
-    Stream<kFilterPlanes> S{sm, bar, kDistPlaneIds};
+    Stream<kFilterPlanes> S{sm, bar, nullptr, kDistPlaneIds};
     S.init();
     const uint64_t item = blockIdx.x;
     const uint64_t tl = item / a.n_chunks, ch = item - tl * a.n_chunks;
@@ -505,7 +524,7 @@ __global__ void __launch_bounds__(kTile, 4) q_verify_kernel(QArgs a, const unsig
                                                             NearLog near) {
     __shared__ alignas(128) double sm[2][kFilterPlanes * kSB];
     __shared__ alignas(8) uint64_t bar[2];
-    Stream<kFilterPlanes> S{sm, bar, kDistPlaneIds};
+    Stream<kFilterPlanes> S{sm, bar, nullptr, kDistPlaneIds};
     S.init();
     const uint64_t nflag = *count;
     for (uint64_t w = blockIdx.x; w < nflag; w += gridDim.x) q_verify_item(a, S, list[w], pass, band2, qD, qP, ncand, near);
@@ -541,11 +560,17 @@ __global__ void q_check_kernel(QArgs a, const double* Bs, double* band2, double*
 // by tau; otherwise (3) the exact reference predicate. (1) and (2) only drop
 // pairs the reference cannot hit (intersects.cu header); degenerate faces
 // (n = 0, c = 0) always reach (3).
+// sub-tiles in flight (Stream): the lanes that reach the exact predicate
+// differ from warp to warp, so warps drift instead of meeting per sub-tile
+#ifndef TDB_QHIT_STAGES
+#define TDB_QHIT_STAGES 8
+#endif
+constexpr int kQHitStages = TDB_QHIT_STAGES;
 __global__ void __launch_bounds__(kTile, 4) q_hit_kernel(QArgs a, const double* Bs, unsigned long long* qhit,
                                                          unsigned long long* nexact, NearLog near) {
-    __shared__ alignas(128) double sm[2][kHitPlanes * kSB];
-    __shared__ alignas(8) uint64_t bar[2];
-    Stream<kHitPlanes> S{sm, bar, kHitPlaneIds};
+    __shared__ alignas(128) double sm[kQHitStages][kHitPlanes * kSB];
+    __shared__ alignas(8) uint64_t bar[kQHitStages], ebar[kQHitStages];
+    Stream<kHitPlanes, kQHitStages> S{sm, bar, ebar, kHitPlaneIds};
     S.init();
     const uint64_t item = blockIdx.x;
     const uint64_t tl = item / a.n_chunks, ch = item - tl * a.n_chunks;
