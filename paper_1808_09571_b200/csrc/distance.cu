@@ -174,6 +174,23 @@ __global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MIN
     // test; a sign is wrong only within rounding of the plane, where the
     // vertex / edge candidates already bound the pair)
     const double cA = dot3(A.n, A.v[0], A.v[1], A.v[2]);
+    // A's bounding sphere (FULL): a FP32 centre near the centroid, the radius
+    // to it rounded up. A B block whose sphere is apart from it holds no face
+    // that A's triangle can meet, so no piercing (the straddle loop only
+    // decides pierce_t in FULL mode).
+    float sAx = 0.f, sAy = 0.f, sAz = 0.f, sAr = 0.f;
+    if (!kEdges) {
+        sAx = (float)((A.v[0] + A.v[3] + A.v[6]) * (1.0 / 3.0));
+        sAy = (float)((A.v[1] + A.v[4] + A.v[7]) * (1.0 / 3.0));
+        sAz = (float)((A.v[2] + A.v[5] + A.v[8]) * (1.0 / 3.0));
+        double r2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const double dx = A.v[3 * k] - sAx, dy = A.v[3 * k + 1] - sAy, dz = A.v[3 * k + 2] - sAz;
+            r2 = fmax(r2, fma(dx, dx, fma(dy, dy, dz * dz)));
+        }
+        sAr = __double2float_ru(sqrt(r2) * (1.0 + 1e-9));
+    }
 #pragma unroll 1
     for (int s = 0; s < nblk; ++s) {
         const int st = s % NS;
@@ -220,6 +237,10 @@ __global__ void __launch_bounds__(kTile, kEdges ? TDB_FILTER_MINB : TDB_FACE_MIN
             const double4 sp = ssph[st];
             const double t = fabs(fma(A.n[0], sp.x, fma(A.n[1], sp.y, fma(A.n[2], sp.z, -cA))));
             maybe = !(t > sp.w * (1.0 + 1e-9) + 1e-9 * (fabs(sp.x) + fabs(sp.y) + fabs(sp.z) + fabs(cA) + sp.w));
+            // the two bounding spheres apart (margin >> the rounding of d2)
+            const double dx = sp.x - sAx, dy = sp.y - sAy, dz = sp.z - sAz;
+            const double rr = (sp.w + sAr) * (1.0 + 1e-9) + 1e-9 * (fabs(sp.x) + fabs(sp.y) + fabs(sp.z));
+            maybe = maybe && !(fma(dx, dx, fma(dy, dy, dz * dz)) > rr * rr);
         }
 #pragma unroll kUF
         for (int j = 0; j < (maybe ? (int)h.x : 0); ++j) {
