@@ -61,9 +61,10 @@ FILTER_LOOP_FACE = (0, 0)      # filter_kernel<false> face loop (straddle test):
 FILTER_LOOP_VERTEX = (13, 19)  # filter_kernel<false> vertex loop: a B vertex against the A face
 FILTER_VERT_PAIR = (13, 19)    # vertex_kernel: an A tile vertex against a B face
 FILTER_EDGE_PAIR = (31, 51)    # edge_kernel: an A tile edge against a B block edge
-FILTER_EDGE_PAIR32 = (30, 47)  # edge32_kernel (FP32, the chunk a multiple of 1,024 faces): 18 FFMA + 5 FMUL +
-                               # 3 FADD + 3 FMUL.SAT + 1 FMNMX per edge pair, + 1 MUFU.RCP (cuobjdump -sass);
-                               # scalar-equivalent (the packed loop issues FFMA2/FMUL2/FADD2: 2 lanes' ops each)
+FILTER_EDGE_PAIR32 = (31, 48)  # edge32_kernel (FP32, the chunk a multiple of 1,024 faces), packed loop in
+                               # scalar-equivalent ops per edge pair: 18 FFMA + 6 FMUL (one is the exact -fw) +
+                               # 3 FADD + 3 FMUL.SAT + 1 FMNMX, + 1 MUFU.RCP (cuobjdump -sass; each FFMA2 /
+                               # FMUL2 / FADD2 counts its two lanes; pinned by tests/test_sass_counts.py)
 U64_MAX = (1 << 64) - 1
 C3S_AXIS, C3S_ANGLE = (1.0, 2.0, 3.0), 0.37  # C3 stress variant rotation
 
